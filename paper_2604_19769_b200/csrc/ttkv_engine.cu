@@ -1,0 +1,1187 @@
+// ttkv_engine.cu -- the C ABI (include/ttkv_gpu.h): handle, memory, step
+// orchestration.  Host side of the B200 TTKV decode path; all compute is in
+// the sm_100a kernels of ttkv_{quantize,select,attention}.cu.  There is no
+// CPU fallback: without a device every call fails with TTKV_ECUDA.
+//
+// Step schedule (Engine::decode_step, engine.cpp:22-93), S streams at once:
+//   s0: append_kv -> [fork] -> score_blocks -> select_topk -> slow_stream_attn
+//   s1:              [fork] -> fast_attn_partial -> [join]
+//   s0: [join] -> combine_partials -> evict_quantize (every B-th step)
+// The fast tier (HBM) overlaps the PCIe-bound slow stream; selection never
+// leaves the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ttkv_gpu.h"
+#include "ttkv_launch.h"
+
+using namespace ttkv_dev;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Err {
+  int code;
+  std::string msg;
+};
+
+uint64_t packed_bytes_u(uint64_t count, uint32_t bits) {
+  if (bits == 16) return count * 4;  // raw float32 (quantizer.cpp:12-15)
+  return (count * bits + 7) / 8;
+}
+uint64_t modeled_bytes_u(uint64_t count, uint32_t bits) {
+  if (bits == 16) return count * 2;  // quantizer.cpp:17-20
+  return (count * bits + 7) / 8;
+}
+uint64_t modeled_block_bytes_cfg(const ttkv_tier_config& c) {  // quantizer.cpp:172-180
+  uint64_t b = modeled_bytes_u(c.block_size * c.d_k, c.key_bits) +
+               modeled_bytes_u(c.block_size * c.d_v, c.value_bits);
+  if (c.key_bits != 16) b += 4 * c.d_k;
+  if (c.value_bits != 16) b += 4 * c.d_v;
+  return b;
+}
+
+// TierConfig::validate (config.hpp:56-74), same messages.
+int validate(const ttkv_tier_config& c, std::string& msg) {
+  auto fail = [&](const char* m) {
+    msg = m;
+    return TTKV_ECONFIG;
+  };
+  if (c.d_k == 0 || c.d_v == 0) return fail("d_k and d_v must be positive");
+  if (c.block_size == 0) return fail("block_size must be positive");
+  if (c.bytes_full_precision == 0) return fail("bytes_full_precision must be positive");
+  auto valid_bits = [](uint32_t b) { return (b >= 2 && b <= 8) || b == 16; };
+  if (!valid_bits(c.key_bits) || !valid_bits(c.value_bits))
+    return fail("bit widths must be in [2,8] or 16");
+  if (c.key_bits < c.value_bits) return fail("key_bits must be >= value_bits");
+  if (c.hbm_budget_bytes < c.block_size * (c.d_k + c.d_v) * c.bytes_full_precision)
+    return fail("HBM budget smaller than one full-precision block");
+  if (!(c.fetch_fraction > 0.0 && c.fetch_fraction <= 1.0) && !c.has_top_k_blocks)
+    return fail("fetch_fraction must be in (0, 1]");
+  if (c.hbm_bandwidth <= 0 || c.pcie_bandwidth <= 0 || c.compute_rate <= 0)
+    return fail("bandwidths and compute_rate must be positive");
+  if (c.transfer_latency < 0) return fail("transfer_latency must be non-negative");
+  return TTKV_OK;
+}
+
+// fast_capacity (tier_store.cpp:36-44)
+int fast_capacity_of(const ttkv_tier_config& c, uint64_t& out, std::string& msg) {
+  int rc = validate(c, msg);
+  if (rc) return rc;
+  const uint64_t per_token = (c.d_k + c.d_v) * c.bytes_full_precision;
+  uint64_t tokens = c.hbm_budget_bytes / per_token;
+  tokens -= tokens % c.block_size;
+  if (tokens < c.block_size) {
+    msg = "HBM budget holds fewer tokens than one block";
+    return TTKV_ECONFIG;
+  }
+  out = tokens;
+  return TTKV_OK;
+}
+
+// SelectionPolicy::resolve (relevance.cpp:10-17)
+int resolve_k(const ttkv_selection_policy& p, uint64_t n, uint64_t& k, std::string& msg) {
+  if (p.has_top_k) {
+    k = std::min<uint64_t>(p.top_k, n);
+    return TTKV_OK;
+  }
+  if (!(p.fetch_fraction > 0.0 && p.fetch_fraction <= 1.0)) {
+    msg = "fetch_fraction must be in (0, 1]";
+    return TTKV_ECONFIG;
+  }
+  const uint64_t kk = (uint64_t)std::ceil(p.fetch_fraction * (double)n);
+  k = std::min<uint64_t>(kk, n);
+  return TTKV_OK;
+}
+
+uint32_t align_up(uint64_t x, uint64_t a) { return (uint32_t)((x + a - 1) / a * a); }
+
+RecordLayout make_layout(uint32_t B, uint32_t d_k, uint32_t d_v, uint32_t kb, uint32_t vb,
+                         uint32_t elem) {
+  RecordLayout r{};
+  r.k_bytes = kb == 16 ? B * d_k * elem : (uint32_t)((uint64_t(B) * d_k * kb + 7) / 8);
+  r.v_bytes = vb == 16 ? B * d_v * elem : (uint32_t)((uint64_t(B) * d_v * vb + 7) / 8);
+  r.v_off = align_up(r.k_bytes, 16);
+  r.kp_off = align_up(r.v_off + r.v_bytes, 16);
+  const uint32_t kp = kb == 16 ? 0 : 8 * d_k;
+  r.vp_off = align_up(r.kp_off + kp, 16);
+  const uint32_t vp = vb == 16 ? 0 : 8 * d_v;
+  r.used = align_up(r.vp_off + vp, 16);
+  r.stride = align_up(r.used, 128);
+  return r;
+}
+
+const char* kKernelNames[] = {"append", "score", "select", "fast", "slow", "combine", "evict"};
+enum Kind { K_APPEND = 0, K_SCORE, K_SELECT, K_FAST, K_SLOW, K_COMBINE, K_EVICT, K_N };
+
+}  // namespace
+
+struct ttkv_gpu {
+  ttkv_tier_config cfg{};
+  ttkv_selection_policy pol{};
+  ttkv_gpu_options opt{};
+  std::string err;
+  int dev = 0;
+  cudaStream_t s0 = nullptr, s1 = nullptr;
+  bool own_s0 = true;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  Geometry g{};
+  uint64_t l_fast = 0;
+  uint32_t copy_mode = 1;
+  uint32_t stages = 1;
+  // lockstep bookkeeping (identical for every stream)
+  uint64_t appended = 0, n_slow = 0, fast_front = 0;
+  uint64_t last_k = 0, last_n = 0;
+  // fast split
+  uint32_t FC = 256, nfc_cap = 1;
+  // device memory
+  void* ring_k = nullptr;
+  void* ring_v = nullptr;
+  float* cent = nullptr;
+  uint8_t* params = nullptr;  // HBM mirror of record params
+  double* scores = nullptr;
+  uint32_t *sel = nullptr, *mask = nullptr, *uids = nullptr, *umask = nullptr, *ucount = nullptr;
+  unsigned long long* counters = nullptr;
+  float* fpart = nullptr;
+  float* spart = nullptr;
+  uint64_t spart_chunks = 0;
+  float *q_dev = nullptr, *out_dev = nullptr;
+  void *kn_dev = nullptr, *vn_dev = nullptr;
+  void *stg_k = nullptr, *stg_v = nullptr;
+  uint64_t stg_tokens = 0;
+  // arena
+  uint8_t* arena_host = nullptr;  // pinned (TTKV_SLOW_PINNED_HOST)
+  uint8_t* arena_dev = nullptr;   // device-visible pointer
+  // pinned staging for the host-buffer API
+  float *h_q = nullptr, *h_out = nullptr;
+  void *h_k = nullptr, *h_v = nullptr;
+  // timing
+  bool timing = false;
+  struct Rec {
+    int kind;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  double ms[K_N] = {};
+  uint64_t cnt[K_N] = {};
+  uint64_t launches = 0;
+};
+
+namespace {
+
+int set_err(ttkv_gpu* h, int code, const std::string& m) {
+  if (h) h->err = m;
+  g_last_error = m;
+  return code;
+}
+
+#define CU(h, call)                                                                        \
+  do {                                                                                     \
+    cudaError_t e__ = (call);                                                              \
+    if (e__ != cudaSuccess)                                                                \
+      return set_err((h), TTKV_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+
+cudaEvent_t take_event(ttkv_gpu* h) {
+  if (!h->pool.empty()) {
+    cudaEvent_t e = h->pool.back();
+    h->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct KTimer {
+  ttkv_gpu* h;
+  int kind;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  KTimer(ttkv_gpu* hh, int k, cudaStream_t s) : h(hh), kind(k), st(s) {
+    h->launches++;
+    if (h->timing) {
+      a = take_event(h);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~KTimer() {
+    if (a) {
+      cudaEvent_t b = take_event(h);
+      cudaEventRecord(b, st);
+      h->recs.push_back({kind, a, b});
+    }
+  }
+};
+
+void drain_timing(ttkv_gpu* h) {
+  for (auto& r : h->recs) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    h->ms[r.kind] += ms;
+    h->cnt[r.kind] += 1;
+    h->pool.push_back(r.a);
+    h->pool.push_back(r.b);
+  }
+  h->recs.clear();
+}
+
+void free_all(ttkv_gpu* h) {
+  auto F = [](void* p) {
+    if (p) cudaFree(p);
+  };
+  F(h->ring_k); F(h->ring_v); F(h->cent); F(h->params); F(h->scores); F(h->sel); F(h->mask); F(h->uids);
+  F(h->umask); F(h->ucount); F(h->counters); F(h->fpart); F(h->spart); F(h->q_dev);
+  F(h->out_dev); F(h->kn_dev); F(h->vn_dev); F(h->stg_k); F(h->stg_v);
+  if (h->arena_host) cudaFreeHost(h->arena_host);
+  else if (h->arena_dev) cudaFree(h->arena_dev);
+  if (h->h_q) cudaFreeHost(h->h_q);
+  if (h->h_out) cudaFreeHost(h->h_out);
+  if (h->h_k) cudaFreeHost(h->h_k);
+  if (h->h_v) cudaFreeHost(h->h_v);
+  for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : h->pool) cudaEventDestroy(e);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->s1) cudaStreamDestroy(h->s1);
+  if (h->s0 && h->own_s0) cudaStreamDestroy(h->s0);
+}
+
+// (Re)allocate the per-block arrays for `need` blocks per stream.
+int ensure_blocks(ttkv_gpu* h, uint64_t need) {
+  if (need <= h->g.n_cap && h->arena_dev) return TTKV_OK;
+  if (need > select_max_blocks())
+    return set_err(h, TTKV_ECONFIG,
+                   "context exceeds the GPU selection capacity (" +
+                       std::to_string(select_max_blocks()) + " blocks per stream)");
+  const uint64_t old_cap = h->arena_dev ? h->g.n_cap : 0;
+  uint64_t cap = std::max<uint64_t>(need, old_cap ? 2 * old_cap : 16);
+  cap = std::min<uint64_t>(cap, select_max_blocks());
+  const uint64_t S = h->g.S, stride = h->g.rec.stride;
+  CU(h, cudaSetDevice(h->dev));
+  CU(h, cudaStreamSynchronize(h->s0));
+  // arena
+  uint8_t *nh = nullptr, *nd = nullptr;
+  const size_t arena_bytes = S * cap * stride;
+  if (h->opt.slow_tier == TTKV_SLOW_PINNED_HOST) {
+    CU(h, cudaHostAlloc((void**)&nh, arena_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    CU(h, cudaHostGetDevicePointer((void**)&nd, nh, 0));
+  } else {
+    CU(h, cudaMalloc((void**)&nd, arena_bytes));
+  }
+  float* ncent = nullptr;
+  CU(h, cudaMalloc((void**)&ncent, S * cap * h->g.d_k * sizeof(float)));
+  const uint64_t pbytes = h->g.rec.used - h->g.rec.kp_off;
+  uint8_t* nparams = nullptr;
+  if (pbytes) CU(h, cudaMalloc((void**)&nparams, S * cap * pbytes));
+  uint32_t* nsel = nullptr;
+  CU(h, cudaMalloc((void**)&nsel, S * h->g.Gs * cap * sizeof(uint32_t)));
+  if (old_cap && h->last_k)  // keep the last step's fetched lists readable
+    CU(h, cudaMemcpy2D(nsel, cap * 4, h->sel, old_cap * 4, h->last_k * 4, S * h->g.Gs,
+                       cudaMemcpyDeviceToDevice));
+  if (old_cap && h->n_slow && pbytes)
+    CU(h, cudaMemcpy2D(nparams, cap * pbytes, h->params, old_cap * pbytes, h->n_slow * pbytes, S,
+                       cudaMemcpyDeviceToDevice));
+  if (old_cap && h->n_slow) {
+    CU(h, cudaMemcpy2D(nh ? (void*)nh : (void*)nd, cap * stride,
+                       h->arena_host ? (void*)h->arena_host : (void*)h->arena_dev,
+                       old_cap * stride, h->n_slow * stride, S, cudaMemcpyDefault));
+    CU(h, cudaMemcpy2D(ncent, cap * h->g.d_k * 4, h->cent, old_cap * h->g.d_k * 4,
+                       h->n_slow * h->g.d_k * 4, S, cudaMemcpyDeviceToDevice));
+  }
+  if (h->arena_host) cudaFreeHost(h->arena_host);
+  else if (h->arena_dev) cudaFree(h->arena_dev);
+  if (h->cent) cudaFree(h->cent);
+  if (h->params) cudaFree(h->params);
+  if (h->sel) cudaFree(h->sel);
+  h->arena_host = nh;
+  h->arena_dev = nd;
+  h->cent = ncent;
+  h->params = nparams;
+  h->sel = nsel;
+  // per-step selection arrays (contents are per step; no copy)
+  auto realloc_dev = [&](void** p, size_t bytes) -> cudaError_t {
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    return cudaMalloc(p, bytes);
+  };
+  CU(h, realloc_dev((void**)&h->scores, S * h->g.Gs * cap * sizeof(double)));
+  CU(h, realloc_dev((void**)&h->mask, S * cap * sizeof(uint32_t)));
+  CU(h, realloc_dev((void**)&h->uids, S * cap * sizeof(uint32_t)));
+  CU(h, realloc_dev((void**)&h->umask, S * cap * sizeof(uint32_t)));
+  h->g.n_cap = cap;
+  return TTKV_OK;
+}
+
+int ensure_spart(ttkv_gpu* h, uint64_t chunks) {
+  if (chunks <= h->spart_chunks) return TTKV_OK;
+  const uint64_t c = std::max<uint64_t>(chunks, 2 * h->spart_chunks);
+  CU(h, cudaStreamSynchronize(h->s0));
+  if (h->spart) cudaFree(h->spart);
+  h->spart = nullptr;
+  CU(h, cudaMalloc((void**)&h->spart,
+                   (size_t)h->g.S * h->g.G * c * (h->g.d_v + 2) * sizeof(float)));
+  h->spart_chunks = c;
+  return TTKV_OK;
+}
+
+int ensure_staging(ttkv_gpu* h, uint64_t tokens) {
+  if (tokens <= h->stg_tokens) return TTKV_OK;
+  CU(h, cudaStreamSynchronize(h->s0));
+  if (h->stg_k) cudaFree(h->stg_k);
+  if (h->stg_v) cudaFree(h->stg_v);
+  h->stg_k = h->stg_v = nullptr;
+  const size_t e = 4;  // sized for f32 input
+  CU(h, cudaMalloc(&h->stg_k, (size_t)h->g.S * tokens * h->g.d_k * e));
+  CU(h, cudaMalloc(&h->stg_v, (size_t)h->g.S * tokens * h->g.d_v * e));
+  h->stg_tokens = tokens;
+  return TTKV_OK;
+}
+
+// Evict every pending block (settle, engine.cpp:88-91; tier_store.cpp:71-98).
+int settle_evictions(ttkv_gpu* h, bool* evicted) {
+  while (h->appended - h->fast_front > h->l_fast) {
+    int rc = ensure_blocks(h, h->n_slow + 1);
+    if (rc) return rc;
+    EvictArgs a{};
+    a.g = h->g;
+    a.ring_k = h->ring_k;
+    a.ring_v = h->ring_v;
+    a.in_k = a.in_v = nullptr;
+    a.in_tokens = 0;
+    a.split_pos = h->appended;  // everything from the ring
+    a.first_block = h->n_slow;
+    a.arena = h->arena_dev;
+    a.cent = h->cent;
+    a.params = h->params;
+    {
+      KTimer t(h, K_EVICT, h->s0);
+      CU(h, launch_evict(a, 1, kInF32, h->s0));
+    }
+    h->n_slow++;
+    h->fast_front += h->g.B;
+    if (evicted) *evicted = true;
+  }
+  return TTKV_OK;
+}
+
+// Bulk prefill of P tokens already on the device (staging layout [S][P][d]).
+int prefill_chunk(ttkv_gpu* h, const void* in_k, const void* in_v, int in_dtype, uint64_t P) {
+  const uint64_t A = h->appended, total = A + P, B = h->g.B;
+  uint64_t nb_after = h->n_slow;
+  if (total > h->l_fast) nb_after = std::max<uint64_t>(nb_after, (total - h->l_fast - 1) / B + 1);
+  int rc = ensure_blocks(h, nb_after);
+  if (rc) return rc;
+  if (nb_after > h->n_slow) {
+    EvictArgs a{};
+    a.g = h->g;
+    a.ring_k = h->ring_k;
+    a.ring_v = h->ring_v;
+    a.in_k = in_k;
+    a.in_v = in_v;
+    a.in_tokens = P;
+    a.split_pos = A;
+    a.first_block = h->n_slow;
+    a.arena = h->arena_dev;
+    a.cent = h->cent;
+    a.params = h->params;
+    KTimer t(h, K_EVICT, h->s0);
+    CU(h, launch_evict(a, (uint32_t)(nb_after - h->n_slow), in_dtype, h->s0));
+  }
+  const uint64_t start = std::max<uint64_t>(A, nb_after * B);
+  if (start < total) {
+    const size_t esz = in_dtype == kInF16 ? 2 : 4;
+    const uint8_t* kb = static_cast<const uint8_t*>(in_k) + (start - A) * h->g.d_k * esz;
+    const uint8_t* vb = static_cast<const uint8_t*>(in_v) + (start - A) * h->g.d_v * esz;
+    KTimer t(h, K_APPEND, h->s0);
+    CU(h, launch_append(h->g, h->ring_k, h->ring_v, kb, vb, in_dtype, start, P, total - start,
+                        h->s0));
+  }
+  h->appended = total;
+  h->n_slow = nb_after;
+  h->fast_front = nb_after * B;
+  return TTKV_OK;
+}
+
+uint64_t prefill_chunk_tokens(const ttkv_gpu* h) {
+  // ~256 MB of f32 staging per chunk, a multiple of B
+  const uint64_t per_tok = (uint64_t)h->g.S * (h->g.d_k + h->g.d_v) * 4;
+  uint64_t P = (256ull << 20) / std::max<uint64_t>(per_tok, 1);
+  P = std::max<uint64_t>(P / h->g.B * h->g.B, h->g.B);
+  return P;
+}
+
+int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int dtype,
+                float* out, ttkv_step_report* rep) {
+  {  // grow before selecting so a settle-time eviction never reallocates
+    int rc0 = ensure_blocks(h, h->n_slow + 1);
+    if (rc0) return rc0;
+  }
+  const Geometry& g = h->g;
+  uint64_t pos = h->appended;
+  // append_kv: the new token attends to itself
+  {
+    KTimer t(h, K_APPEND, h->s0);
+    CU(h, launch_append(g, h->ring_k, h->ring_v, kn, vn, dtype, pos % g.C, 1, 1, h->s0));
+  }
+  h->appended = pos + 1;
+  const uint64_t F = h->appended - h->fast_front;
+  const uint64_t n = h->n_slow;
+  uint64_t k = 0;
+  {
+    std::string m;
+    int rc = resolve_k(h->pol, n, k, m);
+    if (rc) return set_err(h, rc, m);
+  }
+  const float scale_log2 = (float)(1.0 / std::sqrt((double)g.d_k) * 1.4426950408889634);
+
+  // fast tier on s1, overlapped with the slow stream on s0
+  CU(h, cudaEventRecord(h->ev_fork, h->s0));
+  CU(h, cudaStreamWaitEvent(h->s1, h->ev_fork, 0));
+  const uint32_t nfc = (uint32_t)((F + h->FC - 1) / h->FC);
+  {
+    FastArgs a{};
+    a.g = g;
+    a.ring_k = h->ring_k;
+    a.ring_v = h->ring_v;
+    a.q = q;
+    a.part = h->fpart;
+    a.front = h->fast_front;
+    a.F = (uint32_t)F;
+    a.FC = h->FC;
+    a.nfc = nfc;
+    a.scale_log2 = scale_log2;
+    KTimer t(h, K_FAST, h->s1);
+    CU(h, launch_fast(a, h->s1));
+  }
+  CU(h, cudaEventRecord(h->ev_join, h->s1));
+
+  uint32_t CH = 4;
+  bool slow = n > 0 && k > 0;
+  CU(h, cudaMemsetAsync(h->counters, 0, sizeof(unsigned long long) * 4, h->s0));
+  if (slow) {
+    // union entries per CTA: ~4 waves of 2 CTAs/SM over the lower bound S*k
+    const uint64_t est = (uint64_t)g.S * k;
+    CH = (uint32_t)std::min<uint64_t>(64, std::max<uint64_t>(4, (est + 1183) / 1184));
+    const uint64_t grid_chunks = (n + CH - 1) / CH;
+    int rc = ensure_spart(h, grid_chunks);
+    if (rc) return rc;
+    {
+      ScoreArgs a{g, q, h->cent, h->scores, (uint32_t)n};
+      KTimer t(h, K_SCORE, h->s0);
+      CU(h, launch_score(a, h->s0));
+    }
+    {
+      SelectArgs a{};
+      a.g = g;
+      a.scores = h->scores;
+      a.sel = h->sel;
+      a.mask = h->mask;
+      a.union_ids = h->uids;
+      a.union_mask = h->umask;
+      a.union_count = h->ucount;
+      a.counters = h->counters;
+      a.n = (uint32_t)n;
+      a.k = (uint32_t)k;
+      KTimer t(h, K_SELECT, h->s0);
+      CU(h, launch_select(a, h->s0));
+    }
+    {
+      SlowArgs a{};
+      a.g = g;
+      a.arena = h->arena_dev;
+      a.params = h->params;
+      a.union_ids = h->uids;
+      a.union_mask = h->umask;
+      a.union_count = h->ucount;
+      a.q = q;
+      a.part = h->spart;
+      a.CH = CH;
+      a.nsc = (uint32_t)h->spart_chunks;
+      a.stages = h->stages;
+      a.scale_log2 = scale_log2;
+      KTimer t(h, K_SLOW, h->s0);
+      CU(h, launch_slow(a, (uint32_t)grid_chunks, (int)h->copy_mode, h->s0));
+    }
+  }
+  CU(h, cudaStreamWaitEvent(h->s0, h->ev_join, 0));
+  {
+    CombineArgs a{};
+    a.g = g;
+    a.fpart = h->fpart;
+    a.nfc = nfc;
+    a.spart = slow ? h->spart : nullptr;
+    a.nsc = (uint32_t)h->spart_chunks;
+    a.CH = CH;
+    a.union_count = slow ? h->ucount : nullptr;
+    a.out = out;
+    KTimer t(h, K_COMBINE, h->s0);
+    CU(h, launch_combine(a, h->s0));
+  }
+  h->last_k = slow ? k : 0;
+  h->last_n = n;
+  bool evicted = false;
+  int rc = settle_evictions(h, &evicted);
+  if (rc) return rc;
+  if (rep) {
+    rep->blocks_scored = n;
+    rep->blocks_fetched = k;
+    rep->bytes_transferred = (double)k * (double)modeled_block_bytes_cfg(h->cfg);
+    rep->fast_tokens = F;
+    rep->eviction_occurred = evicted ? 1 : 0;
+    rep->union_blocks = 0;
+    rep->pcie_bytes = 0;
+  }
+  return TTKV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ttkv_abi_version(void) { return TTKV_ABI_VERSION; }
+const char* ttkv_last_error(void) { return g_last_error.c_str(); }
+const char* ttkv_gpu_last_error(const ttkv_gpu* h) {
+  return h ? h->err.c_str() : g_last_error.c_str();
+}
+
+int ttkv_device_count(int* n) {
+  if (!n) return set_err(nullptr, TTKV_EINVAL, "null pointer");
+  cudaError_t e = cudaGetDeviceCount(n);
+  if (e != cudaSuccess) {
+    *n = 0;
+    return set_err(nullptr, TTKV_ECUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+  }
+  return TTKV_OK;
+}
+
+void ttkv_default_config(ttkv_tier_config* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof(*c));
+  c->hbm_budget_bytes = 0;
+  c->d_k = 64;
+  c->d_v = 64;
+  c->bytes_full_precision = 2;
+  c->block_size = 128;
+  c->key_bits = 8;
+  c->value_bits = 4;
+  c->fetch_fraction = 0.45;
+  c->has_top_k_blocks = 0;
+  c->top_k_blocks = 0;
+  c->hbm_bandwidth = 2.0e12;
+  c->pcie_bandwidth = 3.2e10;
+  c->transfer_latency = 1.0e-5;
+  c->compute_rate = 4.0e11;
+}
+
+int ttkv_validate_config(const ttkv_tier_config* c) {
+  if (!c) return set_err(nullptr, TTKV_EINVAL, "null config");
+  std::string m;
+  int rc = validate(*c, m);
+  if (rc) set_err(nullptr, rc, m);
+  return rc;
+}
+
+uint64_t ttkv_fast_capacity(const ttkv_tier_config* c) {
+  if (!c) return 0;
+  uint64_t out = 0;
+  std::string m;
+  if (fast_capacity_of(*c, out, m)) {
+    set_err(nullptr, TTKV_ECONFIG, m);
+    return 0;
+  }
+  return out;
+}
+
+uint64_t ttkv_modeled_block_bytes(const ttkv_tier_config* c) {
+  return c ? modeled_block_bytes_cfg(*c) : 0;
+}
+uint64_t ttkv_packed_bytes(uint64_t count, uint32_t bits) { return packed_bytes_u(count, bits); }
+
+uint64_t ttkv_resolve(const ttkv_selection_policy* p, uint64_t n) {
+  if (!p) return UINT64_MAX;
+  uint64_t k = 0;
+  std::string m;
+  if (resolve_k(*p, n, k, m)) {
+    set_err(nullptr, TTKV_ECONFIG, m);
+    return UINT64_MAX;
+  }
+  return k;
+}
+
+int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* pol,
+                    const ttkv_gpu_options* opt, ttkv_gpu** out) {
+  if (!cfg || !pol || !opt || !out) return set_err(nullptr, TTKV_EINVAL, "null argument");
+  *out = nullptr;
+  std::string m;
+  uint64_t l_fast = 0;
+  int rc = fast_capacity_of(*cfg, l_fast, m);
+  if (rc) return set_err(nullptr, rc, m);
+  if (!pol->has_top_k && !(pol->fetch_fraction > 0.0 && pol->fetch_fraction <= 1.0))
+    return set_err(nullptr, TTKV_ECONFIG, "fetch_fraction must be in (0, 1]");
+  // B200 engine limits (documented in DESIGN.md)
+  if (cfg->d_k > (uint64_t)kMaxD || cfg->d_v > (uint64_t)kMaxD)
+    return set_err(nullptr, TTKV_ECONFIG, "GPU engine supports d_k, d_v <= 128");
+  if (cfg->bytes_full_precision != 2 && cfg->bytes_full_precision != 4)
+    return set_err(nullptr, TTKV_ECONFIG,
+                   "GPU engine supports bytes_full_precision 2 (fp16 ring) or 4 (fp32 ring)");
+  if (cfg->block_size > 512)
+    return set_err(nullptr, TTKV_ECONFIG, "GPU engine supports block_size <= 512");
+  if (opt->n_streams == 0 || opt->heads_per_stream == 0 || opt->heads_per_stream > (uint32_t)kMaxG)
+    return set_err(nullptr, TTKV_ECONFIG, "n_streams >= 1 and heads_per_stream in [1, 8]");
+
+  int ndev = 0;
+  cudaError_t ce = cudaGetDeviceCount(&ndev);
+  if (ce != cudaSuccess || ndev == 0)
+    return set_err(nullptr, TTKV_ECUDA,
+                   std::string("no CUDA device: ") + (ce != cudaSuccess ? cudaGetErrorString(ce) : "0 devices"));
+  if (opt->device < 0 || opt->device >= ndev)
+    return set_err(nullptr, TTKV_ECUDA, "device ordinal out of range");
+
+  ttkv_gpu* h = new ttkv_gpu();
+  h->cfg = *cfg;
+  h->pol = *pol;
+  h->opt = *opt;
+  h->dev = opt->device;
+  h->l_fast = l_fast;
+  Geometry& g = h->g;
+  g.S = opt->n_streams;
+  g.G = opt->heads_per_stream;
+  g.Gs = opt->group_select ? 1 : g.G;
+  g.d_k = (uint32_t)cfg->d_k;
+  g.d_v = (uint32_t)cfg->d_v;
+  g.B = (uint32_t)cfg->block_size;
+  g.kb = cfg->key_bits;
+  g.vb = cfg->value_bits;
+  g.elem = (uint32_t)cfg->bytes_full_precision;
+  g.C = l_fast + g.B;
+  g.n_cap = 0;
+  g.rec = make_layout(g.B, g.d_k, g.d_v, g.kb, g.vb, g.elem);
+  if (evict_smem_bytes(g) > 220 * 1024) {
+    delete h;
+    return set_err(nullptr, TTKV_ECONFIG, "block too large for the GPU quantizer");
+  }
+  h->stages = slow_stages_for(g);
+  if (h->stages == 0) {
+    delete h;
+    return set_err(nullptr, TTKV_ECONFIG, "slow-tier record too large to stage in shared memory");
+  }
+  h->copy_mode = opt->copy_mode ? opt->copy_mode : 1;
+  if (const char* env = std::getenv("TTKV_COPY_MODE")) {
+    if (!std::strcmp(env, "ldg")) h->copy_mode = 2;
+    if (!std::strcmp(env, "bulk")) h->copy_mode = 1;
+  }
+  // fast split: ~8 waves of 4-warp CTAs
+  {
+    const uint64_t Fmax = l_fast + 1;
+    const uint64_t target = std::max<uint64_t>(1, (148ull * 8 + g.S - 1) / g.S);
+    uint64_t FC = (Fmax + target - 1) / target;
+    FC = std::max<uint64_t>(64, std::min<uint64_t>(1024, (FC + 31) / 32 * 32));
+    h->FC = (uint32_t)FC;
+    h->nfc_cap = (uint32_t)((Fmax + FC - 1) / FC);
+  }
+
+#define CREATE_CU(call)                                                                      \
+  do {                                                                                       \
+    cudaError_t e__ = (call);                                                                \
+    if (e__ != cudaSuccess) {                                                                \
+      std::string msg__ = std::string(#call) + ": " + cudaGetErrorString(e__);               \
+      free_all(h);                                                                           \
+      delete h;                                                                              \
+      return set_err(nullptr, TTKV_ECUDA, msg__);                                            \
+    }                                                                                        \
+  } while (0)
+
+  CREATE_CU(cudaSetDevice(h->dev));
+  CREATE_CU(cudaStreamCreateWithFlags(&h->s0, cudaStreamNonBlocking));
+  CREATE_CU(cudaStreamCreateWithFlags(&h->s1, cudaStreamNonBlocking));
+  CREATE_CU(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+  CREATE_CU(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+  const size_t S = g.S;
+  CREATE_CU(cudaMalloc(&h->ring_k, S * g.C * g.d_k * g.elem));
+  CREATE_CU(cudaMalloc(&h->ring_v, S * g.C * g.d_v * g.elem));
+  CREATE_CU(cudaMemset(h->ring_k, 0, S * g.C * g.d_k * g.elem));
+  CREATE_CU(cudaMemset(h->ring_v, 0, S * g.C * g.d_v * g.elem));
+  CREATE_CU(cudaMalloc((void**)&h->ucount, S * sizeof(uint32_t)));
+  CREATE_CU(cudaMemset(h->ucount, 0, S * sizeof(uint32_t)));
+  CREATE_CU(cudaMalloc((void**)&h->counters, 4 * sizeof(unsigned long long)));
+  CREATE_CU(cudaMalloc((void**)&h->fpart, S * g.G * h->nfc_cap * (g.d_v + 2) * sizeof(float)));
+  CREATE_CU(cudaMalloc((void**)&h->q_dev, S * g.G * g.d_k * sizeof(float)));
+  CREATE_CU(cudaMalloc((void**)&h->out_dev, S * g.G * g.d_v * sizeof(float)));
+  CREATE_CU(cudaMalloc(&h->kn_dev, S * g.d_k * 4));
+  CREATE_CU(cudaMalloc(&h->vn_dev, S * g.d_v * 4));
+  CREATE_CU(cudaHostAlloc((void**)&h->h_q, S * g.G * g.d_k * sizeof(float), cudaHostAllocPortable));
+  CREATE_CU(cudaHostAlloc((void**)&h->h_out, S * g.G * g.d_v * sizeof(float), cudaHostAllocPortable));
+  CREATE_CU(cudaHostAlloc(&h->h_k, S * g.d_k * 4, cudaHostAllocPortable));
+  CREATE_CU(cudaHostAlloc(&h->h_v, S * g.d_v * 4, cudaHostAllocPortable));
+  const uint64_t reserve_blocks =
+      std::max<uint64_t>(16, (opt->reserve_tokens + g.B - 1) / g.B + 2);
+  rc = ensure_blocks(h, std::min<uint64_t>(reserve_blocks, select_max_blocks()));
+  if (rc) {
+    std::string msg = h->err;
+    free_all(h);
+    delete h;
+    return set_err(nullptr, rc, msg);
+  }
+#undef CREATE_CU
+  *out = h;
+  return TTKV_OK;
+}
+
+void ttkv_gpu_destroy(ttkv_gpu* h) {
+  if (!h) return;
+  cudaSetDevice(h->dev);
+  if (h->s0) cudaStreamSynchronize(h->s0);
+  if (h->s1) cudaStreamSynchronize(h->s1);
+  free_all(h);
+  delete h;
+}
+
+int ttkv_gpu_set_stream(ttkv_gpu* h, void* stream) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  CU(h, cudaSetDevice(h->dev));
+  CU(h, cudaStreamSynchronize(h->s0));
+  if (h->own_s0) cudaStreamDestroy(h->s0);
+  if (stream) {
+    h->s0 = static_cast<cudaStream_t>(stream);
+    h->own_s0 = false;
+  } else {
+    CU(h, cudaStreamCreateWithFlags(&h->s0, cudaStreamNonBlocking));
+    h->own_s0 = true;
+  }
+  return TTKV_OK;
+}
+
+void* ttkv_gpu_get_stream(ttkv_gpu* h) { return h ? (void*)h->s0 : nullptr; }
+
+int ttkv_gpu_synchronize(ttkv_gpu* h) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  CU(h, cudaSetDevice(h->dev));
+  CU(h, cudaStreamSynchronize(h->s0));
+  CU(h, cudaStreamSynchronize(h->s1));
+  return TTKV_OK;
+}
+
+int ttkv_gpu_prefill(ttkv_gpu* h, const void* keys, const void* values, uint64_t n, int dtype) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  if (n == 0) return TTKV_OK;
+  if (!keys || !values) return set_err(h, TTKV_EINVAL, "null key/value pointer");
+  if (dtype != TTKV_DTYPE_F32 && dtype != TTKV_DTYPE_F16)
+    return set_err(h, TTKV_ESHAPE, "prefill: unknown dtype");
+  CU(h, cudaSetDevice(h->dev));
+  const uint64_t P = std::min<uint64_t>(prefill_chunk_tokens(h), n);
+  int rc = ensure_staging(h, P);
+  if (rc) return rc;
+  const size_t esz = dtype == TTKV_DTYPE_F16 ? 2 : 4;
+  const Geometry& g = h->g;
+  for (uint64_t t0 = 0; t0 < n; t0 += P) {
+    const uint64_t m = std::min<uint64_t>(P, n - t0);
+    // [S][n][d] host -> [S][m][d] device, one 2D copy per tensor
+    CU(h, cudaMemcpy2DAsync(h->stg_k, m * g.d_k * esz,
+                            static_cast<const uint8_t*>(keys) + t0 * g.d_k * esz, n * g.d_k * esz,
+                            m * g.d_k * esz, g.S, cudaMemcpyHostToDevice, h->s0));
+    CU(h, cudaMemcpy2DAsync(h->stg_v, m * g.d_v * esz,
+                            static_cast<const uint8_t*>(values) + t0 * g.d_v * esz,
+                            n * g.d_v * esz, m * g.d_v * esz, g.S, cudaMemcpyHostToDevice, h->s0));
+    rc = prefill_chunk(h, h->stg_k, h->stg_v, dtype == TTKV_DTYPE_F16 ? kInF16 : kInF32, m);
+    if (rc) return rc;
+  }
+  CU(h, cudaStreamSynchronize(h->s0));
+  return TTKV_OK;
+}
+
+int ttkv_gpu_prefill_synthetic(ttkv_gpu* h, uint64_t n, uint64_t seed) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  CU(h, cudaSetDevice(h->dev));
+  const uint64_t P = std::min<uint64_t>(prefill_chunk_tokens(h), std::max<uint64_t>(n, 1));
+  int rc = ensure_staging(h, P);
+  if (rc) return rc;
+  const int in_dt = h->g.elem == 2 ? kInF16 : kInF32;
+  for (uint64_t t0 = 0; t0 < n; t0 += P) {
+    const uint64_t m = std::min<uint64_t>(P, n - t0);
+    CU(h, launch_synth(h->g, h->stg_k, h->stg_v, m, h->appended, seed, h->s0));
+    rc = prefill_chunk(h, h->stg_k, h->stg_v, in_dt, m);
+    if (rc) return rc;
+  }
+  CU(h, cudaStreamSynchronize(h->s0));
+  return TTKV_OK;
+}
+
+int ttkv_gpu_decode_step_device(ttkv_gpu* h, const float* q, const void* kn, const void* vn,
+                                int dtype, float* out, ttkv_step_report* rep) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  if (!q || !kn || !vn || !out) return set_err(h, TTKV_EINVAL, "null pointer");
+  if (dtype != TTKV_DTYPE_F32 && dtype != TTKV_DTYPE_F16)
+    return set_err(h, TTKV_ESHAPE, "decode_step: unknown dtype");
+  CU(h, cudaSetDevice(h->dev));
+  return decode_core(h, q, kn, vn, dtype == TTKV_DTYPE_F16 ? kInF16 : kInF32, out, rep);
+}
+
+int ttkv_gpu_decode_step(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int dtype,
+                         float* out, ttkv_step_report* rep) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  if (!q || !kn || !vn || !out) return set_err(h, TTKV_EINVAL, "null pointer");
+  if (dtype != TTKV_DTYPE_F32 && dtype != TTKV_DTYPE_F16)
+    return set_err(h, TTKV_ESHAPE, "decode_step: unknown dtype");
+  CU(h, cudaSetDevice(h->dev));
+  const Geometry& g = h->g;
+  const size_t esz = dtype == TTKV_DTYPE_F16 ? 2 : 4;
+  const size_t qb = (size_t)g.S * g.G * g.d_k * 4, ob = (size_t)g.S * g.G * g.d_v * 4;
+  const size_t kb = (size_t)g.S * g.d_k * esz, vb = (size_t)g.S * g.d_v * esz;
+  std::memcpy(h->h_q, q, qb);
+  std::memcpy(h->h_k, kn, kb);
+  std::memcpy(h->h_v, vn, vb);
+  CU(h, cudaMemcpyAsync(h->q_dev, h->h_q, qb, cudaMemcpyHostToDevice, h->s0));
+  CU(h, cudaMemcpyAsync(h->kn_dev, h->h_k, kb, cudaMemcpyHostToDevice, h->s0));
+  CU(h, cudaMemcpyAsync(h->vn_dev, h->h_v, vb, cudaMemcpyHostToDevice, h->s0));
+  int rc = decode_core(h, h->q_dev, h->kn_dev, h->vn_dev,
+                       dtype == TTKV_DTYPE_F16 ? kInF16 : kInF32, h->out_dev, rep);
+  if (rc) return rc;
+  CU(h, cudaMemcpyAsync(h->h_out, h->out_dev, ob, cudaMemcpyDeviceToHost, h->s0));
+  unsigned long long ctr[4] = {};
+  CU(h, cudaMemcpyAsync(ctr, h->counters, sizeof(ctr), cudaMemcpyDeviceToHost, h->s0));
+  CU(h, cudaStreamSynchronize(h->s0));
+  std::memcpy(out, h->h_out, ob);
+  if (rep) {
+    rep->union_blocks = ctr[0];
+    rep->pcie_bytes = ctr[0] * (uint64_t)h->g.rec.kp_off;
+  }
+  return TTKV_OK;
+}
+
+int ttkv_gpu_read_step_counters(ttkv_gpu* h, uint64_t* union_blocks, uint64_t* pcie_bytes) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  unsigned long long ctr[4] = {};
+  CU(h, cudaSetDevice(h->dev));
+  CU(h, cudaMemcpyAsync(ctr, h->counters, sizeof(ctr), cudaMemcpyDeviceToHost, h->s0));
+  CU(h, cudaStreamSynchronize(h->s0));
+  if (union_blocks) *union_blocks = ctr[0];
+  if (pcie_bytes) *pcie_bytes = ctr[0] * (uint64_t)h->g.rec.kp_off;
+  return TTKV_OK;
+}
+
+int ttkv_gpu_state(ttkv_gpu* h, ttkv_state* st) {
+  if (!h || !st) return set_err(h, TTKV_EINVAL, "null argument");
+  st->appended = h->appended;
+  st->fast_tokens = h->appended - h->fast_front;
+  st->slow_blocks = h->n_slow;
+  st->l_fast = h->l_fast;
+  st->record_bytes = h->g.rec.used;
+  st->modeled_block_bytes = modeled_block_bytes_cfg(h->cfg);
+  st->n_streams = h->g.S;
+  st->heads_per_stream = h->g.G;
+  st->block_capacity = h->g.n_cap;
+  st->launches = h->launches;
+  return TTKV_OK;
+}
+
+int ttkv_gpu_read_fetched(ttkv_gpu* h, uint32_t stream, uint32_t head, uint64_t* out,
+                          uint64_t cap, uint64_t* n) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  if (stream >= h->g.S || head >= h->g.G) return set_err(h, TTKV_ESHAPE, "stream/head out of range");
+  const uint64_t k = h->last_k;
+  if (n) *n = k;
+  if (!out || k == 0) return TTKV_OK;
+  const uint32_t hs = h->g.Gs == h->g.G ? head : 0;
+  std::vector<uint32_t> tmp(k);
+  CU(h, cudaSetDevice(h->dev));
+  CU(h, cudaStreamSynchronize(h->s0));
+  CU(h, cudaMemcpy(tmp.data(), h->sel + ((uint64_t)stream * h->g.Gs + hs) * h->g.n_cap,
+                   k * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  for (uint64_t i = 0; i < k && i < cap; ++i) out[i] = tmp[i];
+  return TTKV_OK;
+}
+
+static float half_bits_to_float(uint16_t b) {
+  const uint32_t sign = (uint32_t)(b >> 15) << 31;
+  uint32_t exp = (b >> 10) & 0x1f, man = b & 0x3ff;
+  uint32_t f;
+  if (exp == 0) {
+    if (man == 0) f = sign;
+    else {
+      exp = 127 - 15 + 1;
+      while (!(man & 0x400)) { man <<= 1; exp--; }
+      man &= 0x3ff;
+      f = sign | (exp << 23) | (man << 13);
+    }
+  } else if (exp == 31) {
+    f = sign | 0x7f800000u | (man << 13);
+  } else {
+    f = sign | ((exp + 127 - 15) << 23) | (man << 13);
+  }
+  float out;
+  std::memcpy(&out, &f, 4);
+  return out;
+}
+
+int ttkv_gpu_read_block(ttkv_gpu* h, uint32_t stream, uint64_t blk, uint8_t* packed_k,
+                        uint8_t* packed_v, float* key_params, float* value_params,
+                        float* centroid, uint64_t* first_position) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  if (stream >= h->g.S) return set_err(h, TTKV_ESHAPE, "stream out of range");
+  if (blk >= h->n_slow)
+    return set_err(h, TTKV_EERROR, "BlockIndex: unknown block " + std::to_string(blk));
+  const Geometry& g = h->g;
+  CU(h, cudaSetDevice(h->dev));
+  CU(h, cudaStreamSynchronize(h->s0));
+  std::vector<uint8_t> rec(g.rec.stride);
+  const uint64_t off = ((uint64_t)stream * g.n_cap + blk) * g.rec.stride;
+  if (h->arena_host) std::memcpy(rec.data(), h->arena_host + off, g.rec.stride);
+  else CU(h, cudaMemcpy(rec.data(), h->arena_dev + off, g.rec.stride, cudaMemcpyDeviceToHost));
+  auto export_payload = [&](const uint8_t* src, uint32_t bits, uint32_t dim, uint8_t* dst) {
+    if (!dst) return;
+    if (bits != 16) {
+      std::memcpy(dst, src, (size_t)((uint64_t(g.B) * dim * bits + 7) / 8));
+      return;
+    }
+    float* f = reinterpret_cast<float*>(dst);
+    const size_t cnt = (size_t)g.B * dim;
+    if (g.elem == 4) std::memcpy(f, src, cnt * 4);
+    else
+      for (size_t i = 0; i < cnt; ++i) {
+        uint16_t b;
+        std::memcpy(&b, src + 2 * i, 2);
+        f[i] = half_bits_to_float(b);
+      }
+  };
+  export_payload(rec.data(), g.kb, g.d_k, packed_k);
+  export_payload(rec.data() + g.rec.v_off, g.vb, g.d_v, packed_v);
+  if (key_params && g.kb != 16) std::memcpy(key_params, rec.data() + g.rec.kp_off, 8 * g.d_k);
+  if (value_params && g.vb != 16) std::memcpy(value_params, rec.data() + g.rec.vp_off, 8 * g.d_v);
+  if (centroid)
+    CU(h, cudaMemcpy(centroid, h->cent + ((uint64_t)stream * g.n_cap + blk) * g.d_k,
+                     g.d_k * sizeof(float), cudaMemcpyDeviceToHost));
+  if (first_position) *first_position = blk * g.B;
+  return TTKV_OK;
+}
+
+// serialize_block (quantizer.cpp:248-274): versioned little-endian layout.
+int ttkv_gpu_serialize_block(ttkv_gpu* h, uint32_t stream, uint64_t blk, uint8_t* out,
+                             uint64_t cap, uint64_t* len) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  const Geometry& g = h->g;
+  const uint64_t kbytes = packed_bytes_u((uint64_t)g.B * g.d_k, g.kb);
+  const uint64_t vbytes = packed_bytes_u((uint64_t)g.B * g.d_v, g.vb);
+  const uint64_t nkp = g.kb == 16 ? 0 : g.d_k, nvp = g.vb == 16 ? 0 : g.d_v;
+  const uint64_t total = 4 + 2 + 24 + 12 + 4 + 8 * (nkp + nvp) + 4 * g.d_k + 8 + kbytes + 8 + vbytes;
+  if (len) *len = total;
+  if (!out) return TTKV_OK;
+  if (cap < total) return set_err(h, TTKV_ESHAPE, "serialize_block: buffer too small");
+  std::vector<uint8_t> pk(kbytes + 1), pv(vbytes + 1);
+  std::vector<float> kp(2 * g.d_k), vp(2 * g.d_v), cen(g.d_k);
+  uint64_t first = 0;
+  int rc = ttkv_gpu_read_block(h, stream, blk, pk.data(), pv.data(), kp.data(), vp.data(),
+                               cen.data(), &first);
+  if (rc) return rc;
+  uint8_t* p = out;
+  auto put = [&](uint64_t v, int n) {
+    for (int i = 0; i < n; ++i) *p++ = (uint8_t)(v >> (8 * i));
+  };
+  auto putf = [&](float f) {
+    uint32_t v;
+    std::memcpy(&v, &f, 4);
+    put(v, 4);
+  };
+  *p++ = 'T'; *p++ = 'T'; *p++ = 'K'; *p++ = 'V';
+  put(1, 2);
+  put(blk, 8);
+  put(first, 8);
+  put(first + g.B - 1, 8);
+  put(g.B, 4);
+  put(g.d_k, 4);
+  put(g.d_v, 4);
+  put(g.kb, 2);
+  put(g.vb, 2);
+  for (uint64_t c = 0; c < nkp; ++c) { putf(kp[2 * c]); putf(kp[2 * c + 1]); }
+  for (uint64_t c = 0; c < nvp; ++c) { putf(vp[2 * c]); putf(vp[2 * c + 1]); }
+  for (uint32_t c = 0; c < g.d_k; ++c) putf(cen[c]);
+  put(kbytes, 8);
+  std::memcpy(p, pk.data(), kbytes);
+  p += kbytes;
+  put(vbytes, 8);
+  std::memcpy(p, pv.data(), vbytes);
+  p += vbytes;
+  return TTKV_OK;
+}
+
+// dump_slow_tier (quantizer.cpp:325-342): "TTKVTIER", v1, count, then
+// length-prefixed serialized blocks.
+int ttkv_gpu_dump_slow_tier(ttkv_gpu* h, uint32_t stream, const char* path) {
+  if (!h || !path) return set_err(h, TTKV_EINVAL, "null argument");
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return set_err(h, TTKV_EIO, std::string("cannot open ") + path + " for writing");
+  std::vector<uint8_t> hdr = {'T', 'T', 'K', 'V', 'T', 'I', 'E', 'R', 1, 0};
+  for (int i = 0; i < 8; ++i) hdr.push_back((uint8_t)(h->n_slow >> (8 * i)));
+  bool ok = std::fwrite(hdr.data(), 1, hdr.size(), f) == hdr.size();
+  std::vector<uint8_t> buf;
+  for (uint64_t b = 0; ok && b < h->n_slow; ++b) {
+    uint64_t len = 0;
+    ttkv_gpu_serialize_block(h, stream, b, nullptr, 0, &len);
+    buf.resize(len);
+    int rc = ttkv_gpu_serialize_block(h, stream, b, buf.data(), len, &len);
+    if (rc) {
+      std::fclose(f);
+      return rc;
+    }
+    uint8_t l8[8];
+    for (int i = 0; i < 8; ++i) l8[i] = (uint8_t)(len >> (8 * i));
+    ok = std::fwrite(l8, 1, 8, f) == 8 && std::fwrite(buf.data(), 1, len, f) == len;
+  }
+  ok = (std::fclose(f) == 0) && ok;
+  if (!ok) return set_err(h, TTKV_EIO, std::string("write failed: ") + path);
+  return TTKV_OK;
+}
+
+int ttkv_gpu_read_fast(ttkv_gpu* h, uint32_t stream, float* keys, float* values,
+                       uint64_t cap, uint64_t* n_tokens, uint64_t* first_position) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  if (stream >= h->g.S) return set_err(h, TTKV_ESHAPE, "stream out of range");
+  const Geometry& g = h->g;
+  const uint64_t F = h->appended - h->fast_front;
+  if (n_tokens) *n_tokens = F;
+  if (first_position) *first_position = h->fast_front;
+  if (!keys && !values) return TTKV_OK;
+  CU(h, cudaSetDevice(h->dev));
+  CU(h, cudaStreamSynchronize(h->s0));
+  std::vector<uint8_t> rk(g.C * g.d_k * g.elem), rv(g.C * g.d_v * g.elem);
+  CU(h, cudaMemcpy(rk.data(), (uint8_t*)h->ring_k + (uint64_t)stream * g.C * g.d_k * g.elem,
+                   rk.size(), cudaMemcpyDeviceToHost));
+  CU(h, cudaMemcpy(rv.data(), (uint8_t*)h->ring_v + (uint64_t)stream * g.C * g.d_v * g.elem,
+                   rv.size(), cudaMemcpyDeviceToHost));
+  auto elem = [&](const std::vector<uint8_t>& r, uint64_t idx) -> float {
+    if (g.elem == 4) {
+      float f;
+      std::memcpy(&f, r.data() + 4 * idx, 4);
+      return f;
+    }
+    uint16_t b;
+    std::memcpy(&b, r.data() + 2 * idx, 2);
+    return half_bits_to_float(b);
+  };
+  for (uint64_t t = 0; t < F && t < cap; ++t) {
+    const uint64_t slot = (h->fast_front + t) % g.C;
+    for (uint32_t c = 0; c < g.d_k && keys; ++c) keys[t * g.d_k + c] = elem(rk, slot * g.d_k + c);
+    for (uint32_t c = 0; c < g.d_v && values; ++c) values[t * g.d_v + c] = elem(rv, slot * g.d_v + c);
+  }
+  return TTKV_OK;
+}
+
+// TierStore::locate (tier_store.cpp:100-105)
+int ttkv_gpu_locate(ttkv_gpu* h, uint64_t p, int* where, uint64_t* block_id) {
+  if (!h || !where) return set_err(h, TTKV_EINVAL, "null argument");
+  if (block_id) *block_id = 0;
+  if (p >= h->appended) { *where = 2; return TTKV_OK; }
+  if (h->appended > h->fast_front && p >= h->fast_front) { *where = 0; return TTKV_OK; }
+  if (p < h->n_slow * h->g.B) {
+    *where = 1;
+    if (block_id) *block_id = p / h->g.B;
+    return TTKV_OK;
+  }
+  *where = 2;
+  return TTKV_OK;
+}
+
+int ttkv_gpu_set_timing(ttkv_gpu* h, int enabled) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  h->timing = enabled != 0;
+  return TTKV_OK;
+}
+
+int ttkv_gpu_kernel_times(ttkv_gpu* h, ttkv_kernel_times* t, int reset) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  CU(h, cudaSetDevice(h->dev));
+  drain_timing(h);
+  if (t) {
+    t->ms_append = h->ms[K_APPEND]; t->n_append = h->cnt[K_APPEND];
+    t->ms_score = h->ms[K_SCORE]; t->n_score = h->cnt[K_SCORE];
+    t->ms_select = h->ms[K_SELECT]; t->n_select = h->cnt[K_SELECT];
+    t->ms_fast = h->ms[K_FAST]; t->n_fast = h->cnt[K_FAST];
+    t->ms_slow = h->ms[K_SLOW]; t->n_slow = h->cnt[K_SLOW];
+    t->ms_combine = h->ms[K_COMBINE]; t->n_combine = h->cnt[K_COMBINE];
+    t->ms_evict = h->ms[K_EVICT]; t->n_evict = h->cnt[K_EVICT];
+  }
+  if (reset) {
+    for (int i = 0; i < K_N; ++i) { h->ms[i] = 0; h->cnt[i] = 0; }
+  }
+  (void)kKernelNames;
+  return TTKV_OK;
+}
+
+// quantize_block (quantizer.cpp:126-155) as a stateless GPU call.  fp32
+// staging (no ring rounding), so any float input round-trips bit-exactly.
+int ttkv_gpu_quantize_block(int device, const float* keys, const float* values, uint64_t rows,
+                            uint32_t d_k, uint32_t d_v, uint32_t kb, uint32_t vb,
+                            uint8_t* packed_k, uint8_t* packed_v, float* key_params,
+                            float* value_params, float* centroid) {
+  if (!keys || !values) return set_err(nullptr, TTKV_EINVAL, "null argument");
+  auto valid_bits = [](uint32_t b) { return (b >= 2 && b <= 8) || b == 16; };
+  if (!valid_bits(kb) || !valid_bits(vb)) return set_err(nullptr, TTKV_ECONFIG, "bit widths must be in [2,8] or 16");
+  if (rows == 0 || d_k == 0 || d_v == 0 || d_k + d_v > 1024)
+    return set_err(nullptr, TTKV_ESHAPE, "quantize_block: tensor sizes inconsistent");
+  Geometry g{};
+  g.S = 1; g.G = 1; g.Gs = 1;
+  g.d_k = d_k; g.d_v = d_v; g.B = (uint32_t)rows; g.kb = kb; g.vb = vb; g.elem = 4;
+  g.C = rows; g.n_cap = 1;
+  g.rec = make_layout(g.B, d_k, d_v, kb, vb, 4);
+  if (evict_smem_bytes(g) > 220 * 1024)
+    return set_err(nullptr, TTKV_ECONFIG, "block too large for the GPU quantizer");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return set_err(nullptr, TTKV_ECUDA, cudaGetErrorString(e));
+  float *dk = nullptr, *dv = nullptr, *dc = nullptr;
+  uint8_t* dr = nullptr;
+  auto cleanup = [&]() {
+    if (dk) cudaFree(dk);
+    if (dv) cudaFree(dv);
+    if (dc) cudaFree(dc);
+    if (dr) cudaFree(dr);
+  };
+#define QCU(call)                                                          \
+  do {                                                                     \
+    cudaError_t e__ = (call);                                              \
+    if (e__ != cudaSuccess) {                                              \
+      cleanup();                                                           \
+      return set_err(nullptr, TTKV_ECUDA, cudaGetErrorString(e__));        \
+    }                                                                      \
+  } while (0)
+  QCU(cudaMalloc((void**)&dk, rows * d_k * 4));
+  QCU(cudaMalloc((void**)&dv, rows * d_v * 4));
+  QCU(cudaMalloc((void**)&dc, d_k * 4));
+  QCU(cudaMalloc((void**)&dr, g.rec.stride));
+  QCU(cudaMemcpy(dk, keys, rows * d_k * 4, cudaMemcpyHostToDevice));
+  QCU(cudaMemcpy(dv, values, rows * d_v * 4, cudaMemcpyHostToDevice));
+  EvictArgs a{};
+  a.g = g;
+  a.ring_k = dk;
+  a.ring_v = dv;
+  a.in_k = dk;
+  a.in_v = dv;
+  a.in_tokens = rows;
+  a.split_pos = 0;
+  a.first_block = 0;
+  a.arena = dr;
+  a.cent = dc;
+  a.params = nullptr;
+  QCU(launch_evict(a, 1, kInF32, 0));
+  std::vector<uint8_t> rec(g.rec.stride);
+  QCU(cudaMemcpy(rec.data(), dr, g.rec.stride, cudaMemcpyDeviceToHost));
+  if (centroid) QCU(cudaMemcpy(centroid, dc, d_k * 4, cudaMemcpyDeviceToHost));
+  cleanup();
+#undef QCU
+  if (packed_k) std::memcpy(packed_k, rec.data(), packed_bytes_u(rows * d_k, kb));
+  if (packed_v) std::memcpy(packed_v, rec.data() + g.rec.v_off, packed_bytes_u(rows * d_v, vb));
+  if (key_params && kb != 16) std::memcpy(key_params, rec.data() + g.rec.kp_off, 8 * d_k);
+  if (value_params && vb != 16) std::memcpy(value_params, rec.data() + g.rec.vp_off, 8 * d_v);
+  return TTKV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,106 @@
+// ttkv_launch.h -- host-side launchers of the sm_100a kernels (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ttkv_kernels.cuh"
+
+namespace ttkv_dev {
+
+constexpr int kInF32 = 0;
+constexpr int kInF16 = 1;
+
+struct EvictArgs {
+  Geometry g;
+  const void* ring_k;
+  const void* ring_v;
+  const void* in_k;      // [S][in_tokens][d_k] (Tin), positions >= split_pos
+  const void* in_v;
+  uint64_t in_tokens;
+  uint64_t split_pos;    // positions < split_pos are read from the ring
+  uint64_t first_block;  // block id of blockIdx.x == 0
+  uint8_t* arena;        // device-visible record base
+  float* cent;
+  uint8_t* params;       // HBM mirror of record bytes [kp_off, used)
+};
+size_t evict_smem_bytes(const Geometry& g);
+cudaError_t launch_evict(const EvictArgs& a, uint32_t n_blocks, int in_dtype, cudaStream_t st);
+
+// ring[s][slot] <- new token (f32 or f16 input), grid-stride
+cudaError_t launch_append(const Geometry& g, void* ring_k, void* ring_v, const void* k_new,
+                          const void* v_new, int in_dtype, uint64_t slot, uint64_t in_stride_tok,
+                          uint64_t n_tok, cudaStream_t st);
+
+// device-generated N(0,1) tokens into staging [S][P][d] of the ring type
+cudaError_t launch_synth(const Geometry& g, void* k, void* v, uint64_t P, uint64_t pos0,
+                         uint64_t seed, cudaStream_t st);
+
+struct ScoreArgs {
+  Geometry g;
+  const float* q;      // [S][G][d_k]
+  const float* cent;   // [S][n_cap][d_k]
+  double* scores;      // [S][Gs][n_cap]
+  uint32_t n;          // slow blocks per stream
+};
+cudaError_t launch_score(const ScoreArgs& a, cudaStream_t st);
+
+struct SelectArgs {
+  Geometry g;
+  const double* scores;
+  uint32_t* sel;          // [S][Gs][n_cap]
+  uint32_t* mask;         // [S][n_cap] scratch
+  uint32_t* union_ids;    // [S][n_cap]
+  uint32_t* union_mask;   // [S][n_cap]
+  uint32_t* union_count;  // [S]
+  unsigned long long* counters;  // [0] += union blocks
+  uint32_t n, k;
+};
+cudaError_t launch_select(const SelectArgs& a, cudaStream_t st);
+uint32_t select_max_blocks();
+
+struct FastArgs {
+  Geometry g;
+  const void* ring_k;
+  const void* ring_v;
+  const float* q;
+  float* part;        // [S][G][nfc][d_v+2]
+  uint64_t front;     // first fast position
+  uint32_t F;         // fast tokens
+  uint32_t FC;        // tokens per chunk
+  uint32_t nfc;
+  float scale_log2;
+};
+cudaError_t launch_fast(const FastArgs& a, cudaStream_t st);
+
+struct SlowArgs {
+  Geometry g;
+  const uint8_t* arena;
+  const uint8_t* params;  // HBM param mirror
+  const uint32_t* union_ids;
+  const uint32_t* union_mask;
+  const uint32_t* union_count;
+  const float* q;
+  float* part;       // [S][G][nsc][d_v+2]
+  uint32_t CH;       // union entries per CTA
+  uint32_t nsc;      // chunk capacity per (s, g) in `part`
+  uint32_t stages;
+  float scale_log2;
+  uint32_t stage_region;  // set by the launcher
+};
+// copy_mode: 1 = cp.async.bulk, 2 = LDG
+cudaError_t launch_slow(const SlowArgs& a, uint32_t grid_chunks, int copy_mode, cudaStream_t st);
+uint32_t slow_stages_for(const Geometry& g);
+
+struct CombineArgs {
+  Geometry g;
+  const float* fpart;
+  uint32_t nfc;
+  const float* spart;
+  uint32_t nsc;
+  uint32_t CH;
+  const uint32_t* union_count;  // null when no slow work this step
+  float* out;                   // [S][G][d_v]
+};
+cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);
+
+}  // namespace ttkv_dev

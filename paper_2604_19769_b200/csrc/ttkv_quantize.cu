@@ -1,0 +1,169 @@
+// ttkv_quantize.cu -- evict_quantize: bit-exact K/V block quantization on B200.
+//
+// Replaces TierStore::evict_and_compress (tier_store.cpp:71-98) +
+// quantize_block / quantize_tensor / pack_codes (quantizer.cpp:126-155, 51-88,
+// 22-32).  One CTA per (block, stream); one thread per channel walks the
+// block's rows sequentially in fp64 exactly as the reference does:
+//   lo/hi with std::min/std::max tie semantics (quantizer.cpp:66-72),
+//   scale = float((double(hi) - lo) / levels)            (77-78),
+//   code  = clamp(round((double(x) - lo) / scale), 0, L) (80-84),
+//   centroid = float(sum_r double(key) / n)              (141-148),
+// with __dadd_rn/__dsub_rn/__ddiv_rn so nothing is FMA-contracted.  Codes are
+// packed LSB-first in smem, then the finished record is written to the arena
+// (pinned host DRAM through the mapping = zero-copy PCIe stores, or HBM) with
+// 16-byte coalesced stores.  Centroids go to HBM.
+//
+// Roofline: per block it reads B*(d_k+d_v)*elem bytes from HBM (64 KB at
+// K/V fp16 128x128) and writes one record (26,624 B) to the arena; the fp64
+// divide per element is the ALU cost (~40 DFMA-equivalents).
+#include "ttkv_kernels.cuh"
+#include "ttkv_launch.h"
+
+namespace ttkv_dev {
+
+template <typename T, typename Tin>
+__global__ void evict_quantize_kernel(EvictArgs a) {
+  const Geometry& g = a.g;
+  const uint32_t s = blockIdx.y;
+  const uint64_t blk = a.first_block + blockIdx.x;
+  const uint64_t pos0 = blk * g.B;
+  const uint32_t dkv = g.d_k + g.d_v;
+
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint8_t* rec = smem;                             // [stride]
+  uint8_t* codes = smem + g.rec.stride;            // [B][d_k + d_v]
+
+  const T* ring_k = static_cast<const T*>(a.ring_k) + (uint64_t)s * g.C * g.d_k;
+  const T* ring_v = static_cast<const T*>(a.ring_v) + (uint64_t)s * g.C * g.d_v;
+  const Tin* in_k = static_cast<const Tin*>(a.in_k) + (uint64_t)s * a.in_tokens * g.d_k;
+  const Tin* in_v = static_cast<const Tin*>(a.in_v) + (uint64_t)s * a.in_tokens * g.d_v;
+
+  // zero the record (padding bytes are deterministic)
+  for (uint32_t i = threadIdx.x * 16; i < g.rec.stride; i += blockDim.x * 16)
+    *reinterpret_cast<uint4*>(rec + i) = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+
+  const uint32_t c = threadIdx.x;
+  if (c < dkv) {
+    const bool is_k = c < g.d_k;
+    const uint32_t ch = is_k ? c : c - g.d_k;
+    const uint32_t dim = is_k ? g.d_k : g.d_v;
+    const uint32_t bits = is_k ? g.kb : g.vb;
+    const T* ring = is_k ? ring_k : ring_v;
+    const Tin* in = is_k ? in_k : in_v;
+    auto load = [&](uint32_t r) -> float {
+      const uint64_t p = pos0 + r;
+      if (p < a.split_pos) return to_f(ring[(p % g.C) * dim + ch]);
+      return through<T, Tin>(in[(p - a.split_pos) * dim + ch]);
+    };
+
+    float lo = __int_as_float(0x7f800000);   // +inf
+    float hi = __int_as_float(0xff800000);   // -inf
+    double sum = 0.0;
+    for (uint32_t r = 0; r < g.B; ++r) {
+      const float x = load(r);
+      lo = (x < lo) ? x : lo;   // std::min(lo, x)
+      hi = (hi < x) ? x : hi;   // std::max(hi, x)
+      if (is_k) sum = __dadd_rn(sum, (double)x);
+    }
+    if (is_k)
+      a.cent[((uint64_t)s * g.n_cap + blk) * g.d_k + ch] =
+          __double2float_rn(__ddiv_rn(sum, (double)g.B));
+
+    if (bits == 16) {
+      // lossless passthrough: the ring element itself (quantizer.cpp:55-59)
+      T* dst = reinterpret_cast<T*>(rec + (is_k ? 0u : g.rec.v_off));
+      for (uint32_t r = 0; r < g.B; ++r) dst[r * dim + ch] = from_f<T>(load(r));
+    } else {
+      float scale, zp = lo;
+      uint8_t* cc = codes + ch + (is_k ? 0u : g.d_k);
+      if (hi == lo) {
+        scale = 1.0f;
+        for (uint32_t r = 0; r < g.B; ++r) cc[r * dkv] = 0;
+      } else {
+        const double levels = (double)((1u << bits) - 1u);
+        scale = __double2float_rn(__ddiv_rn(__dsub_rn((double)hi, (double)lo), levels));
+        const double dlo = (double)lo, dscale = (double)scale;
+        for (uint32_t r = 0; r < g.B; ++r) {
+          double q = round(__ddiv_rn(__dsub_rn((double)load(r), dlo), dscale));
+          q = q < 0.0 ? 0.0 : (levels < q ? levels : q);
+          cc[r * dkv] = (uint8_t)(uint32_t)q;
+        }
+      }
+      float* par = reinterpret_cast<float*>(rec + (is_k ? g.rec.kp_off : g.rec.vp_off)) + 2 * ch;
+      par[0] = scale;
+      par[1] = zp;
+    }
+  }
+  __syncthreads();
+
+  // LSB-first packing over the flat row-major index (quantizer.cpp:22-32)
+  for (int t = 0; t < 2; ++t) {
+    const uint32_t bits = t == 0 ? g.kb : g.vb;
+    if (bits == 16) continue;
+    const uint32_t dim = t == 0 ? g.d_k : g.d_v;
+    const uint32_t coff = t == 0 ? 0u : g.d_k;
+    const uint32_t nbytes = t == 0 ? g.rec.k_bytes : g.rec.v_bytes;
+    uint8_t* dst = rec + (t == 0 ? 0u : g.rec.v_off);
+    for (uint32_t j = threadIdx.x; j < nbytes; j += blockDim.x) {
+      uint32_t byte = 0;
+      if (bits == 8) {
+        byte = codes[(j / dim) * dkv + coff + j % dim];
+      } else if (bits == 4) {
+        const uint32_t i0 = 2 * j, i1 = 2 * j + 1;
+        byte = codes[(i0 / dim) * dkv + coff + i0 % dim];
+        if (i1 < g.B * dim) byte |= (uint32_t)codes[(i1 / dim) * dkv + coff + i1 % dim] << 4;
+      } else {
+        const uint32_t b0 = 8 * j, total = g.B * dim;
+        for (uint32_t i = b0 / bits; i < total && i * bits < b0 + 8; ++i) {
+          const uint32_t v = codes[(i / dim) * dkv + coff + i % dim];
+          const int sh = (int)(i * bits) - (int)b0;
+          byte |= sh >= 0 ? (v << sh) : (v >> (-sh));
+        }
+        byte &= 0xffu;
+      }
+      dst[j] = (uint8_t)byte;
+    }
+  }
+  __syncthreads();
+
+  // record -> arena (pinned DRAM via PCIe posted writes, or HBM)
+  uint8_t* out = a.arena + ((uint64_t)s * g.n_cap + blk) * g.rec.stride;
+  for (uint32_t i = threadIdx.x * 16; i < g.rec.stride; i += blockDim.x * 16)
+    *reinterpret_cast<uint4*>(out + i) = *reinterpret_cast<const uint4*>(rec + i);
+  // params -> HBM mirror (staged by slow_stream_attn from HBM, not PCIe)
+  const uint32_t pbytes = g.rec.used - g.rec.kp_off;
+  if (a.params && pbytes) {
+    uint8_t* pm = a.params + ((uint64_t)s * g.n_cap + blk) * pbytes;
+    for (uint32_t i = threadIdx.x * 16; i < pbytes; i += blockDim.x * 16)
+      *reinterpret_cast<uint4*>(pm + i) = *reinterpret_cast<const uint4*>(rec + g.rec.kp_off + i);
+  }
+}
+
+size_t evict_smem_bytes(const Geometry& g) {
+  return (size_t)g.rec.stride + (size_t)g.B * (g.d_k + g.d_v);
+}
+
+template <typename T, typename Tin>
+static cudaError_t launch_evict_t(const EvictArgs& a, uint32_t n_blocks, cudaStream_t st) {
+  const size_t smem = evict_smem_bytes(a.g);
+  auto kern = evict_quantize_kernel<T, Tin>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const uint32_t threads = ((a.g.d_k + a.g.d_v + 31) / 32) * 32;
+  dim3 grid(n_blocks, a.g.S);
+  kern<<<grid, threads < 64 ? 64 : threads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_evict(const EvictArgs& a, uint32_t n_blocks, int in_dtype, cudaStream_t st) {
+  if (n_blocks == 0) return cudaSuccess;
+  if (a.g.elem == 2) {
+    if (in_dtype == kInF16) return launch_evict_t<__half, __half>(a, n_blocks, st);
+    return launch_evict_t<__half, float>(a, n_blocks, st);
+  }
+  if (in_dtype == kInF16) return launch_evict_t<float, __half>(a, n_blocks, st);
+  return launch_evict_t<float, float>(a, n_blocks, st);
+}
+
+}  // namespace ttkv_dev

@@ -1,0 +1,273 @@
+// ttkv_select.cu -- block relevance scoring and top-k selection on B200.
+//
+// score_blocks replaces the engine's scoring loop (engine.cpp:51-56) over
+// score_block (relevance.cpp:19-27): s = sum_i double(q_i) * double(c_i),
+// sequential in i, unfused (__dmul_rn/__dadd_rn) -- bit-exact with the
+// reference, so top-k ties are decided exactly as on the CPU.
+// select_topk replaces SelectionPolicy::resolve + select_top_k
+// (relevance.cpp:10-17, 29-43): a block-wide bitonic sort of (score desc,
+// block_id desc) -- a total order, so the result equals std::stable_sort's.
+// For GQA it also builds the per-stream union of the G selected sets plus a
+// per-block head mask, so every record crosses PCIe once per step.
+//
+// Roofline: scoring reads the resident centroids once per step,
+// n_blk * d_k * 4 bytes per stream (508 KB at 128K ctx), plus G * n_blk * d_k
+// fp64 mul+add; both are microseconds at cfg2 and hide under the PCIe stream.
+#include "ttkv_kernels.cuh"
+#include "ttkv_launch.h"
+
+namespace ttkv_dev {
+
+constexpr int kScoreTile = 32;   // blocks per CTA
+constexpr int kSelectThreads = 1024;
+constexpr uint32_t kSelectMaxN = 16384;  // blocks per stream (2M tokens at B=128)
+
+__global__ void __launch_bounds__(128) score_kernel(ScoreArgs a) {
+  const Geometry& g = a.g;
+  const uint32_t s = blockIdx.y;
+  const uint32_t b0 = blockIdx.x * kScoreTile;
+  extern __shared__ __align__(16) uint8_t smem[];
+  double* qs = reinterpret_cast<double*>(smem);                 // [Gs][d_k]
+  float* ct = reinterpret_cast<float*>(qs + g.Gs * g.d_k);      // [tile][d_k + 1]
+  const uint32_t pitch = g.d_k + 1;
+
+  for (uint32_t i = threadIdx.x; i < g.Gs * g.d_k; i += blockDim.x) {
+    const uint32_t h = i / g.d_k, c = i % g.d_k;
+    const float* qb = a.q + (uint64_t)s * g.G * g.d_k;
+    if (g.Gs == g.G) {
+      qs[i] = (double)qb[h * g.d_k + c];
+    } else {  // group-shared query q' = sum_g q_g (fp32, sequential g)
+      float acc = qb[c];
+      for (uint32_t hh = 1; hh < g.G; ++hh) acc = __fadd_rn(acc, qb[hh * g.d_k + c]);
+      qs[i] = (double)acc;
+    }
+  }
+  const float* cb = a.cent + ((uint64_t)s * g.n_cap + b0) * g.d_k;
+  for (uint32_t i = threadIdx.x; i < kScoreTile * g.d_k; i += blockDim.x) {
+    const uint32_t r = i / g.d_k, c = i % g.d_k;
+    ct[r * pitch + c] = (b0 + r < a.n) ? cb[i] : 0.0f;
+  }
+  __syncthreads();
+
+  for (uint32_t t = threadIdx.x; t < kScoreTile * g.Gs; t += blockDim.x) {
+    const uint32_t r = t % kScoreTile, h = t / kScoreTile;
+    if (b0 + r >= a.n) continue;
+    const double* qh = qs + h * g.d_k;
+    const float* cr = ct + r * pitch;
+    double acc = 0.0;
+    for (uint32_t c = 0; c < g.d_k; ++c) acc = __dadd_rn(acc, __dmul_rn(qh[c], (double)cr[c]));
+    a.scores[((uint64_t)s * g.Gs + h) * g.n_cap + b0 + r] = acc;
+  }
+}
+
+cudaError_t launch_score(const ScoreArgs& a, cudaStream_t st) {
+  if (a.n == 0) return cudaSuccess;
+  const size_t smem = (size_t)a.g.Gs * a.g.d_k * 8 + (size_t)kScoreTile * (a.g.d_k + 1) * 4;
+  cudaError_t e = cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((a.n + kScoreTile - 1) / kScoreTile, a.g.S);
+  score_kernel<<<grid, 128, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+// orderable key: ascending u64 == ascending double; -0.0 folded onto +0.0
+// because the reference compares with != (relevance.cpp:35).
+__device__ __forceinline__ uint64_t order_key(double d) {
+  if (d == 0.0) d = 0.0;
+  const uint64_t b = (uint64_t)__double_as_longlong(d);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void __launch_bounds__(kSelectThreads) select_kernel(SelectArgs a, uint32_t N2) {
+  const Geometry& g = a.g;
+  const uint32_t s = blockIdx.x;
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* key = reinterpret_cast<uint64_t*>(smem);
+  uint32_t* id = reinterpret_cast<uint32_t*>(key + N2);
+  __shared__ uint32_t warp_tot[kSelectThreads / 32];
+  __shared__ uint32_t base_sh;
+
+  uint32_t* mask = a.mask + (uint64_t)s * g.n_cap;
+  for (uint32_t b = threadIdx.x; b < a.n; b += blockDim.x) mask[b] = 0;
+  __syncthreads();
+
+  const uint32_t all_heads = (g.G >= 32) ? 0xffffffffu : ((1u << g.G) - 1u);
+  for (uint32_t h = 0; h < g.Gs; ++h) {
+    const double* sc = a.scores + ((uint64_t)s * g.Gs + h) * g.n_cap;
+    for (uint32_t i = threadIdx.x; i < N2; i += blockDim.x) {
+      key[i] = i < a.n ? order_key(sc[i]) : 0ull;
+      id[i] = i < a.n ? i : 0u;
+    }
+    __syncthreads();
+    // bitonic sort, descending by (key, id)
+    for (uint32_t size = 2; size <= N2; size <<= 1) {
+      for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+        for (uint32_t i = threadIdx.x; i < N2 / 2; i += blockDim.x) {
+          const uint32_t lo = 2 * i - (i & (stride - 1));
+          const uint32_t hi = lo + stride;
+          const bool desc = (lo & size) == 0;
+          const uint64_t kl = key[lo], kh = key[hi];
+          const uint32_t il = id[lo], ih = id[hi];
+          const bool less = (kl < kh) || (kl == kh && il < ih);  // (lo) < (hi)
+          if (less == desc) {
+            key[lo] = kh; key[hi] = kl;
+            id[lo] = ih; id[hi] = il;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    uint32_t* out = a.sel + ((uint64_t)s * g.Gs + h) * g.n_cap;
+    const uint32_t bit = (g.Gs == g.G) ? (1u << h) : all_heads;
+    for (uint32_t i = threadIdx.x; i < a.k; i += blockDim.x) {
+      out[i] = id[i];
+      atomicOr(&mask[id[i]], bit);
+    }
+    __syncthreads();
+  }
+
+  // compact the union in ascending block id (records are then read in
+  // arena order; the merge is order-independent)
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t nwarps = blockDim.x >> 5;
+  if (threadIdx.x == 0) base_sh = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < a.n; base += blockDim.x) {
+    const uint32_t b = base + threadIdx.x;
+    const uint32_t m = b < a.n ? mask[b] : 0u;
+    const uint32_t ballot = __ballot_sync(0xffffffffu, m != 0u);
+    if (lane == 0) warp_tot[warp] = __popc(ballot);
+    __syncthreads();
+    uint32_t before = 0, total = 0;
+    for (uint32_t w = 0; w < nwarps; ++w) {
+      const uint32_t t = warp_tot[w];
+      before += (w < warp) ? t : 0u;
+      total += t;
+    }
+    if (m != 0u) {
+      const uint32_t pos = base_sh + before + __popc(ballot & ((1u << lane) - 1u));
+      a.union_ids[(uint64_t)s * g.n_cap + pos] = b;
+      a.union_mask[(uint64_t)s * g.n_cap + pos] = m;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) base_sh += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    a.union_count[s] = base_sh;
+    atomicAdd(&a.counters[0], (unsigned long long)base_sh);
+  }
+}
+
+uint32_t select_max_blocks() { return kSelectMaxN; }
+
+cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
+  if (a.n == 0) return cudaSuccess;
+  uint32_t N2 = 2;
+  while (N2 < a.n) N2 <<= 1;
+  const size_t smem = (size_t)N2 * 12;
+  cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  const uint32_t threads = N2 / 2 < kSelectThreads ? (N2 / 2 < 64 ? 64 : N2 / 2) : kSelectThreads;
+  select_kernel<<<a.g.S, threads, smem, st>>>(a, N2);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// append_kv: TierStore::append_token's push into the fast tier
+// (tier_store.cpp:49-67) -- the new token lands in ring slot pos mod C.
+// Also used by prefill to copy tokens [in_stride] into consecutive slots.
+// ---------------------------------------------------------------------------
+template <typename T, typename Tin>
+__global__ void append_kernel(Geometry g, T* ring_k, T* ring_v, const Tin* kn, const Tin* vn,
+                              uint64_t slot0, uint64_t in_stride_tok, uint64_t n_tok) {
+  const uint32_t dkv = g.d_k + g.d_v;
+  const uint64_t total = (uint64_t)g.S * n_tok * dkv;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = (uint32_t)(i % dkv);
+    const uint64_t st = i / dkv;
+    const uint64_t t = st % n_tok, s = st / n_tok;
+    const uint64_t slot = (slot0 + t) % g.C;
+    if (c < g.d_k)
+      ring_k[(s * g.C + slot) * g.d_k + c] = from_f<T>(to_f(kn[(s * in_stride_tok + t) * g.d_k + c]));
+    else
+      ring_v[(s * g.C + slot) * g.d_v + (c - g.d_k)] =
+          from_f<T>(to_f(vn[(s * in_stride_tok + t) * g.d_v + (c - g.d_k)]));
+  }
+}
+
+cudaError_t launch_append(const Geometry& g, void* ring_k, void* ring_v, const void* k_new,
+                          const void* v_new, int in_dtype, uint64_t slot, uint64_t in_stride_tok,
+                          uint64_t n_tok, cudaStream_t st) {
+  if (n_tok == 0) return cudaSuccess;
+  const uint64_t total = (uint64_t)g.S * n_tok * (g.d_k + g.d_v);
+  uint64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (g.elem == 2) {
+    if (in_dtype == kInF16)
+      append_kernel<__half, __half><<<(unsigned)blocks, 256, 0, st>>>(
+          g, (__half*)ring_k, (__half*)ring_v, (const __half*)k_new, (const __half*)v_new, slot,
+          in_stride_tok, n_tok);
+    else
+      append_kernel<__half, float><<<(unsigned)blocks, 256, 0, st>>>(
+          g, (__half*)ring_k, (__half*)ring_v, (const float*)k_new, (const float*)v_new, slot,
+          in_stride_tok, n_tok);
+  } else {
+    if (in_dtype == kInF16)
+      append_kernel<float, __half><<<(unsigned)blocks, 256, 0, st>>>(
+          g, (float*)ring_k, (float*)ring_v, (const __half*)k_new, (const __half*)v_new, slot,
+          in_stride_tok, n_tok);
+    else
+      append_kernel<float, float><<<(unsigned)blocks, 256, 0, st>>>(
+          g, (float*)ring_k, (float*)ring_v, (const float*)k_new, (const float*)v_new, slot,
+          in_stride_tok, n_tok);
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// synthetic N(0,1) KV for perf runs (on-device generation is
+// acceptable at cfg2-5 scale): counter-based hash + Box-Muller.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 30; x *= 0xbf58476d1ce4e5b9ull;
+  x ^= x >> 27; x *= 0x94d049bb133111ebull;
+  x ^= x >> 31;
+  return x;
+}
+
+template <typename T>
+__global__ void synth_kernel(Geometry g, T* k, T* v, uint64_t P, uint64_t pos0, uint64_t seed) {
+  const uint32_t dkv = g.d_k + g.d_v;
+  const uint64_t total = (uint64_t)g.S * P * dkv;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = (uint32_t)(i % dkv);
+    const uint64_t st = i / dkv;
+    const uint64_t t = st % P, s = st / P;
+    const uint64_t ctr = ((s * 0x9E3779B97F4A7C15ull) ^ ((pos0 + t) << 9) ^ c) + seed * 0xD1B54A32D192ED03ull;
+    const uint64_t h = mix64(ctr), h2 = mix64(ctr ^ 0x5851F42D4C957F2Dull);
+    const float u1 = ((float)(h >> 40) + 1.0f) * (1.0f / 16777216.0f);
+    const float u2 = (float)(h2 >> 40) * (1.0f / 16777216.0f);
+    const float z = sqrtf(-2.0f * __logf(u1)) * __cosf(6.283185307f * u2);
+    if (c < g.d_k) k[(s * P + t) * g.d_k + c] = from_f<T>(z);
+    else v[(s * P + t) * g.d_v + (c - g.d_k)] = from_f<T>(z);
+  }
+}
+
+cudaError_t launch_synth(const Geometry& g, void* k, void* v, uint64_t P, uint64_t pos0,
+                         uint64_t seed, cudaStream_t st) {
+  const uint64_t total = (uint64_t)g.S * P * (g.d_k + g.d_v);
+  uint64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (g.elem == 2)
+    synth_kernel<__half><<<(unsigned)blocks, 256, 0, st>>>(g, (__half*)k, (__half*)v, P, pos0, seed);
+  else
+    synth_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(g, (float*)k, (float*)v, P, pos0, seed);
+  return cudaGetLastError();
+}
+
+}  // namespace ttkv_dev

@@ -1,0 +1,165 @@
+// pcie_probe.cu -- measures the host->device paths the slow tier can use
+// (SURVEY 7.5): copy-engine memcpy, zero-copy LDG.128 and cp.async.bulk from
+// mapped pinned memory, on 26,624-byte records gathered in random order.
+// Prints one JSON object per measurement.  Build: make -C tools
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <numeric>
+#include <random>
+#include <vector>
+
+#define CK(x)                                                                      \
+  do {                                                                             \
+    cudaError_t e = (x);                                                           \
+    if (e != cudaSuccess) {                                                        \
+      std::printf("{\"error\": \"%s: %s\"}\n", #x, cudaGetErrorString(e));        \
+      std::exit(1);                                                                \
+    }                                                                              \
+  } while (0)
+
+constexpr unsigned kRec = 26624;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+// zero-copy LDG.128 over scattered records: one CTA streams its list of records
+__global__ void ldg_records(const uint8_t* base, const unsigned* order, unsigned n,
+                            unsigned long long* sink) {
+  unsigned long long acc = 0;
+  for (unsigned r = blockIdx.x; r < n; r += gridDim.x) {
+    const uint4* p = reinterpret_cast<const uint4*>(base + (size_t)order[r] * kRec);
+    for (unsigned j = threadIdx.x; j < kRec / 16; j += blockDim.x) {
+      const uint4 v = p[j];
+      acc += v.x ^ v.y ^ v.z ^ v.w;
+    }
+  }
+  if (acc == 0x123456789ull) *sink = acc;
+}
+
+// cp.async.bulk of whole records into a 3-stage smem ring
+__global__ void bulk_records(const uint8_t* base, const unsigned* order, unsigned n,
+                             unsigned long long* sink) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ __align__(8) unsigned long long bar[3];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 3; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  unsigned long long acc = 0;
+  unsigned it = 0;
+  // prologue / steady state handled by a single thread issuing, all waiting
+  const unsigned mine = (n > blockIdx.x) ? (n - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto issue = [&](unsigned i) {
+    const unsigned r = blockIdx.x + i * gridDim.x;
+    const uint8_t* src = base + (size_t)order[r] * kRec;
+    uint8_t* dst = sm + (i % 3) * kRec;
+    const unsigned b = smem_u32(&bar[i % 3]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(kRec));
+    for (unsigned off = 0; off < kRec; off += 16384) {
+      const unsigned sz = min(16384u, kRec - off);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(dst + off)),
+          "l"(src + off), "r"(sz), "r"(b)
+          : "memory");
+    }
+  };
+  if (threadIdx.x == 0)
+    for (unsigned i = 0; i < 3 && i < mine; ++i) issue(i);
+  for (it = 0; it < mine; ++it) {
+    const unsigned b = smem_u32(&bar[it % 3]);
+    const unsigned par = (it / 3) & 1;
+    asm volatile(
+        "{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(b),
+        "r"(par)
+        : "memory");
+    const uint4* p = reinterpret_cast<const uint4*>(sm + (it % 3) * kRec);
+    for (unsigned j = threadIdx.x; j < kRec / 16; j += blockDim.x) {
+      const uint4 v = p[j];
+      acc += v.x ^ v.w;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && it + 3 < mine) issue(it + 3);
+  }
+  if (acc == 0x123456789ull) *sink = acc;
+}
+
+int main(int argc, char** argv) {
+  const size_t nrec = argc > 1 ? std::atoll(argv[1]) : 10000;  // 266 MB
+  const size_t bytes = nrec * kRec;
+  int dev = 0;
+  CK(cudaSetDevice(dev));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, dev));
+  std::printf("{\"device\": \"%s\", \"sms\": %d, \"pci_bus\": %d}\n", prop.name,
+              prop.multiProcessorCount, prop.pciBusID);
+  uint8_t *h = nullptr, *hd = nullptr, *d = nullptr;
+  CK(cudaHostAlloc((void**)&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  CK(cudaHostGetDevicePointer((void**)&hd, h, 0));
+  CK(cudaMalloc((void**)&d, bytes));
+  for (size_t i = 0; i < bytes; i += 4096) h[i] = (uint8_t)i;
+  std::vector<unsigned> order(nrec);
+  std::iota(order.begin(), order.end(), 0u);
+  std::shuffle(order.begin(), order.end(), std::mt19937(1));
+  unsigned* d_order;
+  unsigned long long* sink;
+  CK(cudaMalloc((void**)&d_order, nrec * 4));
+  CK(cudaMalloc((void**)&sink, 8));
+  CK(cudaMemcpy(d_order, order.data(), nrec * 4, cudaMemcpyHostToDevice));
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  auto best = [&](auto&& fn, int reps) {
+    float bestms = 1e30f;
+    for (int r = 0; r < reps; ++r) {
+      cudaEventRecord(a);
+      fn();
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      bestms = std::min(bestms, ms);
+    }
+    return bestms;
+  };
+  float ms = best([&] { cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice); }, 10);
+  std::printf("{\"path\": \"memcpy_h2d\", \"bytes\": %zu, \"gbs\": %.2f}\n", bytes, bytes / ms / 1e6);
+  ms = best([&] { cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost); }, 10);
+  std::printf("{\"path\": \"memcpy_d2h\", \"bytes\": %zu, \"gbs\": %.2f}\n", bytes, bytes / ms / 1e6);
+  // per-record memcpy (copy engine, one call per 26 KB record)
+  ms = best([&] {
+    for (size_t i = 0; i < std::min<size_t>(nrec, 2000); ++i)
+      cudaMemcpyAsync(d + i * kRec, h + (size_t)order[i] * kRec, kRec, cudaMemcpyHostToDevice);
+  }, 3);
+  std::printf("{\"path\": \"memcpy_per_record\", \"records\": %zu, \"gbs\": %.2f}\n",
+              std::min<size_t>(nrec, 2000), std::min<size_t>(nrec, 2000) * kRec / ms / 1e6);
+  for (int grid_mult : {1, 2, 4, 8}) {
+    const int grid = prop.multiProcessorCount * grid_mult;
+    ms = best([&] { ldg_records<<<grid, 256>>>(hd, d_order, (unsigned)nrec, sink); }, 5);
+    CK(cudaGetLastError());
+    std::printf("{\"path\": \"zero_copy_ldg128\", \"grid\": %d, \"gbs\": %.2f}\n", grid,
+                bytes / ms / 1e6);
+  }
+  CK(cudaFuncSetAttribute(bulk_records, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * kRec));
+  for (int grid_mult : {1, 2}) {
+    const int grid = prop.multiProcessorCount * grid_mult;
+    ms = best([&] { bulk_records<<<grid, 128, 3 * kRec>>>(hd, d_order, (unsigned)nrec, sink); }, 5);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      std::printf("{\"path\": \"zero_copy_bulk\", \"error\": \"%s\"}\n", cudaGetErrorString(e));
+      return 0;
+    }
+    std::printf("{\"path\": \"zero_copy_bulk\", \"grid\": %d, \"gbs\": %.2f}\n", grid,
+                bytes / ms / 1e6);
+  }
+  // HBM reference for the same gather
+  ms = best([&] { ldg_records<<<prop.multiProcessorCount * 8, 256>>>(d, d_order, (unsigned)nrec, sink); }, 5);
+  std::printf("{\"path\": \"hbm_ldg128_gather\", \"gbs\": %.2f}\n", bytes / ms / 1e6);
+  return 0;
+}
