@@ -30,3 +30,30 @@ clean:
 	$(MAKE) -C oracle clean
 
 .PHONY: all lib oracle clean
+
+# ---- C++ drop-in (reference ttkv:: API over the C ABI) ---------------------------
+CXX      ?= g++
+REF      ?= /root/reference
+dropin: $(LIBDIR)/libttkv.so
+
+$(LIBDIR)/libttkv.so: $(PKG)/cpp/ttkv_dropin.cpp include/ttkv/gpu_dropin.hpp include/ttkv_gpu.h $(LIBDIR)/libttkv_gpu.so
+	$(CXX) -std=c++20 -O2 -fPIC -shared -Iinclude -o $@ $(PKG)/cpp/ttkv_dropin.cpp \
+	  -L$(LIBDIR) -lttkv_gpu -Wl,-rpath,'$$ORIGIN'
+
+# The reference's own unit tests, compiled UNMODIFIED (in place, read-only)
+# against the drop-in headers + tests/cpp/doctest.h.  Built here, where the
+# reference tree exists; the binary travels to the GPU box.
+REF_TESTS := test_quantizer.cpp test_relevance.cpp test_attention.cpp test_tier_store.cpp test_engine.cpp
+reftests: build/ref_unit_tests_on_gpu
+ifneq ($(wildcard $(REF)/proj/tests/test_engine.cpp),)
+build/ref_unit_tests_on_gpu: $(LIBDIR)/libttkv.so tests/cpp/doctest.h
+	@mkdir -p build
+	$(CXX) -std=c++20 -O2 -Iinclude -Itests/cpp \
+	  -o $@ tests/cpp/doctest_main.cpp $(addprefix $(REF)/proj/tests/,$(REF_TESTS)) \
+	  -L$(LIBDIR) -lttkv -lttkv_gpu -Wl,-rpath,'$$ORIGIN/../$(LIBDIR)'
+else
+build/ref_unit_tests_on_gpu:
+	@echo "reference tree absent: keeping prebuilt $@ (if any)"
+endif
+
+.PHONY: dropin reftests

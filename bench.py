@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""Benchmark of the TTKV decode hot path on B200 (BASELINE.json metric).
+
+Workload (N=1): BASELINE.json configs[1] -- LLaMA-3-8B GQA decode at 128K
+context, batch 1, all 32 layers x 8 KV heads = 256 KV streams, 4 query heads
+each, d=128, 4096-token fp16 fast tier per stream, K8/V4 slow tier in pinned
+host DRAM, fetch fraction 0.45, per-head selection (== 1024 reference Engines).
+One step = one decode step of every layer/head (one generated token).
+N>1 (configs[3]): the same request head-sharded over N GPUs -- rank r owns KV
+heads [8r/N, 8(r+1)/N) of every layer, streams its records over its own PCIe
+link, and the per-head outputs are all-gathered over NVLink (NCCL).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`value` is tokens/s with inputs resident in HBM; `e2e` is the same metric
+through the public C ABI with host buffers (q/k/v H2D + output D2H inside the
+timed region).  `--impl reference` times the unmodified reference engine
+(oracle/_ref) on the host cores on a bounded sample, extrapolated.
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LAYERS, KV_HEADS, G, D, B = 32, 8, 4, 128, 128
+CTX = 131072
+L_FAST = 4096
+FRAC = 0.45
+METRIC = "decode tokens/s at 128K ctx (LLaMA-3-8B GQA, all layers, batch 1)"
+UNIT = "tok/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--ctx", type=int, default=CTX)
+    p.add_argument("--group-select", action="store_true",
+                   help="one selection per KV head (q' = sum_g q_g) instead of per query head")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--slow-tier", default="host", choices=["host", "device"])
+    return p.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+# ---------------------------------------------------------------------------
+# reference arm / cpu baseline (oracle/_ref: the unmodified reference engine)
+# ---------------------------------------------------------------------------
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def ref_sample(ctx, steps, engines=None, threads=None):
+    """Runs `engines` reference Engines (one per (stream, query head)) at ctx,
+    prefilled, then `steps` decode steps on `threads` host threads.  Returns
+    per-step wall ms of the sample and the sample description."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import numpy as np
+    import _oracle as O
+    if not O.ref_available():
+        raise RuntimeError("oracle/_ref/libttkv_ref.so missing (built by __graft_entry__.build())")
+    threads = threads or host_cores()
+    engines = engines or threads
+    ms = np.zeros(steps, np.float64)
+    pre = C.c_double()
+    rc = O.ref().ref_bench_decode(engines, G, ctx, steps, threads, L_FAST * 2 * D * 2, D, B, 8, 4,
+                                  FRAC, 1234, ms, C.byref(pre))
+    if rc != 0:
+        raise RuntimeError(O.ref().ref_last_error().decode())
+    return ms, pre.value, engines, threads
+
+
+def cpu_throughput(ms_step, engines, total_engines):
+    """tokens/s of the full workload, extrapolated linearly from the sample:
+    a full step needs total_engines/engines sample steps."""
+    full_ms = ms_step * total_engines / engines
+    return 1000.0 / full_ms
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    total_engines = LAYERS * KV_HEADS * G  # one reference Engine per (stream, q-head)
+    n = args.warmup + args.steps
+    ms, pre_s, engines, threads = ref_sample(args.ctx, n)
+    timed = ms[args.warmup:]
+    vals = [cpu_throughput(m, engines, total_engines) for m in timed]
+    value = statistics.mean(vals)
+    sample = (f"{engines} reference Engines (1 per stream x q-head) at {args.ctx} ctx on "
+              f"{threads} threads, {args.steps} timed decode steps after {args.warmup} warm-up; "
+              f"extrapolated x{total_engines // engines} to {total_engines} engines")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 / value, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference GaussianSource)",
+        "config": {"workload": "cfg2: LLaMA-3-8B GQA 32L x 8KV x 4Q, 128K ctx, batch 1",
+                   "ctx": args.ctx, "streams": LAYERS * KV_HEADS, "heads_per_stream": G,
+                   "d": D, "block": B, "l_fast": L_FAST, "bits": "K8/V4", "fetch_fraction": FRAC},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "sample_ms_per_step": [round(float(x), 2) for x in timed],
+        "prefill_s": round(pre_s, 2),
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def measure_h2d_peak(torch, dev):
+    """pinned H2D copy-engine peak (256 MiB, best of 10): the PCIe roofline."""
+    n = 256 << 20
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    best = 1e30
+    for _ in range(10):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        d.copy_(h, non_blocking=True)
+        b.record()
+        b.synchronize()
+        best = min(best, a.elapsed_time(b))
+    return n / best / 1e6  # GB/s
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2604_19769_b200 as T
+
+    rank, local, world = dist_env()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if KV_HEADS % world:
+        raise SystemExit("world size must divide the 8 KV heads")
+    S = LAYERS * KV_HEADS // world  # streams on this rank (head sharding)
+
+    cfg = T.TierConfig(hbm_budget_bytes=L_FAST * 2 * D * 2, d_k=D, d_v=D, bytes_full_precision=2,
+                       block_size=B, key_bits=8, value_bits=4, fetch_fraction=FRAC)
+    n_steps_total = args.warmup + 2 * args.steps + 2
+    eng = T.MultiStreamEngine(cfg, T.SelectionPolicy(None, FRAC), n_streams=S,
+                              heads_per_stream=G, group_select=args.group_select, device=local,
+                              reserve_tokens=args.ctx + n_steps_total + B,
+                              slow_tier=0 if args.slow_tier == "host" else 1)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    eng.set_stream(stream.cuda_stream)
+    t0 = time.time()
+    eng.prefill_synthetic(args.ctx, seed=1000 + rank)
+    prefill_s = time.time() - t0
+    h2d_peak = measure_h2d_peak(torch, dev)
+
+    gen = torch.Generator(device=dev).manual_seed(rank)
+    NPOOL = 4
+    qs = [torch.randn(S, G, D, device=dev, generator=gen) for _ in range(NPOOL)]
+    ks = [torch.randn(S, D, device=dev, generator=gen).half() for _ in range(NPOOL)]
+    vs = [torch.randn(S, D, device=dev, generator=gen).half() for _ in range(NPOOL)]
+    out = torch.empty(S, G, D, device=dev)
+    gathered = torch.empty(world * S, G, D, device=dev) if world > 1 else None
+
+    def step(i):
+        eng.decode_step_device(qs[i % NPOOL].data_ptr(), ks[i % NPOOL].data_ptr(),
+                               vs[i % NPOOL].data_ptr(), out.data_ptr(), dtype=1)
+        if world > 1:  # per-head outputs -> every rank (NVLink, NCCL)
+            dist.all_gather_into_tensor(gathered, out)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        step(i)
+    barrier()
+    st0 = eng.state()
+    eng.kernel_times(reset=True)
+    eng.set_timing(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        barrier()
+        ev0.record()
+        union_total = 0
+        for i in range(args.steps):
+            step(args.warmup + i)
+        ev1.record()
+        barrier()
+    eng.set_timing(False)
+    ms_total = ev0.elapsed_time(ev1)
+    kt = eng.kernel_times(reset=True)
+    st1 = eng.state()
+    union_last, pcie_last = eng.step_counters()
+    launches = st1["launches"] - st0["launches"]
+
+    # --- e2e through the public C ABI with host buffers -----------------------
+    rng = np.random.default_rng(rank)
+    hq = [rng.standard_normal((S, G, D)).astype(np.float32) for _ in range(NPOOL)]
+    hk = [rng.standard_normal((S, D)).astype(np.float16) for _ in range(NPOOL)]
+    hv = [rng.standard_normal((S, D)).astype(np.float16) for _ in range(NPOOL)]
+    h2d = hq[0].nbytes + hk[0].nbytes + hv[0].nbytes
+    d2h = S * G * D * 4
+    barrier()
+    t_e2e0 = time.perf_counter()
+    for i in range(args.steps):
+        r = eng.decode_step(hq[i % NPOOL], hk[i % NPOOL], hv[i % NPOOL])
+        if world > 1:
+            o = torch.from_numpy(r.output).to(dev)
+            g_ = torch.empty(world * S, G, D, device=dev)
+            dist.all_gather_into_tensor(g_, o)
+            _ = g_.cpu()
+            d2h_step = world * S * G * D * 4
+    barrier()
+    e2e_ms = (time.perf_counter() - t_e2e0) * 1000.0 / args.steps
+
+    # --- max over ranks ---------------------------------------------------------
+    vals = torch.tensor([ms_total, e2e_ms, kt["ms_slow"], kt["ms_fast"]], device=dev,
+                        dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    ms_total, e2e_ms = float(vals[0]), float(vals[1])
+    ms_step = ms_total / args.steps
+    tokens_per_step = 1  # batch 1: one token per step for the whole model
+    value = tokens_per_step * 1000.0 / ms_step
+
+    # --- roofline of the dominant kernel (slow_stream_attn, PCIe-bound) ---------
+    rec = st1["record_bytes"]
+    payload = st1["payload_bytes"]  # params are staged from the HBM mirror
+    n_slow = kt["n_slow"] or 1
+    slow_ms = kt["ms_slow"] / n_slow
+    pcie_bytes_launch = union_last * payload
+    achieved = pcie_bytes_launch / (slow_ms * 1e-3) / 1e9
+    fast_ms = kt["ms_fast"] / max(1, kt["n_fast"])
+    F = st1["fast_tokens"]
+    fast_bytes = S * F * 2 * D * 2
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_bytes_step = fast_bytes + S * st1["slow_blocks"] * D * 4 + union_last * (rec - payload)
+    t_roof_ms = max(hbm_bytes_step / (hbm_peak * 1e9), pcie_bytes_launch / (h2d_peak * 1e9)) * 1e3
+    traffic = load_traffic()
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (device N(0,1) KV rounded to fp16, random queries)",
+        "config": {
+            "workload": ("cfg2: LLaMA-3-8B GQA 32L x 8KV x 4Q, 128K ctx, batch 1" if world == 1
+                         else f"cfg4: cfg2 head-sharded over {world} GPUs + NCCL all-gather"),
+            "ctx": args.ctx, "streams_per_gpu": S, "heads_per_stream": G, "d": D, "block": B,
+            "l_fast": L_FAST, "bits": "K8/V4", "fetch_fraction": FRAC,
+            "selection": "group-shared" if args.group_select else "per-query-head (reference)",
+            "slow_tier": "pinned host DRAM, zero-copy PCIe" if args.slow_tier == "host" else "HBM",
+            "storage": "fp16 ring, u8 keys / u4 values, f32 params", "parallelism":
+                f"head-shard{world}" if world > 1 else "single",
+            "l2": "inputs larger than L2 (ring 553 MB, slow tier 6.8 GB in host DRAM)",
+        },
+        "roofline": {
+            "bound": "pcie_h2d", "kernel": "slow_stream_attn", "achieved": achieved,
+            "peak": h2d_peak, "unit": "GB/s", "frac": achieved / h2d_peak,
+            "peak_source": "pinned cudaMemcpy H2D 256 MiB best of 10, measured in this run",
+            "traffic": traffic.get("slow_dram_bytes_per_launch") if traffic else None,
+            "algorithmic_bytes_per_launch": pcie_bytes_launch,
+            "launch_ms": slow_ms,
+            "tier_roofline_ms": t_roof_ms, "tier_frac": t_roof_ms / ms_step,
+            "fast_attn": {"ms": fast_ms, "hbm_gbs": fast_bytes / (fast_ms * 1e-3) / 1e9,
+                          "hbm_peak": hbm_peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+        },
+        "pcie_bytes_per_token": pcie_bytes_launch * world / tokens_per_step,
+        "union_blocks_per_step": union_last,
+        "kernel_ms_per_step": {k[3:]: v / args.steps for k, v in kt.items() if k.startswith("ms_")},
+        "gpu_launches": launches,
+        "e2e": {"value": tokens_per_step * 1000.0 / e2e_ms, "unit": UNIT,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h * (world if world > 1 else 1),
+                "ms_per_step": e2e_ms},
+        "prefill_s": round(prefill_s, 2),
+    }
+    if rank == 0:
+        line["clocks"] = clk.summary()
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            ms, pre_s, engines, threads = ref_sample(args.ctx, 2)
+            total = LAYERS * KV_HEADS * G
+            cv = cpu_throughput(float(ms[-1]), engines, total)
+            line["cpu_baseline"] = {
+                "value": cv, "unit": UNIT, "cores": threads, "kind": "reference",
+                "sample": (f"{engines} unmodified reference Engines at {args.ctx} ctx, "
+                           f"2 decode steps on {threads} threads (last timed: "
+                           f"{ms[-1]:.0f} ms), extrapolated x{total // engines} to "
+                           f"{total} engines")}
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": host_cores(),
+                                    "kind": "reference", "sample": f"unavailable: {e}"}
+    eng.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -99,6 +99,8 @@ typedef struct {
   uint64_t reserve_tokens;     /* context to preallocate for (grows on demand) */
   uint32_t slow_tier;          /* TTKV_SLOW_* */
   uint32_t copy_mode;          /* slow-block staging: 0 auto, 1 cp.async.bulk, 2 LDG */
+  uint32_t literal_additive_merge; /* EngineOptions (engine.hpp:14-19): sum of
+                                      per-partition normalized outputs (A/B only) */
 } ttkv_gpu_options;
 
 /* DecodeStepReport (engine.hpp:21-29) plus measured quantities. */
@@ -124,6 +126,8 @@ typedef struct {
   uint64_t heads_per_stream;
   uint64_t block_capacity;  /* slow blocks allocated per stream */
   uint64_t launches;        /* kernels launched by this handle so far */
+  uint64_t payload_bytes;   /* bytes of each record streamed over PCIe (codes);
+                               the per-channel params are staged from HBM */
 } ttkv_state;
 
 /* Kernel timing (enabled by ttkv_gpu_set_timing); milliseconds summed over
@@ -168,6 +172,18 @@ int ttkv_gpu_decode_step_device(struct ttkv_gpu* h, const float* q, const void* 
 int ttkv_gpu_read_step_counters(struct ttkv_gpu* h, uint64_t* union_blocks,
                                 uint64_t* pcie_bytes);
 
+/* TierStore::append_token (tier_store.cpp:49-67) WITHOUT settling evictions:
+ * appends n tokens (host arrays [S][n][d]) to every stream.  Fails with
+ * TTKV_EERROR when the fast tier would outgrow its ring (L_fast + block_size
+ * tokens); settle pending evictions with ttkv_gpu_evict first. */
+int ttkv_gpu_append(struct ttkv_gpu* h, const void* keys, const void* values, uint64_t n_tokens,
+                    int dtype);
+/* TierStore::evict_and_compress (tier_store.cpp:71-98): quantizes the oldest
+ * fast-tier block of every stream into the slow tier.  TTKV_EERROR when no
+ * eviction is pending. */
+int ttkv_gpu_evict(struct ttkv_gpu* h, uint64_t* block_id);
+int ttkv_gpu_eviction_pending(struct ttkv_gpu* h, int* pending);
+
 /* ---- state / cold path ------------------------------------------------------ */
 int ttkv_gpu_state(struct ttkv_gpu* h, ttkv_state* st);
 /* fetched_blocks of the last step for (stream, head), schedule order. */
@@ -199,6 +215,20 @@ int ttkv_gpu_quantize_block(int device, const float* keys, const float* values, 
                             uint32_t d_k, uint32_t d_v, uint32_t key_bits, uint32_t value_bits,
                             uint8_t* packed_k, uint8_t* packed_v, float* key_params,
                             float* value_params, float* centroid);
+/* dequantize_block (quantizer.cpp:157-170) on the GPU, bit-exact:
+ * x = float(double(code) * scale + zp); 16-bit payloads are raw float32. */
+int ttkv_gpu_dequantize_block(int device, const uint8_t* packed_k, const uint8_t* packed_v,
+                              const float* key_params, const float* value_params, uint64_t rows,
+                              uint32_t d_k, uint32_t d_v, uint32_t key_bits, uint32_t value_bits,
+                              float* keys, float* values);
+/* score_block (relevance.cpp:19-27) for n centroids [n][d]: fp64, sequential,
+ * unfused -- bit-exact. */
+int ttkv_gpu_score_blocks(int device, const float* query, const float* centroids, uint64_t n,
+                          uint32_t d, double* scores);
+/* select_top_k (relevance.cpp:29-43): the k ids ordered by (score desc, id
+ * desc).  n <= 8192. */
+int ttkv_gpu_select_top_k(int device, const double* scores, const uint64_t* ids, uint64_t n,
+                          uint64_t k, uint64_t* out);
 uint64_t ttkv_fast_capacity(const ttkv_tier_config* cfg); /* 0 + last_error on error */
 uint64_t ttkv_modeled_block_bytes(const ttkv_tier_config* cfg);
 uint64_t ttkv_packed_bytes(uint64_t count, uint32_t bits);

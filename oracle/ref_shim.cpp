@@ -63,10 +63,10 @@ const char* ref_last_error() { return g_err.c_str(); }
 // ---- Engine ------------------------------------------------------------------
 void* ref_engine_create(uint64_t budget, uint32_t d_k, uint32_t d_v, uint32_t bytes_fp,
                         uint32_t block_size, uint32_t kb, uint32_t vb, int has_top_k,
-                        uint64_t top_k, double frac) {
+                        uint64_t top_k, double frac, int literal_merge) {
   try {
     return new Engine(make_cfg(budget, d_k, d_v, bytes_fp, block_size, kb, vb),
-                      make_policy(has_top_k, top_k, frac));
+                      make_policy(has_top_k, top_k, frac), EngineOptions{literal_merge != 0});
   } catch (const std::exception& e) {
     g_err = e.what();
     return nullptr;

@@ -369,6 +369,8 @@ int tko_engine_decode_step(tko_engine* e, const float* q, size_t G, int mode,
   const tko_config* c = &e->cfg;
   const size_t dk = c->d_k, dv = c->d_v, B = c->block_size;
   if (G == 0) return -1;
+  const int smode = mode & 1;         /* selection: per-head / group-shared */
+  const int literal = (mode >> 1) & 1; /* EngineOptions::literal_additive_merge */
   append_token(e, key, value); /* engine.cpp:28 */
   const double scale = 1.0 / sqrt((double)dk); /* engine.cpp:30 */
   const size_t n = e->n_slow;
@@ -382,7 +384,7 @@ int tko_engine_decode_step(tko_engine* e, const float* q, size_t G, int mode,
   float* dv_buf = (float*)malloc(B * dv * sizeof(float));
   uint8_t* in_union = (uint8_t*)calloc(n ? n : 1, 1);
   float* qshared = (float*)calloc(dk, sizeof(float));
-  if (mode == 1)
+  if (smode == 1)
     for (size_t g = 0; g < G; ++g)
       for (size_t i = 0; i < dk; ++i) qshared[i] += q[g * dk + i];
 
@@ -395,8 +397,15 @@ int tko_engine_decode_step(tko_engine* e, const float* q, size_t G, int mode,
     /* engine.cpp:36-40: fast tier including the new token */
     for (size_t t = 0; t < e->fast_n; ++t)
       acc_absorb(&acc, qg, e->fk + (e->fast_off + t) * dk, e->fv + (e->fast_off + t) * dv, 1, dk);
+    /* engine.cpp:44-48: literal additive merge keeps the fast partition's
+     * normalized output and sums every block's normalized output onto it */
+    double* lit = NULL;
+    if (literal) {
+      lit = (double*)calloc(dv, sizeof(double));
+      for (size_t i = 0; i < dv; ++i) lit[i] = acc.wv[i] / acc.den;
+    }
     /* engine.cpp:51-58 */
-    const float* qs = (mode == 1) ? qshared : qg;
+    const float* qs = (smode == 1) ? qshared : qg;
     for (size_t b = 0; b < n; ++b) scores[b] = tko_score_block(qs, e->slow[b].centroid, dk);
     tko_select_top_k(scores, NULL, n, k, sel);
     /* engine.cpp:61-83 */
@@ -406,11 +415,20 @@ int tko_engine_decode_step(tko_engine* e, const float* q, size_t G, int mode,
       bytes += (double)blk_bytes;
       tko_dequantize_tensor(b->packed_k, B, dk, c->key_bits, b->k_params, dk_buf);
       tko_dequantize_tensor(b->packed_v, B, dv, c->value_bits, b->v_params, dv_buf);
-      acc_absorb(&acc, qg, dk_buf, dv_buf, B, dk);
+      if (literal) { /* engine.cpp:67-72 */
+        accum part;
+        acc_init(&part, dv, scale);
+        acc_absorb(&part, qg, dk_buf, dv_buf, B, dk);
+        for (size_t j = 0; j < dv; ++j) lit[j] += part.wv[j] / part.den;
+        free(part.wv);
+      } else {
+        acc_absorb(&acc, qg, dk_buf, dv_buf, B, dk);
+      }
     }
     /* attention.hpp:54-61 */
-    for (size_t i = 0; i < dv; ++i) out[g * dv + i] = acc.wv[i] / acc.den;
+    for (size_t i = 0; i < dv; ++i) out[g * dv + i] = literal ? lit[i] : acc.wv[i] / acc.den;
     free(acc.wv);
+    free(lit);
     if (fetched)
       for (size_t i = 0; i < k && i < fetched_cap; ++i) fetched[g * fetched_cap + i] = sel[i];
     if (n_fetched) n_fetched[g] = k;

@@ -85,6 +85,7 @@ int tko_engine_prefill(tko_engine* e, const float* keys, const float* values, si
  *   mode 0 (per-head): head g == one reference Engine fed q_g.
  *   mode 1 (group-shared): selection scored with q' = sum_g q_g (float,
  *          sequential g), every head attends that set.
+ *   mode | 2: EngineOptions::literal_additive_merge (engine.cpp:44-48, 67-72).
  * out: G x d_v doubles.  fetched: G x cap ids (schedule order), n_fetched[G].
  * Returns 0, or a negative code on shape/config errors. */
 int tko_engine_decode_step(tko_engine* e, const float* q, size_t G, int mode,

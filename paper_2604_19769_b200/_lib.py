@@ -33,7 +33,7 @@ class OptionsC(C.Structure):
     _fields_ = [("device", C.c_int32), ("n_streams", C.c_uint32),
                 ("heads_per_stream", C.c_uint32), ("group_select", C.c_uint32),
                 ("reserve_tokens", C.c_uint64), ("slow_tier", C.c_uint32),
-                ("copy_mode", C.c_uint32)]
+                ("copy_mode", C.c_uint32), ("literal_additive_merge", C.c_uint32)]
 
 
 class StepReportC(C.Structure):
@@ -46,7 +46,8 @@ class StepReportC(C.Structure):
 class StateC(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "appended", "fast_tokens", "slow_blocks", "l_fast", "record_bytes",
-        "modeled_block_bytes", "n_streams", "heads_per_stream", "block_capacity", "launches")]
+        "modeled_block_bytes", "n_streams", "heads_per_stream", "block_capacity", "launches",
+        "payload_bytes")]
 
 
 class KernelTimesC(C.Structure):
@@ -64,7 +65,9 @@ EXPORTS = [
     "ttkv_gpu_decode_step", "ttkv_gpu_decode_step_device", "ttkv_gpu_read_step_counters",
     "ttkv_gpu_state", "ttkv_gpu_read_fetched", "ttkv_gpu_read_block", "ttkv_gpu_serialize_block",
     "ttkv_gpu_dump_slow_tier", "ttkv_gpu_read_fast", "ttkv_gpu_locate", "ttkv_gpu_set_timing",
-    "ttkv_gpu_kernel_times", "ttkv_gpu_quantize_block", "ttkv_fast_capacity",
+    "ttkv_gpu_kernel_times", "ttkv_gpu_quantize_block", "ttkv_gpu_append", "ttkv_gpu_evict",
+    "ttkv_gpu_eviction_pending", "ttkv_gpu_dequantize_block", "ttkv_gpu_score_blocks",
+    "ttkv_gpu_select_top_k", "ttkv_fast_capacity",
     "ttkv_modeled_block_bytes", "ttkv_packed_bytes", "ttkv_resolve", "ttkv_validate_config",
     "ttkv_default_config",
 ]
@@ -109,6 +112,13 @@ def lib():
         "ttkv_gpu_kernel_times": (i32, [vp, P(KernelTimesC), i32]),
         "ttkv_gpu_quantize_block": (i32, [i32, vp, vp, u64, u32, u32, u32, u32, vp, vp, vp, vp,
                                           vp]),
+        "ttkv_gpu_append": (i32, [vp, vp, vp, u64, i32]),
+        "ttkv_gpu_evict": (i32, [vp, P(u64)]),
+        "ttkv_gpu_eviction_pending": (i32, [vp, P(i32)]),
+        "ttkv_gpu_dequantize_block": (i32, [i32, vp, vp, vp, vp, u64, u32, u32, u32, u32, vp,
+                                            vp]),
+        "ttkv_gpu_score_blocks": (i32, [i32, vp, vp, u64, u32, vp]),
+        "ttkv_gpu_select_top_k": (i32, [i32, vp, vp, u64, u64, vp]),
         "ttkv_fast_capacity": (u64, [P(TierConfigC)]),
         "ttkv_modeled_block_bytes": (u64, [P(TierConfigC)]),
         "ttkv_packed_bytes": (u64, [u64, u32]),

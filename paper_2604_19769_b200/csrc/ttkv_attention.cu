@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32) slow_attn_kernel
       for (uint32_t t = lane; t < g.B; t += 32) bm = fmaxf(bm, row[t]);
       bm = warp_max(bm);
       const float m_old = mst[h];
-      const float m_new = fmaxf(m_old, bm);
+      const float m_new = a.literal ? bm : fmaxf(m_old, bm);
       float sum = 0.0f;
       for (uint32_t t = lane; t < g.B; t += 32) {
         const float p = exp2f(row[t] - m_new);
@@ -326,6 +326,14 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32) slow_attn_kernel
       }
       sum = warp_sum(sum);
       __syncwarp();
+      if (a.literal) {
+        // literal additive merge (engine.cpp:67-72): each block is its own
+        // normalized partition, summed without rescaling
+        const float inv = 1.0f / sum;
+        for (uint32_t t = lane; t < g.B; t += 32) row[t] *= inv;
+        if (lane == 0) ast[h] = 1.0f;
+        continue;
+      }
       if (lane == 0) {
         const float alpha = exp2f(m_old - m_new);  // 0 when m_old = -inf
         lst[h] = lst[h] * alpha + sum;
@@ -393,8 +401,8 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32) slow_attn_kernel
     const bool any = (seen >> h) & 1u;
     p[c] = any ? A : 0.0f;
     if (c == 0) {
-      p[g.d_v] = any ? mst[h] : -INFINITY;
-      p[g.d_v + 1] = any ? lst[h] : 0.0f;
+      p[g.d_v] = any ? (a.literal ? 0.0f : mst[h]) : -INFINITY;
+      p[g.d_v + 1] = any ? (a.literal ? 1.0f : lst[h]) : 0.0f;
     }
   }
 }
@@ -472,10 +480,12 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
   const float* fp = a.fpart + (uint64_t)idx * a.nfc * pitch;
   const float* sp = a.spart ? a.spart + (uint64_t)idx * a.nsc * pitch : nullptr;
 
+  // literal additive merge: slow partials are already normalized sums
+  const uint32_t nlse = a.literal ? 0u : nsc_used;
   float M = -INFINITY;
   for (uint32_t i = lane; i < a.nfc; i += 32)
     if (fp[i * pitch + g.d_v + 1] > 0.0f) M = fmaxf(M, fp[i * pitch + g.d_v]);
-  for (uint32_t i = lane; i < nsc_used; i += 32)
+  for (uint32_t i = lane; i < nlse; i += 32)
     if (sp[i * pitch + g.d_v + 1] > 0.0f) M = fmaxf(M, sp[i * pitch + g.d_v]);
   M = warp_max(M);
 
@@ -484,7 +494,7 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
     const float l = fp[i * pitch + g.d_v + 1];
     if (l > 0.0f) L += l * exp2f(fp[i * pitch + g.d_v] - M);
   }
-  for (uint32_t i = lane; i < nsc_used; i += 32) {
+  for (uint32_t i = lane; i < nlse; i += 32) {
     const float l = sp[i * pitch + g.d_v + 1];
     if (l > 0.0f) L += l * exp2f(sp[i * pitch + g.d_v] - M);
   }
@@ -497,11 +507,15 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
       const float l = fp[i * pitch + g.d_v + 1];
       if (l > 0.0f) A += fp[i * pitch + c] * exp2f(fp[i * pitch + g.d_v] - M);
     }
-    for (uint32_t i = 0; i < nsc_used; ++i) {
+    for (uint32_t i = 0; i < nlse; ++i) {
       const float l = sp[i * pitch + g.d_v + 1];
       if (l > 0.0f) A += sp[i * pitch + c] * exp2f(sp[i * pitch + g.d_v] - M);
     }
-    a.out[(uint64_t)idx * g.d_v + c] = A * inv;
+    float o = A * inv;
+    if (a.literal)
+      for (uint32_t i = 0; i < nsc_used; ++i)
+        if (sp[i * pitch + g.d_v + 1] > 0.0f) o += sp[i * pitch + c];
+    a.out[(uint64_t)idx * g.d_v + c] = o;
   }
 }
 

@@ -124,6 +124,8 @@ enum Kind { K_APPEND = 0, K_SCORE, K_SELECT, K_FAST, K_SLOW, K_COMBINE, K_EVICT,
 
 }  // namespace
 
+void ttkv_dev::set_last_error(const char* msg) { g_last_error = msg ? msg : ""; }
+
 struct ttkv_gpu {
   ttkv_tier_config cfg{};
   ttkv_selection_policy pol{};
@@ -429,6 +431,9 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
   }
   const Geometry& g = h->g;
   uint64_t pos = h->appended;
+  if (pos - h->fast_front + 1 > g.C)
+    return set_err(h, TTKV_EERROR,
+                   "decode_step: fast tier would exceed its ring; settle pending evictions");
   // append_kv: the new token attends to itself
   {
     KTimer t(h, K_APPEND, h->s0);
@@ -510,6 +515,7 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       a.nsc = (uint32_t)h->spart_chunks;
       a.stages = h->stages;
       a.scale_log2 = scale_log2;
+      a.literal = h->opt.literal_additive_merge ? 1u : 0u;
       KTimer t(h, K_SLOW, h->s0);
       CU(h, launch_slow(a, (uint32_t)grid_chunks, (int)h->copy_mode, h->s0));
     }
@@ -525,6 +531,7 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
     a.CH = CH;
     a.union_count = slow ? h->ucount : nullptr;
     a.out = out;
+    a.literal = h->opt.literal_additive_merge ? 1u : 0u;
     KTimer t(h, K_COMBINE, h->s0);
     CU(h, launch_combine(a, h->s0));
   }
@@ -683,7 +690,7 @@ int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* po
   }
   // fast split: ~8 waves of 4-warp CTAs
   {
-    const uint64_t Fmax = l_fast + 1;
+    const uint64_t Fmax = l_fast + g.B;  // ring capacity bounds the fast tier
     const uint64_t target = std::max<uint64_t>(1, (148ull * 8 + g.S - 1) / g.S);
     uint64_t FC = (Fmax + target - 1) / target;
     FC = std::max<uint64_t>(64, std::min<uint64_t>(1024, (FC + 31) / 32 * 32));
@@ -817,6 +824,68 @@ int ttkv_gpu_prefill_synthetic(ttkv_gpu* h, uint64_t n, uint64_t seed) {
   return TTKV_OK;
 }
 
+int ttkv_gpu_append(ttkv_gpu* h, const void* keys, const void* values, uint64_t n, int dtype) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  if (n == 0) return TTKV_OK;
+  if (!keys || !values) return set_err(h, TTKV_EINVAL, "null key/value pointer");
+  if (dtype != TTKV_DTYPE_F32 && dtype != TTKV_DTYPE_F16)
+    return set_err(h, TTKV_ESHAPE, "append_token: unknown dtype");
+  const Geometry& g = h->g;
+  if (h->appended - h->fast_front + n > g.C)
+    return set_err(h, TTKV_EERROR,
+                   "append_token: fast tier would exceed its ring (L_fast + block_size); "
+                   "settle pending evictions first");
+  CU(h, cudaSetDevice(h->dev));
+  int rc = ensure_staging(h, n);
+  if (rc) return rc;
+  const size_t esz = dtype == TTKV_DTYPE_F16 ? 2 : 4;
+  CU(h, cudaMemcpyAsync(h->stg_k, keys, (size_t)g.S * n * g.d_k * esz, cudaMemcpyHostToDevice,
+                        h->s0));
+  CU(h, cudaMemcpyAsync(h->stg_v, values, (size_t)g.S * n * g.d_v * esz, cudaMemcpyHostToDevice,
+                        h->s0));
+  {
+    KTimer t(h, K_APPEND, h->s0);
+    CU(h, launch_append(g, h->ring_k, h->ring_v, h->stg_k, h->stg_v,
+                        dtype == TTKV_DTYPE_F16 ? kInF16 : kInF32, h->appended, n, n, h->s0));
+  }
+  h->appended += n;
+  CU(h, cudaStreamSynchronize(h->s0));
+  return TTKV_OK;
+}
+
+int ttkv_gpu_eviction_pending(ttkv_gpu* h, int* pending) {
+  if (!h || !pending) return set_err(h, TTKV_EINVAL, "null argument");
+  *pending = (h->appended - h->fast_front > h->l_fast) ? 1 : 0;
+  return TTKV_OK;
+}
+
+int ttkv_gpu_evict(ttkv_gpu* h, uint64_t* block_id) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  if (h->appended - h->fast_front <= h->l_fast)
+    return set_err(h, TTKV_EERROR, "evict_and_compress: no eviction pending");
+  CU(h, cudaSetDevice(h->dev));
+  int rc = ensure_blocks(h, h->n_slow + 1);
+  if (rc) return rc;
+  EvictArgs a{};
+  a.g = h->g;
+  a.ring_k = h->ring_k;
+  a.ring_v = h->ring_v;
+  a.split_pos = h->appended;
+  a.first_block = h->n_slow;
+  a.arena = h->arena_dev;
+  a.cent = h->cent;
+  a.params = h->params;
+  {
+    KTimer t(h, K_EVICT, h->s0);
+    CU(h, launch_evict(a, 1, kInF32, h->s0));
+  }
+  if (block_id) *block_id = h->n_slow;
+  h->n_slow++;
+  h->fast_front += h->g.B;
+  CU(h, cudaStreamSynchronize(h->s0));
+  return TTKV_OK;
+}
+
 int ttkv_gpu_decode_step_device(ttkv_gpu* h, const float* q, const void* kn, const void* vn,
                                 int dtype, float* out, ttkv_step_report* rep) {
   if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
@@ -882,6 +951,7 @@ int ttkv_gpu_state(ttkv_gpu* h, ttkv_state* st) {
   st->heads_per_stream = h->g.G;
   st->block_capacity = h->g.n_cap;
   st->launches = h->launches;
+  st->payload_bytes = h->g.rec.kp_off;
   return TTKV_OK;
 }
 

@@ -1,0 +1,190 @@
+// ttkv_freefn.cu -- the reference's stateless numeric free functions on the GPU
+// (the cold-path API surface of the drop-in; the hot path fuses these):
+//   dequantize_block  quantizer.cpp:90-113, 157-170  (bit-exact fp64 affine)
+//   score_block       relevance.cpp:19-27            (bit-exact fp64, unfused)
+//   select_top_k      relevance.cpp:29-43            (bitonic, total order)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/ttkv_gpu.h"
+#include "ttkv_kernels.cuh"
+#include "ttkv_launch.h"
+
+namespace ttkv_dev {
+
+__global__ void dequant_kernel(const uint8_t* packed, const float* params, uint64_t rows,
+                               uint32_t dim, uint32_t bits, float* out) {
+  const uint64_t n = rows * dim;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (bits == 16) {
+      out[i] = reinterpret_cast<const float*>(packed)[i];
+      continue;
+    }
+    const uint64_t bit = i * bits;
+    const uint32_t lo = packed[bit >> 3];
+    const uint32_t hi = (((bit & 7) + bits) > 8) ? packed[(bit >> 3) + 1] : 0u;
+    const uint32_t code = ((lo | (hi << 8)) >> (bit & 7)) & ((1u << bits) - 1u);
+    const uint32_t c = (uint32_t)(i % dim);
+    const double x = __dadd_rn(__dmul_rn((double)code, (double)params[2 * c]),
+                               (double)params[2 * c + 1]);
+    out[i] = __double2float_rn(x);
+  }
+}
+
+__global__ void score_free_kernel(const float* q, const float* cent, uint64_t n, uint32_t d,
+                                  double* out) {
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < n;
+       b += (uint64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (uint32_t i = 0; i < d; ++i)
+      acc = __dadd_rn(acc, __dmul_rn((double)q[i], (double)cent[b * d + i]));
+    out[b] = acc;
+  }
+}
+
+__device__ __forceinline__ uint64_t order_key_free(double d) {
+  if (d == 0.0) d = 0.0;
+  const uint64_t b = (uint64_t)__double_as_longlong(d);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void topk_free_kernel(const double* scores, const uint64_t* ids, uint32_t n,
+                                 uint32_t N2, uint32_t k, uint64_t* out) {
+  extern __shared__ __align__(16) uint64_t sm[];
+  uint64_t* key = sm;
+  uint64_t* id = sm + N2;
+  for (uint32_t i = threadIdx.x; i < N2; i += blockDim.x) {
+    key[i] = i < n ? order_key_free(scores[i]) : 0ull;
+    id[i] = i < n ? ids[i] : 0ull;
+  }
+  __syncthreads();
+  for (uint32_t size = 2; size <= N2; size <<= 1) {
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      for (uint32_t i = threadIdx.x; i < N2 / 2; i += blockDim.x) {
+        const uint32_t lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const bool desc = (lo & size) == 0;
+        const uint64_t kl = key[lo], kh = key[hi], il = id[lo], ih = id[hi];
+        const bool less = (kl < kh) || (kl == kh && il < ih);
+        if (less == desc) {
+          key[lo] = kh; key[hi] = kl;
+          id[lo] = ih; id[hi] = il;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) out[i] = id[i];
+}
+
+}  // namespace ttkv_dev
+
+namespace {
+
+
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t alloc(size_t n) { return cudaMalloc(&p, n ? n : 16); }
+};
+
+int fail(cudaError_t e) {
+  ttkv_dev::set_last_error(cudaGetErrorString(e));
+  return TTKV_ECUDA;
+}
+}  // namespace
+
+#define FCU(x)                          \
+  do {                                  \
+    cudaError_t e__ = (x);              \
+    if (e__ != cudaSuccess) return fail(e__); \
+  } while (0)
+
+extern "C" {
+
+
+int ttkv_gpu_dequantize_block(int device, const uint8_t* packed_k, const uint8_t* packed_v,
+                              const float* key_params, const float* value_params, uint64_t rows,
+                              uint32_t d_k, uint32_t d_v, uint32_t kb, uint32_t vb, float* keys,
+                              float* values) {
+  auto valid_bits = [](uint32_t b) { return (b >= 2 && b <= 8) || b == 16; };
+  if (!valid_bits(kb) || !valid_bits(vb)) return TTKV_EINTEGRITY;
+  FCU(cudaSetDevice(device));
+  auto bytes = [](uint64_t cnt, uint32_t bits) -> size_t {
+    return bits == 16 ? cnt * 4 : (cnt * bits + 7) / 8;
+  };
+  for (int t = 0; t < 2; ++t) {
+    const uint8_t* pk = t ? packed_v : packed_k;
+    const float* pp = t ? value_params : key_params;
+    const uint32_t dim = t ? d_v : d_k, bits = t ? vb : kb;
+    float* out = t ? values : keys;
+    if (!out || rows * dim == 0) continue;
+    DevBuf dp, dpar, dout;
+    const size_t nb = bytes(rows * dim, bits);
+    FCU(dp.alloc(nb + 8));
+    FCU(cudaMemset(dp.p, 0, nb + 8));
+    FCU(cudaMemcpy(dp.p, pk, nb, cudaMemcpyHostToDevice));
+    FCU(dpar.alloc(8 * dim));
+    if (bits != 16) FCU(cudaMemcpy(dpar.p, pp, 8 * dim, cudaMemcpyHostToDevice));
+    FCU(dout.alloc(rows * dim * 4));
+    const unsigned grid = (unsigned)std::min<uint64_t>((rows * dim + 255) / 256, 148 * 8);
+    ttkv_dev::dequant_kernel<<<grid, 256>>>((const uint8_t*)dp.p, (const float*)dpar.p, rows,
+                                             dim, bits, (float*)dout.p);
+    FCU(cudaGetLastError());
+    FCU(cudaMemcpy(out, dout.p, rows * dim * 4, cudaMemcpyDeviceToHost));
+  }
+  return TTKV_OK;
+}
+
+int ttkv_gpu_score_blocks(int device, const float* query, const float* centroids, uint64_t n,
+                          uint32_t d, double* scores) {
+  if (n == 0) return TTKV_OK;
+  if (!query || !centroids || !scores) return TTKV_EINVAL;
+  FCU(cudaSetDevice(device));
+  DevBuf dq, dc, ds;
+  FCU(dq.alloc(d * 4));
+  FCU(dc.alloc(n * d * 4));
+  FCU(ds.alloc(n * 8));
+  FCU(cudaMemcpy(dq.p, query, d * 4, cudaMemcpyHostToDevice));
+  FCU(cudaMemcpy(dc.p, centroids, n * d * 4, cudaMemcpyHostToDevice));
+  const unsigned grid = (unsigned)std::min<uint64_t>((n + 127) / 128, 148 * 8);
+  ttkv_dev::score_free_kernel<<<grid, 128>>>((const float*)dq.p, (const float*)dc.p, n, d,
+                                              (double*)ds.p);
+  FCU(cudaGetLastError());
+  FCU(cudaMemcpy(scores, ds.p, n * 8, cudaMemcpyDeviceToHost));
+  return TTKV_OK;
+}
+
+int ttkv_gpu_select_top_k(int device, const double* scores, const uint64_t* ids, uint64_t n,
+                          uint64_t k, uint64_t* out) {
+  if (k > n) k = n;
+  if (n == 0 || k == 0) return TTKV_OK;
+  if (n > 8192) {
+    ttkv_dev::set_last_error("select_top_k: more than 8192 blocks");
+    return TTKV_ECONFIG;
+  }
+  FCU(cudaSetDevice(device));
+  uint32_t N2 = 2;
+  while (N2 < n) N2 <<= 1;
+  DevBuf ds, di, dout;
+  FCU(ds.alloc(n * 8));
+  FCU(di.alloc(n * 8));
+  FCU(dout.alloc(k * 8));
+  FCU(cudaMemcpy(ds.p, scores, n * 8, cudaMemcpyHostToDevice));
+  FCU(cudaMemcpy(di.p, ids, n * 8, cudaMemcpyHostToDevice));
+  const size_t smem = (size_t)N2 * 16;
+  FCU(cudaFuncSetAttribute(ttkv_dev::topk_free_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem));
+  ttkv_dev::topk_free_kernel<<<1, 1024, smem>>>((const double*)ds.p, (const uint64_t*)di.p,
+                                                 (uint32_t)n, N2, (uint32_t)k, (uint64_t*)dout.p);
+  FCU(cudaGetLastError());
+  FCU(cudaMemcpy(out, dout.p, k * 8, cudaMemcpyDeviceToHost));
+  return TTKV_OK;
+}
+
+}  // extern "C"

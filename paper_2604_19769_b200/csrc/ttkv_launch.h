@@ -10,6 +10,9 @@ namespace ttkv_dev {
 constexpr int kInF32 = 0;
 constexpr int kInF16 = 1;
 
+// thread-local message behind ttkv_last_error() (defined in ttkv_engine.cu)
+void set_last_error(const char* msg);
+
 struct EvictArgs {
   Geometry g;
   const void* ring_k;
@@ -86,6 +89,7 @@ struct SlowArgs {
   uint32_t stages;
   float scale_log2;
   uint32_t stage_region;  // set by the launcher
+  uint32_t literal;       // EngineOptions::literal_additive_merge
 };
 // copy_mode: 1 = cp.async.bulk, 2 = LDG
 cudaError_t launch_slow(const SlowArgs& a, uint32_t grid_chunks, int copy_mode, cudaStream_t st);
@@ -100,6 +104,7 @@ struct CombineArgs {
   uint32_t CH;
   const uint32_t* union_count;  // null when no slow work this step
   float* out;                   // [S][G][d_v]
+  uint32_t literal;
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);
 

@@ -87,7 +87,8 @@ def ref():
         u32, u64 = C.c_uint32, C.c_uint64
         L.ref_last_error.restype = C.c_char_p
         L.ref_engine_create.restype = C.c_void_p
-        L.ref_engine_create.argtypes = [u64, u32, u32, u32, u32, u32, u32, C.c_int, u64, C.c_double]
+        L.ref_engine_create.argtypes = [u64, u32, u32, u32, u32, u32, u32, C.c_int, u64, C.c_double,
+                                        C.c_int]
         L.ref_engine_destroy.argtypes = [C.c_void_p]
         L.ref_engine_prefill.argtypes = [C.c_void_p, _f32p, _f32p, u64]
         L.ref_engine_decode_step.argtypes = [C.c_void_p, _f32p, _f32p, _f32p, _f64p, _u64p, u64,
@@ -228,10 +229,10 @@ class RefEngine:
     """The unmodified reference ttkv::Engine (oracle/_ref)."""
 
     def __init__(self, budget, d_k, d_v, block_size, key_bits=8, value_bits=4, bytes_fp=2,
-                 top_k=None, fetch_fraction=0.45):
+                 top_k=None, fetch_fraction=0.45, literal_merge=False):
         self.h = ref().ref_engine_create(budget, d_k, d_v, bytes_fp, block_size, key_bits,
                                          value_bits, int(top_k is not None), top_k or 0,
-                                         fetch_fraction)
+                                         fetch_fraction, int(literal_merge))
         if not self.h:
             raise ValueError(ref().ref_last_error().decode())
         self.d_k, self.d_v = d_k, d_v

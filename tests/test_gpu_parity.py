@@ -116,7 +116,8 @@ def make_inputs(S, ctx, T, dk, dv, G, seed, fp16):
     extra GQA queries come from the same generator family."""
     pk, pv, dkk, dvv, dq = [], [], [], [], []
     for s in range(S):
-        a, b, c, d, q = O.generate_workload(ctx, T, dk, dv, seed + s)
+        a, b, c, d, q = O.generate_workload(max(ctx, 1), T, dk, dv, seed + s)
+        a, b = a[:ctx], b[:ctx]  # ctx == 0: decode from an empty store
         qs = [q]
         for g in range(1, G):
             *_, qg = O.generate_workload(1, T, dk, dv, 7919 * (seed + s) + g)
@@ -131,7 +132,7 @@ def make_inputs(S, ctx, T, dk, dv, G, seed, fp16):
 
 def run_parity(T_, *, S=2, G=1, d=32, dv=None, B=32, l_fast=128, kb=8, vb=4, elem=2, ctx=600,
                steps=6, frac=0.45, top_k=None, mode=0, seed=100, prefill_chunks=1,
-               check_blocks=True):
+               check_blocks=True, literal=False):
     dv = dv or d
     cfg = T_.TierConfig(hbm_budget_bytes=l_fast * (d + dv) * elem, d_k=d, d_v=dv,
                         bytes_full_precision=elem, block_size=B, key_bits=kb, value_bits=vb,
@@ -139,14 +140,16 @@ def run_parity(T_, *, S=2, G=1, d=32, dv=None, B=32, l_fast=128, kb=8, vb=4, ele
     pol = T_.SelectionPolicy(top_k, frac)
     assert T_.fast_capacity(cfg) == l_fast
     pk, pv, dk_, dv_, dq = make_inputs(S, ctx, steps, d, dv, G, seed, fp16=(elem == 2))
-    eng = T_.MultiStreamEngine(cfg, pol, n_streams=S, heads_per_stream=G, group_select=bool(mode))
+    eng = T_.MultiStreamEngine(cfg, pol, n_streams=S, heads_per_stream=G, group_select=bool(mode),
+                               literal_additive_merge=literal)
     orc = [O.OracleEngine(d, dv, B, l_fast, kb, vb, top_k, frac) for _ in range(S)]
     bounds = np.linspace(0, ctx, prefill_chunks + 1).astype(int)
     for a, b in zip(bounds[:-1], bounds[1:]):
         if b > a:
             eng.prefill(pk[:, a:b], pv[:, a:b])
     for s in range(S):
-        orc[s].prefill(pk[s], pv[s])
+        if ctx:
+            orc[s].prefill(pk[s], pv[s])
     st = eng.state()
     assert st["slow_blocks"] == orc[0].slow_blocks()
     assert st["fast_tokens"] == orc[0].fast_tokens()
@@ -154,7 +157,7 @@ def run_parity(T_, *, S=2, G=1, d=32, dv=None, B=32, l_fast=128, kb=8, vb=4, ele
     for t in range(steps):
         rep = eng.decode_step(dq[:, t], dk_[:, t], dv_[:, t], fetched=True)
         for s in range(S):
-            o = orc[s].decode_step(dq[s, t], dk_[s, t], dv_[s, t], mode=mode)
+            o = orc[s].decode_step(dq[s, t], dk_[s, t], dv_[s, t], mode=mode | (2 * literal))
             assert rep.blocks_scored == o["blocks_scored"]
             assert rep.eviction_occurred == o["eviction_occurred"]
             assert rep.bytes_transferred == o["bytes_transferred"]
@@ -194,6 +197,12 @@ def test_engine_gqa_per_head(gpu):
 
 def test_engine_gqa_group_shared(gpu):
     run_parity(gpu, S=3, G=4, d=64, B=64, l_fast=256, ctx=2000, steps=6, mode=1)
+
+
+def test_engine_literal_additive_merge(gpu):
+    # EngineOptions::literal_additive_merge (engine.cpp:44-48, 67-72)
+    run_parity(gpu, S=2, G=2, d=16, B=32, l_fast=128, ctx=600, steps=4, literal=True)
+    run_parity(gpu, S=2, G=4, d=64, B=64, l_fast=256, ctx=2000, steps=3, literal=True, mode=1)
 
 
 def test_engine_eviction_cycle(gpu):

@@ -251,6 +251,20 @@ def test_engine_bit_identical_to_reference(cfg):
 
 
 @needs_ref
+def test_literal_merge_bit_identical_to_reference():
+    # EngineOptions::literal_additive_merge (engine.cpp:44-48, 67-72)
+    pk, pv, dk, dv, dq = O.generate_workload(512, 6, 16, 16, 13)
+    e = O.OracleEngine(16, 16, 32, 128, 8, 4, None, 0.45)
+    r = O.RefEngine(128 * 32 * 2, 16, 16, 32, 8, 4, literal_merge=True)
+    e.prefill(pk, pv)
+    r.prefill(pk, pv)
+    for t in range(6):
+        x = e.decode_step(dq[t], dk[t], dv[t], mode=2)
+        y = r.decode_step(dq[t], dk[t], dv[t])
+        assert np.array_equal(x["output"][0], y["output"])
+
+
+@needs_ref
 def test_quantize_bit_identical_to_reference():
     rng = np.random.default_rng(2)
     for trial in range(40):
