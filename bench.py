@@ -213,9 +213,9 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    if KV_HEADS % world:
-        raise SystemExit("world size must divide the 8 KV heads")
-    S = LAYERS * KV_HEADS // world  # streams on this rank (head sharding)
+    from paper_2604_19769_b200.sharding import ShardPlan, gather_outputs
+    plan = ShardPlan(rank, world, LAYERS, KV_HEADS, 1, "heads")
+    S = plan.n_local  # streams on this rank (head sharding: 8/N KV heads x 32 layers)
 
     cfg = T.TierConfig(hbm_budget_bytes=L_FAST * 2 * D * 2, d_k=D, d_v=D, bytes_full_precision=2,
                        block_size=B, key_bits=8, value_bits=4, fetch_fraction=FRAC)
@@ -238,13 +238,12 @@ def run_ours(args):
     ks = [torch.randn(S, D, device=dev, generator=gen).half() for _ in range(NPOOL)]
     vs = [torch.randn(S, D, device=dev, generator=gen).half() for _ in range(NPOOL)]
     out = torch.empty(S, G, D, device=dev)
-    gathered = torch.empty(world * S, G, D, device=dev) if world > 1 else None
 
     def step(i):
         eng.decode_step_device(qs[i % NPOOL].data_ptr(), ks[i % NPOOL].data_ptr(),
                                vs[i % NPOOL].data_ptr(), out.data_ptr(), dtype=1)
-        if world > 1:  # per-head outputs -> every rank (NVLink, NCCL)
-            dist.all_gather_into_tensor(gathered, out)
+        if plan.needs_gather:  # per-head outputs -> every rank (NVLink, NCCL)
+            gather_outputs(out, plan)
 
     def barrier():
         if world > 1:
@@ -284,12 +283,8 @@ def run_ours(args):
     t_e2e0 = time.perf_counter()
     for i in range(args.steps):
         r = eng.decode_step(hq[i % NPOOL], hk[i % NPOOL], hv[i % NPOOL])
-        if world > 1:
-            o = torch.from_numpy(r.output).to(dev)
-            g_ = torch.empty(world * S, G, D, device=dev)
-            dist.all_gather_into_tensor(g_, o)
-            _ = g_.cpu()
-            d2h_step = world * S * G * D * 4
+        if plan.needs_gather:
+            _ = gather_outputs(torch.from_numpy(r.output).to(dev), plan).cpu()
     barrier()
     e2e_ms = (time.perf_counter() - t_e2e0) * 1000.0 / args.steps
 

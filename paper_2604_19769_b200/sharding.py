@@ -1,0 +1,74 @@
+"""Work partitioning across GPUs.
+
+Streams are independent in the reference (one Engine per KV stream,
+SPEC.md:113), so the decode path shards without any exchange inside
+attention:
+
+* head sharding (configs[3]): rank r of N owns KV heads [r*H/N, (r+1)*H/N) of
+  every layer; its slow-tier records live in its own pinned arena and cross
+  its own PCIe link.  The per-head outputs are all-gathered (NCCL over
+  NVLink) because the next layer's o_proj needs every head.
+* request sharding (configs[2] at N>1): rank r owns requests
+  [r*R/N, (r+1)*R/N); no collective at all.
+
+Global stream order is (request, layer, kv_head) row-major, matching the
+S = layers x kv_heads x requests streams of one handle.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    rank: int
+    world: int
+    layers: int
+    kv_heads: int
+    requests: int
+    mode: str  # "heads" | "requests"
+
+    def local_streams(self) -> List[int]:
+        """Global stream ids owned by this rank, in local handle order."""
+        L, H, R, N, r = self.layers, self.kv_heads, self.requests, self.world, self.rank
+        if self.mode == "heads":
+            if H % N:
+                raise ValueError(f"{N} ranks do not divide {H} KV heads")
+            h0, h1 = r * H // N, (r + 1) * H // N
+            return [(q * L + l) * H + h for q in range(R) for l in range(L) for h in range(h0, h1)]
+        if R % N:
+            raise ValueError(f"{N} ranks do not divide {R} requests")
+        q0, q1 = r * R // N, (r + 1) * R // N
+        return [(q * L + l) * H + h for q in range(q0, q1) for l in range(L) for h in range(H)]
+
+    @property
+    def n_local(self) -> int:
+        return self.layers * self.kv_heads * self.requests // self.world
+
+    @property
+    def needs_gather(self) -> bool:
+        return self.mode == "heads" and self.world > 1
+
+
+def gather_outputs(local_out, plan: ShardPlan, group=None):
+    """All-gather per-head outputs [n_local, G, d] into global stream order
+    [S, G, d] on every rank (head sharding).  Works on any torch.distributed
+    backend (NCCL on the GPU box, gloo in the CPU tests)."""
+    import torch
+    import torch.distributed as dist
+
+    N = plan.world
+    if N == 1:
+        return local_out
+    gathered = torch.empty((N * local_out.shape[0],) + tuple(local_out.shape[1:]),
+                           dtype=local_out.dtype, device=local_out.device)
+    dist.all_gather_into_tensor(gathered, local_out.contiguous(), group=group)
+    L, H, R = plan.layers, plan.kv_heads, plan.requests
+    G, d = local_out.shape[1], local_out.shape[2]
+    if plan.mode == "heads":
+        # [N][R][L][H/N][G][d] -> [R][L][N][H/N][G][d]: rank-major -> head-major
+        x = gathered.view(N, R, L, H // N, G, d).permute(1, 2, 0, 3, 4, 5)
+    else:
+        x = gathered.view(N, R // N, L, H, G, d)
+    return x.reshape(R * L * H, G, d)
