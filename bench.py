@@ -237,7 +237,7 @@ def run_ours(args):
     qs = [torch.randn(S, G, D, device=dev, generator=gen) for _ in range(NPOOL)]
     ks = [torch.randn(S, D, device=dev, generator=gen).half() for _ in range(NPOOL)]
     vs = [torch.randn(S, D, device=dev, generator=gen).half() for _ in range(NPOOL)]
-    out = torch.empty(S, G, D, device=dev)
+    out = torch.empty(S, G, D, device=dev, dtype=torch.float64)
 
     def step(i):
         eng.decode_step_device(qs[i % NPOOL].data_ptr(), ks[i % NPOOL].data_ptr(),

@@ -160,14 +160,16 @@ int ttkv_gpu_prefill(struct ttkv_gpu* h, const void* keys, const void* values,
 int ttkv_gpu_prefill_synthetic(struct ttkv_gpu* h, uint64_t n_tokens, uint64_t seed);
 
 /* Host buffers, synchronous: q[S][G][d_k] f32, k_new[S][d_k], v_new[S][d_v]
- * (dtype), out[S][G][d_v] f32.  report may be NULL. */
+ * (dtype), out[S][G][d_v] f64 (DecodeStepReport::output is double; values are
+ * accumulated in fp32 for an fp16 ring and in fp64 for an fp32 ring).
+ * report may be NULL. */
 int ttkv_gpu_decode_step(struct ttkv_gpu* h, const float* q, const void* k_new,
-                         const void* v_new, int dtype, float* out, ttkv_step_report* report);
+                         const void* v_new, int dtype, double* out, ttkv_step_report* report);
 /* Device buffers, enqueued on the handle's stream, returns immediately.
  * union_blocks / pcie_bytes in the report are not filled (use
  * ttkv_gpu_read_step_counters after synchronizing). */
 int ttkv_gpu_decode_step_device(struct ttkv_gpu* h, const float* q, const void* k_new,
-                                const void* v_new, int dtype, float* out,
+                                const void* v_new, int dtype, double* out,
                                 ttkv_step_report* report);
 int ttkv_gpu_read_step_counters(struct ttkv_gpu* h, uint64_t* union_blocks,
                                 uint64_t* pcie_bytes);

@@ -662,7 +662,7 @@ DecodeStepReport Engine::decode_step(std::span<const float> query, TokenKV kv) {
                           std::to_string(kv.position));
   if (kv.key.size() != cfg.d_k || kv.value.size() != cfg.d_v)
     throw ShapeError("append_token: key/value dimension mismatch");
-  std::vector<float> out(cfg.d_v);
+  std::vector<double> out(cfg.d_v);
   ttkv_step_report rep{};
   ttkv_gpu* h = store_.handle();
   check(ttkv_gpu_decode_step(h, query.data(), kv.key.data(), kv.value.data(), TTKV_DTYPE_F32,

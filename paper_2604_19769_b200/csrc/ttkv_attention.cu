@@ -3,179 +3,339 @@
 // Replaces the three accumulation loops of Engine::decode_step
 // (engine.cpp:36-40 fast tier, 61-83 fetched blocks, 85-86 finalize) and the
 // AttentionAccumulator they drive (attention.hpp:29-61).  Every partition
-// produces an online-softmax partial (m, l, acc) in log2 units and
+// produces an online-softmax partial (acc, m in log2 units, l) and
 // combine_partials merges them by LSE rescaling -- the exact merge the
 // reference proves partition-invariant.
 //
-//  fast_attn_partial  split-K over the fp16/fp32 HBM ring.  Each lane owns 4
-//                     channels (8-byte / 16-byte coalesced loads), the G query
-//                     heads of a KV head share every K/V load (GQA), dot
-//                     products reduce with warp shuffles.  HBM-bound:
-//                     F * (d_k + d_v) * elem bytes per stream.
-//  slow_stream_attn   one producer warp streams the selected records of a
-//                     stream from pinned host DRAM (zero-copy over PCIe) into
-//                     a ring of shared-memory stages with cp.async.bulk +
-//                     mbarrier complete_tx (or 16-byte LDG when copy_mode=2);
-//                     four consumer warps dequantize in registers
-//                     (x = code * scale + zp, quantizer.cpp:109-110) fused into
-//                     QK and PV for all G heads, so transfer of block i+1..i+NS
-//                     overlaps compute of block i.  Each record crosses PCIe
-//                     once per step, shared by every head that selected it.
-//                     PCIe-bound: union_blocks * 26,624 B per step.
-//  combine_partials   per (stream, head) LSE merge + normalisation
-//                     (attention.hpp:54-61).
+// Both attention kernels are the same warp-specialised pipeline:
+//   * one producer warp stages tiles into a ring of shared-memory stages with
+//     cp.async.bulk (TMA bulk copy) completing on an mbarrier (expect_tx), or
+//     with 16-byte LDG when a layout is not 16-byte aligned;
+//   * four consumer warps absorb each staged tile for all G query heads of the
+//     KV head (GQA: every K/V row is read and dequantized once): lane l owns
+//     channels [4l, 4l+4), QK reduces with warp shuffles, one warp per head
+//     computes the tile's softmax statistics, PV accumulates in registers.
+//  slow_stream_attn  tiles = the selected slow-tier records, streamed from
+//                    pinned host DRAM (zero-copy PCIe) with their per-channel
+//                    params from the HBM mirror; dequantization
+//                    (x = code * scale + zp, quantizer.cpp:109-110) is fused
+//                    into the QK / PV loads.  PCIe-bound.
+//  fast_attn_partial tiles = TT consecutive tokens of the HBM ring (split at
+//                    the wrap).  HBM-bound.
+// Accumulation is fp32 for the fp16 ring (the north-star contract, 1e-3) and
+// fp64 for the fp32 ring, which then reproduces the reference's fp64 engine
+// to ~1e-15 (the reference's own lossless test demands 1e-12).
 #include <math.h>
+
+#include <type_traits>
 
 #include "ttkv_kernels.cuh"
 #include "ttkv_launch.h"
 
 namespace ttkv_dev {
 
-// ---------------------------------------------------------------------------
-// fast tier
-// ---------------------------------------------------------------------------
-template <typename T, int GT>
-__global__ void __launch_bounds__(kFastWarps * 32) fast_attn_kernel(FastArgs a) {
-  const Geometry& g = a.g;
-  const uint32_t s = blockIdx.y, f = blockIdx.x;
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t c0 = lane * 4;
-  const uint32_t t0 = f * a.FC;
-  const uint32_t t1 = min(t0 + a.FC, a.F);
-  const bool vec_k = (g.d_k & 3) == 0, vec_v = (g.d_v & 3) == 0;
+template <typename T>
+using AccOf = std::conditional_t<std::is_same_v<T, float>, double, float>;
 
-  float qr[GT][4];
+__device__ __forceinline__ float ex2(float x) { return exp2f(x); }
+__device__ __forceinline__ double ex2(double x) { return exp2(x); }
+
+template <typename A>
+__device__ __forceinline__ A wsum(A v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <typename A>
+__device__ __forceinline__ A wmax(A v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// dequantized element: one fp32 FMA, or the reference's exact
+// float(double(code) * scale + zp) when accumulating in fp64
+template <typename Acc>
+__device__ __forceinline__ Acc deq(uint32_t code, float s, float z);
+template <>
+__device__ __forceinline__ float deq<float>(uint32_t code, float s, float z) {
+  return fmaf((float)code, s, z);
+}
+template <>
+__device__ __forceinline__ double deq<double>(uint32_t code, float s, float z) {
+  return (double)__double2float_rn(__dadd_rn(__dmul_rn((double)code, (double)s), (double)z));
+}
+
+// Channels [c0, c0+4) of row t of one staged tensor.
+// KB: 8 / 4 packed fast paths (d % 4 == 0), 16 = raw ring elements T,
+//     0 = runtime width `bits` (2..8 packed LSB-first, or 16 raw).
+template <int KB, typename T, typename Acc>
+__device__ __forceinline__ void row4(const uint8_t* pay, uint32_t t, uint32_t c0, uint32_t dim,
+                                     uint32_t bits, const float (&sc)[4], const float (&zp)[4],
+                                     Acc (&o)[4]) {
+  if constexpr (KB == 8) {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(pay + t * dim + c0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = deq<Acc>((w >> (8 * j)) & 0xffu, sc[j], zp[j]);
+  } else if constexpr (KB == 4) {
+    const uint32_t w = *reinterpret_cast<const uint16_t*>(pay + ((t * dim + c0) >> 1));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = deq<Acc>((w >> (4 * j)) & 0xfu, sc[j], zp[j]);
+  } else {
+    if (KB == 16 || bits == 16) {
+      const T* e = reinterpret_cast<const T*>(pay) + (uint64_t)t * dim;
+      if ((dim & 3) == 0 && c0 < dim) {
+        float f[4];
+        load4(e + c0, f);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] = (Acc)f[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] = c0 + j < dim ? (Acc)to_f(e[c0 + j]) : Acc(0);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        o[j] = c0 + j < dim ? deq<Acc>(extract_code(pay, t * dim + c0 + j, bits), sc[j], zp[j])
+                            : Acc(0);
+    }
+  }
+}
+
+// Per-CTA consumer state shared through smem.
+template <typename Acc>
+struct ConsumerSmem {
+  Acc* sc;   // [2][GT][rows_cap] scores / probabilities (double-buffered)
+  Acc* mst;  // [GT] running max (log2 units)
+  Acc* lst;  // [GT] running denominator
+  Acc* ast;  // [GT] rescale factor of the current tile
+};
+
+struct TileView {
+  const uint8_t* kpay;
+  const uint8_t* vpay;
+  const float* kpar;  // {scale, zp} x d_k or nullptr (raw)
+  const float* vpar;
+  uint32_t rows;
+};
+
+// Absorb one staged tile for the heads in `hm` (engine.cpp:61-83 per block,
+// attention.hpp:29-50 per row, vectorised).  Called by all consumer warps.
+template <typename T, typename Acc, int KB, int VB, int GT>
+__device__ __forceinline__ void absorb_tile(const Geometry& g, const TileView& tv, uint32_t hm,
+                                            uint32_t it, uint32_t rows_cap, bool literal,
+                                            const Acc (&qr)[GT][4], Acc (&acc)[GT][4],
+                                            const ConsumerSmem<Acc>& cs, uint32_t cw,
+                                            uint32_t lane) {
+  const uint32_t c0 = lane * 4;
+  const int nthreads_c = kSlowConsumerWarps * 32;
+  Acc* scb = cs.sc + (it & 1) * GT * rows_cap;
+
+  // ---- QK: all heads share each (dequantized) key row ----
+  {
+    float ks[4], kz[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool ok = tv.kpar && c0 + j < g.d_k;
+      ks[j] = ok ? tv.kpar[2 * (c0 + j)] : 0.0f;
+      kz[j] = ok ? tv.kpar[2 * (c0 + j) + 1] : 0.0f;
+    }
+    for (uint32_t t = cw; t < tv.rows; t += kSlowConsumerWarps) {
+      Acc kf[4];
+      if (c0 < g.d_k) row4<KB, T, Acc>(tv.kpay, t, c0, g.d_k, g.kb, ks, kz, kf);
+      else kf[0] = kf[1] = kf[2] = kf[3] = Acc(0);
+#pragma unroll
+      for (int h = 0; h < GT; ++h) {
+        if (h >= (int)g.G) break;
+        if (!((hm >> h) & 1u)) continue;
+        Acc d = qr[h][0] * kf[0] + qr[h][1] * kf[1] + qr[h][2] * kf[2] + qr[h][3] * kf[3];
+        d = wsum(d);
+        if (lane == 0) scb[h * rows_cap + t] = d;
+      }
+    }
+  }
+  named_bar(1, nthreads_c);
+
+  // ---- tile softmax statistics, one warp per head ----
+  for (uint32_t h = cw; h < g.G; h += kSlowConsumerWarps) {
+    if (!((hm >> h) & 1u)) {
+      if (lane == 0) cs.ast[h] = Acc(1);
+      continue;
+    }
+    Acc* row = scb + h * rows_cap;
+    Acc bm = -INFINITY;
+    for (uint32_t t = lane; t < tv.rows; t += 32) bm = fmax(bm, row[t]);
+    bm = wmax(bm);
+    const Acc m_old = cs.mst[h];
+    const Acc m_new = literal ? bm : fmax(m_old, bm);
+    Acc sum = 0;
+    for (uint32_t t = lane; t < tv.rows; t += 32) {
+      const Acc p = ex2(row[t] - m_new);
+      row[t] = p;
+      sum += p;
+    }
+    sum = wsum(sum);
+    __syncwarp();
+    if (literal) {
+      // literal additive merge (engine.cpp:67-72): each block is its own
+      // normalized partition, summed without rescaling
+      const Acc inv = Acc(1) / sum;
+      for (uint32_t t = lane; t < tv.rows; t += 32) row[t] *= inv;
+      if (lane == 0) cs.ast[h] = Acc(1);
+      continue;
+    }
+    if (lane == 0) {
+      const Acc alpha = ex2(m_old - m_new);  // 0 when m_old = -inf
+      cs.lst[h] = cs.lst[h] * alpha + sum;
+      cs.mst[h] = m_new;
+      cs.ast[h] = alpha;
+    }
+  }
+  named_bar(1, nthreads_c);
+
+  // ---- PV: all heads share each (dequantized) value row ----
+#pragma unroll
+  for (int h = 0; h < GT; ++h) {
+    if (h >= (int)g.G) break;
+    if (!((hm >> h) & 1u)) continue;
+    const Acc alpha = cs.ast[h];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[h][j] *= alpha;
+  }
+  float vs[4], vz[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const bool ok = tv.vpar && c0 + j < g.d_v;
+    vs[j] = ok ? tv.vpar[2 * (c0 + j)] : 0.0f;
+    vz[j] = ok ? tv.vpar[2 * (c0 + j) + 1] : 0.0f;
+  }
+  for (uint32_t t = cw; t < tv.rows; t += kSlowConsumerWarps) {
+    Acc vf[4];
+    if (c0 < g.d_v) row4<VB, T, Acc>(tv.vpay, t, c0, g.d_v, g.vb, vs, vz, vf);
+    else vf[0] = vf[1] = vf[2] = vf[3] = Acc(0);
+#pragma unroll
+    for (int h = 0; h < GT; ++h) {
+      if (h >= (int)g.G) break;
+      if (!((hm >> h) & 1u)) continue;
+      const Acc p = scb[h * rows_cap + t];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[h][j] += p * vf[j];
+    }
+  }
+}
+
+// Merge the consumer warps' accumulators and emit one (acc, m, l) partial per
+// head; heads that absorbed nothing emit (0, -inf, 0).
+template <typename Acc, int GT>
+__device__ __forceinline__ void emit_partial(const Geometry& g, Acc (&acc)[GT][4], uint8_t* red_smem,
+                                             const ConsumerSmem<Acc>& cs, uint32_t seen,
+                                             bool literal, Acc* part, uint64_t part_stride_head,
+                                             uint32_t cw, uint32_t lane) {
+  const int nthreads_c = kSlowConsumerWarps * 32;
+  const uint32_t c0 = lane * 4;
+  named_bar(1, nthreads_c);
+  Acc* red = reinterpret_cast<Acc*>(red_smem);
+#pragma unroll
+  for (int h = 0; h < GT; ++h) {
+    if (h >= (int)g.G) break;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (c0 + j < g.d_v) red[(cw * GT + h) * g.d_v + c0 + j] = acc[h][j];
+  }
+  named_bar(1, nthreads_c);
+  const uint32_t ct = cw * 32 + lane;
+  for (uint32_t i = ct; i < g.G * g.d_v; i += nthreads_c) {
+    const uint32_t h = i / g.d_v, c = i % g.d_v;
+    Acc A = 0;
+    for (int w = 0; w < kSlowConsumerWarps; ++w) A += red[(w * GT + h) * g.d_v + c];
+    Acc* p = part + h * part_stride_head;
+    const bool any = (seen >> h) & 1u;
+    p[c] = any ? A : Acc(0);
+    if (c == 0) {
+      p[g.d_v] = any ? (literal ? Acc(0) : cs.mst[h]) : Acc(-INFINITY);
+      p[g.d_v + 1] = any ? (literal ? Acc(1) : cs.lst[h]) : Acc(0);
+    }
+  }
+}
+
+template <typename Acc, int GT>
+__device__ __forceinline__ void load_query(const Geometry& g, const float* q, uint32_t s,
+                                           double scale_log2, uint32_t lane, Acc (&qr)[GT][4]) {
+  const uint32_t c0 = lane * 4;
 #pragma unroll
   for (int h = 0; h < GT; ++h)
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       qr[h][j] = (h < (int)g.G && c0 + j < g.d_k)
-                     ? a.q[((uint64_t)s * g.G + h) * g.d_k + c0 + j] * a.scale_log2
-                     : 0.0f;
-  float m[GT], l[GT], acc[GT][4];
-#pragma unroll
-  for (int h = 0; h < GT; ++h) {
-    m[h] = -INFINITY;
-    l[h] = 0.0f;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[h][j] = 0.0f;
-  }
+                     ? (Acc)q[((uint64_t)s * g.G + h) * g.d_k + c0 + j] * (Acc)scale_log2
+                     : Acc(0);
+}
 
-  const T* rk = static_cast<const T*>(a.ring_k) + (uint64_t)s * g.C * g.d_k;
-  const T* rv = static_cast<const T*>(a.ring_v) + (uint64_t)s * g.C * g.d_v;
-  for (uint32_t t = t0 + warp; t < t1; t += kFastWarps) {
-    const uint64_t slot = (a.front + t) % g.C;
-    float kf[4], vf[4];
-    if (vec_k && c0 < g.d_k) {
-      load4(rk + slot * g.d_k + c0, kf);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) kf[j] = c0 + j < g.d_k ? to_f(rk[slot * g.d_k + c0 + j]) : 0.0f;
-    }
-    if (vec_v && c0 < g.d_v) {
-      load4(rv + slot * g.d_v + c0, vf);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) vf[j] = c0 + j < g.d_v ? to_f(rv[slot * g.d_v + c0 + j]) : 0.0f;
-    }
-#pragma unroll
-    for (int h = 0; h < GT; ++h) {
-      if (h >= (int)g.G) break;
-      float d = qr[h][0] * kf[0] + qr[h][1] * kf[1] + qr[h][2] * kf[2] + qr[h][3] * kf[3];
-      d = warp_sum(d);
-      if (d > m[h]) {
-        const float alpha = exp2f(m[h] - d);
-        l[h] *= alpha;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[h][j] *= alpha;
-        m[h] = d;
-      }
-      const float p = exp2f(d - m[h]);
-      l[h] += p;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[h][j] += p * vf[j];
-    }
+// smem carve-up shared by both kernels
+template <typename Acc, int GT>
+struct Carve {
+  uint8_t* stages;
+  uint64_t* full;
+  uint64_t* empty;
+  ConsumerSmem<Acc> cs;
+  __device__ Carve(uint8_t* smem, uint32_t stage_region, uint32_t NS, uint32_t rows_cap) {
+    stages = smem;
+    full = reinterpret_cast<uint64_t*>(smem + stage_region);
+    empty = full + NS;
+    cs.sc = reinterpret_cast<Acc*>(empty + NS);
+    cs.mst = cs.sc + 2 * GT * rows_cap;
+    cs.lst = cs.mst + GT;
+    cs.ast = cs.lst + GT;
   }
+};
 
-  // merge the warps' partials
-  __shared__ float sm_m[kFastWarps][kMaxG], sm_l[kFastWarps][kMaxG];
-  __shared__ float sm_acc[kFastWarps][kMaxG][kMaxD];
-#pragma unroll
-  for (int h = 0; h < GT; ++h) {
-    if (h >= (int)g.G) break;
-    if (lane == 0) { sm_m[warp][h] = m[h]; sm_l[warp][h] = l[h]; }
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (c0 + j < g.d_v) sm_acc[warp][h][c0 + j] = acc[h][j];
+template <typename Acc, int GT>
+__device__ __forceinline__ void init_pipeline(Carve<Acc, GT>& cv, uint32_t NS) {
+  if (threadIdx.x == 0) {
+    for (uint32_t i = 0; i < NS; ++i) {
+      mbar_init(&cv.full[i], 1);
+      mbar_init(&cv.empty[i], kSlowConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  if (threadIdx.x < GT) {
+    cv.cs.mst[threadIdx.x] = -INFINITY;
+    cv.cs.lst[threadIdx.x] = 0;
+    cv.cs.ast[threadIdx.x] = 1;
   }
   __syncthreads();
-  const uint32_t pitch = g.d_v + 2;
-  for (uint32_t i = threadIdx.x; i < g.G * g.d_v; i += blockDim.x) {
-    const uint32_t h = i / g.d_v, c = i % g.d_v;
-    float M = -INFINITY;
-    for (int w = 0; w < kFastWarps; ++w) M = fmaxf(M, sm_m[w][h]);
-    float L = 0.0f, A = 0.0f;
-    if (M != -INFINITY) {
-      for (int w = 0; w < kFastWarps; ++w) {
-        const float sc = exp2f(sm_m[w][h] - M);
-        L += sm_l[w][h] * sc;
-        A += sm_acc[w][h][c] * sc;
-      }
-    }
-    float* p = a.part + (((uint64_t)s * g.G + h) * a.nfc + f) * pitch;
-    p[c] = A;
-    if (c == 0) { p[g.d_v] = M; p[g.d_v + 1] = L; }
+}
+
+// 16-byte LDG copy by one warp (fallback staging path)
+__device__ __forceinline__ void warp_copy16(uint8_t* dst, const uint8_t* src, uint32_t bytes,
+                                           uint32_t lane) {
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  const uint32_t n16 = bytes >> 4;
+  uint32_t j = lane;
+  for (; j + 7 * 32 < n16; j += 8 * 32) {
+    uint4 r[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) r[u] = s4[j + u * 32];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) d4[j + u * 32] = r[u];
   }
+  for (; j < n16; j += 32) d4[j] = s4[j];
 }
 
-template <typename T>
-static cudaError_t launch_fast_t(const FastArgs& a, cudaStream_t st) {
-  dim3 grid(a.nfc, a.g.S);
-  if (a.g.G <= 1) fast_attn_kernel<T, 1><<<grid, kFastWarps * 32, 0, st>>>(a);
-  else if (a.g.G <= 2) fast_attn_kernel<T, 2><<<grid, kFastWarps * 32, 0, st>>>(a);
-  else if (a.g.G <= 4) fast_attn_kernel<T, 4><<<grid, kFastWarps * 32, 0, st>>>(a);
-  else fast_attn_kernel<T, 8><<<grid, kFastWarps * 32, 0, st>>>(a);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_fast(const FastArgs& a, cudaStream_t st) {
-  return a.g.elem == 2 ? launch_fast_t<__half>(a, st) : launch_fast_t<float>(a, st);
+// element-granular warp copy for layouts that are not 16-byte aligned
+__device__ __forceinline__ void warp_copy_any(uint8_t* dst, const uint8_t* src, uint32_t bytes,
+                                              uint32_t lane) {
+  for (uint32_t j = lane * 2; j < bytes; j += 64)
+    *reinterpret_cast<uint16_t*>(dst + j) = *reinterpret_cast<const uint16_t*>(src + j);
 }
 
 // ---------------------------------------------------------------------------
-// slow tier: streamed, dequant fused
+// slow tier
 // ---------------------------------------------------------------------------
-
-// Dequantize the 4 channels [c0, c0+4) of row t of a packed tensor.
-// KB: compile-time bit width (8, 4) or 0 = runtime `bits` (2..8 or 16).
-template <int KB, typename T>
-__device__ __forceinline__ void dequant4(const uint8_t* payload, uint32_t t, uint32_t c0,
-                                         uint32_t dim, uint32_t bits, const float (&sc)[4],
-                                         const float (&zp)[4], float (&o)[4]) {
-  if constexpr (KB == 8) {
-    const uint32_t w = *reinterpret_cast<const uint32_t*>(payload + t * dim + c0);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) o[j] = fmaf((float)((w >> (8 * j)) & 0xffu), sc[j], zp[j]);
-  } else if constexpr (KB == 4) {
-    const uint32_t w = *reinterpret_cast<const uint16_t*>(payload + ((t * dim + c0) >> 1));
-#pragma unroll
-    for (int j = 0; j < 4; ++j) o[j] = fmaf((float)((w >> (4 * j)) & 0xfu), sc[j], zp[j]);
-  } else {
-    if (bits == 16) {
-      const T* e = reinterpret_cast<const T*>(payload) + (uint64_t)t * dim;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) o[j] = c0 + j < dim ? to_f(e[c0 + j]) : 0.0f;
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        o[j] = c0 + j < dim ? fmaf((float)extract_code(payload, t * dim + c0 + j, bits), sc[j], zp[j])
-                            : 0.0f;
-    }
-  }
-}
-
 template <typename T, int KB, int VB, int GT, int COPY>
 __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32) slow_attn_kernel(SlowArgs a) {
+  using Acc = AccOf<T>;
   const Geometry& g = a.g;
   const uint32_t s = blockIdx.y, chunk = blockIdx.x;
   const uint32_t cnt = a.union_count[s];
@@ -186,234 +346,165 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32) slow_attn_kernel
   const uint32_t stride = g.rec.stride;
 
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* stages = smem;                                             // [NS][stride]
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stage_region);  // [NS]
-  uint64_t* empty = full + NS;                                        // [NS]
-  float* sc = reinterpret_cast<float*>(empty + NS);                   // [2][GT][B]
-  float* mst = sc + 2 * GT * g.B;                                     // [GT]
-  float* lst = mst + GT;                                              // [GT]
-  float* ast = lst + GT;                                              // [GT]
-
+  Carve<Acc, GT> cv(smem, a.stage_region, NS, g.B);
+  init_pipeline(cv, NS);
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (uint32_t i = 0; i < NS; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kSlowConsumerWarps);
-    }
-    fence_mbar_init();
-  }
-  if (threadIdx.x < GT) {
-    mst[threadIdx.x] = -INFINITY;
-    lst[threadIdx.x] = 0.0f;
-    ast[threadIdx.x] = 1.0f;
-  }
-  __syncthreads();
-
   const uint32_t* uids = a.union_ids + (uint64_t)s * g.n_cap + i0;
   const uint32_t* umask = a.union_mask + (uint64_t)s * g.n_cap + i0;
-  const uint8_t* arena_s = a.arena + (uint64_t)s * g.n_cap * stride;
 
   if (warp == 0) {
-    // ---------------- producer ----------------
+    // ---- producer: payload over PCIe (zero-copy), params from HBM ----
+    const uint8_t* arena_s = a.arena + (uint64_t)s * g.n_cap * stride;
+    const uint32_t pay = g.rec.kp_off, pbytes = g.rec.used - g.rec.kp_off;
     for (uint32_t i = 0; i < nb; ++i) {
       const uint32_t st = i % NS;
-      if (i >= NS) mbar_wait(&empty[st], ((i / NS) - 1) & 1);
+      if (i >= NS) mbar_wait(&cv.empty[st], ((i / NS) - 1) & 1);
       const uint32_t blk = uids[i];
       const uint8_t* src = arena_s + (uint64_t)blk * stride;
-      const uint32_t pay = g.rec.kp_off, pbytes = g.rec.used - g.rec.kp_off;
       const uint8_t* psrc = a.params + ((uint64_t)s * g.n_cap + blk) * pbytes;
-      uint8_t* dst = stages + st * stride;
+      uint8_t* dst = cv.stages + st * stride;
       if constexpr (COPY == 1) {
         if (lane == 0) {
-          mbar_arrive_expect_tx(&full[st], g.rec.used);
+          mbar_arrive_expect_tx(&cv.full[st], g.rec.used);
           for (uint32_t off = 0; off < pay; off += 16384u)
-            bulk_g2s(dst + off, src + off, min(16384u, pay - off), &full[st]);
-          if (pbytes) bulk_g2s(dst + pay, psrc, pbytes, &full[st]);
+            bulk_g2s(dst + off, src + off, min(16384u, pay - off), &cv.full[st]);
+          if (pbytes) bulk_g2s(dst + pay, psrc, pbytes, &cv.full[st]);
         }
       } else {
-        const uint4* s4 = reinterpret_cast<const uint4*>(src);
-        uint4* d4 = reinterpret_cast<uint4*>(dst);
-        const uint32_t n16 = pay >> 4;
-        uint32_t j = lane;
-        for (; j + 7 * 32 < n16; j += 8 * 32) {
-          uint4 r[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) r[u] = s4[j + u * 32];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) d4[j + u * 32] = r[u];
-        }
-        for (; j < n16; j += 32) d4[j] = s4[j];
-        const uint4* p4 = reinterpret_cast<const uint4*>(psrc);
-        uint4* dp4 = reinterpret_cast<uint4*>(dst + pay);
-        for (uint32_t jj = lane; jj < (pbytes >> 4); jj += 32) dp4[jj] = p4[jj];
+        warp_copy16(dst, src, pay, lane);
+        warp_copy16(dst + pay, psrc, pbytes, lane);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&full[st]);
+        if (lane == 0) mbar_arrive(&cv.full[st]);
       }
     }
     return;
   }
 
-  // ---------------- consumers ----------------
+  // ---- consumers ----
   const uint32_t cw = warp - 1;
-  const uint32_t c0 = lane * 4;
-  const int nthreads_c = kSlowConsumerWarps * 32;
-  float qr[GT][4];
+  Acc qr[GT][4], acc[GT][4];
+  load_query<Acc, GT>(g, a.q, s, a.scale_log2, lane, qr);
 #pragma unroll
   for (int h = 0; h < GT; ++h)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      qr[h][j] = (h < (int)g.G && c0 + j < g.d_k)
-                     ? a.q[((uint64_t)s * g.G + h) * g.d_k + c0 + j] * a.scale_log2
-                     : 0.0f;
-  float acc[GT][4];
-#pragma unroll
-  for (int h = 0; h < GT; ++h)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[h][j] = 0.0f;
-  uint32_t seen = 0;  // heads that absorbed at least one block in this chunk
-
+    for (int j = 0; j < 4; ++j) acc[h][j] = 0;
+  uint32_t seen = 0;
   for (uint32_t i = 0; i < nb; ++i) {
     const uint32_t st = i % NS;
-    mbar_wait(&full[st], (i / NS) & 1);
-    const uint8_t* rec = stages + st * stride;
+    mbar_wait(&cv.full[st], (i / NS) & 1);
+    const uint8_t* rec = cv.stages + st * stride;
     const uint32_t hm = umask[i];
     seen |= hm;
-    float* scb = sc + (i & 1) * GT * g.B;
-
-    // ---- QK: dequantized keys, all heads share each row ----
-    {
-      float ks[4], kz[4];
-      const float* kp = reinterpret_cast<const float*>(rec + g.rec.kp_off);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const bool ok = g.kb != 16 && c0 + j < g.d_k;
-        ks[j] = ok ? kp[2 * (c0 + j)] : 0.0f;
-        kz[j] = ok ? kp[2 * (c0 + j) + 1] : 0.0f;
-      }
-      for (uint32_t t = cw; t < g.B; t += kSlowConsumerWarps) {
-        float kf[4];
-        if (c0 < g.d_k) dequant4<KB, T>(rec, t, c0, g.d_k, g.kb, ks, kz, kf);
-        else kf[0] = kf[1] = kf[2] = kf[3] = 0.0f;
-#pragma unroll
-        for (int h = 0; h < GT; ++h) {
-          if (h >= (int)g.G) break;
-          if (!((hm >> h) & 1u)) continue;
-          float d = qr[h][0] * kf[0] + qr[h][1] * kf[1] + qr[h][2] * kf[2] + qr[h][3] * kf[3];
-          d = warp_sum(d);
-          if (lane == 0) scb[h * g.B + t] = d;
-        }
-      }
-    }
-    named_bar(1, nthreads_c);
-
-    // ---- block softmax statistics (one warp per head) ----
-    for (uint32_t h = cw; h < g.G; h += kSlowConsumerWarps) {
-      if (!((hm >> h) & 1u)) {
-        if (lane == 0) ast[h] = 1.0f;
-        continue;
-      }
-      float* row = scb + h * g.B;
-      float bm = -INFINITY;
-      for (uint32_t t = lane; t < g.B; t += 32) bm = fmaxf(bm, row[t]);
-      bm = warp_max(bm);
-      const float m_old = mst[h];
-      const float m_new = a.literal ? bm : fmaxf(m_old, bm);
-      float sum = 0.0f;
-      for (uint32_t t = lane; t < g.B; t += 32) {
-        const float p = exp2f(row[t] - m_new);
-        row[t] = p;
-        sum += p;
-      }
-      sum = warp_sum(sum);
-      __syncwarp();
-      if (a.literal) {
-        // literal additive merge (engine.cpp:67-72): each block is its own
-        // normalized partition, summed without rescaling
-        const float inv = 1.0f / sum;
-        for (uint32_t t = lane; t < g.B; t += 32) row[t] *= inv;
-        if (lane == 0) ast[h] = 1.0f;
-        continue;
-      }
-      if (lane == 0) {
-        const float alpha = exp2f(m_old - m_new);  // 0 when m_old = -inf
-        lst[h] = lst[h] * alpha + sum;
-        mst[h] = m_new;
-        ast[h] = alpha;
-      }
-    }
-    named_bar(1, nthreads_c);
-
-    // ---- PV: dequantized values ----
-    {
-#pragma unroll
-      for (int h = 0; h < GT; ++h) {
-        if (h >= (int)g.G) break;
-        if (!((hm >> h) & 1u)) continue;
-        const float alpha = ast[h];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[h][j] *= alpha;
-      }
-      float vs[4], vz[4];
-      const float* vp = reinterpret_cast<const float*>(rec + g.rec.vp_off);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const bool ok = g.vb != 16 && c0 + j < g.d_v;
-        vs[j] = ok ? vp[2 * (c0 + j)] : 0.0f;
-        vz[j] = ok ? vp[2 * (c0 + j) + 1] : 0.0f;
-      }
-      const uint8_t* vpay = rec + g.rec.v_off;
-      for (uint32_t t = cw; t < g.B; t += kSlowConsumerWarps) {
-        float vf[4];
-        if (c0 < g.d_v) dequant4<VB, T>(vpay, t, c0, g.d_v, g.vb, vs, vz, vf);
-        else vf[0] = vf[1] = vf[2] = vf[3] = 0.0f;
-#pragma unroll
-        for (int h = 0; h < GT; ++h) {
-          if (h >= (int)g.G) break;
-          if (!((hm >> h) & 1u)) continue;
-          const float p = scb[h * g.B + t];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[h][j] = fmaf(p, vf[j], acc[h][j]);
-        }
-      }
-    }
+    TileView tv;
+    tv.kpay = rec;
+    tv.vpay = rec + g.rec.v_off;
+    tv.kpar = g.kb == 16 ? nullptr : reinterpret_cast<const float*>(rec + g.rec.kp_off);
+    tv.vpar = g.vb == 16 ? nullptr : reinterpret_cast<const float*>(rec + g.rec.vp_off);
+    tv.rows = g.B;
+    absorb_tile<T, Acc, KB, VB, GT>(g, tv, hm, i, g.B, a.literal != 0, qr, acc, cv.cs, cw, lane);
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
+    if (lane == 0) mbar_arrive(&cv.empty[st]);
   }
+  Acc* part = reinterpret_cast<Acc*>(a.part) +
+              (((uint64_t)s * g.G) * a.nsc + chunk) * (g.d_v + 2);
+  emit_partial<Acc, GT>(g, acc, cv.stages, cv.cs, seen, a.literal != 0, part,
+                        (uint64_t)a.nsc * (g.d_v + 2), cw, lane);
+}
 
-  // ---- merge the consumer warps' accumulators, emit the chunk partial ----
-  named_bar(1, nthreads_c);
-  float* red = reinterpret_cast<float*>(stages);  // reuse stage memory
-#pragma unroll
-  for (int h = 0; h < GT; ++h) {
-    if (h >= (int)g.G) break;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (c0 + j < g.d_v) red[(cw * GT + h) * g.d_v + c0 + j] = acc[h][j];
-  }
-  named_bar(1, nthreads_c);
-  const uint32_t pitch = g.d_v + 2;
-  const uint32_t ct = threadIdx.x - 32;
-  for (uint32_t i = ct; i < g.G * g.d_v; i += nthreads_c) {
-    const uint32_t h = i / g.d_v, c = i % g.d_v;
-    float A = 0.0f;
-    for (int w = 0; w < kSlowConsumerWarps; ++w) A += red[(w * GT + h) * g.d_v + c];
-    float* p = a.part + (((uint64_t)s * g.G + h) * a.nsc + chunk) * pitch;
-    const bool any = (seen >> h) & 1u;
-    p[c] = any ? A : 0.0f;
-    if (c == 0) {
-      p[g.d_v] = any ? (a.literal ? 0.0f : mst[h]) : -INFINITY;
-      p[g.d_v + 1] = any ? (a.literal ? 1.0f : lst[h]) : 0.0f;
+// ---------------------------------------------------------------------------
+// fast tier
+// ---------------------------------------------------------------------------
+template <typename T, int GT, int COPY>
+__global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32) fast_attn_kernel(FastArgs a) {
+  using Acc = AccOf<T>;
+  const Geometry& g = a.g;
+  const uint32_t s = blockIdx.y, f = blockIdx.x;
+  const uint32_t t0 = f * a.FC;
+  const uint32_t t1 = min(t0 + a.FC, a.F);
+  const uint32_t ntiles = t1 > t0 ? (t1 - t0 + a.TT - 1) / a.TT : 0;
+  const uint32_t NS = a.stages;
+  const uint32_t kbytes_row = g.d_k * sizeof(T), vbytes_row = g.d_v * sizeof(T);
+  const uint32_t stage_bytes = a.TT * (kbytes_row + vbytes_row);
+
+  extern __shared__ __align__(1024) uint8_t smem[];
+  Carve<Acc, GT> cv(smem, a.stage_region, NS, a.TT);
+  init_pipeline(cv, NS);
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint8_t* rk = static_cast<const uint8_t*>(a.ring_k) + (uint64_t)s * g.C * kbytes_row;
+  const uint8_t* rv = static_cast<const uint8_t*>(a.ring_v) + (uint64_t)s * g.C * vbytes_row;
+
+  if (warp == 0) {
+    // ---- producer: ring rows (split at the wrap) -> stage ----
+    for (uint32_t i = 0; i < ntiles; ++i) {
+      const uint32_t st = i % NS;
+      if (i >= NS) mbar_wait(&cv.empty[st], ((i / NS) - 1) & 1);
+      const uint32_t tt0 = t0 + i * a.TT;
+      const uint32_t rows = min(a.TT, t1 - tt0);
+      const uint64_t slot0 = (a.front + tt0) % g.C;
+      const uint64_t room = g.C - slot0;
+      const uint32_t n1 = room < rows ? (uint32_t)room : rows, n2 = rows - n1;
+      uint8_t* dk = cv.stages + st * stage_bytes;
+      uint8_t* dv = dk + a.TT * kbytes_row;
+      if constexpr (COPY == 1) {
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&cv.full[st], rows * (kbytes_row + vbytes_row));
+          bulk_g2s(dk, rk + slot0 * kbytes_row, n1 * kbytes_row, &cv.full[st]);
+          bulk_g2s(dv, rv + slot0 * vbytes_row, n1 * vbytes_row, &cv.full[st]);
+          if (n2) {
+            bulk_g2s(dk + n1 * kbytes_row, rk, n2 * kbytes_row, &cv.full[st]);
+            bulk_g2s(dv + n1 * vbytes_row, rv, n2 * vbytes_row, &cv.full[st]);
+          }
+        }
+      } else {
+        warp_copy_any(dk, rk + slot0 * kbytes_row, n1 * kbytes_row, lane);
+        warp_copy_any(dv, rv + slot0 * vbytes_row, n1 * vbytes_row, lane);
+        if (n2) {
+          warp_copy_any(dk + n1 * kbytes_row, rk, n2 * kbytes_row, lane);
+          warp_copy_any(dv + n1 * vbytes_row, rv, n2 * vbytes_row, lane);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&cv.full[st]);
+      }
     }
+    return;
   }
+
+  const uint32_t cw = warp - 1;
+  Acc qr[GT][4], acc[GT][4];
+  load_query<Acc, GT>(g, a.q, s, a.scale_log2, lane, qr);
+#pragma unroll
+  for (int h = 0; h < GT; ++h)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[h][j] = 0;
+  const uint32_t all = (1u << g.G) - 1u;
+  for (uint32_t i = 0; i < ntiles; ++i) {
+    const uint32_t st = i % NS;
+    mbar_wait(&cv.full[st], (i / NS) & 1);
+    TileView tv;
+    tv.kpay = cv.stages + st * stage_bytes;
+    tv.vpay = tv.kpay + a.TT * kbytes_row;
+    tv.kpar = tv.vpar = nullptr;
+    tv.rows = min(a.TT, t1 - (t0 + i * a.TT));
+    absorb_tile<T, Acc, 16, 16, GT>(g, tv, all, i, a.TT, false, qr, acc, cv.cs, cw, lane);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&cv.empty[st]);
+  }
+  Acc* part = reinterpret_cast<Acc*>(a.part) + (((uint64_t)s * g.G) * a.nfc + f) * (g.d_v + 2);
+  emit_partial<Acc, GT>(g, acc, cv.stages, cv.cs, ntiles ? all : 0u, false, part,
+                        (uint64_t)a.nfc * (g.d_v + 2), cw, lane);
 }
 
-static size_t slow_fixed_smem(const Geometry& g, uint32_t GT) {
-  return (size_t)2 * GT * g.B * 4 + 3 * GT * 4 + 64;
+// ---------------------------------------------------------------------------
+// launch helpers
+// ---------------------------------------------------------------------------
+static size_t consumer_smem(const Geometry& g, uint32_t GT, uint32_t rows_cap, size_t acc) {
+  return (size_t)2 * GT * rows_cap * acc + 3 * GT * acc + 64;
 }
+static size_t acc_bytes(const Geometry& g) { return g.elem == 4 ? 8 : 4; }
 
 uint32_t slow_stages_for(const Geometry& g) {
   const size_t budget = 110 * 1024;  // two CTAs per SM
-  const size_t fixed = slow_fixed_smem(g, kMaxG);
+  const size_t fixed = consumer_smem(g, kMaxG, g.B, acc_bytes(g));
   size_t ns = budget > fixed ? (budget - fixed) / (g.rec.stride + 16) : 0;
   if (ns > 4) ns = 4;
   if (ns < 1) {  // large records: one CTA per SM
@@ -424,14 +515,28 @@ uint32_t slow_stages_for(const Geometry& g) {
   return (uint32_t)ns;
 }
 
+uint32_t fast_tile_rows(const Geometry& g) {
+  const uint32_t row = (g.d_k + g.d_v) * g.elem;
+  uint32_t tt = 32768u / row;
+  tt = tt > 128 ? 128 : tt;
+  tt = tt < 16 ? 16 : (tt / 16) * 16;
+  return tt;
+}
+
+template <typename Acc>
+static uint32_t stage_region_for(size_t stage_total, uint32_t GT, const Geometry& g) {
+  const size_t red = (size_t)kSlowConsumerWarps * GT * g.d_v * sizeof(Acc);
+  size_t r = stage_total > red ? stage_total : red;
+  return (uint32_t)((r + 15) & ~size_t(15));
+}
+
 template <typename T, int KB, int VB, int GT, int COPY>
 static cudaError_t launch_slow_t(const SlowArgs& a, uint32_t grid_chunks, cudaStream_t st) {
+  using Acc = AccOf<T>;
   const Geometry& g = a.g;
   SlowArgs b = a;
-  const size_t red = (size_t)kSlowConsumerWarps * GT * g.d_v * 4;
-  b.stage_region = (uint32_t)((size_t)a.stages * g.rec.stride > red ? (size_t)a.stages * g.rec.stride : red);
-  b.stage_region = (b.stage_region + 15u) & ~15u;
-  const size_t smem = (size_t)b.stage_region + 16 * a.stages + slow_fixed_smem(g, GT);
+  b.stage_region = stage_region_for<Acc>((size_t)a.stages * g.rec.stride, GT, g);
+  const size_t smem = (size_t)b.stage_region + 16 * a.stages + consumer_smem(g, GT, g.B, sizeof(Acc));
   auto kern = slow_attn_kernel<T, KB, VB, GT, COPY>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -466,9 +571,42 @@ cudaError_t launch_slow(const SlowArgs& a, uint32_t grid_chunks, int copy_mode, 
                         : launch_slow_bits<float, 1>(a, grid_chunks, st);
 }
 
+template <typename T, int GT, int COPY>
+static cudaError_t launch_fast_t(const FastArgs& a, cudaStream_t st) {
+  using Acc = AccOf<T>;
+  const Geometry& g = a.g;
+  FastArgs b = a;
+  const size_t stage_bytes = (size_t)a.TT * (g.d_k + g.d_v) * sizeof(T);
+  b.stage_region = stage_region_for<Acc>(stage_bytes * a.stages, GT, g);
+  const size_t smem = (size_t)b.stage_region + 16 * a.stages + consumer_smem(g, GT, a.TT, sizeof(Acc));
+  auto kern = fast_attn_kernel<T, GT, COPY>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid(a.nfc, g.S);
+  kern<<<grid, 32 + kSlowConsumerWarps * 32, smem, st>>>(b);
+  return cudaGetLastError();
+}
+
+template <typename T, int COPY>
+static cudaError_t launch_fast_g(const FastArgs& a, cudaStream_t st) {
+  if (a.g.G <= 1) return launch_fast_t<T, 1, COPY>(a, st);
+  if (a.g.G <= 2) return launch_fast_t<T, 2, COPY>(a, st);
+  if (a.g.G <= 4) return launch_fast_t<T, 4, COPY>(a, st);
+  return launch_fast_t<T, 8, COPY>(a, st);
+}
+
+cudaError_t launch_fast(const FastArgs& a, cudaStream_t st) {
+  const Geometry& g = a.g;
+  // bulk copies need 16-byte aligned ring rows
+  const bool aligned = ((g.d_k * g.elem) % 16 == 0) && ((g.d_v * g.elem) % 16 == 0);
+  if (g.elem == 2) return aligned ? launch_fast_g<__half, 1>(a, st) : launch_fast_g<__half, 2>(a, st);
+  return aligned ? launch_fast_g<float, 1>(a, st) : launch_fast_g<float, 2>(a, st);
+}
+
 // ---------------------------------------------------------------------------
-// combine
+// combine (attention.hpp:54-61)
 // ---------------------------------------------------------------------------
+template <typename Acc>
 __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
   const Geometry& g = a.g;
   const uint32_t idx = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -477,51 +615,50 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
   const uint32_t s = idx / g.G;
   const uint32_t pitch = g.d_v + 2;
   const uint32_t nsc_used = a.union_count ? (a.union_count[s] + a.CH - 1) / a.CH : 0u;
-  const float* fp = a.fpart + (uint64_t)idx * a.nfc * pitch;
-  const float* sp = a.spart ? a.spart + (uint64_t)idx * a.nsc * pitch : nullptr;
-
+  const Acc* fp = reinterpret_cast<const Acc*>(a.fpart) + (uint64_t)idx * a.nfc * pitch;
+  const Acc* sp = a.spart ? reinterpret_cast<const Acc*>(a.spart) + (uint64_t)idx * a.nsc * pitch
+                          : nullptr;
   // literal additive merge: slow partials are already normalized sums
   const uint32_t nlse = a.literal ? 0u : nsc_used;
-  float M = -INFINITY;
+  Acc M = -INFINITY;
   for (uint32_t i = lane; i < a.nfc; i += 32)
-    if (fp[i * pitch + g.d_v + 1] > 0.0f) M = fmaxf(M, fp[i * pitch + g.d_v]);
+    if (fp[i * pitch + g.d_v + 1] > 0) M = fmax(M, fp[i * pitch + g.d_v]);
   for (uint32_t i = lane; i < nlse; i += 32)
-    if (sp[i * pitch + g.d_v + 1] > 0.0f) M = fmaxf(M, sp[i * pitch + g.d_v]);
-  M = warp_max(M);
-
-  float L = 0.0f;
+    if (sp[i * pitch + g.d_v + 1] > 0) M = fmax(M, sp[i * pitch + g.d_v]);
+  M = wmax(M);
+  Acc L = 0;
   for (uint32_t i = lane; i < a.nfc; i += 32) {
-    const float l = fp[i * pitch + g.d_v + 1];
-    if (l > 0.0f) L += l * exp2f(fp[i * pitch + g.d_v] - M);
+    const Acc l = fp[i * pitch + g.d_v + 1];
+    if (l > 0) L += l * ex2(fp[i * pitch + g.d_v] - M);
   }
   for (uint32_t i = lane; i < nlse; i += 32) {
-    const float l = sp[i * pitch + g.d_v + 1];
-    if (l > 0.0f) L += l * exp2f(sp[i * pitch + g.d_v] - M);
+    const Acc l = sp[i * pitch + g.d_v + 1];
+    if (l > 0) L += l * ex2(sp[i * pitch + g.d_v] - M);
   }
-  L = warp_sum(L);
-  const float inv = 1.0f / L;
-
+  L = wsum(L);
+  const Acc inv = Acc(1) / L;
   for (uint32_t c = lane; c < g.d_v; c += 32) {
-    float A = 0.0f;
+    Acc A = 0;
     for (uint32_t i = 0; i < a.nfc; ++i) {
-      const float l = fp[i * pitch + g.d_v + 1];
-      if (l > 0.0f) A += fp[i * pitch + c] * exp2f(fp[i * pitch + g.d_v] - M);
+      const Acc l = fp[i * pitch + g.d_v + 1];
+      if (l > 0) A += fp[i * pitch + c] * ex2(fp[i * pitch + g.d_v] - M);
     }
     for (uint32_t i = 0; i < nlse; ++i) {
-      const float l = sp[i * pitch + g.d_v + 1];
-      if (l > 0.0f) A += sp[i * pitch + c] * exp2f(sp[i * pitch + g.d_v] - M);
+      const Acc l = sp[i * pitch + g.d_v + 1];
+      if (l > 0) A += sp[i * pitch + c] * ex2(sp[i * pitch + g.d_v] - M);
     }
-    float o = A * inv;
+    Acc o = A * inv;
     if (a.literal)
       for (uint32_t i = 0; i < nsc_used; ++i)
-        if (sp[i * pitch + g.d_v + 1] > 0.0f) o += sp[i * pitch + c];
-    a.out[(uint64_t)idx * g.d_v + c] = o;
+        if (sp[i * pitch + g.d_v + 1] > 0) o += sp[i * pitch + c];
+    a.out[(uint64_t)idx * g.d_v + c] = (double)o;
   }
 }
 
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
   const uint32_t warps = a.g.S * a.g.G;
-  combine_kernel<<<(warps + 7) / 8, 256, 0, st>>>(a);
+  if (a.g.elem == 4) combine_kernel<double><<<(warps + 7) / 8, 256, 0, st>>>(a);
+  else combine_kernel<float><<<(warps + 7) / 8, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -143,7 +143,8 @@ struct ttkv_gpu {
   uint64_t appended = 0, n_slow = 0, fast_front = 0;
   uint64_t last_k = 0, last_n = 0;
   // fast split
-  uint32_t FC = 256, nfc_cap = 1;
+  uint32_t FC = 256, nfc_cap = 1, TT = 64;
+  size_t acc = 4;  // bytes of the accumulation type (fp32, or fp64 for the fp32 ring)
   // device memory
   void* ring_k = nullptr;
   void* ring_v = nullptr;
@@ -152,10 +153,11 @@ struct ttkv_gpu {
   double* scores = nullptr;
   uint32_t *sel = nullptr, *mask = nullptr, *uids = nullptr, *umask = nullptr, *ucount = nullptr;
   unsigned long long* counters = nullptr;
-  float* fpart = nullptr;
-  float* spart = nullptr;
+  void* fpart = nullptr;
+  void* spart = nullptr;
   uint64_t spart_chunks = 0;
-  float *q_dev = nullptr, *out_dev = nullptr;
+  float* q_dev = nullptr;
+  double* out_dev = nullptr;
   void *kn_dev = nullptr, *vn_dev = nullptr;
   void *stg_k = nullptr, *stg_v = nullptr;
   uint64_t stg_tokens = 0;
@@ -163,7 +165,8 @@ struct ttkv_gpu {
   uint8_t* arena_host = nullptr;  // pinned (TTKV_SLOW_PINNED_HOST)
   uint8_t* arena_dev = nullptr;   // device-visible pointer
   // pinned staging for the host-buffer API
-  float *h_q = nullptr, *h_out = nullptr;
+  float* h_q = nullptr;
+  double* h_out = nullptr;
   void *h_k = nullptr, *h_v = nullptr;
   // timing
   bool timing = false;
@@ -331,8 +334,7 @@ int ensure_spart(ttkv_gpu* h, uint64_t chunks) {
   CU(h, cudaStreamSynchronize(h->s0));
   if (h->spart) cudaFree(h->spart);
   h->spart = nullptr;
-  CU(h, cudaMalloc((void**)&h->spart,
-                   (size_t)h->g.S * h->g.G * c * (h->g.d_v + 2) * sizeof(float)));
+  CU(h, cudaMalloc((void**)&h->spart, (size_t)h->g.S * h->g.G * c * (h->g.d_v + 2) * h->acc));
   h->spart_chunks = c;
   return TTKV_OK;
 }
@@ -424,7 +426,7 @@ uint64_t prefill_chunk_tokens(const ttkv_gpu* h) {
 }
 
 int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int dtype,
-                float* out, ttkv_step_report* rep) {
+                double* out, ttkv_step_report* rep) {
   {  // grow before selecting so a settle-time eviction never reallocates
     int rc0 = ensure_blocks(h, h->n_slow + 1);
     if (rc0) return rc0;
@@ -448,7 +450,8 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
     int rc = resolve_k(h->pol, n, k, m);
     if (rc) return set_err(h, rc, m);
   }
-  const float scale_log2 = (float)(1.0 / std::sqrt((double)g.d_k) * 1.4426950408889634);
+  // softmax scale 1/sqrt(d_k) (engine.cpp:30), folded with log2(e) for exp2
+  const double scale_log2 = 1.0 / std::sqrt((double)g.d_k) * 1.4426950408889634;
 
   // fast tier on s1, overlapped with the slow stream on s0
   CU(h, cudaEventRecord(h->ev_fork, h->s0));
@@ -465,6 +468,8 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
     a.F = (uint32_t)F;
     a.FC = h->FC;
     a.nfc = nfc;
+    a.TT = h->TT;
+    a.stages = kFastStages;
     a.scale_log2 = scale_log2;
     KTimer t(h, K_FAST, h->s1);
     CU(h, launch_fast(a, h->s1));
@@ -688,12 +693,14 @@ int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* po
     if (!std::strcmp(env, "ldg")) h->copy_mode = 2;
     if (!std::strcmp(env, "bulk")) h->copy_mode = 1;
   }
-  // fast split: ~8 waves of 4-warp CTAs
+  // fast split: chunks of whole TT-token tiles, ~4 waves of 2 CTAs per SM
+  h->acc = g.elem == 4 ? 8 : 4;
   {
+    h->TT = fast_tile_rows(g);
     const uint64_t Fmax = l_fast + g.B;  // ring capacity bounds the fast tier
-    const uint64_t target = std::max<uint64_t>(1, (148ull * 8 + g.S - 1) / g.S);
+    const uint64_t target = std::max<uint64_t>(1, (148ull * 2 * 4 + g.S - 1) / g.S);
     uint64_t FC = (Fmax + target - 1) / target;
-    FC = std::max<uint64_t>(64, std::min<uint64_t>(1024, (FC + 31) / 32 * 32));
+    FC = std::max<uint64_t>(h->TT, (FC + h->TT - 1) / h->TT * h->TT);
     h->FC = (uint32_t)FC;
     h->nfc_cap = (uint32_t)((Fmax + FC - 1) / FC);
   }
@@ -722,13 +729,13 @@ int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* po
   CREATE_CU(cudaMalloc((void**)&h->ucount, S * sizeof(uint32_t)));
   CREATE_CU(cudaMemset(h->ucount, 0, S * sizeof(uint32_t)));
   CREATE_CU(cudaMalloc((void**)&h->counters, 4 * sizeof(unsigned long long)));
-  CREATE_CU(cudaMalloc((void**)&h->fpart, S * g.G * h->nfc_cap * (g.d_v + 2) * sizeof(float)));
+  CREATE_CU(cudaMalloc((void**)&h->fpart, S * g.G * h->nfc_cap * (g.d_v + 2) * h->acc));
   CREATE_CU(cudaMalloc((void**)&h->q_dev, S * g.G * g.d_k * sizeof(float)));
-  CREATE_CU(cudaMalloc((void**)&h->out_dev, S * g.G * g.d_v * sizeof(float)));
+  CREATE_CU(cudaMalloc((void**)&h->out_dev, S * g.G * g.d_v * sizeof(double)));
   CREATE_CU(cudaMalloc(&h->kn_dev, S * g.d_k * 4));
   CREATE_CU(cudaMalloc(&h->vn_dev, S * g.d_v * 4));
   CREATE_CU(cudaHostAlloc((void**)&h->h_q, S * g.G * g.d_k * sizeof(float), cudaHostAllocPortable));
-  CREATE_CU(cudaHostAlloc((void**)&h->h_out, S * g.G * g.d_v * sizeof(float), cudaHostAllocPortable));
+  CREATE_CU(cudaHostAlloc((void**)&h->h_out, S * g.G * g.d_v * sizeof(double), cudaHostAllocPortable));
   CREATE_CU(cudaHostAlloc(&h->h_k, S * g.d_k * 4, cudaHostAllocPortable));
   CREATE_CU(cudaHostAlloc(&h->h_v, S * g.d_v * 4, cudaHostAllocPortable));
   const uint64_t reserve_blocks =
@@ -887,7 +894,7 @@ int ttkv_gpu_evict(ttkv_gpu* h, uint64_t* block_id) {
 }
 
 int ttkv_gpu_decode_step_device(ttkv_gpu* h, const float* q, const void* kn, const void* vn,
-                                int dtype, float* out, ttkv_step_report* rep) {
+                                int dtype, double* out, ttkv_step_report* rep) {
   if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
   if (!q || !kn || !vn || !out) return set_err(h, TTKV_EINVAL, "null pointer");
   if (dtype != TTKV_DTYPE_F32 && dtype != TTKV_DTYPE_F16)
@@ -897,7 +904,7 @@ int ttkv_gpu_decode_step_device(ttkv_gpu* h, const float* q, const void* kn, con
 }
 
 int ttkv_gpu_decode_step(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int dtype,
-                         float* out, ttkv_step_report* rep) {
+                         double* out, ttkv_step_report* rep) {
   if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
   if (!q || !kn || !vn || !out) return set_err(h, TTKV_EINVAL, "null pointer");
   if (dtype != TTKV_DTYPE_F32 && dtype != TTKV_DTYPE_F16)
@@ -905,7 +912,7 @@ int ttkv_gpu_decode_step(ttkv_gpu* h, const float* q, const void* kn, const void
   CU(h, cudaSetDevice(h->dev));
   const Geometry& g = h->g;
   const size_t esz = dtype == TTKV_DTYPE_F16 ? 2 : 4;
-  const size_t qb = (size_t)g.S * g.G * g.d_k * 4, ob = (size_t)g.S * g.G * g.d_v * 4;
+  const size_t qb = (size_t)g.S * g.G * g.d_k * 4, ob = (size_t)g.S * g.G * g.d_v * 8;
   const size_t kb = (size_t)g.S * g.d_k * esz, vb = (size_t)g.S * g.d_v * esz;
   std::memcpy(h->h_q, q, qb);
   std::memcpy(h->h_k, kn, kb);

@@ -66,14 +66,19 @@ struct FastArgs {
   const void* ring_k;
   const void* ring_v;
   const float* q;
-  float* part;        // [S][G][nfc][d_v+2]
+  void* part;         // [S][G][nfc][d_v+2] of the accumulation type
   uint64_t front;     // first fast position
   uint32_t F;         // fast tokens
-  uint32_t FC;        // tokens per chunk
+  uint32_t FC;        // tokens per chunk (multiple of TT)
   uint32_t nfc;
-  float scale_log2;
+  uint32_t TT;        // tokens per staged tile
+  uint32_t stages;
+  double scale_log2;
+  uint32_t stage_region;  // set by the launcher
 };
 cudaError_t launch_fast(const FastArgs& a, cudaStream_t st);
+uint32_t fast_tile_rows(const Geometry& g);
+constexpr uint32_t kFastStages = 3;
 
 struct SlowArgs {
   Geometry g;
@@ -83,11 +88,11 @@ struct SlowArgs {
   const uint32_t* union_mask;
   const uint32_t* union_count;
   const float* q;
-  float* part;       // [S][G][nsc][d_v+2]
+  void* part;        // [S][G][nsc][d_v+2] of the accumulation type
   uint32_t CH;       // union entries per CTA
   uint32_t nsc;      // chunk capacity per (s, g) in `part`
   uint32_t stages;
-  float scale_log2;
+  double scale_log2;
   uint32_t stage_region;  // set by the launcher
   uint32_t literal;       // EngineOptions::literal_additive_merge
 };
@@ -97,13 +102,13 @@ uint32_t slow_stages_for(const Geometry& g);
 
 struct CombineArgs {
   Geometry g;
-  const float* fpart;
+  const void* fpart;
   uint32_t nfc;
-  const float* spart;
+  const void* spart;
   uint32_t nsc;
   uint32_t CH;
   const uint32_t* union_count;  // null when no slow work this step
-  float* out;                   // [S][G][d_v]
+  double* out;                  // [S][G][d_v] (reference output is double)
   uint32_t literal;
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);

@@ -241,7 +241,7 @@ class MultiStreamEngine:
             raise ShapeError("decode_step: query dimension mismatch")
         if k.size != self.S * self.config.d_k or v.size != self.S * self.config.d_v:
             raise ShapeError("append_token: key/value dimension mismatch")
-        out = np.zeros((self.S, self.G, self.config.d_v), np.float32)
+        out = np.zeros((self.S, self.G, self.config.d_v), np.float64)
         rep = L.StepReportC()
         _check(self._lib.ttkv_gpu_decode_step(self._h, _ptr(q), _ptr(k), _ptr(v), dt, _ptr(out),
                                               C.byref(rep)), self._h)
@@ -363,7 +363,7 @@ class Engine:
             raise ShapeError("decode_step: query dimension mismatch")
         r = self._m.decode_step(_f32(query).reshape(1, 1, -1), np.asarray(key).reshape(1, -1),
                                 np.asarray(value).reshape(1, -1))
-        r.output = r.output.reshape(-1).astype(np.float64)
+        r.output = r.output.reshape(-1)
         r.fetched_blocks = self._m.read_fetched(0, 0)
         return r
 

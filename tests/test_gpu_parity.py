@@ -165,7 +165,8 @@ def run_parity(T_, *, S=2, G=1, d=32, dv=None, B=32, l_fast=128, kb=8, vb=4, ele
                 assert np.array_equal(rep.fetched_blocks[s][g], o["fetched"][g]), (t, s, g)
                 e = rel_err(rep.output[s, g], o["output"][g])
                 worst = max(worst, e)
-                assert e < OUT_TOL, (t, s, g, e)
+                # fp16 ring: fp32 accumulation (north star 1e-3); fp32 ring: fp64
+                assert e < (OUT_TOL if elem == 2 else 1e-9), (t, s, g, e)
     st = eng.state()
     assert st["slow_blocks"] == orc[0].slow_blocks()
     assert st["fast_tokens"] == orc[0].fast_tokens()
@@ -257,7 +258,7 @@ def test_lossless_fetch_all_matches_dense(gpu):
         dense = np.zeros(d, np.float64)
         O.oracle().tko_dense_attention(dq[t], d, np.ascontiguousarray(hk).reshape(-1),
                                        np.ascontiguousarray(hv).reshape(-1), len(hk), d, dense)
-        assert rel_err(r.output, dense) < 1e-5  # fp32 accumulation (attention_test 1e-5)
+        assert rel_err(r.output, dense) < 1e-12  # fp32 ring -> fp64 accumulation
         assert r.blocks_fetched == r.blocks_scored
     eng.close()
 
