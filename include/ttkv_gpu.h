@@ -64,8 +64,9 @@ extern "C" {
 #define TTKV_SLOW_PINNED_HOST 0 /* north-star path: pinned DRAM, PCIe zero-copy */
 #define TTKV_SLOW_DEVICE 1      /* flagged variant: records in HBM */
 
-/* Mirror of ttkv::TierConfig (config.hpp:14-41).  bytes_full_precision selects
- * the fast-tier storage: 2 = fp16 ring, 4 = fp32 ring. */
+/* Mirror of ttkv::TierConfig (config.hpp:14-41).  As in the reference,
+ * bytes_full_precision is accounting (fast_capacity); the GPU storage type of
+ * the fast tier is ttkv_gpu_options::ring_bytes. */
 typedef struct {
   uint64_t hbm_budget_bytes;
   uint64_t d_k;
@@ -101,6 +102,10 @@ typedef struct {
   uint32_t copy_mode;          /* slow-block staging: 0 auto, 1 cp.async.bulk, 2 LDG */
   uint32_t literal_additive_merge; /* EngineOptions (engine.hpp:14-19): sum of
                                       per-partition normalized outputs (A/B only) */
+  uint32_t ring_bytes;         /* fast-tier storage: 0 auto (fp16 if
+                                  bytes_full_precision <= 2, else fp32),
+                                  2 fp16 (fp32 accumulation), 4 fp32 (fp64
+                                  accumulation; bit-faithful to float inputs) */
 } ttkv_gpu_options;
 
 /* DecodeStepReport (engine.hpp:21-29) plus measured quantities. */

@@ -33,7 +33,8 @@ class OptionsC(C.Structure):
     _fields_ = [("device", C.c_int32), ("n_streams", C.c_uint32),
                 ("heads_per_stream", C.c_uint32), ("group_select", C.c_uint32),
                 ("reserve_tokens", C.c_uint64), ("slow_tier", C.c_uint32),
-                ("copy_mode", C.c_uint32), ("literal_additive_merge", C.c_uint32)]
+                ("copy_mode", C.c_uint32), ("literal_additive_merge", C.c_uint32),
+                ("ring_bytes", C.c_uint32)]
 
 
 class StepReportC(C.Structure):

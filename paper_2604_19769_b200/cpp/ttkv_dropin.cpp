@@ -403,6 +403,11 @@ ttkv_gpu* open_store(const TierConfig& cfg, const SelectionPolicy& pol, bool lit
   o.heads_per_stream = 1;
   o.slow_tier = TTKV_SLOW_PINNED_HOST;
   o.literal_additive_merge = literal ? 1u : 0u;
+  // The reference keeps float32 tokens whatever bytes_full_precision accounts
+  // for (kv_types.hpp:14-15): default to an fp32 ring (fp64 accumulation).
+  // TTKV_RING=fp16 selects the fp16 ring of the batched performance path.
+  const char* ring = std::getenv("TTKV_RING");
+  o.ring_bytes = (ring && std::strcmp(ring, "fp16") == 0) ? 2u : 4u;
   ttkv_gpu* h = nullptr;
   check(ttkv_gpu_create(&c, &p, &o, &h));
   return h;

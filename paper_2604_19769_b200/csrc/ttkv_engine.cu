@@ -644,9 +644,8 @@ int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* po
   // B200 engine limits (documented in DESIGN.md)
   if (cfg->d_k > (uint64_t)kMaxD || cfg->d_v > (uint64_t)kMaxD)
     return set_err(nullptr, TTKV_ECONFIG, "GPU engine supports d_k, d_v <= 128");
-  if (cfg->bytes_full_precision != 2 && cfg->bytes_full_precision != 4)
-    return set_err(nullptr, TTKV_ECONFIG,
-                   "GPU engine supports bytes_full_precision 2 (fp16 ring) or 4 (fp32 ring)");
+  if (opt->ring_bytes != 0 && opt->ring_bytes != 2 && opt->ring_bytes != 4)
+    return set_err(nullptr, TTKV_ECONFIG, "ring_bytes must be 0 (auto), 2 (fp16) or 4 (fp32)");
   if (cfg->block_size > 512)
     return set_err(nullptr, TTKV_ECONFIG, "GPU engine supports block_size <= 512");
   if (opt->n_streams == 0 || opt->heads_per_stream == 0 || opt->heads_per_stream > (uint32_t)kMaxG)
@@ -675,7 +674,8 @@ int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* po
   g.B = (uint32_t)cfg->block_size;
   g.kb = cfg->key_bits;
   g.vb = cfg->value_bits;
-  g.elem = (uint32_t)cfg->bytes_full_precision;
+  // fast-tier storage: explicit, else fp16 when the config accounts <= 2 B/elem
+  g.elem = opt->ring_bytes ? opt->ring_bytes : (cfg->bytes_full_precision <= 2 ? 2u : 4u);
   g.C = l_fast + g.B;
   g.n_cap = 0;
   g.rec = make_layout(g.B, g.d_k, g.d_v, g.kb, g.vb, g.elem);

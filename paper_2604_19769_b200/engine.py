@@ -179,7 +179,8 @@ class MultiStreamEngine:
     def __init__(self, config: TierConfig, policy: SelectionPolicy = None, n_streams: int = 1,
                  heads_per_stream: int = 1, group_select: bool = False, device: int = 0,
                  reserve_tokens: int = 0, slow_tier: int = L.SLOW_PINNED_HOST,
-                 copy_mode: int = 0, literal_additive_merge: bool = False):
+                 copy_mode: int = 0, literal_additive_merge: bool = False,
+                 ring_bytes: int = 0):
         self.config = config
         self.policy = policy or SelectionPolicy(config.top_k_blocks, config.fetch_fraction)
         self.S, self.G = n_streams, heads_per_stream
@@ -188,7 +189,7 @@ class MultiStreamEngine:
         self._c_pol = self.policy.to_c()
         self._c_opt = L.OptionsC(device, n_streams, heads_per_stream, int(group_select),
                                  reserve_tokens, slow_tier, copy_mode,
-                                 int(literal_additive_merge))
+                                 int(literal_additive_merge), ring_bytes)
         h = C.c_void_p()
         _check(self._lib.ttkv_gpu_create(C.byref(self._c_cfg), C.byref(self._c_pol),
                                          C.byref(self._c_opt), C.byref(h)))
@@ -348,9 +349,12 @@ class Engine:
     stream, one query per step, reference report semantics."""
 
     def __init__(self, config: TierConfig, policy: SelectionPolicy = None, device: int = 0,
-                 reserve_tokens: int = 0):
+                 reserve_tokens: int = 0, ring_bytes: int = 4):
+        # The reference stores float32 tokens whatever bytes_full_precision
+        # says (kv_types.hpp:14-15), so the single-stream drop-in defaults to
+        # an fp32 ring (fp64 accumulation); ring_bytes=2 selects fp16.
         self._m = MultiStreamEngine(config, policy, 1, 1, device=device,
-                                    reserve_tokens=reserve_tokens)
+                                    reserve_tokens=reserve_tokens, ring_bytes=ring_bytes)
         self.config = config
         self.policy = self._m.policy
 

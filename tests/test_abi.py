@@ -86,7 +86,7 @@ def test_gpu_limits_are_config_errors():
     with pytest.raises(T.ConfigError):
         T.MultiStreamEngine(T.TierConfig(hbm_budget_bytes=1 << 24, d_k=256, d_v=128))
     with pytest.raises(T.ConfigError):
-        T.MultiStreamEngine(T.TierConfig(hbm_budget_bytes=1 << 24, bytes_full_precision=1))
+        T.MultiStreamEngine(T.TierConfig(hbm_budget_bytes=1 << 24), ring_bytes=3)
     with pytest.raises(T.ConfigError):
         T.MultiStreamEngine(T.TierConfig(hbm_budget_bytes=1 << 20), heads_per_stream=9)
 

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <numeric>
@@ -139,6 +140,43 @@ int main(int argc, char** argv) {
   }, 3);
   std::printf("{\"path\": \"memcpy_per_record\", \"records\": %zu, \"gbs\": %.2f}\n",
               std::min<size_t>(nrec, 2000), std::min<size_t>(nrec, 2000) * kRec / ms / 1e6);
+  // batched copy engine: one cudaMemcpyBatchAsync of scattered 24,576 B payloads
+  {
+    cudaStream_t cs;
+    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    for (size_t batch : {size_t(1000), size_t(10000)}) {
+      batch = std::min(batch, nrec);
+      std::vector<void*> dsts(batch), srcs(batch);
+      std::vector<size_t> sizes(batch, 24576);
+      for (size_t i = 0; i < batch; ++i) {
+        dsts[i] = d + i * kRec;
+        srcs[i] = h + (size_t)order[i] * kRec;
+      }
+      cudaMemcpyAttributes attr{};
+      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+      size_t aidx = 0, fail = 0;
+      float bestms = 1e30f, api_us = 0;
+      for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(a, cs);
+        auto t0 = std::chrono::steady_clock::now();
+        cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), batch, &attr,
+                                             &aidx, 1, &fail, cs);
+        api_us = std::chrono::duration<float, std::micro>(std::chrono::steady_clock::now() - t0).count();
+        cudaEventRecord(b, cs);
+        cudaEventSynchronize(b);
+        if (e != cudaSuccess) {
+          std::printf("{\"path\": \"memcpy_batch\", \"error\": \"%s\"}\n", cudaGetErrorString(e));
+          break;
+        }
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        bestms = std::min(bestms, ms);
+      }
+      std::printf("{\"path\": \"memcpy_batch_scattered\", \"records\": %zu, \"gbs\": %.2f, "
+                  "\"api_us\": %.1f}\n", batch, batch * 24576.0 / bestms / 1e6, api_us);
+    }
+    cudaStreamDestroy(cs);
+  }
   for (int grid_mult : {1, 2, 4, 8}) {
     const int grid = prop.multiProcessorCount * grid_mult;
     ms = best([&] { ldg_records<<<grid, 256>>>(hd, d_order, (unsigned)nrec, sink); }, 5);
