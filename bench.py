@@ -1,14 +1,17 @@
 #!/usr/bin/env python
 """Benchmark of the TTKV decode hot path on B200 (BASELINE.json metric).
 
-Workload (N=1): BASELINE.json configs[1] -- LLaMA-3-8B GQA decode at 128K
-context, batch 1, all 32 layers x 8 KV heads = 256 KV streams, 4 query heads
-each, d=128, 4096-token fp16 fast tier per stream, K8/V4 slow tier in pinned
-host DRAM, fetch fraction 0.45, per-head selection (== 1024 reference Engines).
-One step = one decode step of every layer/head (one generated token).
-N>1 (configs[3]): the same request head-sharded over N GPUs -- rank r owns KV
-heads [8r/N, 8(r+1)/N) of every layer, streams its records over its own PCIe
-link, and the per-head outputs are all-gathered over NVLink (NCCL).
+Default workload (N=1): BASELINE.json configs[1] (cfg2) -- LLaMA-3-8B GQA
+decode at 128K context, batch 1, all 32 layers x 8 KV heads = 256 KV streams,
+4 query heads each, d=128, 4096-token fp16 fast tier per stream, K8/V4 slow
+tier in pinned host DRAM, fetch fraction 0.45, per-query-head selection
+(== 1024 reference Engines).  One step = one decode step of every layer/head
+(one generated token per request).
+N>1 (configs[3], cfg4): the same request head-sharded over N GPUs -- rank r
+owns KV heads [8r/N, 8(r+1)/N) of every layer, streams its records over its
+own PCIe link, and the per-head outputs are all-gathered over NVLink (NCCL).
+--workload cfg1|cfg3|cfg5 selects the other BASELINE configs (cfg3 shards
+by request at N>1, no collective).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -29,12 +32,24 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-LAYERS, KV_HEADS, G, D, B = 32, 8, 4, 128, 128
-CTX = 131072
-L_FAST = 4096
-FRAC = 0.45
-METRIC = "decode tokens/s at 128K ctx (LLaMA-3-8B GQA, all layers, batch 1)"
+D, B, L_FAST, FRAC = 128, 128, 4096, 0.45
 UNIT = "tok/s"
+WORKLOADS = {
+    "cfg1": dict(layers=1, kv_heads=32, G=1, batch=1, ctx=32768,
+                 desc="cfg1: single-layer LLaMA-7B-shape MHA (32 heads, d=128), 32K ctx, batch 1"),
+    "cfg2": dict(layers=32, kv_heads=8, G=4, batch=1, ctx=131072,
+                 desc="cfg2: LLaMA-3-8B GQA 32L x 8KV x 4Q, 128K ctx, batch 1"),
+    "cfg3": dict(layers=32, kv_heads=8, G=4, batch=16, ctx=32768,
+                 desc="cfg3: LLaMA-3-8B GQA 32L x 8KV x 4Q, 32K ctx, batch 16"),
+    "cfg5": dict(layers=32, kv_heads=8, G=4, batch=1, ctx=262144,
+                 desc="cfg5: LLaMA-3-8B GQA at 256K ctx (end of 128K->256K growth)"),
+}
+
+
+def metric_for(w):
+    if w == "cfg2":
+        return "decode tokens/s at 128K ctx (LLaMA-3-8B GQA, all layers, batch 1)"
+    return f"decode tokens/s ({WORKLOADS[w]['desc']})"
 
 
 def parse():
@@ -43,12 +58,17 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--ctx", type=int, default=CTX)
+    p.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    p.add_argument("--ctx", type=int, default=None, help="override the workload's context")
     p.add_argument("--group-select", action="store_true",
                    help="one selection per KV head (q' = sum_g q_g) instead of per query head")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--slow-tier", default="host", choices=["host", "device"])
-    return p.parse_args()
+    a = p.parse_args()
+    a.w = dict(WORKLOADS[a.workload])
+    if a.ctx:
+        a.w["ctx"] = a.ctx
+    return a
 
 
 def dist_env():
@@ -66,10 +86,10 @@ def host_cores():
         return os.cpu_count() or 1
 
 
-def ref_sample(ctx, steps, engines=None, threads=None):
+def ref_sample(ctx, steps, G, engines=None, threads=None):
     """Runs `engines` reference Engines (one per (stream, query head)) at ctx,
     prefilled, then `steps` decode steps on `threads` host threads.  Returns
-    per-step wall ms of the sample and the sample description."""
+    per-step wall ms of the sample."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import numpy as np
     import _oracle as O
@@ -86,35 +106,37 @@ def ref_sample(ctx, steps, engines=None, threads=None):
     return ms, pre.value, engines, threads
 
 
-def cpu_throughput(ms_step, engines, total_engines):
+def cpu_throughput(ms_step, engines, total_engines, tokens_per_step):
     """tokens/s of the full workload, extrapolated linearly from the sample:
     a full step needs total_engines/engines sample steps."""
     full_ms = ms_step * total_engines / engines
-    return 1000.0 / full_ms
+    return tokens_per_step * 1000.0 / full_ms
 
 
 def run_reference(args):
     rank, _, world = dist_env()
     if rank != 0:
         return
-    total_engines = LAYERS * KV_HEADS * G  # one reference Engine per (stream, q-head)
+    w = args.w
+    S = w["layers"] * w["kv_heads"] * w["batch"]
+    total_engines = S * w["G"]  # one reference Engine per (stream, q-head)
     n = args.warmup + args.steps
-    ms, pre_s, engines, threads = ref_sample(args.ctx, n)
+    ms, pre_s, engines, threads = ref_sample(w["ctx"], n, w["G"])
     timed = ms[args.warmup:]
-    vals = [cpu_throughput(m, engines, total_engines) for m in timed]
+    vals = [cpu_throughput(m, engines, total_engines, w["batch"]) for m in timed]
     value = statistics.mean(vals)
-    sample = (f"{engines} reference Engines (1 per stream x q-head) at {args.ctx} ctx on "
+    sample = (f"{engines} reference Engines (1 per stream x q-head) at {w['ctx']} ctx on "
               f"{threads} threads, {args.steps} timed decode steps after {args.warmup} warm-up; "
-              f"extrapolated x{total_engines // engines} to {total_engines} engines")
+              f"extrapolated x{total_engines / engines:g} to {total_engines} engines")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "impl": "reference", "metric": metric_for(args.workload), "value": value, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 / value, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference GaussianSource)",
-        "config": {"workload": "cfg2: LLaMA-3-8B GQA 32L x 8KV x 4Q, 128K ctx, batch 1",
-                   "ctx": args.ctx, "streams": LAYERS * KV_HEADS, "heads_per_stream": G,
-                   "d": D, "block": B, "l_fast": L_FAST, "bits": "K8/V4", "fetch_fraction": FRAC},
+        "ms_per_step": w["batch"] * 1000.0 / value, "higher_is_better": True,
+        "scaling": "strong" if world > 1 and w["batch"] == 1 else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (reference GaussianSource)",
+        "config": {"workload": w["desc"], "ctx": w["ctx"], "streams": S,
+                   "heads_per_stream": w["G"], "d": D, "block": B, "l_fast": L_FAST,
+                   "bits": "K8/V4", "fetch_fraction": FRAC},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -135,6 +157,7 @@ class Clocks:
     def __init__(self, device):
         self.device = device
         self.proc = None
+        self.lines = []
 
     def __enter__(self):
         try:
@@ -147,7 +170,6 @@ class Clocks:
         return self
 
     def __exit__(self, *a):
-        self.lines = []
         if self.proc:
             self.proc.terminate()
             try:
@@ -160,7 +182,7 @@ class Clocks:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in getattr(self, "lines", []):
+        for l in self.lines:
             f = [x.strip() for x in l.split(",")]
             try:
                 sm.append(float(f[1]))
@@ -194,9 +216,8 @@ def measure_h2d_peak(torch, dev):
 
 
 def load_traffic():
-    p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
-        with open(p) as f:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             return json.load(f)
     except Exception:
         return None
@@ -207,28 +228,31 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     import paper_2604_19769_b200 as T
+    from paper_2604_19769_b200.sharding import ShardPlan, gather_outputs
 
     rank, local, world = dist_env()
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    from paper_2604_19769_b200.sharding import ShardPlan, gather_outputs
-    plan = ShardPlan(rank, world, LAYERS, KV_HEADS, 1, "heads")
-    S = plan.n_local  # streams on this rank (head sharding: 8/N KV heads x 32 layers)
+    w = args.w
+    G, ctx, batch = w["G"], w["ctx"], w["batch"]
+    mode = "heads" if batch == 1 else "requests"
+    plan = ShardPlan(rank, world, w["layers"], w["kv_heads"], batch, mode)
+    S = plan.n_local  # streams on this rank
 
     cfg = T.TierConfig(hbm_budget_bytes=L_FAST * 2 * D * 2, d_k=D, d_v=D, bytes_full_precision=2,
                        block_size=B, key_bits=8, value_bits=4, fetch_fraction=FRAC)
     n_steps_total = args.warmup + 2 * args.steps + 2
     eng = T.MultiStreamEngine(cfg, T.SelectionPolicy(None, FRAC), n_streams=S,
                               heads_per_stream=G, group_select=args.group_select, device=local,
-                              reserve_tokens=args.ctx + n_steps_total + B,
+                              reserve_tokens=ctx + n_steps_total + B,
                               slow_tier=0 if args.slow_tier == "host" else 1)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
     eng.set_stream(stream.cuda_stream)
     t0 = time.time()
-    eng.prefill_synthetic(args.ctx, seed=1000 + rank)
+    eng.prefill_synthetic(ctx, seed=1000 + rank)
     prefill_s = time.time() - t0
     h2d_peak = measure_h2d_peak(torch, dev)
 
@@ -260,7 +284,6 @@ def run_ours(args):
     with Clocks(local) as clk:
         barrier()
         ev0.record()
-        union_total = 0
         for i in range(args.steps):
             step(args.warmup + i)
         ev1.record()
@@ -269,7 +292,7 @@ def run_ours(args):
     ms_total = ev0.elapsed_time(ev1)
     kt = eng.kernel_times(reset=True)
     st1 = eng.state()
-    union_last, pcie_last = eng.step_counters()
+    union_last, _ = eng.step_counters()
     launches = st1["launches"] - st0["launches"]
 
     # --- e2e through the public C ABI with host buffers -----------------------
@@ -278,7 +301,7 @@ def run_ours(args):
     hk = [rng.standard_normal((S, D)).astype(np.float16) for _ in range(NPOOL)]
     hv = [rng.standard_normal((S, D)).astype(np.float16) for _ in range(NPOOL)]
     h2d = hq[0].nbytes + hk[0].nbytes + hv[0].nbytes
-    d2h = S * G * D * 4
+    d2h = S * G * D * 8 * (world if plan.needs_gather else 1)
     barrier()
     t_e2e0 = time.perf_counter()
     for i in range(args.steps):
@@ -289,13 +312,12 @@ def run_ours(args):
     e2e_ms = (time.perf_counter() - t_e2e0) * 1000.0 / args.steps
 
     # --- max over ranks ---------------------------------------------------------
-    vals = torch.tensor([ms_total, e2e_ms, kt["ms_slow"], kt["ms_fast"]], device=dev,
-                        dtype=torch.float64)
+    vals = torch.tensor([ms_total, e2e_ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
     ms_total, e2e_ms = float(vals[0]), float(vals[1])
     ms_step = ms_total / args.steps
-    tokens_per_step = 1  # batch 1: one token per step for the whole model
+    tokens_per_step = batch  # one generated token per request per step
     value = tokens_per_step * 1000.0 / ms_step
 
     # --- roofline of the dominant kernel (slow_stream_attn, PCIe-bound) ---------
@@ -304,7 +326,7 @@ def run_ours(args):
     n_slow = kt["n_slow"] or 1
     slow_ms = kt["ms_slow"] / n_slow
     pcie_bytes_launch = union_last * payload
-    achieved = pcie_bytes_launch / (slow_ms * 1e-3) / 1e9
+    achieved = pcie_bytes_launch / (slow_ms * 1e-3) / 1e9 if slow_ms > 0 else 0.0
     fast_ms = kt["ms_fast"] / max(1, kt["n_fast"])
     F = st1["fast_tokens"]
     fast_bytes = S * F * 2 * D * 2
@@ -316,57 +338,63 @@ def run_ours(args):
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     hbm_bytes_step = fast_bytes + S * st1["slow_blocks"] * D * 4 + union_last * (rec - payload)
-    t_roof_ms = max(hbm_bytes_step / (hbm_peak * 1e9), pcie_bytes_launch / (h2d_peak * 1e9)) * 1e3
-    traffic = load_traffic()
+    t_roof_ms = max(hbm_bytes_step / (hbm_peak * 1e9),
+                    pcie_bytes_launch / (h2d_peak * 1e9)) * 1e3
+    traffic = load_traffic() if args.workload == "cfg2" else None
 
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+        "metric": metric_for(args.workload), "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "strong" if world > 1 and mode == "heads" else "weak", "vs_baseline": None,
+        "dtype": "f32",
         "data": "synthetic (device N(0,1) KV rounded to fp16, random queries)",
         "config": {
-            "workload": ("cfg2: LLaMA-3-8B GQA 32L x 8KV x 4Q, 128K ctx, batch 1" if world == 1
-                         else f"cfg4: cfg2 head-sharded over {world} GPUs + NCCL all-gather"),
-            "ctx": args.ctx, "streams_per_gpu": S, "heads_per_stream": G, "d": D, "block": B,
-            "l_fast": L_FAST, "bits": "K8/V4", "fetch_fraction": FRAC,
+            "workload": w["desc"] + (f", head-sharded over {world} GPUs + NCCL all-gather"
+                                     if plan.needs_gather else
+                                     (f", request-sharded over {world} GPUs" if world > 1 else "")),
+            "ctx": ctx, "streams_per_gpu": S, "heads_per_stream": G, "batch": batch, "d": D,
+            "block": B, "l_fast": L_FAST, "bits": "K8/V4", "fetch_fraction": FRAC,
             "selection": "group-shared" if args.group_select else "per-query-head (reference)",
             "slow_tier": "pinned host DRAM, zero-copy PCIe" if args.slow_tier == "host" else "HBM",
-            "storage": "fp16 ring, u8 keys / u4 values, f32 params", "parallelism":
-                f"head-shard{world}" if world > 1 else "single",
-            "l2": "inputs larger than L2 (ring 553 MB, slow tier 6.8 GB in host DRAM)",
+            "storage": "fp16 ring, u8 keys / u4 values, f32 params",
+            "parallelism": f"{mode}-shard{world}" if world > 1 else "single",
+            "l2": "inputs larger than L2 (fp16 ring + slow tier far above 126 MB)",
         },
         "roofline": {
             "bound": "pcie_h2d", "kernel": "slow_stream_attn", "achieved": achieved,
             "peak": h2d_peak, "unit": "GB/s", "frac": achieved / h2d_peak,
             "peak_source": "pinned cudaMemcpy H2D 256 MiB best of 10, measured in this run",
             "traffic": traffic.get("slow_dram_bytes_per_launch") if traffic else None,
+            "pcie_traffic": traffic.get("slow_sysmem_read_bytes_per_launch") if traffic else None,
             "algorithmic_bytes_per_launch": pcie_bytes_launch,
             "launch_ms": slow_ms,
             "tier_roofline_ms": t_roof_ms, "tier_frac": t_roof_ms / ms_step,
-            "fast_attn": {"ms": fast_ms, "hbm_gbs": fast_bytes / (fast_ms * 1e-3) / 1e9,
-                          "hbm_peak": hbm_peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+            "fast_attn": {"ms": fast_ms, "hbm_gbs": fast_bytes / (fast_ms * 1e-3) / 1e9
+                          if fast_ms > 0 else None,
+                          "hbm_peak": hbm_peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                          "note": "timed concurrently with slow_stream_attn on a second stream"},
         },
         "pcie_bytes_per_token": pcie_bytes_launch * world / tokens_per_step,
         "union_blocks_per_step": union_last,
         "kernel_ms_per_step": {k[3:]: v / args.steps for k, v in kt.items() if k.startswith("ms_")},
         "gpu_launches": launches,
         "e2e": {"value": tokens_per_step * 1000.0 / e2e_ms, "unit": UNIT,
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h * (world if world > 1 else 1),
-                "ms_per_step": e2e_ms},
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "prefill_s": round(prefill_s, 2),
     }
     if rank == 0:
         line["clocks"] = clk.summary()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            ms, pre_s, engines, threads = ref_sample(args.ctx, 2)
-            total = LAYERS * KV_HEADS * G
-            cv = cpu_throughput(float(ms[-1]), engines, total)
+            ms, _, engines, threads = ref_sample(ctx, 2, G)
+            total = S * G
+            cv = cpu_throughput(float(ms[-1]), engines, total, tokens_per_step)
             line["cpu_baseline"] = {
                 "value": cv, "unit": UNIT, "cores": threads, "kind": "reference",
-                "sample": (f"{engines} unmodified reference Engines at {args.ctx} ctx, "
+                "sample": (f"{engines} unmodified reference Engines at {ctx} ctx, "
                            f"2 decode steps on {threads} threads (last timed: "
-                           f"{ms[-1]:.0f} ms), extrapolated x{total // engines} to "
+                           f"{ms[-1]:.0f} ms), extrapolated x{total / engines:g} to "
                            f"{total} engines")}
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": host_cores(),
