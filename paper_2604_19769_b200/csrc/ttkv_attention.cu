@@ -606,12 +606,12 @@ cudaError_t launch_fast(const FastArgs& a, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // combine (attention.hpp:54-61)
 // ---------------------------------------------------------------------------
+// One CTA per (stream, head): weights w_i = exp2(m_i - M) of every partial
+// are computed once into smem, then each thread reduces one output channel.
 template <typename Acc>
-__global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
+__global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
   const Geometry& g = a.g;
-  const uint32_t idx = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const uint32_t lane = threadIdx.x & 31;
-  if (idx >= g.S * g.G) return;
+  const uint32_t idx = blockIdx.x;  // s * G + head
   const uint32_t s = idx / g.G;
   const uint32_t pitch = g.d_v + 2;
   const uint32_t nsc_used = a.union_count ? (a.union_count[s] + a.CH - 1) / a.CH : 0u;
@@ -620,33 +620,36 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
                           : nullptr;
   // literal additive merge: slow partials are already normalized sums
   const uint32_t nlse = a.literal ? 0u : nsc_used;
+  const uint32_t np = a.nfc + nlse;
+  extern __shared__ __align__(16) uint8_t csm[];
+  Acc* w = reinterpret_cast<Acc*>(csm);  // [np]
+  __shared__ Acc red[4];
+  auto part = [&](uint32_t i) { return i < a.nfc ? fp + i * pitch : sp + (i - a.nfc) * pitch; };
+
   Acc M = -INFINITY;
-  for (uint32_t i = lane; i < a.nfc; i += 32)
-    if (fp[i * pitch + g.d_v + 1] > 0) M = fmax(M, fp[i * pitch + g.d_v]);
-  for (uint32_t i = lane; i < nlse; i += 32)
-    if (sp[i * pitch + g.d_v + 1] > 0) M = fmax(M, sp[i * pitch + g.d_v]);
-  M = wmax(M);
-  Acc L = 0;
-  for (uint32_t i = lane; i < a.nfc; i += 32) {
-    const Acc l = fp[i * pitch + g.d_v + 1];
-    if (l > 0) L += l * ex2(fp[i * pitch + g.d_v] - M);
+  for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
+    const Acc* p = part(i);
+    if (p[g.d_v + 1] > 0) M = fmax(M, p[g.d_v]);
   }
-  for (uint32_t i = lane; i < nlse; i += 32) {
-    const Acc l = sp[i * pitch + g.d_v + 1];
-    if (l > 0) L += l * ex2(sp[i * pitch + g.d_v] - M);
+  M = wmax(M);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = M;
+  __syncthreads();
+  M = fmax(fmax(red[0], red[1]), fmax(red[2], red[3]));
+  __syncthreads();
+  Acc L = 0;
+  for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
+    const Acc* p = part(i);
+    const Acc wi = p[g.d_v + 1] > 0 ? ex2(p[g.d_v] - M) : Acc(0);
+    w[i] = wi;
+    L += wi * p[g.d_v + 1];
   }
   L = wsum(L);
-  const Acc inv = Acc(1) / L;
-  for (uint32_t c = lane; c < g.d_v; c += 32) {
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = L;
+  __syncthreads();
+  const Acc inv = Acc(1) / (red[0] + red[1] + red[2] + red[3]);
+  for (uint32_t c = threadIdx.x; c < g.d_v; c += blockDim.x) {
     Acc A = 0;
-    for (uint32_t i = 0; i < a.nfc; ++i) {
-      const Acc l = fp[i * pitch + g.d_v + 1];
-      if (l > 0) A += fp[i * pitch + c] * ex2(fp[i * pitch + g.d_v] - M);
-    }
-    for (uint32_t i = 0; i < nlse; ++i) {
-      const Acc l = sp[i * pitch + g.d_v + 1];
-      if (l > 0) A += sp[i * pitch + c] * ex2(sp[i * pitch + g.d_v] - M);
-    }
+    for (uint32_t i = 0; i < np; ++i) A += w[i] * part(i)[c];
     Acc o = A * inv;
     if (a.literal)
       for (uint32_t i = 0; i < nsc_used; ++i)
@@ -656,9 +659,18 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
 }
 
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
-  const uint32_t warps = a.g.S * a.g.G;
-  if (a.g.elem == 4) combine_kernel<double><<<(warps + 7) / 8, 256, 0, st>>>(a);
-  else combine_kernel<float><<<(warps + 7) / 8, 256, 0, st>>>(a);
+  const size_t acc = a.g.elem == 4 ? 8 : 4;
+  const size_t smem = (size_t)(a.nfc + a.nsc + 1) * acc;
+  const uint32_t grid = a.g.S * a.g.G;
+  if (a.g.elem == 4) {
+    cudaFuncSetAttribute(combine_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    combine_kernel<double><<<grid, 128, smem, st>>>(a);
+  } else {
+    cudaFuncSetAttribute(combine_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    combine_kernel<float><<<grid, 128, smem, st>>>(a);
+  }
   return cudaGetLastError();
 }
 

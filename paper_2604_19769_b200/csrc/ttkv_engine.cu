@@ -453,11 +453,13 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
   // softmax scale 1/sqrt(d_k) (engine.cpp:30), folded with log2(e) for exp2
   const double scale_log2 = 1.0 / std::sqrt((double)g.d_k) * 1.4426950408889634;
 
-  // fast tier on s1, overlapped with the slow stream on s0
-  CU(h, cudaEventRecord(h->ev_fork, h->s0));
-  CU(h, cudaStreamWaitEvent(h->s1, h->ev_fork, 0));
+  // Fast tier on s1 (low priority), overlapped with the PCIe-bound slow
+  // stream on s0.  It is forked after select so it never competes with the
+  // critical path append -> score -> select for SM slots.
   const uint32_t nfc = (uint32_t)((F + h->FC - 1) / h->FC);
-  {
+  auto fork_fast = [&]() -> int {
+    CU(h, cudaEventRecord(h->ev_fork, h->s0));
+    CU(h, cudaStreamWaitEvent(h->s1, h->ev_fork, 0));
     FastArgs a{};
     a.g = g;
     a.ring_k = h->ring_k;
@@ -471,10 +473,13 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
     a.TT = h->TT;
     a.stages = kFastStages;
     a.scale_log2 = scale_log2;
-    KTimer t(h, K_FAST, h->s1);
-    CU(h, launch_fast(a, h->s1));
-  }
-  CU(h, cudaEventRecord(h->ev_join, h->s1));
+    {
+      KTimer t(h, K_FAST, h->s1);
+      CU(h, launch_fast(a, h->s1));
+    }
+    CU(h, cudaEventRecord(h->ev_join, h->s1));
+    return TTKV_OK;
+  };
 
   uint32_t CH = 4;
   bool slow = n > 0 && k > 0;
@@ -506,6 +511,7 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       KTimer t(h, K_SELECT, h->s0);
       CU(h, launch_select(a, h->s0));
     }
+    if (int rcf = fork_fast()) return rcf;
     {
       SlowArgs a{};
       a.g = g;
@@ -524,6 +530,8 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       KTimer t(h, K_SLOW, h->s0);
       CU(h, launch_slow(a, (uint32_t)grid_chunks, (int)h->copy_mode, h->s0));
     }
+  } else {
+    if (int rcf = fork_fast()) return rcf;
   }
   CU(h, cudaStreamWaitEvent(h->s0, h->ev_join, 0));
   {
@@ -717,8 +725,12 @@ int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* po
   } while (0)
 
   CREATE_CU(cudaSetDevice(h->dev));
-  CREATE_CU(cudaStreamCreateWithFlags(&h->s0, cudaStreamNonBlocking));
-  CREATE_CU(cudaStreamCreateWithFlags(&h->s1, cudaStreamNonBlocking));
+  {  // s0 carries the critical path (high priority), s1 the overlapped fast tier
+    int lo = 0, hi = 0;
+    CREATE_CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CREATE_CU(cudaStreamCreateWithPriority(&h->s0, cudaStreamNonBlocking, hi));
+    CREATE_CU(cudaStreamCreateWithPriority(&h->s1, cudaStreamNonBlocking, lo));
+  }
   CREATE_CU(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
   CREATE_CU(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   const size_t S = g.S;
