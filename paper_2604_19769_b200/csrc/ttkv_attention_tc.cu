@@ -1,0 +1,334 @@
+// ttkv_attention_tc.cu -- tensor-core fast-tier attention (fp16 ring).
+//
+// fast_attn_partial for the fp16 ring when d_k = d_v in {64, 128} and the
+// block size is a multiple of 64 (64-token tiles then never straddle the
+// ring wrap).  Replaces engine.cpp:36-40 / attention.hpp:29-50 for the fast
+// tier, like the CUDA-core kernel in ttkv_attention.cu, but:
+//   * the producer loads 64-token K and V tiles with TMA tensor copies
+//     (cp.async.bulk.tensor.2d, 128B swizzle) into a 3-stage smem ring;
+//   * QK^T and PV run on tensor cores (mma.sync m16n8k16, f16 in, f32
+//     accumulate): the M dimension carries the G <= 8 query heads of the KV
+//     head, ldmatrix (swizzle-aware, conflict-free) feeds K as B and V as B^T;
+//   * q and P are split into fp16 hi + lo parts (two MMAs each), so operand
+//     rounding stays ~2^-22 relative: the result matches the fp32 CUDA-core
+//     path well inside the 1e-3 contract;
+//   * each consumer warp owns a quarter of the output channels, so PV needs
+//     no cross-warp reduction; online-softmax statistics are per 64-token tile.
+// HBM-bound: F * (d_k + d_v) * 2 bytes per stream.
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <math.h>
+
+#include "ttkv_kernels.cuh"
+#include "ttkv_launch.h"
+
+namespace ttkv_dev {
+
+namespace {
+
+constexpr int kTT = 64;          // tokens per tile
+constexpr int kStages = 3;
+constexpr uint32_t kBox = kTT * 128;  // one 64-token x 128-byte box
+
+__device__ __forceinline__ uint32_t swz128(uint32_t off) {  // TMA SWIZZLE_128B
+  return off ^ (((off >> 7) & 7u) << 4);
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                        uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                          uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+// D += A(16x16, rows = heads, only a0/a2 non-zero) * B(16x8)
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(x0, x1);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+}  // namespace
+
+template <int ND, int GT>
+__global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
+    fast_attn_tc_kernel(const __grid_constant__ FastTcArgs a) {
+  constexpr int D = 64 * ND;        // head dim
+  constexpr int KSTEPS = D / 16;    // QK k-steps
+  constexpr uint32_t STAGE = 2 * ND * kBox;
+  const Geometry& g = a.g;
+  const uint32_t s = blockIdx.y, f = blockIdx.x;
+  const uint32_t t0 = f * a.FC;
+  const uint32_t t1 = min(t0 + a.FC, a.F);
+  const uint32_t ntiles = t1 > t0 ? (t1 - t0 + kTT - 1) / kTT : 0;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + kStages * STAGE);
+  uint64_t* empty = full + kStages;
+  float* sc = reinterpret_cast<float*>(empty + kStages);  // [2][GT][kTT]
+  float* mst = sc + 2 * GT * kTT;
+  float* lst = mst + GT;
+  float* ast = lst + GT;
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kSlowConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  if (threadIdx.x < GT) {
+    mst[threadIdx.x] = -INFINITY;
+    lst[threadIdx.x] = 0.0f;
+    ast[threadIdx.x] = 1.0f;
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ---- producer: TMA tensor loads of K and V tiles ----
+    if (lane == 0) {
+      for (uint32_t i = 0; i < ntiles; ++i) {
+        const uint32_t st = i % kStages;
+        if (i >= kStages) mbar_wait(&empty[st], ((i / kStages) - 1) & 1);
+        const int row = (int)(s * g.C + (a.front + t0 + i * kTT) % g.C);
+        uint8_t* kb = base + st * STAGE;
+        uint8_t* vb = kb + ND * kBox;
+        mbar_arrive_expect_tx(&full[st], STAGE);
+#pragma unroll
+        for (int b = 0; b < ND; ++b) {
+          tma_load_2d(kb + b * kBox, &a.tk, 64 * b, row, &full[st]);
+          tma_load_2d(vb + b * kBox, &a.tv, 64 * b, row, &full[st]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumers ----
+  const uint32_t cw = warp - 1;
+  const uint32_t gq = lane >> 2, qq = lane & 3;  // mma group (head row) / thread in group
+  const bool head_ok = gq < g.G;
+  // A fragments of q (scaled into log2 units), hi + lo
+  uint32_t aqh[KSTEPS][2], aql[KSTEPS][2];
+  {
+    const float* qr = a.q + ((uint64_t)s * g.G + (head_ok ? gq : 0)) * D;
+    const float sl = (float)a.scale_log2;
+#pragma unroll
+    for (int ks = 0; ks < KSTEPS; ++ks) {
+      const int c = 16 * ks + 2 * qq;
+      const float x0 = head_ok ? qr[c] * sl : 0.f, x1 = head_ok ? qr[c + 1] * sl : 0.f;
+      const float x8 = head_ok ? qr[c + 8] * sl : 0.f, x9 = head_ok ? qr[c + 9] * sl : 0.f;
+      split2(x0, x1, aqh[ks][0], aql[ks][0]);
+      split2(x8, x9, aqh[ks][1], aql[ks][1]);
+    }
+  }
+  constexpr int NT_PV = D / 8 / kSlowConsumerWarps;  // output n-tiles per warp
+  float acc[NT_PV][4];
+#pragma unroll
+  for (int j = 0; j < NT_PV; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+  const int nthreads_c = kSlowConsumerWarps * 32;
+
+  for (uint32_t i = 0; i < ntiles; ++i) {
+    const uint32_t st = i % kStages;
+    mbar_wait(&full[st], (i / kStages) & 1);
+    const uint32_t kb = smem_u32(base + st * STAGE);
+    const uint32_t vb = kb + ND * kBox;
+    const uint32_t rows = min((uint32_t)kTT, t1 - (t0 + i * kTT));
+    float* scb = sc + (i & 1) * GT * kTT;
+
+    // ---- QK^T: warp cw -> tokens [16cw, 16cw + 16) ----
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int nt = 2 * cw + h;
+      float c[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int kp = 0; kp < KSTEPS / 2; ++kp) {
+        // matrices: (ks lo8, ks hi8, ks+1 lo8, ks+1 hi8) of tokens [8nt, 8nt+8)
+        const int m = lane >> 3;
+        const int row = 8 * nt + (lane & 7);
+        const int ch = 16 * (2 * kp + (m >> 1)) + 8 * (m & 1);
+        const uint32_t addr = kb + (ch >> 6) * kBox + swz128(row * 128 + (ch & 63) * 2);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(addr, b0, b1, b2, b3);
+        mma16816(c, aqh[2 * kp][0], aqh[2 * kp][1], b0, b1);
+        mma16816(c, aql[2 * kp][0], aql[2 * kp][1], b0, b1);
+        mma16816(c, aqh[2 * kp + 1][0], aqh[2 * kp + 1][1], b2, b3);
+        mma16816(c, aql[2 * kp + 1][0], aql[2 * kp + 1][1], b2, b3);
+      }
+      if (head_ok) {
+        const uint32_t tA = 8 * nt + 2 * qq;
+        scb[gq * kTT + tA] = tA < rows ? c[0] : -INFINITY;
+        scb[gq * kTT + tA + 1] = tA + 1 < rows ? c[1] : -INFINITY;
+      }
+    }
+    named_bar(1, nthreads_c);
+
+    // ---- tile softmax statistics, one warp per head ----
+    for (uint32_t h = cw; h < g.G; h += kSlowConsumerWarps) {
+      float* row = scb + h * kTT;
+      float bm = fmaxf(row[lane], row[lane + 32]);
+      bm = warp_max(bm);
+      const float m_old = mst[h];
+      const float m_new = fmaxf(m_old, bm);
+      const float p0 = exp2f(row[lane] - m_new), p1 = exp2f(row[lane + 32] - m_new);
+      row[lane] = p0;
+      row[lane + 32] = p1;
+      const float sum = warp_sum(p0 + p1);
+      if (lane == 0) {
+        const float alpha = exp2f(m_old - m_new);
+        lst[h] = lst[h] * alpha + sum;
+        mst[h] = m_new;
+        ast[h] = alpha;
+      }
+    }
+    named_bar(1, nthreads_c);
+
+    // ---- PV: warp cw -> channels [8 NT_PV cw, 8 NT_PV (cw+1)) ----
+    {
+      const float alpha = head_ok ? ast[gq] : 1.0f;
+#pragma unroll
+      for (int j = 0; j < NT_PV; ++j) {
+        acc[j][0] *= alpha;
+        acc[j][1] *= alpha;
+      }
+#pragma unroll
+      for (int ks = 0; ks < kTT / 16; ++ks) {
+        uint32_t ph0, pl0, ph1, pl1;
+        {
+          const float* pr = scb + (head_ok ? gq : 0) * kTT + 16 * ks + 2 * qq;
+          const float2 p01 = head_ok ? *reinterpret_cast<const float2*>(pr) : make_float2(0, 0);
+          const float2 p89 = head_ok ? *reinterpret_cast<const float2*>(pr + 8) : make_float2(0, 0);
+          split2(p01.x, p01.y, ph0, pl0);
+          split2(p89.x, p89.y, ph1, pl1);
+        }
+#pragma unroll
+        for (int jp = 0; jp < NT_PV / 2; ++jp) {
+          // matrices: (tok lo8, ntA), (tok hi8, ntA), (tok lo8, ntB), (tok hi8, ntB)
+          const int m = lane >> 3;
+          const int ntc = NT_PV * cw + 2 * jp + (m >> 1);
+          const int row = 16 * ks + 8 * (m & 1) + (lane & 7);
+          const int ch = 8 * ntc;
+          const uint32_t addr = vb + (ch >> 6) * kBox + swz128(row * 128 + (ch & 63) * 2);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(addr, b0, b1, b2, b3);
+          mma16816(acc[2 * jp], ph0, ph1, b0, b1);
+          mma16816(acc[2 * jp], pl0, pl1, b0, b1);
+          mma16816(acc[2 * jp + 1], ph0, ph1, b2, b3);
+          mma16816(acc[2 * jp + 1], pl0, pl1, b2, b3);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+
+  // ---- emit the (acc, m, l) partial of every head ----
+  named_bar(1, nthreads_c);
+  const uint32_t pitch = D + 2;
+  float* part = reinterpret_cast<float*>(a.part) + (((uint64_t)s * g.G) * a.nfc + f) * pitch;
+  const uint64_t head_stride = (uint64_t)a.nfc * pitch;
+  if (head_ok) {
+    float* p = part + gq * head_stride;
+#pragma unroll
+    for (int j = 0; j < NT_PV; ++j) {
+      const int ch = 8 * (NT_PV * cw + j) + 2 * qq;
+      p[ch] = ntiles ? acc[j][0] : 0.f;
+      p[ch + 1] = ntiles ? acc[j][1] : 0.f;
+    }
+    if (cw == 0 && qq == 0) {
+      p[D] = ntiles ? mst[gq] : -INFINITY;
+      p[D + 1] = ntiles ? lst[gq] : 0.f;
+    }
+  }
+}
+
+bool fast_tc_supported(const Geometry& g) {
+  return g.elem == 2 && g.d_k == g.d_v && (g.d_k == 64 || g.d_k == 128) && g.B % kTT == 0 &&
+         g.G <= 8;
+}
+
+uint32_t fast_tc_tile() { return kTT; }
+
+static size_t fast_tc_smem(const Geometry& g) {
+  const int ND = g.d_k / 64;
+  return 1024 + (size_t)kStages * 2 * ND * kBox + 2 * kStages * 8 + (2 * 8 * kTT + 3 * 8) * 4 + 64;
+}
+
+template <int ND, int GT>
+static cudaError_t launch_fast_tc_t(const FastTcArgs& a, cudaStream_t st) {
+  const size_t smem = fast_tc_smem(a.g);
+  auto kern = fast_attn_tc_kernel<ND, GT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid(a.nfc, a.g.S);
+  kern<<<grid, 32 + kSlowConsumerWarps * 32, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int ND>
+static cudaError_t launch_fast_tc_g(const FastTcArgs& a, cudaStream_t st) {
+  if (a.g.G <= 1) return launch_fast_tc_t<ND, 1>(a, st);
+  if (a.g.G <= 2) return launch_fast_tc_t<ND, 2>(a, st);
+  if (a.g.G <= 4) return launch_fast_tc_t<ND, 4>(a, st);
+  return launch_fast_tc_t<ND, 8>(a, st);
+}
+
+cudaError_t launch_fast_tc(const FastTcArgs& a, cudaStream_t st) {
+  return a.g.d_k == 128 ? launch_fast_tc_g<2>(a, st) : launch_fast_tc_g<1>(a, st);
+}
+
+// Tensor maps of the fp16 ring: [S*C rows][d] halves, 64 x 64 boxes, 128B swizzle.
+cudaError_t make_ring_tmaps(const Geometry& g, void* ring_k, void* ring_v, FastTcArgs& a) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
+    encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  const cuuint64_t dims[2] = {g.d_k, (cuuint64_t)g.S * g.C};
+  const cuuint64_t strides[1] = {(cuuint64_t)g.d_k * 2};
+  const cuuint32_t box[2] = {64, (cuuint32_t)kTT};
+  const cuuint32_t estr[2] = {1, 1};
+  for (int t = 0; t < 2; ++t) {
+    CUresult r = encode(t ? &a.tv : &a.tk, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, t ? ring_v : ring_k,
+                        dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace ttkv_dev

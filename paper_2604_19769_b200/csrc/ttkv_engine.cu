@@ -144,6 +144,8 @@ struct ttkv_gpu {
   uint64_t last_k = 0, last_n = 0;
   // fast split
   uint32_t FC = 256, nfc_cap = 1, TT = 64;
+  bool fast_tc = false;      // tensor-core fast tier (TMA tensor maps)
+  FastTcArgs tc{};           // ring tensor maps, encoded once at create
   size_t acc = 4;  // bytes of the accumulation type (fp32, or fp64 for the fp32 ring)
   // device memory
   void* ring_k = nullptr;
@@ -460,6 +462,23 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
   auto fork_fast = [&]() -> int {
     CU(h, cudaEventRecord(h->ev_fork, h->s0));
     CU(h, cudaStreamWaitEvent(h->s1, h->ev_fork, 0));
+    if (h->fast_tc) {
+      FastTcArgs& a = h->tc;
+      a.g = g;
+      a.q = q;
+      a.part = h->fpart;
+      a.front = h->fast_front;
+      a.F = (uint32_t)F;
+      a.FC = h->FC;
+      a.nfc = nfc;
+      a.scale_log2 = scale_log2;
+      {
+        KTimer t(h, K_FAST, h->s1);
+        CU(h, launch_fast_tc(a, h->s1));
+      }
+      CU(h, cudaEventRecord(h->ev_join, h->s1));
+      return TTKV_OK;
+    }
     FastArgs a{};
     a.g = g;
     a.ring_k = h->ring_k;
@@ -704,7 +723,9 @@ int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* po
   // fast split: chunks of whole TT-token tiles, ~4 waves of 2 CTAs per SM
   h->acc = g.elem == 4 ? 8 : 4;
   {
-    h->TT = fast_tile_rows(g);
+    const char* tc_env = std::getenv("TTKV_FAST_TC");
+    h->fast_tc = fast_tc_supported(g) && !(tc_env && tc_env[0] == '0');
+    h->TT = h->fast_tc ? fast_tc_tile() : fast_tile_rows(g);
     const uint64_t Fmax = l_fast + g.B;  // ring capacity bounds the fast tier
     const uint64_t target = std::max<uint64_t>(1, (148ull * 2 * 4 + g.S - 1) / g.S);
     uint64_t FC = (Fmax + target - 1) / target;
@@ -738,6 +759,10 @@ int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* po
   CREATE_CU(cudaMalloc(&h->ring_v, S * g.C * g.d_v * g.elem));
   CREATE_CU(cudaMemset(h->ring_k, 0, S * g.C * g.d_k * g.elem));
   CREATE_CU(cudaMemset(h->ring_v, 0, S * g.C * g.d_v * g.elem));
+  if (h->fast_tc && make_ring_tmaps(g, h->ring_k, h->ring_v, h->tc) != cudaSuccess) {
+    // tensor-map encoding unavailable: keep the CUDA-core fast tier (64-token tiles)
+    h->fast_tc = false;
+  }
   CREATE_CU(cudaMalloc((void**)&h->ucount, S * sizeof(uint32_t)));
   CREATE_CU(cudaMemset(h->ucount, 0, S * sizeof(uint32_t)));
   CREATE_CU(cudaMalloc((void**)&h->counters, 4 * sizeof(unsigned long long)));

@@ -1,5 +1,6 @@
 // ttkv_launch.h -- host-side launchers of the sm_100a kernels (internal).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -79,6 +80,23 @@ struct FastArgs {
 cudaError_t launch_fast(const FastArgs& a, cudaStream_t st);
 uint32_t fast_tile_rows(const Geometry& g);
 constexpr uint32_t kFastStages = 3;
+
+// Tensor-core fast tier (fp16 ring, d in {64,128}, B % 64 == 0): TMA tensor
+// maps of the ring + mma.sync consumers (ttkv_attention_tc.cu).
+struct alignas(64) FastTcArgs {
+  CUtensorMap tk;
+  CUtensorMap tv;
+  Geometry g;
+  const float* q;
+  void* part;  // float [S][G][nfc][d_v+2]
+  uint64_t front;
+  uint32_t F, FC, nfc;
+  double scale_log2;
+};
+bool fast_tc_supported(const Geometry& g);
+uint32_t fast_tc_tile();
+cudaError_t make_ring_tmaps(const Geometry& g, void* ring_k, void* ring_v, FastTcArgs& a);
+cudaError_t launch_fast_tc(const FastTcArgs& a, cudaStream_t st);
 
 struct SlowArgs {
   Geometry g;
