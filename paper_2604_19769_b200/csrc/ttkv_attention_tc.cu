@@ -268,6 +268,373 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
   }
 }
 
+// ---------------------------------------------------------------------------
+// slow tier on tensor cores: K8/V4, d = 128, B = 128, fp16 ring (fp32 accum).
+// Per record: K codes [128 tok][128 B] by TMA (128B swizzle), V nibbles
+// [128 tok][64 B] by TMA (64B swizzle), params (2 KB) by bulk copy from the
+// HBM mirror.  QK^T = (q * s) . code + q . z  (scales folded into the A
+// operand, codes exact in fp16); PV = s * (P . code) + z *
+// sum(P) applied per block in the epilogue.  ldmatrix on the u8 code rows
+// yields 4 consecutive channels per thread, so the contraction index is
+// permuted identically in A and B (any permutation of a dot product's terms
+// is exact in real arithmetic).
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int kSlowTcStages = 2;
+constexpr uint32_t kKBox = 128 * 128;  // K codes
+constexpr uint32_t kVBox = 128 * 64;   // V nibbles
+constexpr uint32_t kPBytes = 2 * 128 * 8;  // {scale, zp} x (128 K + 128 V)
+constexpr uint32_t kSlowStage = kKBox + kVBox + kPBytes;  // 26,624 B
+
+__device__ __forceinline__ uint32_t swz64(uint32_t off) {  // TMA SWIZZLE_64B
+  return off ^ (((off >> 7) & 3u) << 4);
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+// 4 u8 codes -> two half2 {c0,c1}, {c2,c3} (exact: 1024 + c minus 1024)
+__device__ __forceinline__ void codes_to_h2(uint32_t w, uint32_t& lo, uint32_t& hi) {
+  const uint32_t a = __byte_perm(w, 0x64646464u, 0x5140u);
+  const uint32_t b = __byte_perm(w, 0x64646464u, 0x7362u);
+  const __half2 off = __floats2half2_rn(1024.f, 1024.f);
+  __half2 ha = __hsub2(*reinterpret_cast<const __half2*>(&a), off);
+  __half2 hb = __hsub2(*reinterpret_cast<const __half2*>(&b), off);
+  lo = *reinterpret_cast<uint32_t*>(&ha);
+  hi = *reinterpret_cast<uint32_t*>(&hb);
+}
+}  // namespace
+
+template <int GT>
+__global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
+    slow_attn_tc_kernel(const __grid_constant__ SlowTcArgs a) {
+  const Geometry& g = a.g;
+  const uint32_t s = blockIdx.y, chunk = blockIdx.x;
+  const uint32_t cnt = a.union_count[s];
+  const uint32_t i0 = chunk * a.CH;
+  if (i0 >= cnt) return;
+  const uint32_t nb = min(i0 + a.CH, cnt) - i0;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* vtile = base + kSlowTcStages * kSlowStage;            // 2 boxes [128][128 B] fp16
+  uint64_t* full = reinterpret_cast<uint64_t*>(vtile + 2 * 128 * 128);
+  uint64_t* empty = full + kSlowTcStages;
+  float* sc2 = reinterpret_cast<float*>(empty + kSlowTcStages);  // [2][GT][128]
+  float* mst = sc2 + 2 * GT * 128;
+  float* lst = mst + GT;
+  float* ast = lst + GT;
+  float* pst = ast + GT;  // sum_t p of the current block
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kSlowTcStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kSlowConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  if (threadIdx.x < GT) {
+    mst[threadIdx.x] = -INFINITY;
+    lst[threadIdx.x] = 0.0f;
+  }
+  __syncthreads();
+  const uint32_t* uids = a.union_ids + (uint64_t)s * g.n_cap + i0;
+  const uint32_t* umask = a.union_mask + (uint64_t)s * g.n_cap + i0;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (uint32_t i = 0; i < nb; ++i) {
+        const uint32_t st = i % kSlowTcStages;
+        if (i >= kSlowTcStages) mbar_wait(&empty[st], ((i / kSlowTcStages) - 1) & 1);
+        const uint32_t blk = uids[i];
+        const int rec = (int)((uint64_t)s * g.n_cap + blk);
+        uint8_t* dst = base + st * kSlowStage;
+        mbar_arrive_expect_tx(&full[st], kSlowStage);
+        tma_load_3d(dst, &a.tk, 0, 0, rec, &full[st]);
+        tma_load_3d(dst + kKBox, &a.tv, 0, 0, rec, &full[st]);
+        bulk_g2s(dst + kKBox + kVBox, a.params + (uint64_t)rec * kPBytes, kPBytes, &full[st]);
+      }
+    }
+    return;
+  }
+
+  const uint32_t cw = warp - 1, ct = threadIdx.x - 32;
+  const uint32_t gq = lane >> 2, qq = lane & 3;
+  const bool head_ok = gq < g.G;
+  const int nthreads_c = kSlowConsumerWarps * 32;
+  // this thread's 32 query channels (permuted order), log2-scaled:
+  // segment j -> channels 16j + 4qq + {0,1,2,3}
+  float qv[8][4];
+  {
+    const float* qr = a.q + ((uint64_t)s * g.G + (head_ok ? gq : 0)) * 128;
+    const float sl = (float)a.scale_log2;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) qv[j][e] = head_ok ? qr[16 * j + 4 * qq + e] * sl : 0.f;
+  }
+  float acc[4][2];  // running output: head gq, channels 8(4cw + j) + 2qq + {0,1}
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.f;
+  uint32_t seen = 0;
+
+  for (uint32_t i = 0; i < nb; ++i) {
+    const uint32_t st = i % kSlowTcStages;
+    mbar_wait(&full[st], (i / kSlowTcStages) & 1);
+    uint8_t* stg = base + st * kSlowStage;
+    const uint32_t kb = smem_u32(stg), vb_nib = kKBox;  // V nibbles at stg + kKBox
+    const float* kp = reinterpret_cast<const float*>(stg + kKBox + kVBox);  // {s,z} x 128
+    const float* vp = kp + 2 * 128;
+    const uint32_t hm = umask[i];
+    seen |= hm;
+    float* sc = sc2 + (i & 1) * GT * 128;  // double-buffered: PV(i-1) may still read
+
+    // ---- A operand: (q * s) hi/lo in the permuted channel order, beta = q . z ----
+    uint32_t ah[8][2], al[8][2];
+    float beta = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float4 sz0 = *reinterpret_cast<const float4*>(kp + 2 * (16 * j + 4 * qq));
+      const float4 sz1 = *reinterpret_cast<const float4*>(kp + 2 * (16 * j + 4 * qq) + 4);
+      const float x0 = qv[j][0] * sz0.x, x1 = qv[j][1] * sz0.z;
+      const float x2 = qv[j][2] * sz1.x, x3 = qv[j][3] * sz1.z;
+      beta += qv[j][0] * sz0.y + qv[j][1] * sz0.w + qv[j][2] * sz1.y + qv[j][3] * sz1.w;
+      split2(x0, x1, ah[j][0], al[j][0]);
+      split2(x2, x3, ah[j][1], al[j][1]);
+    }
+    beta += __shfl_xor_sync(0xffffffffu, beta, 1);
+    beta += __shfl_xor_sync(0xffffffffu, beta, 2);
+
+    // ---- QK^T: warp cw -> tokens [32cw, 32cw + 32) ----
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int nt = 4 * cw + h;
+      float c[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int jp = 0; jp < 2; ++jp) {
+        const int m = lane >> 3;
+        const int row = 8 * nt + (lane & 7);
+        const uint32_t addr = kb + swz128(row * 128 + (4 * jp + m) * 16);
+        uint32_t r[4];
+        ldsm_x4(addr, r[0], r[1], r[2], r[3]);
+#pragma unroll
+        for (int mm = 0; mm < 4; ++mm) {
+          uint32_t b0, b1;
+          codes_to_h2(r[mm], b0, b1);
+          const int j = 4 * jp + mm;
+          mma16816(c, ah[j][0], ah[j][1], b0, b1);
+          mma16816(c, al[j][0], al[j][1], b0, b1);
+        }
+      }
+      if (head_ok) {
+        const uint32_t tA = 8 * nt + 2 * qq;
+        sc[gq * 128 + tA] = c[0] + beta;
+        sc[gq * 128 + tA + 1] = c[1] + beta;
+      }
+    }
+    named_bar(1, nthreads_c);
+
+    // ---- block softmax statistics (one warp per selecting head) ----
+    for (uint32_t h = cw; h < g.G; h += kSlowConsumerWarps) {
+      if (!((hm >> h) & 1u)) continue;
+      float* row = sc + h * 128;
+      float bm = fmaxf(fmaxf(row[lane], row[lane + 32]), fmaxf(row[lane + 64], row[lane + 96]));
+      bm = warp_max(bm);
+      const float m_old = mst[h];
+      const float m_new = a.literal ? bm : fmaxf(m_old, bm);
+      float sum = 0.f;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float p = exp2f(row[lane + 32 * k] - m_new);
+        row[lane + 32 * k] = p;
+        sum += p;
+      }
+      sum = warp_sum(sum);
+      if (a.literal) {  // each block its own normalized partition (engine.cpp:67-72)
+        const float inv = 1.0f / sum;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) row[lane + 32 * k] *= inv;
+      }
+      if (lane == 0) {
+        if (a.literal) {
+          ast[h] = 1.0f;
+          pst[h] = 1.0f;
+        } else {
+          const float alpha = exp2f(m_old - m_new);
+          lst[h] = lst[h] * alpha + sum;
+          mst[h] = m_new;
+          ast[h] = alpha;
+          pst[h] = sum;
+        }
+      }
+    }
+    // ---- V nibbles -> fp16 codes tile (thread ct converts token row ct) ----
+    {
+      const uint8_t* vn = stg + vb_nib;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {  // 16-byte chunks = 32 channels each
+        const uint4 w = *reinterpret_cast<const uint4*>(vn + swz64(ct * 64 + 16 * cc));
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // 8 channels: 32cc + 8u .. + 7
+          const uint32_t e = ws[u] & 0x0F0F0F0Fu, o = (ws[u] >> 4) & 0x0F0F0F0Fu;
+          uint32_t h2[4];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            // result bytes [e.b, o.b, -, -] -> halves {e.b, o.b} = channels 2b, 2b+1
+            const uint32_t x = __byte_perm(e, o, (uint32_t)b | ((4u + (uint32_t)b) << 4));
+            const uint32_t hx = (x & 0x000000FFu) | ((x & 0x0000FF00u) << 8) | 0x64006400u;
+            const __half2 hv = __hsub2(*reinterpret_cast<const __half2*>(&hx),
+                                       __floats2half2_rn(1024.f, 1024.f));
+            h2[b] = *reinterpret_cast<const uint32_t*>(&hv);
+          }
+          const int ch = 32 * cc + 8 * u;
+          *reinterpret_cast<uint4*>(vtile + (ch >> 6) * (128 * 128) +
+                                    swz128(ct * 128 + (ch & 63) * 2)) =
+              make_uint4(h2[0], h2[1], h2[2], h2[3]);
+        }
+      }
+    }
+    named_bar(1, nthreads_c);
+
+    // ---- PV on codes: warp cw -> channels [32cw, 32cw + 32) ----
+    {
+      const uint32_t vt = smem_u32(vtile);
+      float cfr[4][4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) cfr[j][0] = cfr[j][1] = cfr[j][2] = cfr[j][3] = 0.f;
+      const bool sel = head_ok && ((hm >> gq) & 1u);
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        uint32_t ph0, pl0, ph1, pl1;
+        {
+          const float* pr = sc + (head_ok ? gq : 0) * 128 + 16 * ks + 2 * qq;
+          const float2 p01 = sel ? *reinterpret_cast<const float2*>(pr) : make_float2(0, 0);
+          const float2 p89 = sel ? *reinterpret_cast<const float2*>(pr + 8) : make_float2(0, 0);
+          split2(p01.x, p01.y, ph0, pl0);
+          split2(p89.x, p89.y, ph1, pl1);
+        }
+#pragma unroll
+        for (int jp = 0; jp < 2; ++jp) {
+          const int m = lane >> 3;
+          const int ntc = 4 * cw + 2 * jp + (m >> 1);
+          const int row = 16 * ks + 8 * (m & 1) + (lane & 7);
+          const int ch = 8 * ntc;
+          const uint32_t addr = vt + (ch >> 6) * (128 * 128) + swz128(row * 128 + (ch & 63) * 2);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(addr, b0, b1, b2, b3);
+          mma16816(cfr[2 * jp], ph0, ph1, b0, b1);
+          mma16816(cfr[2 * jp], pl0, pl1, b0, b1);
+          mma16816(cfr[2 * jp + 1], ph0, ph1, b2, b3);
+          mma16816(cfr[2 * jp + 1], pl0, pl1, b2, b3);
+        }
+      }
+      // affine epilogue: acc = acc * alpha + s_c * (P . code) + z_c * sum(P)
+      if (sel) {
+        const float alpha = ast[gq], psum = pst[gq];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int ch = 8 * (4 * cw + j) + 2 * qq;
+          const float4 sz = *reinterpret_cast<const float4*>(vp + 2 * ch);
+          acc[j][0] = acc[j][0] * alpha + sz.x * cfr[j][0] + sz.y * psum;
+          acc[j][1] = acc[j][1] * alpha + sz.z * cfr[j][1] + sz.w * psum;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+
+  named_bar(1, nthreads_c);
+  const uint32_t pitch = 128 + 2;
+  if (head_ok) {
+    float* p = reinterpret_cast<float*>(a.part) +
+               (((uint64_t)s * g.G + gq) * a.nsc + chunk) * pitch;
+    const bool any = (seen >> gq) & 1u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int ch = 8 * (4 * cw + j) + 2 * qq;
+      p[ch] = any ? acc[j][0] : 0.f;
+      p[ch + 1] = any ? acc[j][1] : 0.f;
+    }
+    if (cw == 0 && qq == 0) {
+      p[128] = any ? (a.literal ? 0.f : mst[gq]) : -INFINITY;
+      p[129] = any ? (a.literal ? 1.f : lst[gq]) : 0.f;
+    }
+  }
+}
+
+bool slow_tc_supported(const Geometry& g) {
+  return g.elem == 2 && g.d_k == 128 && g.d_v == 128 && g.B == 128 && g.kb == 8 && g.vb == 4 &&
+         g.G <= 8 && g.rec.kp_off == kKBox + kVBox && g.rec.used == kSlowStage;
+}
+
+static size_t slow_tc_smem() {
+  return 1024 + (size_t)kSlowTcStages * kSlowStage + 2 * 128 * 128 + 2 * kSlowTcStages * 8 +
+         (2 * 8 * 128 + 4 * 8) * 4 + 64;
+}
+
+template <int GT>
+static cudaError_t launch_slow_tc_t(const SlowTcArgs& a, uint32_t grid_chunks, cudaStream_t st) {
+  const size_t smem = slow_tc_smem();
+  auto kern = slow_attn_tc_kernel<GT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid(grid_chunks, a.g.S);
+  kern<<<grid, 32 + kSlowConsumerWarps * 32, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_slow_tc(const SlowTcArgs& a, uint32_t grid_chunks, cudaStream_t st) {
+  if (grid_chunks == 0) return cudaSuccess;
+  if (a.g.G <= 1) return launch_slow_tc_t<1>(a, grid_chunks, st);
+  if (a.g.G <= 2) return launch_slow_tc_t<2>(a, grid_chunks, st);
+  if (a.g.G <= 4) return launch_slow_tc_t<4>(a, grid_chunks, st);
+  return launch_slow_tc_t<8>(a, grid_chunks, st);
+}
+
+// Tensor maps over the record arena (device or mapped host pointer):
+//   K codes  [S*n_cap records][128 tok][128 B], box 128 x 128 x 1, 128B swizzle
+//   V nibbles[S*n_cap records][128 tok][64 B],  box  64 x 128 x 1,  64B swizzle
+cudaError_t make_arena_tmaps(const Geometry& g, uint8_t* arena, SlowTcArgs& a) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
+  EncodeFn encode = reinterpret_cast<EncodeFn>(fn);
+  const cuuint64_t recs = (cuuint64_t)g.S * g.n_cap;
+  const cuuint32_t estr[3] = {1, 1, 1};
+  {
+    const cuuint64_t dims[3] = {128, 128, recs};
+    const cuuint64_t strides[2] = {128, g.rec.stride};
+    const cuuint32_t box[3] = {128, 128, 1};
+    if (encode(&a.tk, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, arena, dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  {
+    const cuuint64_t dims[3] = {64, 128, recs};
+    const cuuint64_t strides[2] = {64, g.rec.stride};
+    const cuuint32_t box[3] = {64, 128, 1};
+    if (encode(&a.tv, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, arena + g.rec.v_off, dims, strides, box,
+               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  return cudaSuccess;
+}
+
 bool fast_tc_supported(const Geometry& g) {
   return g.elem == 2 && g.d_k == g.d_v && (g.d_k == 64 || g.d_k == 128) && g.B % kTT == 0 &&
          g.G <= 8;

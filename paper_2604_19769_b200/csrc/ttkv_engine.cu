@@ -146,6 +146,8 @@ struct ttkv_gpu {
   uint32_t FC = 256, nfc_cap = 1, TT = 64;
   bool fast_tc = false;      // tensor-core fast tier (TMA tensor maps)
   FastTcArgs tc{};           // ring tensor maps, encoded once at create
+  bool slow_tc = false;      // tensor-core slow tier (arena tensor maps)
+  SlowTcArgs stc{};          // re-encoded whenever the arena is reallocated
   size_t acc = 4;  // bytes of the accumulation type (fp32, or fp64 for the fp32 ring)
   // device memory
   void* ring_k = nullptr;
@@ -327,6 +329,8 @@ int ensure_blocks(ttkv_gpu* h, uint64_t need) {
   CU(h, realloc_dev((void**)&h->uids, S * cap * sizeof(uint32_t)));
   CU(h, realloc_dev((void**)&h->umask, S * cap * sizeof(uint32_t)));
   h->g.n_cap = cap;
+  if (h->slow_tc && make_arena_tmaps(h->g, h->arena_dev, h->stc) != cudaSuccess)
+    h->slow_tc = false;  // fall back to the CUDA-core slow tier
   return TTKV_OK;
 }
 
@@ -531,7 +535,22 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       CU(h, launch_select(a, h->s0));
     }
     if (int rcf = fork_fast()) return rcf;
-    {
+    if (h->slow_tc) {
+      SlowTcArgs& a = h->stc;
+      a.g = g;
+      a.params = h->params;
+      a.union_ids = h->uids;
+      a.union_mask = h->umask;
+      a.union_count = h->ucount;
+      a.q = q;
+      a.part = h->spart;
+      a.CH = CH;
+      a.nsc = (uint32_t)h->spart_chunks;
+      a.literal = h->opt.literal_additive_merge ? 1u : 0u;
+      a.scale_log2 = scale_log2;
+      KTimer t(h, K_SLOW, h->s0);
+      CU(h, launch_slow_tc(a, (uint32_t)grid_chunks, h->s0));
+    } else {
       SlowArgs a{};
       a.g = g;
       a.arena = h->arena_dev;
@@ -725,6 +744,11 @@ int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* po
   {
     const char* tc_env = std::getenv("TTKV_FAST_TC");
     h->fast_tc = fast_tc_supported(g) && !(tc_env && tc_env[0] == '0');
+    // tensor-core slow tier: HBM-resident records (the CUDA-core consumer has
+    // 3x headroom over the PCIe link); TTKV_SLOW_TC=1/0 forces it on/off
+    const char* stc_env = std::getenv("TTKV_SLOW_TC");
+    h->slow_tc = slow_tc_supported(g) &&
+                 (stc_env ? stc_env[0] == '1' : opt->slow_tier == TTKV_SLOW_DEVICE);
     h->TT = h->fast_tc ? fast_tc_tile() : fast_tile_rows(g);
     const uint64_t Fmax = l_fast + g.B;  // ring capacity bounds the fast tier
     const uint64_t target = std::max<uint64_t>(1, (148ull * 2 * 4 + g.S - 1) / g.S);

@@ -93,6 +93,25 @@ struct alignas(64) FastTcArgs {
   uint32_t F, FC, nfc;
   double scale_log2;
 };
+// Tensor-core slow tier (K8/V4, d = B = 128): TMA tensor maps over the
+// record arena + mma.sync on raw codes with the affine params folded in.
+struct alignas(64) SlowTcArgs {
+  CUtensorMap tk;  // K codes
+  CUtensorMap tv;  // V nibbles
+  Geometry g;
+  const uint8_t* params;  // HBM param mirror [S*n_cap][2048 B]
+  const uint32_t* union_ids;
+  const uint32_t* union_mask;
+  const uint32_t* union_count;
+  const float* q;
+  void* part;
+  uint32_t CH, nsc, literal;
+  double scale_log2;
+};
+bool slow_tc_supported(const Geometry& g);
+cudaError_t make_arena_tmaps(const Geometry& g, uint8_t* arena, SlowTcArgs& a);
+cudaError_t launch_slow_tc(const SlowTcArgs& a, uint32_t grid_chunks, cudaStream_t st);
+
 bool fast_tc_supported(const Geometry& g);
 uint32_t fast_tc_tile();
 cudaError_t make_ring_tmaps(const Geometry& g, void* ring_k, void* ring_v, FastTcArgs& a);

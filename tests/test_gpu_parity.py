@@ -132,7 +132,7 @@ def make_inputs(S, ctx, T, dk, dv, G, seed, fp16):
 
 def run_parity(T_, *, S=2, G=1, d=32, dv=None, B=32, l_fast=128, kb=8, vb=4, elem=2, ctx=600,
                steps=6, frac=0.45, top_k=None, mode=0, seed=100, prefill_chunks=1,
-               check_blocks=True, literal=False):
+               check_blocks=True, literal=False, slow_tier=0):
     dv = dv or d
     cfg = T_.TierConfig(hbm_budget_bytes=l_fast * (d + dv) * elem, d_k=d, d_v=dv,
                         bytes_full_precision=elem, block_size=B, key_bits=kb, value_bits=vb,
@@ -141,7 +141,7 @@ def run_parity(T_, *, S=2, G=1, d=32, dv=None, B=32, l_fast=128, kb=8, vb=4, ele
     assert T_.fast_capacity(cfg) == l_fast
     pk, pv, dk_, dv_, dq = make_inputs(S, ctx, steps, d, dv, G, seed, fp16=(elem == 2))
     eng = T_.MultiStreamEngine(cfg, pol, n_streams=S, heads_per_stream=G, group_select=bool(mode),
-                               literal_additive_merge=literal)
+                               literal_additive_merge=literal, slow_tier=slow_tier)
     orc = [O.OracleEngine(d, dv, B, l_fast, kb, vb, top_k, frac) for _ in range(S)]
     bounds = np.linspace(0, ctx, prefill_chunks + 1).astype(int)
     for a, b in zip(bounds[:-1], bounds[1:]):
@@ -240,6 +240,20 @@ def test_engine_chunked_prefill(gpu):
 def test_engine_hot_shape_small(gpu):
     # the hot-path shape (d=128, B=128, K8/V4, G=4) at a small context
     run_parity(gpu, S=4, G=4, d=128, B=128, l_fast=1024, ctx=6000, steps=4, check_blocks=True)
+
+
+@pytest.mark.parametrize("G,mode,literal", [(4, 0, False), (4, 1, False), (1, 0, False),
+                                            (8, 0, False), (4, 0, True)])
+def test_engine_hbm_resident_slow_tier(gpu, G, mode, literal):
+    # slow tier in HBM: the tensor-core slow kernel (TMA tensor maps, mma.sync
+    # on raw codes) for K8/V4, d = B = 128; records still bit-exact
+    run_parity(gpu, S=3, G=G, d=128, B=128, l_fast=512, ctx=5000, steps=4, mode=mode,
+               literal=literal, slow_tier=1)
+
+
+def test_engine_hbm_resident_generic_shape(gpu):
+    # a shape the tensor-core kernel does not cover -> CUDA-core slow kernel on HBM
+    run_parity(gpu, S=2, G=2, d=32, B=32, l_fast=128, ctx=900, steps=4, slow_tier=1)
 
 
 def test_lossless_fetch_all_matches_dense(gpu):
