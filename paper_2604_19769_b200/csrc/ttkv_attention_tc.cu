@@ -86,8 +86,9 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
   const uint32_t ntiles = t1 > t0 ? (t1 - t0 + kTT - 1) / kTT : 0;
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-align by offsetting the shared array itself so the compiler keeps
+  // the shared address space (LDS, not generic LD)
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + kStages * STAGE);
   uint64_t* empty = full + kStages;
   float* sc = reinterpret_cast<float*>(empty + kStages);  // [2][GT][kTT]
@@ -280,7 +281,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
 // is exact in real arithmetic).
 // ---------------------------------------------------------------------------
 namespace {
-constexpr int kSlowTcStages = 2;
+constexpr int kSlowTcStages = 3;
 constexpr uint32_t kKBox = 128 * 128;  // K codes
 constexpr uint32_t kVBox = 128 * 64;   // V nibbles
 constexpr uint32_t kPBytes = 2 * 128 * 8;  // {scale, zp} x (128 K + 128 V)
@@ -320,10 +321,11 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
   const uint32_t nb = min(i0 + a.CH, cnt) - i0;
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* vtile = base + kSlowTcStages * kSlowStage;            // 2 boxes [128][128 B] fp16
-  uint64_t* full = reinterpret_cast<uint64_t*>(vtile + 2 * 128 * 128);
+  // 1024-align by offsetting the shared array itself so the compiler keeps
+  // the shared address space (LDS, not generic LD)
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* vtile = base + kSlowTcStages * kSlowStage;  // 2 boxes [64 tok][128 B] fp16 codes
+  uint64_t* full = reinterpret_cast<uint64_t*>(vtile + 2 * 64 * 128);
   uint64_t* empty = full + kSlowTcStages;
   float* sc2 = reinterpret_cast<float*>(empty + kSlowTcStages);  // [2][GT][128]
   float* mst = sc2 + 2 * GT * 128;
@@ -474,67 +476,76 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
         }
       }
     }
-    // ---- V nibbles -> fp16 codes tile (thread ct converts token row ct) ----
+    // ---- PV on codes, in two 64-token halves: V nibbles -> fp16 codes into a
+    // 16 KB swizzled tile (two threads per token row), then mma.  Warp cw owns
+    // channels [32cw, 32cw + 32). ----
+    const bool sel = head_ok && ((hm >> gq) & 1u);
+    float cfr[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) cfr[j][0] = cfr[j][1] = cfr[j][2] = cfr[j][3] = 0.f;
     {
+      const uint32_t vt = smem_u32(vtile);
       const uint8_t* vn = stg + vb_nib;
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {  // 16-byte chunks = 32 channels each
-        const uint4 w = *reinterpret_cast<const uint4*>(vn + swz64(ct * 64 + 16 * cc));
-        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+      for (int half = 0; half < 2; ++half) {
+        if (half) named_bar(1, nthreads_c);  // first-half PV done before overwrite
+        {
+          const uint32_t lr = ct >> 1, tr = 64 * half + lr;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {  // 8 channels: 32cc + 8u .. + 7
-          const uint32_t e = ws[u] & 0x0F0F0F0Fu, o = (ws[u] >> 4) & 0x0F0F0F0Fu;
-          uint32_t h2[4];
+          for (int c2 = 0; c2 < 2; ++c2) {
+            const int cc = 2 * (ct & 1) + c2;  // 16-byte chunk = channels 32cc .. 32cc+31
+            const uint4 w = *reinterpret_cast<const uint4*>(vn + swz64(tr * 64 + 16 * cc));
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            // result bytes [e.b, o.b, -, -] -> halves {e.b, o.b} = channels 2b, 2b+1
-            const uint32_t x = __byte_perm(e, o, (uint32_t)b | ((4u + (uint32_t)b) << 4));
-            const uint32_t hx = (x & 0x000000FFu) | ((x & 0x0000FF00u) << 8) | 0x64006400u;
-            const __half2 hv = __hsub2(*reinterpret_cast<const __half2*>(&hx),
-                                       __floats2half2_rn(1024.f, 1024.f));
-            h2[b] = *reinterpret_cast<const uint32_t*>(&hv);
+            for (int u = 0; u < 4; ++u) {  // 8 channels: 32cc + 8u .. + 7
+              const uint32_t e = ws[u] & 0x0F0F0F0Fu, o = (ws[u] >> 4) & 0x0F0F0F0Fu;
+              uint32_t h2[4];
+#pragma unroll
+              for (int b = 0; b < 4; ++b) {
+                // result bytes [e.b, o.b, -, -] -> halves {e.b, o.b} = channels 2b, 2b+1
+                const uint32_t x = __byte_perm(e, o, (uint32_t)b | ((4u + (uint32_t)b) << 4));
+                const uint32_t hx = (x & 0x000000FFu) | ((x & 0x0000FF00u) << 8) | 0x64006400u;
+                const __half2 hv = __hsub2(*reinterpret_cast<const __half2*>(&hx),
+                                           __floats2half2_rn(1024.f, 1024.f));
+                h2[b] = *reinterpret_cast<const uint32_t*>(&hv);
+              }
+              const int ch = 32 * cc + 8 * u;
+              *reinterpret_cast<uint4*>(vtile + (ch >> 6) * (64 * 128) +
+                                        swz128(lr * 128 + (ch & 63) * 2)) =
+                  make_uint4(h2[0], h2[1], h2[2], h2[3]);
+            }
           }
-          const int ch = 32 * cc + 8 * u;
-          *reinterpret_cast<uint4*>(vtile + (ch >> 6) * (128 * 128) +
-                                    swz128(ct * 128 + (ch & 63) * 2)) =
-              make_uint4(h2[0], h2[1], h2[2], h2[3]);
+        }
+        named_bar(1, nthreads_c);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const int ks = 4 * half + kk;
+          uint32_t ph0, pl0, ph1, pl1;
+          {
+            const float* pr = sc + (head_ok ? gq : 0) * 128 + 16 * ks + 2 * qq;
+            const float2 p01 = sel ? *reinterpret_cast<const float2*>(pr) : make_float2(0, 0);
+            const float2 p89 = sel ? *reinterpret_cast<const float2*>(pr + 8) : make_float2(0, 0);
+            split2(p01.x, p01.y, ph0, pl0);
+            split2(p89.x, p89.y, ph1, pl1);
+          }
+#pragma unroll
+          for (int jp = 0; jp < 2; ++jp) {
+            const int m = lane >> 3;
+            const int ntc = 4 * cw + 2 * jp + (m >> 1);
+            const int row = 16 * kk + 8 * (m & 1) + (lane & 7);
+            const int ch = 8 * ntc;
+            const uint32_t addr = vt + (ch >> 6) * (64 * 128) + swz128(row * 128 + (ch & 63) * 2);
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4_t(addr, b0, b1, b2, b3);
+            mma16816(cfr[2 * jp], ph0, ph1, b0, b1);
+            mma16816(cfr[2 * jp], pl0, pl1, b0, b1);
+            mma16816(cfr[2 * jp + 1], ph0, ph1, b2, b3);
+            mma16816(cfr[2 * jp + 1], pl0, pl1, b2, b3);
+          }
         }
       }
     }
-    named_bar(1, nthreads_c);
-
-    // ---- PV on codes: warp cw -> channels [32cw, 32cw + 32) ----
     {
-      const uint32_t vt = smem_u32(vtile);
-      float cfr[4][4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) cfr[j][0] = cfr[j][1] = cfr[j][2] = cfr[j][3] = 0.f;
-      const bool sel = head_ok && ((hm >> gq) & 1u);
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        uint32_t ph0, pl0, ph1, pl1;
-        {
-          const float* pr = sc + (head_ok ? gq : 0) * 128 + 16 * ks + 2 * qq;
-          const float2 p01 = sel ? *reinterpret_cast<const float2*>(pr) : make_float2(0, 0);
-          const float2 p89 = sel ? *reinterpret_cast<const float2*>(pr + 8) : make_float2(0, 0);
-          split2(p01.x, p01.y, ph0, pl0);
-          split2(p89.x, p89.y, ph1, pl1);
-        }
-#pragma unroll
-        for (int jp = 0; jp < 2; ++jp) {
-          const int m = lane >> 3;
-          const int ntc = 4 * cw + 2 * jp + (m >> 1);
-          const int row = 16 * ks + 8 * (m & 1) + (lane & 7);
-          const int ch = 8 * ntc;
-          const uint32_t addr = vt + (ch >> 6) * (128 * 128) + swz128(row * 128 + (ch & 63) * 2);
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4_t(addr, b0, b1, b2, b3);
-          mma16816(cfr[2 * jp], ph0, ph1, b0, b1);
-          mma16816(cfr[2 * jp], pl0, pl1, b0, b1);
-          mma16816(cfr[2 * jp + 1], ph0, ph1, b2, b3);
-          mma16816(cfr[2 * jp + 1], pl0, pl1, b2, b3);
-        }
-      }
       // affine epilogue: acc = acc * alpha + s_c * (P . code) + z_c * sum(P)
       if (sel) {
         const float alpha = ast[gq], psum = pst[gq];
@@ -576,7 +587,7 @@ bool slow_tc_supported(const Geometry& g) {
 }
 
 static size_t slow_tc_smem() {
-  return 1024 + (size_t)kSlowTcStages * kSlowStage + 2 * 128 * 128 + 2 * kSlowTcStages * 8 +
+  return 1024 + (size_t)kSlowTcStages * kSlowStage + 2 * 64 * 128 + 2 * kSlowTcStages * 8 +
          (2 * 8 * 128 + 4 * 8) * 4 + 64;
 }
 
