@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
     if (lane == 0) {
       for (uint32_t i = 0; i < ntiles; ++i) {
         const uint32_t st = i % kStages;
-        if (i >= kStages) mbar_wait(&empty[st], ((i / kStages) - 1) & 1);
+        if (i >= kStages) mbar_wait_backoff(&empty[st], ((i / kStages) - 1) & 1);
         const int row = (int)(s * g.C + (a.front + t0 + i * kTT) % g.C);
         uint8_t* kb = base + st * STAGE;
         uint8_t* vb = kb + ND * kBox;
@@ -150,9 +150,11 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
     }
   }
   constexpr int NT_PV = D / 8 / kSlowConsumerWarps;  // output n-tiles per warp
-  float acc[NT_PV][4];
+  float acc[NT_PV][4], acl[NT_PV][4];  // P_hi . V and P_lo . V (independent chains)
 #pragma unroll
-  for (int j = 0; j < NT_PV; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+  for (int j = 0; j < NT_PV; ++j)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[j][e] = acl[j][e] = 0.f;
   const int nthreads_c = kSlowConsumerWarps * 32;
 
   for (uint32_t i = 0; i < ntiles; ++i) {
@@ -163,29 +165,38 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
     const uint32_t rows = min((uint32_t)kTT, t1 - (t0 + i * kTT));
     float* scb = sc + (i & 1) * GT * kTT;
 
-    // ---- QK^T: warp cw -> tokens [16cw, 16cw + 16) ----
+    // ---- QK^T: warp cw -> tokens [16cw, 16cw + 16); 4 independent
+    // accumulator chains (2 n-tiles x hi/lo) ----
+    {
+      float c[2][2][4];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int nt = 2 * cw + h;
-      float c[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) c[h][0][e] = c[h][1][e] = 0.f;
 #pragma unroll
       for (int kp = 0; kp < KSTEPS / 2; ++kp) {
-        // matrices: (ks lo8, ks hi8, ks+1 lo8, ks+1 hi8) of tokens [8nt, 8nt+8)
-        const int m = lane >> 3;
-        const int row = 8 * nt + (lane & 7);
-        const int ch = 16 * (2 * kp + (m >> 1)) + 8 * (m & 1);
-        const uint32_t addr = kb + (ch >> 6) * kBox + swz128(row * 128 + (ch & 63) * 2);
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4(addr, b0, b1, b2, b3);
-        mma16816(c, aqh[2 * kp][0], aqh[2 * kp][1], b0, b1);
-        mma16816(c, aql[2 * kp][0], aql[2 * kp][1], b0, b1);
-        mma16816(c, aqh[2 * kp + 1][0], aqh[2 * kp + 1][1], b2, b3);
-        mma16816(c, aql[2 * kp + 1][0], aql[2 * kp + 1][1], b2, b3);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          // matrices: (ks lo8, ks hi8, ks+1 lo8, ks+1 hi8) of tokens [8nt, 8nt+8)
+          const int m = lane >> 3;
+          const int row = 8 * (2 * cw + h) + (lane & 7);
+          const int ch = 16 * (2 * kp + (m >> 1)) + 8 * (m & 1);
+          const uint32_t addr = kb + (ch >> 6) * kBox + swz128(row * 128 + (ch & 63) * 2);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(addr, b0, b1, b2, b3);
+          mma16816(c[h][0], aqh[2 * kp][0], aqh[2 * kp][1], b0, b1);
+          mma16816(c[h][1], aql[2 * kp][0], aql[2 * kp][1], b0, b1);
+          mma16816(c[h][0], aqh[2 * kp + 1][0], aqh[2 * kp + 1][1], b2, b3);
+          mma16816(c[h][1], aql[2 * kp + 1][0], aql[2 * kp + 1][1], b2, b3);
+        }
       }
       if (head_ok) {
-        const uint32_t tA = 8 * nt + 2 * qq;
-        scb[gq * kTT + tA] = tA < rows ? c[0] : -INFINITY;
-        scb[gq * kTT + tA + 1] = tA + 1 < rows ? c[1] : -INFINITY;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t tA = 8 * (2 * cw + h) + 2 * qq;
+          scb[gq * kTT + tA] = tA < rows ? c[h][0][0] + c[h][1][0] : -INFINITY;
+          scb[gq * kTT + tA + 1] = tA + 1 < rows ? c[h][0][1] + c[h][1][1] : -INFINITY;
+        }
       }
     }
     named_bar(1, nthreads_c);
@@ -217,6 +228,8 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
       for (int j = 0; j < NT_PV; ++j) {
         acc[j][0] *= alpha;
         acc[j][1] *= alpha;
+        acl[j][0] *= alpha;
+        acl[j][1] *= alpha;
       }
 #pragma unroll
       for (int ks = 0; ks < kTT / 16; ++ks) {
@@ -239,9 +252,9 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
           uint32_t b0, b1, b2, b3;
           ldsm_x4_t(addr, b0, b1, b2, b3);
           mma16816(acc[2 * jp], ph0, ph1, b0, b1);
-          mma16816(acc[2 * jp], pl0, pl1, b0, b1);
+          mma16816(acl[2 * jp], pl0, pl1, b0, b1);
           mma16816(acc[2 * jp + 1], ph0, ph1, b2, b3);
-          mma16816(acc[2 * jp + 1], pl0, pl1, b2, b3);
+          mma16816(acl[2 * jp + 1], pl0, pl1, b2, b3);
         }
       }
     }
@@ -259,8 +272,8 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
 #pragma unroll
     for (int j = 0; j < NT_PV; ++j) {
       const int ch = 8 * (NT_PV * cw + j) + 2 * qq;
-      p[ch] = ntiles ? acc[j][0] : 0.f;
-      p[ch + 1] = ntiles ? acc[j][1] : 0.f;
+      p[ch] = ntiles ? acc[j][0] + acl[j][0] : 0.f;
+      p[ch + 1] = ntiles ? acc[j][1] + acl[j][1] : 0.f;
     }
     if (cw == 0 && qq == 0) {
       p[D] = ntiles ? mst[gq] : -INFINITY;
@@ -353,7 +366,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
     if (lane == 0) {
       for (uint32_t i = 0; i < nb; ++i) {
         const uint32_t st = i % kSlowTcStages;
-        if (i >= kSlowTcStages) mbar_wait(&empty[st], ((i / kSlowTcStages) - 1) & 1);
+        if (i >= kSlowTcStages) mbar_wait_backoff(&empty[st], ((i / kSlowTcStages) - 1) & 1);
         const uint32_t blk = uids[i];
         const int rec = (int)((uint64_t)s * g.n_cap + blk);
         uint8_t* dst = base + st * kSlowStage;
@@ -413,31 +426,40 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
     beta += __shfl_xor_sync(0xffffffffu, beta, 1);
     beta += __shfl_xor_sync(0xffffffffu, beta, 2);
 
-    // ---- QK^T: warp cw -> tokens [32cw, 32cw + 32) ----
+    // ---- QK^T: warp cw -> tokens [32cw, 32cw + 32); 8 independent
+    // accumulator chains (4 n-tiles x hi/lo) keep the tensor pipe busy ----
+    {
+      float c[4][2][4];
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      const int nt = 4 * cw + h;
-      float c[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int h = 0; h < 4; ++h)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) c[h][0][e] = c[h][1][e] = 0.f;
 #pragma unroll
       for (int jp = 0; jp < 2; ++jp) {
-        const int m = lane >> 3;
-        const int row = 8 * nt + (lane & 7);
-        const uint32_t addr = kb + swz128(row * 128 + (4 * jp + m) * 16);
-        uint32_t r[4];
-        ldsm_x4(addr, r[0], r[1], r[2], r[3]);
 #pragma unroll
-        for (int mm = 0; mm < 4; ++mm) {
-          uint32_t b0, b1;
-          codes_to_h2(r[mm], b0, b1);
-          const int j = 4 * jp + mm;
-          mma16816(c, ah[j][0], ah[j][1], b0, b1);
-          mma16816(c, al[j][0], al[j][1], b0, b1);
+        for (int h = 0; h < 4; ++h) {
+          const int m = lane >> 3;
+          const int row = 8 * (4 * cw + h) + (lane & 7);
+          const uint32_t addr = kb + swz128(row * 128 + (4 * jp + m) * 16);
+          uint32_t r[4];
+          ldsm_x4(addr, r[0], r[1], r[2], r[3]);
+#pragma unroll
+          for (int mm = 0; mm < 4; ++mm) {
+            uint32_t b0, b1;
+            codes_to_h2(r[mm], b0, b1);
+            const int j = 4 * jp + mm;
+            mma16816(c[h][0], ah[j][0], ah[j][1], b0, b1);
+            mma16816(c[h][1], al[j][0], al[j][1], b0, b1);
+          }
         }
       }
       if (head_ok) {
-        const uint32_t tA = 8 * nt + 2 * qq;
-        sc[gq * 128 + tA] = c[0] + beta;
-        sc[gq * 128 + tA + 1] = c[1] + beta;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const uint32_t tA = 8 * (4 * cw + h) + 2 * qq;
+          sc[gq * 128 + tA] = c[h][0][0] + c[h][1][0] + beta;
+          sc[gq * 128 + tA + 1] = c[h][0][1] + c[h][1][1] + beta;
+        }
       }
     }
     named_bar(1, nthreads_c);
@@ -480,9 +502,11 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
     // 16 KB swizzled tile (two threads per token row), then mma.  Warp cw owns
     // channels [32cw, 32cw + 32). ----
     const bool sel = head_ok && ((hm >> gq) & 1u);
-    float cfr[4][4];
+    float cfr[4][4], cfl[4][4];  // P_hi . code and P_lo . code (independent chains)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) cfr[j][0] = cfr[j][1] = cfr[j][2] = cfr[j][3] = 0.f;
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) cfr[j][e] = cfl[j][e] = 0.f;
     {
       const uint32_t vt = smem_u32(vtile);
       const uint8_t* vn = stg + vb_nib;
@@ -538,9 +562,9 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
             uint32_t b0, b1, b2, b3;
             ldsm_x4_t(addr, b0, b1, b2, b3);
             mma16816(cfr[2 * jp], ph0, ph1, b0, b1);
-            mma16816(cfr[2 * jp], pl0, pl1, b0, b1);
+            mma16816(cfl[2 * jp], pl0, pl1, b0, b1);
             mma16816(cfr[2 * jp + 1], ph0, ph1, b2, b3);
-            mma16816(cfr[2 * jp + 1], pl0, pl1, b2, b3);
+            mma16816(cfl[2 * jp + 1], pl0, pl1, b2, b3);
           }
         }
       }
@@ -553,8 +577,8 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
         for (int j = 0; j < 4; ++j) {
           const int ch = 8 * (4 * cw + j) + 2 * qq;
           const float4 sz = *reinterpret_cast<const float4*>(vp + 2 * ch);
-          acc[j][0] = acc[j][0] * alpha + sz.x * cfr[j][0] + sz.y * psum;
-          acc[j][1] = acc[j][1] * alpha + sz.z * cfr[j][1] + sz.w * psum;
+          acc[j][0] = acc[j][0] * alpha + sz.x * (cfr[j][0] + cfl[j][0]) + sz.y * psum;
+          acc[j][1] = acc[j][1] * alpha + sz.z * (cfr[j][1] + cfl[j][1]) + sz.w * psum;
         }
       }
     }
