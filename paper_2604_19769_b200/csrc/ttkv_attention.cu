@@ -538,6 +538,7 @@ static cudaError_t launch_slow_t(const SlowArgs& a, uint32_t grid_chunks, cudaSt
   b.stage_region = stage_region_for<Acc>((size_t)a.stages * g.rec.stride, GT, g);
   const size_t smem = (size_t)b.stage_region + 16 * a.stages + consumer_smem(g, GT, g.B, sizeof(Acc));
   auto kern = slow_attn_kernel<T, KB, VB, GT, COPY>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // max smem
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid(grid_chunks, g.S);
@@ -580,6 +581,7 @@ static cudaError_t launch_fast_t(const FastArgs& a, cudaStream_t st) {
   b.stage_region = stage_region_for<Acc>(stage_bytes * a.stages, GT, g);
   const size_t smem = (size_t)b.stage_region + 16 * a.stages + consumer_smem(g, GT, a.TT, sizeof(Acc));
   auto kern = fast_attn_kernel<T, GT, COPY>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // max smem
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid(a.nfc, g.S);

@@ -323,8 +323,9 @@ __device__ __forceinline__ void codes_to_h2(uint32_t w, uint32_t& lo, uint32_t& 
 }
 }  // namespace
 
+// 2 CTAs/SM: 10 warps over 4 SMSPs -> <= 168 registers per thread
 template <int GT>
-__global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
+__global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, 2)
     slow_attn_tc_kernel(const __grid_constant__ SlowTcArgs a) {
   const Geometry& g = a.g;
   const uint32_t s = blockIdx.y, chunk = blockIdx.x;
@@ -385,15 +386,16 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
   const int nthreads_c = kSlowConsumerWarps * 32;
   // this thread's 32 query channels (permuted order), log2-scaled:
   // segment j -> channels 16j + 4qq + {0,1,2,3}
-  float qv[8][4];
+  // the (log2-scaled) queries live in smem, not registers (2 CTAs/SM budget)
+  float* qsm = pst + GT;  // [GT][128]
   {
-    const float* qr = a.q + ((uint64_t)s * g.G + (head_ok ? gq : 0)) * 128;
+    const float* qb = a.q + (uint64_t)s * g.G * 128;
     const float sl = (float)a.scale_log2;
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) qv[j][e] = head_ok ? qr[16 * j + 4 * qq + e] * sl : 0.f;
+    for (uint32_t i2 = ct; i2 < GT * 128; i2 += nthreads_c)
+      qsm[i2] = (i2 / 128 < g.G) ? qb[i2] * sl : 0.f;
+    named_bar(1, nthreads_c);
   }
+  const float* qrow = qsm + (head_ok ? gq : 0) * 128;
   float acc[4][2];  // running output: head gq, channels 8(4cw + j) + 2qq + {0,1}
 #pragma unroll
   for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.f;
@@ -417,29 +419,31 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
     for (int j = 0; j < 8; ++j) {
       const float4 sz0 = *reinterpret_cast<const float4*>(kp + 2 * (16 * j + 4 * qq));
       const float4 sz1 = *reinterpret_cast<const float4*>(kp + 2 * (16 * j + 4 * qq) + 4);
-      const float x0 = qv[j][0] * sz0.x, x1 = qv[j][1] * sz0.z;
-      const float x2 = qv[j][2] * sz1.x, x3 = qv[j][3] * sz1.z;
-      beta += qv[j][0] * sz0.y + qv[j][1] * sz0.w + qv[j][2] * sz1.y + qv[j][3] * sz1.w;
+      const float4 qv = *reinterpret_cast<const float4*>(qrow + 16 * j + 4 * qq);
+      const float x0 = qv.x * sz0.x, x1 = qv.y * sz0.z;
+      const float x2 = qv.z * sz1.x, x3 = qv.w * sz1.z;
+      beta += qv.x * sz0.y + qv.y * sz0.w + qv.z * sz1.y + qv.w * sz1.w;
       split2(x0, x1, ah[j][0], al[j][0]);
       split2(x2, x3, ah[j][1], al[j][1]);
     }
     beta += __shfl_xor_sync(0xffffffffu, beta, 1);
     beta += __shfl_xor_sync(0xffffffffu, beta, 2);
 
-    // ---- QK^T: warp cw -> tokens [32cw, 32cw + 32); 8 independent
-    // accumulator chains (4 n-tiles x hi/lo) keep the tensor pipe busy ----
-    {
-      float c[4][2][4];
+    // ---- QK^T: warp cw -> tokens [32cw, 32cw + 32), two n-tiles at a time:
+    // 4 independent accumulator chains (2 n-tiles x hi/lo) ----
 #pragma unroll
-      for (int h = 0; h < 4; ++h)
+    for (int hp = 0; hp < 2; ++hp) {
+      float c[2][2][4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
 #pragma unroll
         for (int e = 0; e < 4; ++e) c[h][0][e] = c[h][1][e] = 0.f;
 #pragma unroll
       for (int jp = 0; jp < 2; ++jp) {
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
+        for (int h = 0; h < 2; ++h) {
           const int m = lane >> 3;
-          const int row = 8 * (4 * cw + h) + (lane & 7);
+          const int row = 8 * (4 * cw + 2 * hp + h) + (lane & 7);
           const uint32_t addr = kb + swz128(row * 128 + (4 * jp + m) * 16);
           uint32_t r[4];
           ldsm_x4(addr, r[0], r[1], r[2], r[3]);
@@ -455,8 +459,8 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
       }
       if (head_ok) {
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const uint32_t tA = 8 * (4 * cw + h) + 2 * qq;
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t tA = 8 * (4 * cw + 2 * hp + h) + 2 * qq;
           sc[gq * 128 + tA] = c[h][0][0] + c[h][1][0] + beta;
           sc[gq * 128 + tA + 1] = c[h][0][1] + c[h][1][1] + beta;
         }
@@ -502,11 +506,9 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
     // 16 KB swizzled tile (two threads per token row), then mma.  Warp cw owns
     // channels [32cw, 32cw + 32). ----
     const bool sel = head_ok && ((hm >> gq) & 1u);
-    float cfr[4][4], cfl[4][4];  // P_hi . code and P_lo . code (independent chains)
+    float cfr[4][4];  // P . code per output n-tile (hi and lo MMAs accumulate here)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) cfr[j][e] = cfl[j][e] = 0.f;
+    for (int j = 0; j < 4; ++j) cfr[j][0] = cfr[j][1] = cfr[j][2] = cfr[j][3] = 0.f;
     {
       const uint32_t vt = smem_u32(vtile);
       const uint8_t* vn = stg + vb_nib;
@@ -562,9 +564,9 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
             uint32_t b0, b1, b2, b3;
             ldsm_x4_t(addr, b0, b1, b2, b3);
             mma16816(cfr[2 * jp], ph0, ph1, b0, b1);
-            mma16816(cfl[2 * jp], pl0, pl1, b0, b1);
             mma16816(cfr[2 * jp + 1], ph0, ph1, b2, b3);
-            mma16816(cfl[2 * jp + 1], pl0, pl1, b2, b3);
+            mma16816(cfr[2 * jp], pl0, pl1, b0, b1);
+            mma16816(cfr[2 * jp + 1], pl0, pl1, b2, b3);
           }
         }
       }
@@ -577,8 +579,8 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
         for (int j = 0; j < 4; ++j) {
           const int ch = 8 * (4 * cw + j) + 2 * qq;
           const float4 sz = *reinterpret_cast<const float4*>(vp + 2 * ch);
-          acc[j][0] = acc[j][0] * alpha + sz.x * (cfr[j][0] + cfl[j][0]) + sz.y * psum;
-          acc[j][1] = acc[j][1] * alpha + sz.z * (cfr[j][1] + cfl[j][1]) + sz.w * psum;
+          acc[j][0] = acc[j][0] * alpha + sz.x * cfr[j][0] + sz.y * psum;
+          acc[j][1] = acc[j][1] * alpha + sz.z * cfr[j][1] + sz.w * psum;
         }
       }
     }
@@ -612,13 +614,14 @@ bool slow_tc_supported(const Geometry& g) {
 
 static size_t slow_tc_smem() {
   return 1024 + (size_t)kSlowTcStages * kSlowStage + 2 * 64 * 128 + 2 * kSlowTcStages * 8 +
-         (2 * 8 * 128 + 4 * 8) * 4 + 64;
+         (2 * 8 * 128 + 4 * 8 + 8 * 128) * 4 + 64;
 }
 
 template <int GT>
 static cudaError_t launch_slow_tc_t(const SlowTcArgs& a, uint32_t grid_chunks, cudaStream_t st) {
   const size_t smem = slow_tc_smem();
   auto kern = slow_attn_tc_kernel<GT>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // max smem
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid(grid_chunks, a.g.S);
@@ -686,6 +689,7 @@ template <int ND, int GT>
 static cudaError_t launch_fast_tc_t(const FastTcArgs& a, cudaStream_t st) {
   const size_t smem = fast_tc_smem(a.g);
   auto kern = fast_attn_tc_kernel<ND, GT>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // max smem
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid(a.nfc, a.g.S);
