@@ -106,6 +106,10 @@ typedef struct {
                                   bytes_full_precision <= 2, else fp32),
                                   2 fp16 (fp32 accumulation), 4 fp32 (fp64
                                   accumulation; bit-faithful to float inputs) */
+  uint32_t serial_schedule;    /* 1: bulk schedule of the reference's serial
+                                  baselines (harness.cpp:22-24): all selected
+                                  records are first gathered into an HBM
+                                  staging arena, then attended (no overlap) */
 } ttkv_gpu_options;
 
 /* DecodeStepReport (engine.hpp:21-29) plus measured quantities. */
@@ -141,6 +145,11 @@ typedef struct {
 typedef struct {
   double ms_append, ms_score, ms_select, ms_fast, ms_slow, ms_combine, ms_evict;
   uint64_t n_append, n_score, n_select, n_fast, n_slow, n_combine, n_evict;
+  double ms_gather;  /* serial schedule: PCIe gather into the staging arena */
+  uint64_t n_gather;
+  double ms_step;    /* whole decode steps (append .. settle), device time */
+  uint64_t n_step;
+  double last_step_ms;
 } ttkv_kernel_times;
 
 /* ---- lifecycle ------------------------------------------------------------ */

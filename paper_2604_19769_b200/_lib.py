@@ -34,7 +34,7 @@ class OptionsC(C.Structure):
                 ("heads_per_stream", C.c_uint32), ("group_select", C.c_uint32),
                 ("reserve_tokens", C.c_uint64), ("slow_tier", C.c_uint32),
                 ("copy_mode", C.c_uint32), ("literal_additive_merge", C.c_uint32),
-                ("ring_bytes", C.c_uint32)]
+                ("ring_bytes", C.c_uint32), ("serial_schedule", C.c_uint32)]
 
 
 class StepReportC(C.Structure):
@@ -55,7 +55,10 @@ class KernelTimesC(C.Structure):
     _fields_ = ([("ms_" + n, C.c_double) for n in
                  ("append", "score", "select", "fast", "slow", "combine", "evict")] +
                 [("n_" + n, C.c_uint64) for n in
-                 ("append", "score", "select", "fast", "slow", "combine", "evict")])
+                 ("append", "score", "select", "fast", "slow", "combine", "evict")] +
+                [("ms_gather", C.c_double), ("n_gather", C.c_uint64),
+                 ("ms_step", C.c_double), ("n_step", C.c_uint64),
+                 ("last_step_ms", C.c_double)])
 
 
 # every symbol include/ttkv_gpu.h declares (checked by tests/test_abi.py)

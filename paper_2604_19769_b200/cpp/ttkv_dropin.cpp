@@ -743,3 +743,36 @@ double relative_error(std::span<const double> a, std::span<const double> b) {
 
 }  // namespace reference
 }  // namespace ttkv
+
+// ---- C entry (include/ttkv_dropin_c.h) --------------------------------------------
+#include "ttkv_dropin_c.h"
+
+extern "C" int ttkv_generate_workload(int needle, uint64_t ctx, uint64_t T, uint32_t d_k,
+                                      uint32_t d_v, uint64_t seed, uint64_t needle_pos,
+                                      double strength, float* pre_k, float* pre_v, float* dec_k,
+                                      float* dec_v, float* dec_q) {
+  try {
+    ttkv::WorkloadSpec s;
+    s.kind = needle ? ttkv::WorkloadSpec::Kind::PlantedNeedle : ttkv::WorkloadSpec::Kind::Gaussian;
+    s.context_length = ctx;
+    s.decode_steps = T;
+    s.d_k = d_k;
+    s.d_v = d_v;
+    s.seed = seed;
+    s.needle_block_position = needle_pos;
+    s.needle_alignment_strength = strength;
+    const ttkv::WorkloadStream w = ttkv::generate_workload(s);
+    for (uint64_t p = 0; p < ctx; ++p) {
+      std::copy(w.prefill[p].key.begin(), w.prefill[p].key.end(), pre_k + p * d_k);
+      std::copy(w.prefill[p].value.begin(), w.prefill[p].value.end(), pre_v + p * d_v);
+    }
+    for (uint64_t t = 0; t < T; ++t) {
+      std::copy(w.decode[t].kv.key.begin(), w.decode[t].kv.key.end(), dec_k + t * d_k);
+      std::copy(w.decode[t].kv.value.begin(), w.decode[t].kv.value.end(), dec_v + t * d_v);
+      std::copy(w.decode[t].query.begin(), w.decode[t].query.end(), dec_q + t * d_k);
+    }
+    return TTKV_OK;
+  } catch (const std::exception&) {
+    return TTKV_ECONFIG;
+  }
+}

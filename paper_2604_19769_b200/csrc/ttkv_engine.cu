@@ -119,8 +119,8 @@ RecordLayout make_layout(uint32_t B, uint32_t d_k, uint32_t d_v, uint32_t kb, ui
   return r;
 }
 
-const char* kKernelNames[] = {"append", "score", "select", "fast", "slow", "combine", "evict"};
-enum Kind { K_APPEND = 0, K_SCORE, K_SELECT, K_FAST, K_SLOW, K_COMBINE, K_EVICT, K_N };
+const char* kKernelNames[] = {"append", "score", "select", "fast", "slow", "combine", "evict", "gather", "step"};
+enum Kind { K_APPEND = 0, K_SCORE, K_SELECT, K_FAST, K_SLOW, K_COMBINE, K_EVICT, K_GATHER, K_STEP, K_N };
 
 }  // namespace
 
@@ -148,6 +148,8 @@ struct ttkv_gpu {
   FastTcArgs tc{};           // ring tensor maps, encoded once at create
   bool slow_tc = false;      // tensor-core slow tier (arena tensor maps)
   SlowTcArgs stc{};          // re-encoded whenever the arena is reallocated
+  uint8_t* stage_arena = nullptr;  // serial schedule: HBM copy of selected records
+  double last_step_ms = 0.0;
   size_t acc = 4;  // bytes of the accumulation type (fp32, or fp64 for the fp32 ring)
   // device memory
   void* ring_k = nullptr;
@@ -211,6 +213,14 @@ cudaEvent_t take_event(ttkv_gpu* h) {
   return e;
 }
 
+// Whole-step device time (append .. settle) on the critical-path stream.
+struct StepTimer {
+  ttkv_gpu* h;
+  cudaEvent_t a = nullptr;
+  explicit StepTimer(ttkv_gpu* hh);
+  ~StepTimer();
+};
+
 struct KTimer {
   ttkv_gpu* h;
   int kind;
@@ -238,6 +248,7 @@ void drain_timing(ttkv_gpu* h) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, r.a, r.b);
     h->ms[r.kind] += ms;
+    if (r.kind == K_STEP) h->last_step_ms = ms;
     h->cnt[r.kind] += 1;
     h->pool.push_back(r.a);
     h->pool.push_back(r.b);
@@ -251,7 +262,7 @@ void free_all(ttkv_gpu* h) {
   };
   F(h->ring_k); F(h->ring_v); F(h->cent); F(h->params); F(h->scores); F(h->sel); F(h->mask); F(h->uids);
   F(h->umask); F(h->ucount); F(h->counters); F(h->fpart); F(h->spart); F(h->q_dev);
-  F(h->out_dev); F(h->kn_dev); F(h->vn_dev); F(h->stg_k); F(h->stg_v);
+  F(h->out_dev); F(h->kn_dev); F(h->vn_dev); F(h->stg_k); F(h->stg_v); F(h->stage_arena);
   if (h->arena_host) cudaFreeHost(h->arena_host);
   else if (h->arena_dev) cudaFree(h->arena_dev);
   if (h->h_q) cudaFreeHost(h->h_q);
@@ -329,7 +340,11 @@ int ensure_blocks(ttkv_gpu* h, uint64_t need) {
   CU(h, realloc_dev((void**)&h->uids, S * cap * sizeof(uint32_t)));
   CU(h, realloc_dev((void**)&h->umask, S * cap * sizeof(uint32_t)));
   h->g.n_cap = cap;
-  if (h->slow_tc && make_arena_tmaps(h->g, h->arena_dev, h->stc) != cudaSuccess)
+  if (h->opt.serial_schedule) {
+    CU(h, realloc_dev((void**)&h->stage_arena, arena_bytes));
+  }
+  uint8_t* attn_arena = h->opt.serial_schedule ? h->stage_arena : h->arena_dev;
+  if (h->slow_tc && make_arena_tmaps(h->g, attn_arena, h->stc) != cudaSuccess)
     h->slow_tc = false;  // fall back to the CUDA-core slow tier
   return TTKV_OK;
 }
@@ -431,8 +446,23 @@ uint64_t prefill_chunk_tokens(const ttkv_gpu* h) {
   return P;
 }
 
+StepTimer::StepTimer(ttkv_gpu* hh) : h(hh) {
+  if (h->timing) {
+    a = take_event(h);
+    cudaEventRecord(a, h->s0);
+  }
+}
+StepTimer::~StepTimer() {
+  if (a) {
+    cudaEvent_t b = take_event(h);
+    cudaEventRecord(b, h->s0);
+    h->recs.push_back({K_STEP, a, b});
+  }
+}
+
 int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int dtype,
                 double* out, ttkv_step_report* rep) {
+  StepTimer step_timer(h);
   {  // grow before selecting so a settle-time eviction never reallocates
     int rc0 = ensure_blocks(h, h->n_slow + 1);
     if (rc0) return rc0;
@@ -534,6 +564,12 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       KTimer t(h, K_SELECT, h->s0);
       CU(h, launch_select(a, h->s0));
     }
+    if (h->opt.serial_schedule) {
+      // bulk phase: every selected record crosses PCIe before any compute
+      KTimer t(h, K_GATHER, h->s0);
+      CU(h, launch_gather(g, h->arena_dev, h->stage_arena, h->uids, h->ucount,
+                          (uint32_t)grid_chunks, CH, h->s0));
+    }
     if (int rcf = fork_fast()) return rcf;
     if (h->slow_tc) {
       SlowTcArgs& a = h->stc;
@@ -553,7 +589,7 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
     } else {
       SlowArgs a{};
       a.g = g;
-      a.arena = h->arena_dev;
+      a.arena = h->opt.serial_schedule ? h->stage_arena : h->arena_dev;
       a.params = h->params;
       a.union_ids = h->uids;
       a.union_mask = h->umask;
@@ -1247,6 +1283,9 @@ int ttkv_gpu_kernel_times(ttkv_gpu* h, ttkv_kernel_times* t, int reset) {
     t->ms_slow = h->ms[K_SLOW]; t->n_slow = h->cnt[K_SLOW];
     t->ms_combine = h->ms[K_COMBINE]; t->n_combine = h->cnt[K_COMBINE];
     t->ms_evict = h->ms[K_EVICT]; t->n_evict = h->cnt[K_EVICT];
+    t->ms_gather = h->ms[K_GATHER]; t->n_gather = h->cnt[K_GATHER];
+    t->ms_step = h->ms[K_STEP]; t->n_step = h->cnt[K_STEP];
+    t->last_step_ms = h->last_step_ms;
   }
   if (reset) {
     for (int i = 0; i < K_N; ++i) { h->ms[i] = 0; h->cnt[i] = 0; }

@@ -137,6 +137,12 @@ struct SlowArgs {
 cudaError_t launch_slow(const SlowArgs& a, uint32_t grid_chunks, int copy_mode, cudaStream_t st);
 uint32_t slow_stages_for(const Geometry& g);
 
+// Serial schedule: copy every selected record's payload from the (mapped
+// host) arena into a device staging arena at the same offsets.
+cudaError_t launch_gather(const Geometry& g, const uint8_t* src, uint8_t* dst,
+                          const uint32_t* union_ids, const uint32_t* union_count,
+                          uint32_t grid_chunks, uint32_t CH, cudaStream_t st);
+
 struct CombineArgs {
   Geometry g;
   const void* fpart;

@@ -271,3 +271,46 @@ cudaError_t launch_synth(const Geometry& g, void* k, void* v, uint64_t P, uint64
 }
 
 }  // namespace ttkv_dev
+
+namespace ttkv_dev {
+
+// ---------------------------------------------------------------------------
+// gather_records: the bulk phase of the serial schedule (harness.cpp:22-24,
+// simulate_serial sim.cpp:90-112 made real): every selected record's payload
+// crosses PCIe into an HBM staging arena before any attention starts.
+// 16-byte zero-copy loads, 8 in flight per thread.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) gather_kernel(Geometry g, const uint8_t* src, uint8_t* dst,
+                                                     const uint32_t* uids, const uint32_t* ucount,
+                                                     uint32_t CH) {
+  const uint32_t s = blockIdx.y;
+  const uint32_t i0 = blockIdx.x * CH, cnt = ucount[s];
+  if (i0 >= cnt) return;
+  const uint32_t i1 = min(i0 + CH, cnt);
+  const uint32_t n16 = g.rec.kp_off >> 4;
+  for (uint32_t i = i0; i < i1; ++i) {
+    const uint64_t off = ((uint64_t)s * g.n_cap + uids[(uint64_t)s * g.n_cap + i]) * g.rec.stride;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + off);
+    uint4* d4 = reinterpret_cast<uint4*>(dst + off);
+    uint32_t j = threadIdx.x;
+    for (; j + 7 * 256 < n16; j += 8 * 256) {
+      uint4 r[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) r[u] = s4[j + u * 256];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) d4[j + u * 256] = r[u];
+    }
+    for (; j < n16; j += 256) d4[j] = s4[j];
+  }
+}
+
+cudaError_t launch_gather(const Geometry& g, const uint8_t* src, uint8_t* dst,
+                          const uint32_t* union_ids, const uint32_t* union_count,
+                          uint32_t grid_chunks, uint32_t CH, cudaStream_t st) {
+  if (grid_chunks == 0) return cudaSuccess;
+  dim3 grid(grid_chunks, g.S);
+  gather_kernel<<<grid, 256, 0, st>>>(g, src, dst, union_ids, union_count, CH);
+  return cudaGetLastError();
+}
+
+}  // namespace ttkv_dev

@@ -180,7 +180,7 @@ class MultiStreamEngine:
                  heads_per_stream: int = 1, group_select: bool = False, device: int = 0,
                  reserve_tokens: int = 0, slow_tier: int = L.SLOW_PINNED_HOST,
                  copy_mode: int = 0, literal_additive_merge: bool = False,
-                 ring_bytes: int = 0):
+                 ring_bytes: int = 0, serial_schedule: bool = False):
         self.config = config
         self.policy = policy or SelectionPolicy(config.top_k_blocks, config.fetch_fraction)
         self.S, self.G = n_streams, heads_per_stream
@@ -189,7 +189,8 @@ class MultiStreamEngine:
         self._c_pol = self.policy.to_c()
         self._c_opt = L.OptionsC(device, n_streams, heads_per_stream, int(group_select),
                                  reserve_tokens, slow_tier, copy_mode,
-                                 int(literal_additive_merge), ring_bytes)
+                                 int(literal_additive_merge), ring_bytes,
+                                 int(serial_schedule))
         h = C.c_void_p()
         _check(self._lib.ttkv_gpu_create(C.byref(self._c_cfg), C.byref(self._c_pol),
                                          C.byref(self._c_opt), C.byref(h)))
