@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
       row[lane] = p0;
       row[lane + 32] = p1;
       const float sum = warp_sum(p0 + p1);
+      __syncwarp();  // all lanes have read mst[h] before lane 0 rewrites it
       if (lane == 0) {
         const float alpha = exp2f(m_old - m_new);
         lst[h] = lst[h] * alpha + sum;
@@ -484,6 +485,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, 2)
         sum += p;
       }
       sum = warp_sum(sum);
+      __syncwarp();  // all lanes have read mst[h] before lane 0 rewrites it
       if (a.literal) {  // each block its own normalized partition (engine.cpp:67-72)
         const float inv = 1.0f / sum;
 #pragma unroll
