@@ -55,7 +55,8 @@ def metric_for(w):
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=None,
+                   help="timed steps (default 10; cfg5: per growth point, default B=128)")
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
@@ -65,6 +66,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--slow-tier", default="host", choices=["host", "device"])
     a = p.parse_args()
+    a.steps_given = a.steps is not None
+    if a.steps is None:
+        a.steps = 10
     a.w = dict(WORKLOADS[a.workload])
     if a.ctx:
         a.w["ctx"] = a.ctx
@@ -223,6 +227,35 @@ def load_traffic():
         return None
 
 
+def init_dist(torch, dist, local, world):
+    """One process per GPU: NCCL over NVLink.  TTKV_DIST_BACKEND=gloo with
+    TTKV_SHARE_DEVICE=1 runs every rank on cuda:0 (exercises the N>1 path on a
+    1-GPU box; the NVLink numbers need NCCL and one GPU per rank)."""
+    share = os.environ.get("TTKV_SHARE_DEVICE") == "1"
+    dev = torch.device("cuda", 0 if share else local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        backend = os.environ.get("TTKV_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    return dev
+
+
+def allreduce_max(t):
+    """max over ranks (device tensor; staged through the host for gloo)."""
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return t
+    if dist.get_backend() == "nccl":
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t
+    c = t.cpu()
+    dist.all_reduce(c, op=dist.ReduceOp.MAX)
+    return c.to(t.device)
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -231,10 +264,7 @@ def run_ours(args):
     from paper_2604_19769_b200.sharding import ShardPlan, gather_outputs
 
     rank, local, world = dist_env()
-    dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    dev = init_dist(torch, dist, local, world)
     w = args.w
     G, ctx, batch = w["G"], w["ctx"], w["batch"]
     mode = "heads" if batch == 1 else "requests"
@@ -245,7 +275,7 @@ def run_ours(args):
                        block_size=B, key_bits=8, value_bits=4, fetch_fraction=FRAC)
     n_steps_total = args.warmup + 2 * args.steps + 2
     eng = T.MultiStreamEngine(cfg, T.SelectionPolicy(None, FRAC), n_streams=S,
-                              heads_per_stream=G, group_select=args.group_select, device=local,
+                              heads_per_stream=G, group_select=args.group_select, device=dev.index,
                               reserve_tokens=ctx + n_steps_total + B,
                               slow_tier=0 if args.slow_tier == "host" else 1)
     stream = torch.cuda.Stream(device=dev)
@@ -281,7 +311,7 @@ def run_ours(args):
     eng.kernel_times(reset=True)
     eng.set_timing(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
+    with Clocks(dev.index) as clk:
         barrier()
         ev0.record()
         for i in range(args.steps):
@@ -314,7 +344,7 @@ def run_ours(args):
     # --- max over ranks ---------------------------------------------------------
     vals = torch.tensor([ms_total, e2e_ms], device=dev, dtype=torch.float64)
     if world > 1:
-        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+        vals = allreduce_max(vals)
     ms_total, e2e_ms = float(vals[0]), float(vals[1])
     ms_step = ms_total / args.steps
     tokens_per_step = batch  # one generated token per request per step
@@ -406,12 +436,228 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+GROWTH_POINTS = (131072, 163840, 196608, 229376, 262144)
+
+
+def run_growth(args):
+    """cfg5 (BASELINE configs[4]): sustained generation 128K -> 256K.
+
+    Generating 131,072 tokens takes hours, so the growth curve is sampled:
+    at each context point (prefill/bulk-append to it, W warm-up steps) one
+    full eviction period of B=128 consecutive decode steps is timed, so each
+    window contains exactly one fast-tier eviction + quantize-to-DRAM of all
+    S streams (a B-th of the steps, as in sustained generation).  Step times
+    are recorded per step with CUDA events on the engine's stream.  `value` is
+    131,072 tokens / the trapezoid integral of ms/step over the growth, i.e.
+    the sustained generation rate of the 128K->256K run; `ms_per_step` is its
+    reciprocal."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2604_19769_b200 as T
+    from paper_2604_19769_b200.sharding import ShardPlan, gather_outputs
+
+    rank, local, world = dist_env()
+    dev = init_dist(torch, dist, local, world)
+    w = args.w
+    G = w["G"]
+    plan = ShardPlan(rank, world, w["layers"], w["kv_heads"], w["batch"], "heads")
+    S = plan.n_local
+    K = args.steps if args.steps_given else B
+    points = GROWTH_POINTS if not args.ctx else (args.ctx,)
+    cfg = T.TierConfig(hbm_budget_bytes=L_FAST * 2 * D * 2, d_k=D, d_v=D, bytes_full_precision=2,
+                       block_size=B, key_bits=8, value_bits=4, fetch_fraction=FRAC)
+    eng = T.MultiStreamEngine(cfg, T.SelectionPolicy(None, FRAC), n_streams=S,
+                              heads_per_stream=G, group_select=args.group_select, device=dev.index,
+                              reserve_tokens=points[-1] + len(points) * (args.warmup + K) + 2 * B,
+                              slow_tier=0 if args.slow_tier == "host" else 1)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    eng.set_stream(stream.cuda_stream)
+    h2d_peak = measure_h2d_peak(torch, dev)
+    gen = torch.Generator(device=dev).manual_seed(rank)
+    NPOOL = 4
+    qs = [torch.randn(S, G, D, device=dev, generator=gen) for _ in range(NPOOL)]
+    ks = [torch.randn(S, D, device=dev, generator=gen).half() for _ in range(NPOOL)]
+    vs = [torch.randn(S, D, device=dev, generator=gen).half() for _ in range(NPOOL)]
+    out = torch.empty(S, G, D, device=dev, dtype=torch.float64)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    curve, non_ev, evict_ms, launches, prefill_s = [], [], [], 0, 0.0
+    kt_tot = {}
+    pcie_last = union_last = 0
+    with Clocks(dev.index) as clk:
+        for pi, ctx in enumerate(points):
+            have = eng.state()["appended"]
+            if have < ctx:
+                t0 = time.time()
+                eng.prefill_synthetic(ctx - have, seed=1000 + 17 * pi + rank)
+                torch.cuda.synchronize()
+                prefill_s += time.time() - t0
+            for i in range(args.warmup):
+                eng.decode_step_device(qs[i % NPOOL].data_ptr(), ks[i % NPOOL].data_ptr(),
+                                       vs[i % NPOOL].data_ptr(), out.data_ptr(), dtype=1)
+            barrier()
+            st0 = eng.state()
+            eng.kernel_times(reset=True)
+            eng.set_timing(True)
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+            ev_flags = []
+            barrier()
+            evs[0].record()
+            for i in range(K):
+                rep = eng.decode_step_device(qs[i % NPOOL].data_ptr(), ks[i % NPOOL].data_ptr(),
+                                             vs[i % NPOOL].data_ptr(), out.data_ptr(), dtype=1)
+                if plan.needs_gather:
+                    gather_outputs(out, plan)
+                evs[i + 1].record()
+                ev_flags.append(bool(rep.eviction_occurred))
+            barrier()
+            eng.set_timing(False)
+            kt = eng.kernel_times(reset=True)
+            for k_, v_ in kt.items():
+                kt_tot[k_] = kt_tot.get(k_, 0) + v_
+            st1 = eng.state()
+            launches += st1["launches"] - st0["launches"]
+            step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(K)]
+            tot = torch.tensor([evs[0].elapsed_time(evs[K])], device=dev, dtype=torch.float64)
+            if world > 1:
+                tot = allreduce_max(tot)
+            union_last, pcie_last = eng.step_counters()
+            ev_idx = [i for i, f in enumerate(ev_flags) if f]
+            evict_ms += [step_ms[i] for i in ev_idx]
+            non_ev += [m for i, m in enumerate(step_ms) if not ev_flags[i]]
+            curve.append({"ctx_start": st0["appended"], "slow_blocks": st1["slow_blocks"],
+                          "ms_per_step": float(tot[0]) / K,
+                          "p50_ms": float(np.percentile(step_ms, 50)),
+                          "p95_ms": float(np.percentile(step_ms, 95)),
+                          "max_ms": float(max(step_ms)),
+                          "eviction_steps": len(ev_idx),
+                          "eviction_step_ms": [round(step_ms[i], 3) for i in ev_idx],
+                          "evict_kernel_ms": kt["ms_evict"] / max(1, kt["n_evict"]),
+                          "slow_kernel_ms": kt["ms_slow"] / max(1, kt["n_slow"]),
+                          "union_blocks": union_last})
+
+    # sustained rate over the growth: integrate ms/step(ctx) (trapezoid)
+    if len(curve) > 1:
+        xs = [c["ctx_start"] for c in curve]
+        ys = [c["ms_per_step"] for c in curve]
+        total_ms = sum((xs[i + 1] - xs[i]) * (ys[i] + ys[i + 1]) / 2 for i in range(len(xs) - 1))
+        ms_step = total_ms / (xs[-1] - xs[0])
+    else:
+        ms_step = curve[0]["ms_per_step"]
+    value = 1000.0 / ms_step
+
+    # e2e through the C ABI with host buffers, at the last (256K) point
+    rng = np.random.default_rng(rank)
+    hq = [rng.standard_normal((S, G, D)).astype(np.float32) for _ in range(NPOOL)]
+    hk = [rng.standard_normal((S, D)).astype(np.float16) for _ in range(NPOOL)]
+    hv = [rng.standard_normal((S, D)).astype(np.float16) for _ in range(NPOOL)]
+    n_e2e = min(K, 16)
+    barrier()
+    t_e2e0 = time.perf_counter()
+    for i in range(n_e2e):
+        r = eng.decode_step(hq[i % NPOOL], hk[i % NPOOL], hv[i % NPOOL])
+        if plan.needs_gather:
+            _ = gather_outputs(torch.from_numpy(r.output).to(dev), plan).cpu()
+    barrier()
+    e2e_ms = (time.perf_counter() - t_e2e0) * 1000.0 / n_e2e
+    vals = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        vals = allreduce_max(vals)
+    e2e_ms = float(vals[0])
+    # e2e at the 256K point vs the device-timed last point: scale the growth
+    # rate by the same host-path overhead
+    e2e_value = value * curve[-1]["ms_per_step"] / e2e_ms
+
+    st = eng.state()
+    rec, payload = st["record_bytes"], st["payload_bytes"]
+    slow_ms = curve[-1]["slow_kernel_ms"]
+    achieved = union_last * payload / (slow_ms * 1e-3) / 1e9 if slow_ms > 0 else 0.0
+    evict_bytes = S * rec  # one record per stream per eviction step
+    ek = [c["evict_kernel_ms"] for c in curve if c["eviction_steps"]]
+    evict_kernel_ms = statistics.mean(ek) if ek else None
+    line = {
+        "metric": metric_for(args.workload), "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": K * len(points), "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (device N(0,1) KV rounded to fp16, random queries)",
+        "config": {
+            "workload": w["desc"] + (f", head-sharded over {world} GPUs + NCCL all-gather"
+                                     if plan.needs_gather else ""),
+            "growth_points": list(points), "steps_per_point": K,
+            "timing": ("per point: one eviction period (B consecutive steps) timed with CUDA "
+                       "events; value = 131072 tokens / trapezoid integral of ms/step over "
+                       "the sampled 128K->256K curve"),
+            "streams_per_gpu": S, "heads_per_stream": G, "batch": 1, "d": D, "block": B,
+            "l_fast": L_FAST, "bits": "K8/V4", "fetch_fraction": FRAC,
+            "selection": "group-shared" if args.group_select else "per-query-head (reference)",
+            "slow_tier": "pinned host DRAM, zero-copy PCIe" if args.slow_tier == "host" else "HBM",
+            "parallelism": f"heads-shard{world}" if world > 1 else "single",
+            "l2": "inputs larger than L2 (slow tier 6.8-13.7 GB)",
+        },
+        "growth_curve": curve,
+        "eviction": {"steps": len(evict_ms),
+                     "step_ms_mean": statistics.mean(evict_ms) if evict_ms else None,
+                     "non_eviction_step_ms_mean": statistics.mean(non_ev) if non_ev else None,
+                     "evict_kernel_ms": evict_kernel_ms,
+                     "d2h_bytes_per_eviction_step": evict_bytes,
+                     "d2h_gbs": (evict_bytes / (evict_kernel_ms * 1e-3) / 1e9
+                                 if evict_kernel_ms else None)},
+        "roofline": {
+            "bound": "pcie_h2d", "kernel": "slow_stream_attn", "at_ctx": curve[-1]["ctx_start"],
+            "achieved": achieved, "peak": h2d_peak, "unit": "GB/s", "frac": achieved / h2d_peak,
+            "peak_source": "pinned cudaMemcpy H2D 256 MiB best of 10, measured in this run",
+            "traffic": None, "algorithmic_bytes_per_launch": union_last * payload,
+            "launch_ms": slow_ms},
+        "kernel_ms_per_step": {k[3:]: v / (K * len(points)) for k, v in kt_tot.items()
+                               if k.startswith("ms_")},
+        "gpu_launches": launches,
+        "e2e": {"value": e2e_value, "unit": UNIT,
+                "h2d_bytes_per_step": hq[0].nbytes + hk[0].nbytes + hv[0].nbytes,
+                "d2h_bytes_per_step": S * G * D * 8 * (world if plan.needs_gather else 1),
+                "ms_per_step_at_last_point": e2e_ms,
+                "note": "host-buffer C-ABI steps at the last point; value scaled by the "
+                        "device/host step-time ratio there"},
+        "prefill_s": round(prefill_s, 2),
+    }
+    if rank == 0:
+        line["clocks"] = clk.summary()
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            ctx = points[-1]
+            ms, _, engines, threads = ref_sample(ctx, 2, G)
+            total = S * G
+            line["cpu_baseline"] = {
+                "value": cpu_throughput(float(ms[-1]), engines, total, 1), "unit": UNIT,
+                "cores": threads, "kind": "reference",
+                "sample": (f"{engines} unmodified reference Engines at {ctx} ctx (the end of the "
+                           f"growth; upper bound on its sustained rate), 2 decode steps on "
+                           f"{threads} threads (last timed: {ms[-1]:.0f} ms), extrapolated "
+                           f"x{total / engines:g} to {total} engines")}
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": host_cores(),
+                                    "kind": "reference", "sample": f"unavailable: {e}"}
+    eng.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "cfg5":
+        run_growth(args)
     else:
         run_ours(args)
 

@@ -61,9 +61,13 @@ def gather_outputs(local_out, plan: ShardPlan, group=None):
     N = plan.world
     if N == 1:
         return local_out
-    gathered = torch.empty((N * local_out.shape[0],) + tuple(local_out.shape[1:]),
-                           dtype=local_out.dtype, device=local_out.device)
-    dist.all_gather_into_tensor(gathered, local_out.contiguous(), group=group)
+    src = local_out.contiguous()
+    if src.is_cuda and dist.get_backend(group) != "nccl":
+        src = src.cpu()  # gloo: stage through the host (test-only path)
+    gathered = torch.empty((N * src.shape[0],) + tuple(src.shape[1:]), dtype=src.dtype,
+                           device=src.device)
+    dist.all_gather_into_tensor(gathered, src, group=group)
+    gathered = gathered.to(local_out.device)
     L, H, R = plan.layers, plan.kv_heads, plan.requests
     G, d = local_out.shape[1], local_out.shape[2]
     if plan.mode == "heads":
