@@ -19,6 +19,8 @@
 #include <cuda_fp16.h>
 #include <math.h>
 
+#include <cstdlib>
+
 #include "ttkv_kernels.cuh"
 #include "ttkv_launch.h"
 
@@ -287,19 +289,27 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
 // slow tier on tensor cores: K8/V4, d = 128, B = 128, fp16 ring (fp32 accum).
 // Per record: K codes [128 tok][128 B] by TMA (128B swizzle), V nibbles
 // [128 tok][64 B] by TMA (64B swizzle), params (2 KB) by bulk copy from the
-// HBM mirror.  QK^T = (q * s) . code + q . z  (scales folded into the A
-// operand, codes exact in fp16); PV = s * (P . code) + z *
-// sum(P) applied per block in the epilogue.  ldmatrix on the u8 code rows
-// yields 4 consecutive channels per thread, so the contraction index is
-// permuted identically in A and B (any permutation of a dot product's terms
-// is exact in real arithmetic).
+// HBM mirror.  The M dimension carries the record's tokens (QK) or channels
+// (PV) and N the G <= 8 query heads, so no MMA row is padding:
+//   S^T = codes_K . (q * s)^T + q . z    (scales folded into the B operand,
+//                                         codes exact in fp16)
+//   O^T = codes_V^T . P^T,  O = s * O^T + z * sum(P)  (affine epilogue)
+// * (q * s) and P are split into fp16 hi + lo (two MMAs, independent
+//   accumulator chains), so operand rounding stays ~2^-22 relative;
+// * the B fragments of (q * s) and P are built once per record by the whole
+//   CTA and staged in shared memory in fragment order (one LDS.128 each);
+// * K codes reach the MMA through ldmatrix + a 2-op u8 -> f16 conversion;
+//   V nibbles are decoded straight into A fragments (token pairs per channel)
+//   with the 0x6400 magic-number trick -- no fp16 V tile in shared memory;
+// * the contraction index of QK is permuted identically in A and B (exact in
+//   real arithmetic), and each thread owns 4 consecutive channels of PV.
 // ---------------------------------------------------------------------------
 namespace {
-constexpr int kSlowTcStages = 3;
 constexpr uint32_t kKBox = 128 * 128;  // K codes
 constexpr uint32_t kVBox = 128 * 64;   // V nibbles
 constexpr uint32_t kPBytes = 2 * 128 * 8;  // {scale, zp} x (128 K + 128 V)
-constexpr uint32_t kSlowStage = kKBox + kVBox + kPBytes;  // 26,624 B
+constexpr uint32_t kSlowStage = kKBox + kVBox + kPBytes;  // 26,624 B = 26 x 1024
+constexpr int kScPitch = 132;  // score row pitch (floats): conflict-free C-fragment stores
 
 __device__ __forceinline__ uint32_t swz64(uint32_t off) {  // TMA SWIZZLE_64B
   return off ^ (((off >> 7) & 3u) << 4);
@@ -312,6 +322,15 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
 }
+// D += A(16x16) * B(16x8), f16 in, f32 accumulate
+__device__ __forceinline__ void mma_a4(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                       uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
 // 4 u8 codes -> two half2 {c0,c1}, {c2,c3} (exact: 1024 + c minus 1024)
 __device__ __forceinline__ void codes_to_h2(uint32_t w, uint32_t& lo, uint32_t& hi) {
   const uint32_t a = __byte_perm(w, 0x64646464u, 0x5140u);
@@ -322,13 +341,49 @@ __device__ __forceinline__ void codes_to_h2(uint32_t w, uint32_t& lo, uint32_t& 
   lo = *reinterpret_cast<uint32_t*>(&ha);
   hi = *reinterpret_cast<uint32_t*>(&hb);
 }
+// x = [t.b0, t.b1, t'.b0, t'.b1] (two tokens' 4 LSB-first nibbles = channels
+// c..c+3) -> half2 {v[t][c+i], v[t'][c+i]} for i = 0..3, exact integers.
+__device__ __forceinline__ void nibbles_to_h2(uint32_t x, uint32_t& c0, uint32_t& c1,
+                                              uint32_t& c2, uint32_t& c3) {
+  const uint32_t y = x >> 8;
+  const uint32_t e0 = (x & 0x000F000Fu) | 0x64006400u;  // 1024 + n
+  const uint32_t o0 = (x & 0x00F000F0u) | 0x64006400u;  // 1024 + 16 n
+  const uint32_t e1 = (y & 0x000F000Fu) | 0x64006400u;
+  const uint32_t o1 = (y & 0x00F000F0u) | 0x64006400u;
+  const __half2 k1024 = __floats2half2_rn(1024.f, 1024.f);
+  const __half2 k16 = __floats2half2_rn(0.0625f, 0.0625f), k64 = __floats2half2_rn(-64.f, -64.f);
+  __half2 r0 = __hsub2(*reinterpret_cast<const __half2*>(&e0), k1024);
+  __half2 r1 = __hfma2(*reinterpret_cast<const __half2*>(&o0), k16, k64);
+  __half2 r2 = __hsub2(*reinterpret_cast<const __half2*>(&e1), k1024);
+  __half2 r3 = __hfma2(*reinterpret_cast<const __half2*>(&o1), k16, k64);
+  c0 = *reinterpret_cast<uint32_t*>(&r0);
+  c1 = *reinterpret_cast<uint32_t*>(&r1);
+  c2 = *reinterpret_cast<uint32_t*>(&r2);
+  c3 = *reinterpret_cast<uint32_t*>(&r3);
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  // try_wait with a suspend-time hint: the producer sleeps in hardware until
+  // the consumers release the stage instead of spinning on issue slots
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(10000000u)
+      : "memory");
+}
+template <int GT>
+constexpr size_t slow_tc_tail_bytes() {
+  // qsf + phl (2 x 256 uint4) | sc [GT][kScPitch] | qsm [GT][128] | 5 x 8 stats
+  return 2 * 256 * 16 + (size_t)GT * kScPitch * 4 + (size_t)GT * 128 * 4 + 5 * 8 * 4;
+}
 }  // namespace
 
-// 2 CTAs/SM: 10 warps over 4 SMSPs -> <= 168 registers per thread
-template <int GT>
-__global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, 2)
+template <int GT, int ST>
+__global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
     slow_attn_tc_kernel(const __grid_constant__ SlowTcArgs a) {
   const Geometry& g = a.g;
+  const uint32_t G = g.G;
   const uint32_t s = blockIdx.y, chunk = blockIdx.x;
   const uint32_t cnt = a.union_count[s];
   const uint32_t i0 = chunk * a.CH;
@@ -339,26 +394,36 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, 2)
   // 1024-align by offsetting the shared array itself so the compiler keeps
   // the shared address space (LDS, not generic LD)
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* vtile = base + kSlowTcStages * kSlowStage;  // 2 boxes [64 tok][128 B] fp16 codes
-  uint64_t* full = reinterpret_cast<uint64_t*>(vtile + 2 * 64 * 128);
-  uint64_t* empty = full + kSlowTcStages;
-  float* sc2 = reinterpret_cast<float*>(empty + kSlowTcStages);  // [2][GT][128]
-  float* mst = sc2 + 2 * GT * 128;
-  float* lst = mst + GT;
-  float* ast = lst + GT;
-  float* pst = ast + GT;  // sum_t p of the current block
+  uint4* qsf = reinterpret_cast<uint4*>(base + ST * kSlowStage);  // [8 j][8 head][4 q]
+  uint4* phl = qsf + 256;                                         // [8 ks][8 head][4 q]
+  float* sc = reinterpret_cast<float*>(phl + 256);                // [GT][kScPitch]
+  float* qsm = sc + GT * kScPitch;                                // [GT][128] log2-scaled q
+  float* mst = qsm + GT * 128;
+  float* lst = mst + 8;
+  float* ast = lst + 8;
+  float* pst = ast + 8;  // sum_t p of the current block
+  float* bst = pst + 8;  // beta = q . z of the current block
+  uint64_t* full = reinterpret_cast<uint64_t*>(bst + 8);
+  uint64_t* empty = full + ST;
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kSlowTcStages; ++i) {
+    for (int i = 0; i < ST; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], kSlowConsumerWarps);
     }
     fence_mbar_init();
   }
-  if (threadIdx.x < GT) {
+  for (uint32_t i = threadIdx.x; i < 512; i += blockDim.x) qsf[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x < 8) {
     mst[threadIdx.x] = -INFINITY;
     lst[threadIdx.x] = 0.0f;
+  }
+  {
+    const float* qb = a.q + (uint64_t)s * G * 128;
+    const float sl = (float)a.scale_log2;
+    for (uint32_t i = threadIdx.x; i < GT * 128; i += blockDim.x)
+      qsm[i] = (i / 128 < G) ? qb[i] * sl : 0.f;
   }
   __syncthreads();
   const uint32_t* uids = a.union_ids + (uint64_t)s * g.n_cap + i0;
@@ -367,10 +432,9 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, 2)
   if (warp == 0) {
     if (lane == 0) {
       for (uint32_t i = 0; i < nb; ++i) {
-        const uint32_t st = i % kSlowTcStages;
-        if (i >= kSlowTcStages) mbar_wait_backoff(&empty[st], ((i / kSlowTcStages) - 1) & 1);
-        const uint32_t blk = uids[i];
-        const int rec = (int)((uint64_t)s * g.n_cap + blk);
+        const uint32_t st = i % ST;
+        if (i >= ST) mbar_wait_sleep(&empty[st], ((i / ST) - 1) & 1);
+        const int rec = (int)((uint64_t)s * g.n_cap + uids[i]);
         uint8_t* dst = base + st * kSlowStage;
         mbar_arrive_expect_tx(&full[st], kSlowStage);
         tma_load_3d(dst, &a.tk, 0, 0, rec, &full[st]);
@@ -382,115 +446,115 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, 2)
   }
 
   const uint32_t cw = warp - 1, ct = threadIdx.x - 32;
-  const uint32_t gq = lane >> 2, qq = lane & 3;
-  const bool head_ok = gq < g.G;
+  const uint32_t gq = lane >> 2, qq = lane & 3;  // fragment row group / thread in group
   const int nthreads_c = kSlowConsumerWarps * 32;
-  // this thread's 32 query channels (permuted order), log2-scaled:
-  // segment j -> channels 16j + 4qq + {0,1,2,3}
-  // the (log2-scaled) queries live in smem, not registers (2 CTAs/SM budget)
-  float* qsm = pst + GT;  // [GT][128]
-  {
-    const float* qb = a.q + (uint64_t)s * g.G * 128;
-    const float sl = (float)a.scale_log2;
-    for (uint32_t i2 = ct; i2 < GT * 128; i2 += nthreads_c)
-      qsm[i2] = (i2 / 128 < g.G) ? qb[i2] * sl : 0.f;
-    named_bar(1, nthreads_c);
-  }
-  const float* qrow = qsm + (head_ok ? gq : 0) * 128;
-  float acc[4][2];  // running output: head gq, channels 8(4cw + j) + 2qq + {0,1}
+  // PV ownership: channels c0 .. c0 + 3, heads 2qq, 2qq + 1
+  const uint32_t c0 = 32 * cw + 4 * gq;
+  float acc[4][2];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.f;
+  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.f;
   uint32_t seen = 0;
 
   for (uint32_t i = 0; i < nb; ++i) {
-    const uint32_t st = i % kSlowTcStages;
-    mbar_wait(&full[st], (i / kSlowTcStages) & 1);
+    const uint32_t st = i % ST;
+    mbar_wait(&full[st], (i / ST) & 1);
     uint8_t* stg = base + st * kSlowStage;
-    const uint32_t kb = smem_u32(stg), vb_nib = kKBox;  // V nibbles at stg + kKBox
+    const uint32_t kb = smem_u32(stg);
+    const uint8_t* vn = stg + kKBox;
     const float* kp = reinterpret_cast<const float*>(stg + kKBox + kVBox);  // {s,z} x 128
     const float* vp = kp + 2 * 128;
     const uint32_t hm = umask[i];
     seen |= hm;
-    float* sc = sc2 + (i & 1) * GT * 128;  // double-buffered: PV(i-1) may still read
 
-    // ---- A operand: (q * s) hi/lo in the permuted channel order, beta = q . z ----
-    uint32_t ah[8][2], al[8][2];
-    float beta = 0.f;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float4 sz0 = *reinterpret_cast<const float4*>(kp + 2 * (16 * j + 4 * qq));
-      const float4 sz1 = *reinterpret_cast<const float4*>(kp + 2 * (16 * j + 4 * qq) + 4);
-      const float4 qv = *reinterpret_cast<const float4*>(qrow + 16 * j + 4 * qq);
-      const float x0 = qv.x * sz0.x, x1 = qv.y * sz0.z;
-      const float x2 = qv.z * sz1.x, x3 = qv.w * sz1.z;
-      beta += qv.x * sz0.y + qv.y * sz0.w + qv.z * sz1.y + qv.w * sz1.w;
-      split2(x0, x1, ah[j][0], al[j][0]);
-      split2(x2, x3, ah[j][1], al[j][1]);
-    }
-    beta += __shfl_xor_sync(0xffffffffu, beta, 1);
-    beta += __shfl_xor_sync(0xffffffffu, beta, 2);
-
-    // ---- QK^T: warp cw -> tokens [32cw, 32cw + 32), two n-tiles at a time:
-    // 4 independent accumulator chains (2 n-tiles x hi/lo) ----
-#pragma unroll
-    for (int hp = 0; hp < 2; ++hp) {
-      float c[2][2][4];
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) c[h][0][e] = c[h][1][e] = 0.f;
-#pragma unroll
-      for (int jp = 0; jp < 2; ++jp) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int m = lane >> 3;
-          const int row = 8 * (4 * cw + 2 * hp + h) + (lane & 7);
-          const uint32_t addr = kb + swz128(row * 128 + (4 * jp + m) * 16);
-          uint32_t r[4];
-          ldsm_x4(addr, r[0], r[1], r[2], r[3]);
-#pragma unroll
-          for (int mm = 0; mm < 4; ++mm) {
-            uint32_t b0, b1;
-            codes_to_h2(r[mm], b0, b1);
-            const int j = 4 * jp + mm;
-            mma16816(c[h][0], ah[j][0], ah[j][1], b0, b1);
-            mma16816(c[h][1], al[j][0], al[j][1], b0, b1);
-          }
-        }
-      }
-      if (head_ok) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t tA = 8 * (4 * cw + 2 * hp + h) + 2 * qq;
-          sc[gq * 128 + tA] = c[h][0][0] + c[h][1][0] + beta;
-          sc[gq * 128 + tA + 1] = c[h][0][1] + c[h][1][1] + beta;
-        }
-      }
+    // ---- (q * s) B fragments (hi/lo) and beta = q . z, once per record ----
+    for (uint32_t e = ct; e < G * 32; e += nthreads_c) {  // warp-uniform: one head per warp
+      const uint32_t h = e >> 5, j = (e >> 2) & 7u, q4 = e & 3u;
+      const uint32_t c = 16 * j + 4 * q4;
+      const float4 qv = *reinterpret_cast<const float4*>(qsm + h * 128 + c);
+      const float4 sz0 = *reinterpret_cast<const float4*>(kp + 2 * c);
+      const float4 sz1 = *reinterpret_cast<const float4*>(kp + 2 * c + 4);
+      uint32_t h01, l01, h23, l23;
+      split2(qv.x * sz0.x, qv.y * sz0.z, h01, l01);
+      split2(qv.z * sz1.x, qv.w * sz1.z, h23, l23);
+      qsf[(j * 8 + h) * 4 + q4] = make_uint4(h01, h23, l01, l23);
+      float beta = qv.x * sz0.y + qv.y * sz0.w + qv.z * sz1.y + qv.w * sz1.w;
+      beta = warp_sum(beta);
+      if (lane == 0) bst[h] = beta;
     }
     named_bar(1, nthreads_c);
 
-    // ---- block softmax statistics (one warp per selecting head) ----
-    for (uint32_t h = cw; h < g.G; h += kSlowConsumerWarps) {
-      if (!((hm >> h) & 1u)) continue;
-      float* row = sc + h * 128;
-      float bm = fmaxf(fmaxf(row[lane], row[lane + 32]), fmaxf(row[lane + 64], row[lane + 96]));
-      bm = warp_max(bm);
+    // ---- QK^T: warp cw -> tokens [32cw, 32cw + 32) = 2 m-tiles; hi and lo
+    // accumulate in independent chains ----
+    {
+      float c[2][2][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) c[mt][0][e] = c[mt][1][e] = 0.f;
+#pragma unroll
+      for (int jp = 0; jp < 4; ++jp) {
+        const uint4 b0 = qsf[((2 * jp) * 8 + gq) * 4 + qq];
+        const uint4 b1 = qsf[((2 * jp + 1) * 8 + gq) * 4 + qq];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          // matrices: (tok 0-7, chunk 2jp), (tok 8-15, 2jp), (tok 0-7, 2jp+1), (tok 8-15, 2jp+1)
+          const int m = lane >> 3;
+          const int tok = 32 * cw + 16 * mt + 8 * (m & 1) + (lane & 7);
+          const uint32_t addr = kb + swz128(tok * 128 + (2 * jp + (m >> 1)) * 16);
+          uint32_t r0, r1, r2, r3, a0, a1, a2, a3;
+          ldsm_x4(addr, r0, r1, r2, r3);
+          codes_to_h2(r0, a0, a2);
+          codes_to_h2(r1, a1, a3);
+          mma_a4(c[mt][0], a0, a1, a2, a3, b0.x, b0.y);
+          mma_a4(c[mt][1], a0, a1, a2, a3, b0.z, b0.w);
+          codes_to_h2(r2, a0, a2);
+          codes_to_h2(r3, a1, a3);
+          mma_a4(c[mt][0], a0, a1, a2, a3, b1.x, b1.y);
+          mma_a4(c[mt][1], a0, a1, a2, a3, b1.z, b1.w);
+        }
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t h = 2 * qq + (e & 1);
+          const uint32_t t = 32 * cw + 16 * mt + gq + 8 * (e >> 1);
+          if (h < G) sc[h * kScPitch + t] = c[mt][0][e] + c[mt][1][e] + bst[h];
+        }
+    }
+    named_bar(1, nthreads_c);
+
+    // ---- block softmax statistics + P fragments (one warp per head); lane
+    // (ks, q) owns tokens 16ks + 2q + {0, 1, 8, 9} ----
+    for (uint32_t h = cw; h < G; h += kSlowConsumerWarps) {
+      const uint32_t ks = lane >> 2, q4 = lane & 3;
+      uint4* dst = phl + (ks * 8 + h) * 4 + q4;
+      if (!((hm >> h) & 1u)) {  // head did not select this block
+        *dst = make_uint4(0, 0, 0, 0);
+        if (lane == 0) {
+          ast[h] = 1.0f;
+          pst[h] = 0.0f;
+        }
+        continue;
+      }
+      const float* row = sc + h * kScPitch + 16 * ks + 2 * q4;
+      const float2 v01 = *reinterpret_cast<const float2*>(row);
+      const float2 v89 = *reinterpret_cast<const float2*>(row + 8);
+      const float bm = warp_max(fmaxf(fmaxf(v01.x, v01.y), fmaxf(v89.x, v89.y)));
       const float m_old = mst[h];
       const float m_new = a.literal ? bm : fmaxf(m_old, bm);
-      float sum = 0.f;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float p = exp2f(row[lane + 32 * k] - m_new);
-        row[lane + 32 * k] = p;
-        sum += p;
-      }
-      sum = warp_sum(sum);
-      __syncwarp();  // all lanes have read mst[h] before lane 0 rewrites it
+      float p0 = exp2f(v01.x - m_new), p1 = exp2f(v01.y - m_new);
+      float p8 = exp2f(v89.x - m_new), p9 = exp2f(v89.y - m_new);
+      const float sum = warp_sum((p0 + p1) + (p8 + p9));
       if (a.literal) {  // each block its own normalized partition (engine.cpp:67-72)
         const float inv = 1.0f / sum;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) row[lane + 32 * k] *= inv;
+        p0 *= inv; p1 *= inv; p8 *= inv; p9 *= inv;
       }
+      uint32_t h01, l01, h89, l89;
+      split2(p0, p1, h01, l01);
+      split2(p8, p9, h89, l89);
+      *dst = make_uint4(h01, h89, l01, l89);
+      __syncwarp();  // all lanes have read mst[h] before lane 0 rewrites it
       if (lane == 0) {
         if (a.literal) {
           ast[h] = 1.0f;
@@ -504,85 +568,50 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, 2)
         }
       }
     }
-    // ---- PV on codes, in two 64-token halves: V nibbles -> fp16 codes into a
-    // 16 KB swizzled tile (two threads per token row), then mma.  Warp cw owns
-    // channels [32cw, 32cw + 32). ----
-    const bool sel = head_ok && ((hm >> gq) & 1u);
-    float cfr[4][4];  // P . code per output n-tile (hi and lo MMAs accumulate here)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) cfr[j][0] = cfr[j][1] = cfr[j][2] = cfr[j][3] = 0.f;
+    named_bar(1, nthreads_c);
+
+    // ---- PV^T: warp cw -> channels [32cw, 32cw + 32) as 2 m-tiles; thread
+    // rows gq / gq + 8 of m-tile 0 = channels c0, c0 + 1, of m-tile 1 =
+    // c0 + 2, c0 + 3 (one u16 of V nibbles per token) ----
     {
-      const uint32_t vt = smem_u32(vtile);
-      const uint8_t* vn = stg + vb_nib;
+      float cf[2][2][4];
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        if (half) named_bar(1, nthreads_c);  // first-half PV done before overwrite
-        {
-          const uint32_t lr = ct >> 1, tr = 64 * half + lr;
+      for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-          for (int c2 = 0; c2 < 2; ++c2) {
-            const int cc = 2 * (ct & 1) + c2;  // 16-byte chunk = channels 32cc .. 32cc+31
-            const uint4 w = *reinterpret_cast<const uint4*>(vn + swz64(tr * 64 + 16 * cc));
-            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+        for (int e = 0; e < 4; ++e) cf[mt][0][e] = cf[mt][1][e] = 0.f;
+      const uint32_t boff = c0 >> 1;  // byte of channel c0 in a token row
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {  // 8 channels: 32cc + 8u .. + 7
-              const uint32_t e = ws[u] & 0x0F0F0F0Fu, o = (ws[u] >> 4) & 0x0F0F0F0Fu;
-              uint32_t h2[4];
-#pragma unroll
-              for (int b = 0; b < 4; ++b) {
-                // result bytes [e.b, o.b, -, -] -> halves {e.b, o.b} = channels 2b, 2b+1
-                const uint32_t x = __byte_perm(e, o, (uint32_t)b | ((4u + (uint32_t)b) << 4));
-                const uint32_t hx = (x & 0x000000FFu) | ((x & 0x0000FF00u) << 8) | 0x64006400u;
-                const __half2 hv = __hsub2(*reinterpret_cast<const __half2*>(&hx),
-                                           __floats2half2_rn(1024.f, 1024.f));
-                h2[b] = *reinterpret_cast<const uint32_t*>(&hv);
-              }
-              const int ch = 32 * cc + 8 * u;
-              *reinterpret_cast<uint4*>(vtile + (ch >> 6) * (64 * 128) +
-                                        swz128(lr * 128 + (ch & 63) * 2)) =
-                  make_uint4(h2[0], h2[1], h2[2], h2[3]);
-            }
-          }
-        }
-        named_bar(1, nthreads_c);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const int ks = 4 * half + kk;
-          uint32_t ph0, pl0, ph1, pl1;
-          {
-            const float* pr = sc + (head_ok ? gq : 0) * 128 + 16 * ks + 2 * qq;
-            const float2 p01 = sel ? *reinterpret_cast<const float2*>(pr) : make_float2(0, 0);
-            const float2 p89 = sel ? *reinterpret_cast<const float2*>(pr + 8) : make_float2(0, 0);
-            split2(p01.x, p01.y, ph0, pl0);
-            split2(p89.x, p89.y, ph1, pl1);
-          }
-#pragma unroll
-          for (int jp = 0; jp < 2; ++jp) {
-            const int m = lane >> 3;
-            const int ntc = 4 * cw + 2 * jp + (m >> 1);
-            const int row = 16 * kk + 8 * (m & 1) + (lane & 7);
-            const int ch = 8 * ntc;
-            const uint32_t addr = vt + (ch >> 6) * (64 * 128) + swz128(row * 128 + (ch & 63) * 2);
-            uint32_t b0, b1, b2, b3;
-            ldsm_x4_t(addr, b0, b1, b2, b3);
-            mma16816(cfr[2 * jp], ph0, ph1, b0, b1);
-            mma16816(cfr[2 * jp + 1], ph0, ph1, b2, b3);
-            mma16816(cfr[2 * jp], pl0, pl1, b0, b1);
-            mma16816(cfr[2 * jp + 1], pl0, pl1, b2, b3);
-          }
-        }
+      for (int ks = 0; ks < 8; ++ks) {
+        const uint32_t t0 = 16 * ks + 2 * qq;
+        const uint32_t u0 = *reinterpret_cast<const uint16_t*>(vn + swz64(t0 * 64 + boff));
+        const uint32_t u1 = *reinterpret_cast<const uint16_t*>(vn + swz64((t0 + 1) * 64 + boff));
+        const uint32_t u8 = *reinterpret_cast<const uint16_t*>(vn + swz64((t0 + 8) * 64 + boff));
+        const uint32_t u9 = *reinterpret_cast<const uint16_t*>(vn + swz64((t0 + 9) * 64 + boff));
+        uint32_t x0, x1, x2, x3, y0, y1, y2, y3;
+        nibbles_to_h2(__byte_perm(u0, u1, 0x5410u), x0, x1, x2, x3);
+        nibbles_to_h2(__byte_perm(u8, u9, 0x5410u), y0, y1, y2, y3);
+        const uint4 pb = phl[(ks * 8 + gq) * 4 + qq];
+        mma_a4(cf[0][0], x0, x1, y0, y1, pb.x, pb.y);
+        mma_a4(cf[0][1], x0, x1, y0, y1, pb.z, pb.w);
+        mma_a4(cf[1][0], x2, x3, y2, y3, pb.x, pb.y);
+        mma_a4(cf[1][1], x2, x3, y2, y3, pb.z, pb.w);
       }
-    }
-    {
       // affine epilogue: acc = acc * alpha + s_c * (P . code) + z_c * sum(P)
-      if (sel) {
-        const float alpha = ast[gq], psum = pst[gq];
+      const float4 sz01 = *reinterpret_cast<const float4*>(vp + 2 * c0);
+      const float4 sz23 = *reinterpret_cast<const float4*>(vp + 2 * c0 + 4);
+      const float vs[4] = {sz01.x, sz01.z, sz23.x, sz23.z};
+      const float vz[4] = {sz01.y, sz01.w, sz23.y, sz23.w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int ch = 8 * (4 * cw + j) + 2 * qq;
-          const float4 sz = *reinterpret_cast<const float4*>(vp + 2 * ch);
-          acc[j][0] = acc[j][0] * alpha + sz.x * cfr[j][0] + sz.y * psum;
-          acc[j][1] = acc[j][1] * alpha + sz.z * cfr[j][1] + sz.w * psum;
+      for (int hh = 0; hh < 2; ++hh) {
+        const uint32_t h = 2 * qq + hh;
+        if (h < G && ((hm >> h) & 1u)) {
+          const float alpha = ast[h], psum = pst[h];
+#pragma unroll
+          for (int ci = 0; ci < 4; ++ci) {
+            const int mt = ci >> 1, e = 2 * (ci & 1) + hh;
+            acc[ci][hh] = acc[ci][hh] * alpha + vs[ci] * (cf[mt][0][e] + cf[mt][1][e]) +
+                          vz[ci] * psum;
+          }
         }
       }
     }
@@ -590,21 +619,20 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, 2)
     if (lane == 0) mbar_arrive(&empty[st]);
   }
 
+  // ---- emit the (acc, m, l) partial of every head ----
   named_bar(1, nthreads_c);
   const uint32_t pitch = 128 + 2;
-  if (head_ok) {
-    float* p = reinterpret_cast<float*>(a.part) +
-               (((uint64_t)s * g.G + gq) * a.nsc + chunk) * pitch;
-    const bool any = (seen >> gq) & 1u;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int ch = 8 * (4 * cw + j) + 2 * qq;
-      p[ch] = any ? acc[j][0] : 0.f;
-      p[ch + 1] = any ? acc[j][1] : 0.f;
-    }
-    if (cw == 0 && qq == 0) {
-      p[128] = any ? (a.literal ? 0.f : mst[gq]) : -INFINITY;
-      p[129] = any ? (a.literal ? 1.f : lst[gq]) : 0.f;
+  for (int hh = 0; hh < 2; ++hh) {
+    const uint32_t h = 2 * qq + hh;
+    if (h >= G) continue;
+    float* p = reinterpret_cast<float*>(a.part) + (((uint64_t)s * G + h) * a.nsc + chunk) * pitch;
+    const bool any = (seen >> h) & 1u;
+#pragma unroll
+    for (int ci = 0; ci < 4; ++ci) p[c0 + ci] = any ? acc[ci][hh] : 0.f;
+    if (cw == 0 && gq == 0) {
+      p[128] = any ? (a.literal ? 0.f : mst[h]) : -INFINITY;
+      p[129] = any ? (a.literal ? 1.f : lst[h]) : 0.f;
     }
   }
 }
@@ -614,15 +642,22 @@ bool slow_tc_supported(const Geometry& g) {
          g.G <= 8 && g.rec.kp_off == kKBox + kVBox && g.rec.used == kSlowStage;
 }
 
-static size_t slow_tc_smem() {
-  return 1024 + (size_t)kSlowTcStages * kSlowStage + 2 * 64 * 128 + 2 * kSlowTcStages * 8 +
-         (2 * 8 * 128 + 4 * 8 + 8 * 128) * 4 + 64;
+// 2 stages x 3 CTAs/SM (measured: 1.34 ms vs 1.66 ms for 3 stages x 2 CTAs/SM
+// at cfg2); TTKV_SLOW_TC_STAGES=3 selects the deeper ring
+static int slow_tc_stages() {
+  const char* e = std::getenv("TTKV_SLOW_TC_STAGES");
+  return (e && e[0] == '3') ? 3 : 2;
 }
 
-template <int GT>
+template <int GT, int ST>
+static size_t slow_tc_smem() {
+  return 1024 + (size_t)ST * kSlowStage + slow_tc_tail_bytes<GT>() + 2 * ST * 8;
+}
+
+template <int GT, int ST>
 static cudaError_t launch_slow_tc_t(const SlowTcArgs& a, uint32_t grid_chunks, cudaStream_t st) {
-  const size_t smem = slow_tc_smem();
-  auto kern = slow_attn_tc_kernel<GT>;
+  const size_t smem = slow_tc_smem<GT, ST>();
+  auto kern = slow_attn_tc_kernel<GT, ST>;
   cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // max smem
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -631,12 +666,19 @@ static cudaError_t launch_slow_tc_t(const SlowTcArgs& a, uint32_t grid_chunks, c
   return cudaGetLastError();
 }
 
+template <int ST>
+static cudaError_t launch_slow_tc_s(const SlowTcArgs& a, uint32_t grid_chunks, cudaStream_t st) {
+  if (a.g.G <= 1) return launch_slow_tc_t<1, ST>(a, grid_chunks, st);
+  if (a.g.G <= 2) return launch_slow_tc_t<2, ST>(a, grid_chunks, st);
+  if (a.g.G <= 4) return launch_slow_tc_t<4, ST>(a, grid_chunks, st);
+  return launch_slow_tc_t<8, ST>(a, grid_chunks, st);
+}
+
 cudaError_t launch_slow_tc(const SlowTcArgs& a, uint32_t grid_chunks, cudaStream_t st) {
   if (grid_chunks == 0) return cudaSuccess;
-  if (a.g.G <= 1) return launch_slow_tc_t<1>(a, grid_chunks, st);
-  if (a.g.G <= 2) return launch_slow_tc_t<2>(a, grid_chunks, st);
-  if (a.g.G <= 4) return launch_slow_tc_t<4>(a, grid_chunks, st);
-  return launch_slow_tc_t<8>(a, grid_chunks, st);
+  static const int stages = slow_tc_stages();
+  return stages == 2 ? launch_slow_tc_s<2>(a, grid_chunks, st)
+                     : launch_slow_tc_s<3>(a, grid_chunks, st);
 }
 
 // Tensor maps over the record arena (device or mapped host pointer):

@@ -337,6 +337,7 @@ int ensure_blocks(ttkv_gpu* h, uint64_t need) {
   };
   CU(h, realloc_dev((void**)&h->scores, S * h->g.Gs * cap * sizeof(double)));
   CU(h, realloc_dev((void**)&h->mask, S * cap * sizeof(uint32_t)));
+  CU(h, cudaMemset(h->mask, 0, S * cap * sizeof(uint32_t)));  // select leaves it zeroed
   CU(h, realloc_dev((void**)&h->uids, S * cap * sizeof(uint32_t)));
   CU(h, realloc_dev((void**)&h->umask, S * cap * sizeof(uint32_t)));
   h->g.n_cap = cap;

@@ -43,9 +43,35 @@ __global__ void __launch_bounds__(128) score_kernel(ScoreArgs a) {
     }
   }
   const float* cb = a.cent + ((uint64_t)s * g.n_cap + b0) * g.d_k;
-  for (uint32_t i = threadIdx.x; i < kScoreTile * g.d_k; i += blockDim.x) {
-    const uint32_t r = i / g.d_k, c = i % g.d_k;
-    ct[r * pitch + c] = (b0 + r < a.n) ? cb[i] : 0.0f;
+  const uint32_t nrow = min((uint32_t)kScoreTile, a.n - b0);
+  if ((g.d_k & 3u) == 0) {
+    // 16-byte loads, all in flight before the first store (the tile is one
+    // contiguous run of centroid rows)
+    const uint32_t n4 = nrow * g.d_k / 4;
+    const float4* c4 = reinterpret_cast<const float4*>(cb);
+    constexpr int kU = 8;
+    for (uint32_t i0 = threadIdx.x; i0 < n4; i0 += kU * blockDim.x) {
+      float4 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t i = i0 + u * blockDim.x;
+        v[u] = i < n4 ? c4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t i = i0 + u * blockDim.x;
+        if (i < n4) {
+          const uint32_t r = 4 * i / g.d_k, c = 4 * i % g.d_k;
+          float* d = ct + r * pitch + c;
+          d[0] = v[u].x; d[1] = v[u].y; d[2] = v[u].z; d[3] = v[u].w;
+        }
+      }
+    }
+  } else {
+    for (uint32_t i = threadIdx.x; i < nrow * g.d_k; i += blockDim.x) {
+      const uint32_t r = i / g.d_k, c = i % g.d_k;
+      ct[r * pitch + c] = cb[i];
+    }
   }
   __syncthreads();
 
@@ -79,56 +105,67 @@ __device__ __forceinline__ uint64_t order_key(double d) {
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
-__global__ void __launch_bounds__(kSelectThreads) select_kernel(SelectArgs a, uint32_t N2) {
+// One CTA per (stream, selection head): bitonic sort of (key, id) descending
+// in shared memory.  Compare-exchange passes whose stride is < 64 stay inside
+// one warp's 64-element window, so they are ordered by __syncwarp; only the
+// passes that cross windows need the CTA barrier (10 of 55 at n = 1024).
+__global__ void __launch_bounds__(kSelectThreads) select_sort_kernel(SelectArgs a, uint32_t N2) {
   const Geometry& g = a.g;
-  const uint32_t s = blockIdx.x;
+  const uint32_t h = blockIdx.x, s = blockIdx.y;
   extern __shared__ __align__(16) uint8_t smem[];
   uint64_t* key = reinterpret_cast<uint64_t*>(smem);
   uint32_t* id = reinterpret_cast<uint32_t*>(key + N2);
+
+  const double* sc = a.scores + ((uint64_t)s * g.Gs + h) * g.n_cap;
+  for (uint32_t i = threadIdx.x; i < N2; i += blockDim.x) {
+    key[i] = i < a.n ? order_key(sc[i]) : 0ull;
+    id[i] = i < a.n ? i : 0u;
+  }
+  __syncthreads();
+  const uint32_t half = N2 / 2;
+  for (uint32_t size = 2; size <= N2; size <<= 1) {
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      for (uint32_t i = threadIdx.x; i < half; i += blockDim.x) {
+        const uint32_t lo = 2 * i - (i & (stride - 1));
+        const uint32_t hi = lo + stride;
+        const bool desc = (lo & size) == 0;
+        const uint64_t kl = key[lo], kh = key[hi];
+        const uint32_t il = id[lo], ih = id[hi];
+        const bool less = (kl < kh) || (kl == kh && il < ih);  // (lo) < (hi)
+        if (less == desc) {
+          key[lo] = kh; key[hi] = kl;
+          id[lo] = ih; id[hi] = il;
+        }
+      }
+      // a pass with stride <= 32 touches only its warp's 64-element windows;
+      // two such passes in a row need only warp-level ordering
+      const bool last = stride == 1 && size == N2;
+      const uint32_t next = stride > 1 ? stride >> 1 : size;  // the next pass's stride
+      if (!last && stride <= 32 && next <= 32)
+        __syncwarp();
+      else
+        __syncthreads();
+    }
+  }
+  uint32_t* out = a.sel + ((uint64_t)s * g.Gs + h) * g.n_cap;
+  uint32_t* mask = a.mask + (uint64_t)s * g.n_cap;
+  const uint32_t all_heads = (g.G >= 32) ? 0xffffffffu : ((1u << g.G) - 1u);
+  const uint32_t bit = (g.Gs == g.G) ? (1u << h) : all_heads;
+  for (uint32_t i = threadIdx.x; i < a.k; i += blockDim.x) {
+    out[i] = id[i];
+    atomicOr(&mask[id[i]], bit);
+  }
+}
+
+// Per stream: compact the union of the G selected sets in ascending block id
+// (records are then read in arena order; the merge is order-independent,
+// SPEC.md:287) and clear the head mask for the next step.
+__global__ void __launch_bounds__(kSelectThreads) select_union_kernel(SelectArgs a) {
+  const Geometry& g = a.g;
+  const uint32_t s = blockIdx.x;
   __shared__ uint32_t warp_tot[kSelectThreads / 32];
   __shared__ uint32_t base_sh;
-
   uint32_t* mask = a.mask + (uint64_t)s * g.n_cap;
-  for (uint32_t b = threadIdx.x; b < a.n; b += blockDim.x) mask[b] = 0;
-  __syncthreads();
-
-  const uint32_t all_heads = (g.G >= 32) ? 0xffffffffu : ((1u << g.G) - 1u);
-  for (uint32_t h = 0; h < g.Gs; ++h) {
-    const double* sc = a.scores + ((uint64_t)s * g.Gs + h) * g.n_cap;
-    for (uint32_t i = threadIdx.x; i < N2; i += blockDim.x) {
-      key[i] = i < a.n ? order_key(sc[i]) : 0ull;
-      id[i] = i < a.n ? i : 0u;
-    }
-    __syncthreads();
-    // bitonic sort, descending by (key, id)
-    for (uint32_t size = 2; size <= N2; size <<= 1) {
-      for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-        for (uint32_t i = threadIdx.x; i < N2 / 2; i += blockDim.x) {
-          const uint32_t lo = 2 * i - (i & (stride - 1));
-          const uint32_t hi = lo + stride;
-          const bool desc = (lo & size) == 0;
-          const uint64_t kl = key[lo], kh = key[hi];
-          const uint32_t il = id[lo], ih = id[hi];
-          const bool less = (kl < kh) || (kl == kh && il < ih);  // (lo) < (hi)
-          if (less == desc) {
-            key[lo] = kh; key[hi] = kl;
-            id[lo] = ih; id[hi] = il;
-          }
-        }
-        __syncthreads();
-      }
-    }
-    uint32_t* out = a.sel + ((uint64_t)s * g.Gs + h) * g.n_cap;
-    const uint32_t bit = (g.Gs == g.G) ? (1u << h) : all_heads;
-    for (uint32_t i = threadIdx.x; i < a.k; i += blockDim.x) {
-      out[i] = id[i];
-      atomicOr(&mask[id[i]], bit);
-    }
-    __syncthreads();
-  }
-
-  // compact the union in ascending block id (records are then read in
-  // arena order; the merge is order-independent)
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t nwarps = blockDim.x >> 5;
   if (threadIdx.x == 0) base_sh = 0;
@@ -136,6 +173,7 @@ __global__ void __launch_bounds__(kSelectThreads) select_kernel(SelectArgs a, ui
   for (uint32_t base = 0; base < a.n; base += blockDim.x) {
     const uint32_t b = base + threadIdx.x;
     const uint32_t m = b < a.n ? mask[b] : 0u;
+    if (b < a.n) mask[b] = 0u;
     const uint32_t ballot = __ballot_sync(0xffffffffu, m != 0u);
     if (lane == 0) warp_tot[warp] = __popc(ballot);
     __syncthreads();
@@ -162,16 +200,21 @@ __global__ void __launch_bounds__(kSelectThreads) select_kernel(SelectArgs a, ui
 
 uint32_t select_max_blocks() { return kSelectMaxN; }
 
+// The head mask (a.mask) must be all-zero on entry; select_union_kernel
+// leaves it zeroed again.
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
   if (a.n == 0) return cudaSuccess;
   uint32_t N2 = 2;
   while (N2 < a.n) N2 <<= 1;
   const size_t smem = (size_t)N2 * 12;
-  cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(select_sort_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const uint32_t threads = N2 / 2 < kSelectThreads ? (N2 / 2 < 64 ? 64 : N2 / 2) : kSelectThreads;
-  select_kernel<<<a.g.S, threads, smem, st>>>(a, N2);
+  select_sort_kernel<<<dim3(a.g.Gs, a.g.S), threads, smem, st>>>(a, N2);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  select_union_kernel<<<a.g.S, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -242,7 +242,7 @@ def test_engine_hot_shape_small(gpu):
     run_parity(gpu, S=4, G=4, d=128, B=128, l_fast=1024, ctx=6000, steps=4, check_blocks=True)
 
 
-@pytest.mark.parametrize("G,mode,literal", [(4, 0, False), (4, 1, False), (1, 0, False),
+@pytest.mark.parametrize("G,mode,literal", [(4, 0, False), (4, 1, False), (1, 0, False), (2, 0, False),
                                             (8, 0, False), (4, 0, True)])
 def test_engine_hbm_resident_slow_tier(gpu, G, mode, literal):
     # slow tier in HBM: the tensor-core slow kernel (TMA tensor maps, mma.sync

@@ -37,6 +37,8 @@ def main():
     gb = r.union_blocks * st["record_bytes"] / 1e9
     print(f"S={S} G={G} ctx={ctx} union={r.union_blocks} step {step:.3f} ms slow {slow:.3f} ms "
           f"({gb / slow * 1e3:.0f} GB/s of records) fast {fast:.3f} ms", flush=True)
+    print("   per-kernel ms:", {k[3:]: round(v / max(1, kt["n" + k[2:]]), 4)
+                               for k, v in kt.items() if k.startswith("ms_")}, flush=True)
     eng.close()
 
 
