@@ -206,8 +206,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
     // ---- tile softmax statistics, one warp per head ----
     for (uint32_t h = cw; h < g.G; h += kSlowConsumerWarps) {
       float* row = scb + h * kTT;
-      float bm = fmaxf(row[lane], row[lane + 32]);
-      bm = warp_max(bm);
+      const float bm = warp_max_redux(fmaxf(row[lane], row[lane + 32]));
       const float m_old = mst[h];
       const float m_new = fmaxf(m_old, bm);
       const float p0 = exp2f(row[lane] - m_new), p1 = exp2f(row[lane + 32] - m_new);
@@ -454,6 +453,20 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
 #pragma unroll
   for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.f;
   uint32_t seen = 0;
+  // Swizzle-folded shared-memory offsets (loop-invariant):
+  //  K (128B swizzle): ldmatrix row address of matrix m = lane / 8 -- token
+  //  32cw + 16mt + 8(m&1) + (lane&7), 16-byte chunk 2jp + (m>>1); the XOR
+  //  term is (token & 7) = (lane & 7)
+  uint32_t koff[4];
+  {
+    const uint32_t m = lane >> 3, r = lane & 7;
+    const uint32_t row = 32 * cw + 8 * (m & 1) + r;
+#pragma unroll
+    for (int jp = 0; jp < 4; ++jp)
+      koff[jp] = row * 128 + ((((uint32_t)(2 * jp)) ^ (r & 6u)) | ((m >> 1) ^ (r & 1u))) * 16;
+  }
+  //  V (64B swizzle): tokens 16ks + 2qq + {0,1,8,9} all have ((t >> 1) & 3) = qq
+  const uint32_t voff = 2 * qq * 64 + ((c0 >> 1) ^ (qq << 4));
 
   for (uint32_t i = 0; i < nb; ++i) {
     const uint32_t st = i % ST;
@@ -466,8 +479,13 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
     const uint32_t hm = umask[i];
     seen |= hm;
 
-    // ---- (q * s) B fragments (hi/lo) and beta = q . z, once per record ----
-    for (uint32_t e = ct; e < G * 32; e += nthreads_c) {  // warp-uniform: one head per warp
+    // ---- (q * s) B fragments (hi/lo) and this lane's share of beta = q . z
+    // for heads cw and cw + 4 (reduced after the QK MMAs are issued) ----
+    float bpart[2] = {0.f, 0.f};
+#pragma unroll
+    for (int rep = 0; rep < 2; ++rep) {
+      const uint32_t e = ct + rep * nthreads_c;  // warp-uniform: one head per warp
+      if (e >= G * 32) break;
       const uint32_t h = e >> 5, j = (e >> 2) & 7u, q4 = e & 3u;
       const uint32_t c = 16 * j + 4 * q4;
       const float4 qv = *reinterpret_cast<const float4*>(qsm + h * 128 + c);
@@ -477,9 +495,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
       split2(qv.x * sz0.x, qv.y * sz0.z, h01, l01);
       split2(qv.z * sz1.x, qv.w * sz1.z, h23, l23);
       qsf[(j * 8 + h) * 4 + q4] = make_uint4(h01, h23, l01, l23);
-      float beta = qv.x * sz0.y + qv.y * sz0.w + qv.z * sz1.y + qv.w * sz1.w;
-      beta = warp_sum(beta);
-      if (lane == 0) bst[h] = beta;
+      bpart[rep] = qv.x * sz0.y + qv.y * sz0.w + qv.z * sz1.y + qv.w * sz1.w;
     }
     named_bar(1, nthreads_c);
 
@@ -498,9 +514,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
           // matrices: (tok 0-7, chunk 2jp), (tok 8-15, 2jp), (tok 0-7, 2jp+1), (tok 8-15, 2jp+1)
-          const int m = lane >> 3;
-          const int tok = 32 * cw + 16 * mt + 8 * (m & 1) + (lane & 7);
-          const uint32_t addr = kb + swz128(tok * 128 + (2 * jp + (m >> 1)) * 16);
+          const uint32_t addr = kb + koff[jp] + mt * 16 * 128;
           uint32_t r0, r1, r2, r3, a0, a1, a2, a3;
           ldsm_x4(addr, r0, r1, r2, r3);
           codes_to_h2(r0, a0, a2);
@@ -514,12 +528,20 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
         }
       }
 #pragma unroll
+      for (int rep = 0; rep < 2; ++rep) {
+        const uint32_t h = cw + rep * kSlowConsumerWarps;
+        if (h < G) {  // warp-uniform
+          const float beta = warp_sum(bpart[rep]);
+          if (lane == 0) bst[h] = beta;
+        }
+      }
+#pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const uint32_t h = 2 * qq + (e & 1);
           const uint32_t t = 32 * cw + 16 * mt + gq + 8 * (e >> 1);
-          if (h < G) sc[h * kScPitch + t] = c[mt][0][e] + c[mt][1][e] + bst[h];
+          if (h < G) sc[h * kScPitch + t] = c[mt][0][e] + c[mt][1][e];
         }
     }
     named_bar(1, nthreads_c);
@@ -538,9 +560,11 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
         continue;
       }
       const float* row = sc + h * kScPitch + 16 * ks + 2 * q4;
-      const float2 v01 = *reinterpret_cast<const float2*>(row);
-      const float2 v89 = *reinterpret_cast<const float2*>(row + 8);
-      const float bm = warp_max(fmaxf(fmaxf(v01.x, v01.y), fmaxf(v89.x, v89.y)));
+      const float beta = bst[h];
+      float2 v01 = *reinterpret_cast<const float2*>(row);
+      float2 v89 = *reinterpret_cast<const float2*>(row + 8);
+      v01.x += beta; v01.y += beta; v89.x += beta; v89.y += beta;
+      const float bm = warp_max_redux(fmaxf(fmaxf(v01.x, v01.y), fmaxf(v89.x, v89.y)));
       const float m_old = mst[h];
       const float m_new = a.literal ? bm : fmaxf(m_old, bm);
       float p0 = exp2f(v01.x - m_new), p1 = exp2f(v01.y - m_new);
@@ -579,14 +603,13 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int e = 0; e < 4; ++e) cf[mt][0][e] = cf[mt][1][e] = 0.f;
-      const uint32_t boff = c0 >> 1;  // byte of channel c0 in a token row
+      const uint8_t* vt = vn + voff;
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
-        const uint32_t t0 = 16 * ks + 2 * qq;
-        const uint32_t u0 = *reinterpret_cast<const uint16_t*>(vn + swz64(t0 * 64 + boff));
-        const uint32_t u1 = *reinterpret_cast<const uint16_t*>(vn + swz64((t0 + 1) * 64 + boff));
-        const uint32_t u8 = *reinterpret_cast<const uint16_t*>(vn + swz64((t0 + 8) * 64 + boff));
-        const uint32_t u9 = *reinterpret_cast<const uint16_t*>(vn + swz64((t0 + 9) * 64 + boff));
+        const uint32_t u0 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024);
+        const uint32_t u1 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 64);
+        const uint32_t u8 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 512);
+        const uint32_t u9 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 576);
         uint32_t x0, x1, x2, x3, y0, y1, y2, y3;
         nibbles_to_h2(__byte_perm(u0, u1, 0x5410u), x0, x1, x2, x3);
         nibbles_to_h2(__byte_perm(u8, u9, 0x5410u), y0, y1, y2, y3);

@@ -79,6 +79,14 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
+// warp-wide fp32 max in one instruction (CREDUX.MAX.F32, sm_100a; NaN-ignoring
+// like fmaxf)
+__device__ __forceinline__ float warp_max_redux(float v) {
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+
 // ---------------------------------------------------------------------------
 // mbarrier / bulk-copy PTX (sm_90+; used on sm_100a)
 // ---------------------------------------------------------------------------

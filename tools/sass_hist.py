@@ -36,3 +36,21 @@ for r in data:
         except ValueError:
             pass
 print("stalls:", ", ".join(f"{k[6:]} {100 * v / tot_s:.1f}%" for k, v in st.most_common(10)))
+
+# per CUDA source line (needs -lineinfo): top lines by stall samples
+out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "source", "--csv", "--print-source",
+                      "cuda,sass"], capture_output=True, text=True).stdout
+lines, fname = [], ""
+for r in csv.reader(io.StringIO(out)):
+    if r and r[0] == "File Path":
+        fname = r[1].rsplit("/", 1)[-1]
+    elif r and r[0] and r[0] not in ("Line No", "Function Name", "File Path") and len(r) > 7:
+        try:
+            lines.append((int(r[4] or 0), int(r[7] or 0), fname, r[0], r[1].strip()[:70]))
+        except ValueError:
+            pass
+tot_l = sum(x[0] for x in lines) or 1
+tot_li = sum(x[1] for x in lines) or 1
+print("top source lines (stall-sample %, instruction %):")
+for smp, ins, f, ln, text in sorted(lines, reverse=True)[:int(sys.argv[2]) if len(sys.argv) > 2 else 25]:
+    print(f"  {100 * smp / tot_l:5.1f}% {100 * ins / tot_li:5.1f}%  {f}:{ln}  {text}")
