@@ -21,6 +21,8 @@
  *   ttkv_gpu_read_block        TierStore::slow_blocks()[i] (tier_store.hpp:58)
  *   ttkv_gpu_serialize_block   serialize_block (quantizer.cpp:248-274)
  *   ttkv_gpu_dump_slow_tier    dump_slow_tier (quantizer.cpp:325-342)
+ *   ttkv_gpu_restore_slow_tier load_slow_tier + deserialize_block
+ *                              (quantizer.cpp:276-365) into a fresh handle
  *   ttkv_gpu_read_fast         TierStore::fast_tokens() (tier_store.hpp:57)
  *   ttkv_gpu_locate            TierStore::locate (tier_store.cpp:100-105)
  *   ttkv_gpu_quantize_block    quantize_block (quantizer.cpp:126-155)
@@ -214,6 +216,12 @@ int ttkv_gpu_read_block(struct ttkv_gpu* h, uint32_t stream, uint64_t block_id,
 int ttkv_gpu_serialize_block(struct ttkv_gpu* h, uint32_t stream, uint64_t block_id,
                              uint8_t* out, uint64_t cap, uint64_t* len);
 int ttkv_gpu_dump_slow_tier(struct ttkv_gpu* h, uint32_t stream, const char* path);
+/* Checkpoint/resume: rebuild a fresh handle's slow tier from one TTKVTIER
+ * file per stream (paths[s], n_paths == n_streams; load_slow_tier +
+ * deserialize_block, quantizer.cpp:276-365, with the same integrity checks).
+ * Blocks must be the contiguous sequence 0..n-1 of this config's geometry.
+ * Afterwards appended == n*B; resume the fast tier with ttkv_gpu_append. */
+int ttkv_gpu_restore_slow_tier(struct ttkv_gpu* h, const char* const* paths, uint32_t n_paths);
 /* Fast tier as float32 rows, oldest first. */
 int ttkv_gpu_read_fast(struct ttkv_gpu* h, uint32_t stream, float* keys, float* values,
                        uint64_t cap_tokens, uint64_t* n_tokens, uint64_t* first_position);

@@ -68,7 +68,7 @@ EXPORTS = [
     "ttkv_gpu_synchronize", "ttkv_gpu_prefill", "ttkv_gpu_prefill_synthetic",
     "ttkv_gpu_decode_step", "ttkv_gpu_decode_step_device", "ttkv_gpu_read_step_counters",
     "ttkv_gpu_state", "ttkv_gpu_read_fetched", "ttkv_gpu_read_block", "ttkv_gpu_serialize_block",
-    "ttkv_gpu_dump_slow_tier", "ttkv_gpu_read_fast", "ttkv_gpu_locate", "ttkv_gpu_set_timing",
+    "ttkv_gpu_dump_slow_tier", "ttkv_gpu_restore_slow_tier", "ttkv_gpu_read_fast", "ttkv_gpu_locate", "ttkv_gpu_set_timing",
     "ttkv_gpu_kernel_times", "ttkv_gpu_quantize_block", "ttkv_gpu_append", "ttkv_gpu_evict",
     "ttkv_gpu_eviction_pending", "ttkv_gpu_dequantize_block", "ttkv_gpu_score_blocks",
     "ttkv_gpu_select_top_k", "ttkv_fast_capacity",
@@ -110,6 +110,7 @@ def lib():
         "ttkv_gpu_read_block": (i32, [vp, u32, u64, vp, vp, vp, vp, vp, P(u64)]),
         "ttkv_gpu_serialize_block": (i32, [vp, u32, u64, vp, u64, P(u64)]),
         "ttkv_gpu_dump_slow_tier": (i32, [vp, u32, C.c_char_p]),
+        "ttkv_gpu_restore_slow_tier": (i32, [vp, P(C.c_char_p), u32]),
         "ttkv_gpu_read_fast": (i32, [vp, u32, vp, vp, u64, P(u64), P(u64)]),
         "ttkv_gpu_locate": (i32, [vp, u64, P(i32), P(u64)]),
         "ttkv_gpu_set_timing": (i32, [vp, i32]),

@@ -1217,6 +1217,183 @@ int ttkv_gpu_dump_slow_tier(ttkv_gpu* h, uint32_t stream, const char* path) {
   return TTKV_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Restore (checkpoint/resume).  The reference can load a slow tier
+// (load_slow_tier / deserialize_block, quantizer.cpp:276-365) but has no
+// TierStore built from one (tier_store.hpp:42); a GPU handle is rebuilt from
+// one TTKVTIER file per stream: every record lands in the arena exactly as
+// evict_quantize would have written it (payloads, interleaved params), the
+// centroid in the resident HBM array.  The fast tier then resumes through
+// ttkv_gpu_append.  Integrity checks and messages are the reference's.
+// ---------------------------------------------------------------------------
+namespace {
+struct ByteReader {
+  const uint8_t* p;
+  size_t n, pos = 0;
+  bool ok = true;
+  bool need(size_t k) {
+    if (pos + k > n) ok = false;
+    return ok;
+  }
+  uint64_t u(int k) {
+    if (!need((size_t)k)) return 0;
+    uint64_t v = 0;
+    for (int i = 0; i < k; ++i) v |= (uint64_t)p[pos + i] << (8 * i);
+    pos += (size_t)k;
+    return v;
+  }
+  float f32() {
+    const uint32_t v = (uint32_t)u(4);
+    float f;
+    std::memcpy(&f, &v, 4);
+    return f;
+  }
+  const uint8_t* blob(size_t k) {
+    if (!need(k)) return nullptr;
+    const uint8_t* b = p + pos;
+    pos += k;
+    return b;
+  }
+};
+
+uint16_t float_to_half_bits(float x) {  // round-to-nearest-even (values come from an fp16 ring)
+  uint32_t f;
+  std::memcpy(&f, &x, 4);
+  const uint32_t sign = (f >> 16) & 0x8000u;
+  int32_t exp = (int32_t)((f >> 23) & 0xff) - 127 + 15;
+  uint32_t man = f & 0x7fffffu;
+  if (((f >> 23) & 0xff) == 0xff) return (uint16_t)(sign | 0x7c00u | (man ? 0x200u : 0u));
+  if (exp >= 31) return (uint16_t)(sign | 0x7c00u);
+  if (exp <= 0) {
+    if (exp < -10) return (uint16_t)sign;
+    man |= 0x800000u;
+    const uint32_t shift = (uint32_t)(14 - exp);
+    uint32_t h = man >> shift;
+    const uint32_t rem = man & ((1u << shift) - 1u), half = 1u << (shift - 1);
+    if (rem > half || (rem == half && (h & 1u))) ++h;
+    return (uint16_t)(sign | h);
+  }
+  uint32_t h = ((uint32_t)exp << 10) | (man >> 13);
+  const uint32_t rem = man & 0x1fffu;
+  if (rem > 0x1000u || (rem == 0x1000u && (h & 1u))) ++h;
+  return (uint16_t)(sign | h);
+}
+}  // namespace
+
+int ttkv_gpu_restore_slow_tier(ttkv_gpu* h, const char* const* paths, uint32_t n_paths) {
+  if (!h || !paths) return set_err(h, TTKV_EINVAL, "null argument");
+  const Geometry& g = h->g;
+  if (n_paths != g.S) return set_err(h, TTKV_ESHAPE, "restore: one slow-tier file per stream");
+  if (h->appended != 0)
+    return set_err(h, TTKV_ESEQUENCE, "restore: the handle already holds tokens");
+  CU(h, cudaSetDevice(h->dev));
+  const uint64_t kbytes = packed_bytes_u((uint64_t)g.B * g.d_k, g.kb);
+  const uint64_t vbytes = packed_bytes_u((uint64_t)g.B * g.d_v, g.vb);
+  const uint64_t pbytes = g.rec.used - g.rec.kp_off;
+  uint64_t n_blocks = 0;
+  std::vector<uint8_t> rec(g.rec.stride), all;
+  std::vector<float> cent(g.d_k);
+  for (uint32_t s = 0; s < g.S; ++s) {
+    FILE* f = std::fopen(paths[s], "rb");
+    if (!f) return set_err(h, TTKV_EIO, std::string("cannot open ") + paths[s]);
+    std::fseek(f, 0, SEEK_END);
+    const long sz = std::ftell(f);
+    std::fseek(f, 0, SEEK_SET);
+    all.resize(sz > 0 ? (size_t)sz : 0);
+    const bool rd = all.empty() || std::fread(all.data(), 1, all.size(), f) == all.size();
+    std::fclose(f);
+    if (!rd) return set_err(h, TTKV_EIO, std::string("read failed: ") + paths[s]);
+    ByteReader r{all.data(), all.size()};
+    const uint8_t* magic = r.blob(8);
+    if (!magic || std::memcmp(magic, "TTKVTIER", 8) != 0)
+      return set_err(h, TTKV_EINTEGRITY, "slow-tier file: bad magic");
+    if (r.u(2) != 1) return set_err(h, TTKV_EINTEGRITY, "slow-tier file: unsupported version");
+    const uint64_t count = r.u(8);
+    if (!r.ok) return set_err(h, TTKV_EINTEGRITY, "deserialize: truncated payload");
+    if (s == 0) {
+      n_blocks = count;
+      int rc = ensure_blocks(h, std::max<uint64_t>(n_blocks, 1));
+      if (rc) return rc;
+    } else if (count != n_blocks) {
+      return set_err(h, TTKV_ESHAPE, "restore: streams hold different slow-tier lengths");
+    }
+    for (uint64_t b = 0; b < count; ++b) {
+      const uint64_t len = r.u(8);
+      const uint8_t* blk = r.blob(len);
+      if (!r.ok) return set_err(h, TTKV_EINTEGRITY, "deserialize: truncated payload");
+      ByteReader q{blk, len};
+      const uint8_t* bm = q.blob(4);
+      if (!bm || std::memcmp(bm, "TTKV", 4) != 0)
+        return set_err(h, TTKV_EINTEGRITY, "deserialize: bad magic");
+      if (q.u(2) != 1) return set_err(h, TTKV_EINTEGRITY, "deserialize: unsupported version");
+      const uint64_t block_id = q.u(8), first = q.u(8), last = q.u(8);
+      const uint32_t tokens = (uint32_t)q.u(4), dk = (uint32_t)q.u(4), dv = (uint32_t)q.u(4);
+      const uint32_t kb = (uint32_t)q.u(2), vb = (uint32_t)q.u(2);
+      auto valid_bits = [](uint32_t x) { return (x >= 2 && x <= 8) || x == 16; };
+      if (!q.ok) return set_err(h, TTKV_EINTEGRITY, "deserialize: truncated payload");
+      if (!valid_bits(kb) || !valid_bits(vb))
+        return set_err(h, TTKV_EINTEGRITY, "deserialize: bad bit widths");
+      if (tokens != g.B || dk != g.d_k || dv != g.d_v || kb != g.kb || vb != g.vb)
+        return set_err(h, TTKV_ECONFIG, "restore: block geometry does not match the tier config");
+      if (block_id != b || first != b * g.B || last != first + g.B - 1)
+        return set_err(h, TTKV_EINTEGRITY, "restore: blocks are not the contiguous sequence 0..n-1");
+      std::fill(rec.begin(), rec.end(), 0);
+      float* kp = reinterpret_cast<float*>(rec.data() + g.rec.kp_off);
+      float* vp = reinterpret_cast<float*>(rec.data() + g.rec.vp_off);
+      for (uint32_t c = 0; c < (kb == 16 ? 0u : dk); ++c) { kp[2 * c] = q.f32(); kp[2 * c + 1] = q.f32(); }
+      for (uint32_t c = 0; c < (vb == 16 ? 0u : dv); ++c) { vp[2 * c] = q.f32(); vp[2 * c + 1] = q.f32(); }
+      for (uint32_t c = 0; c < dk; ++c) cent[c] = q.f32();
+      auto payload = [&](uint64_t want, uint32_t bits, uint32_t dim, uint8_t* dst,
+                         const char* what) -> int {
+        const uint64_t l = q.u(8);
+        if (!q.ok) return set_err(h, TTKV_EINTEGRITY, "deserialize: truncated payload");
+        if (l != want)
+          return set_err(h, TTKV_EINTEGRITY, std::string("deserialize: ") + what +
+                                                 " payload length mismatch");
+        const uint8_t* src = q.blob(l);
+        if (!src) return set_err(h, TTKV_EINTEGRITY, "deserialize: truncated payload");
+        if (bits != 16) {
+          std::memcpy(dst, src, l);
+        } else {  // lossless payload is float32 in the file, the ring type in the record
+          const uint64_t cnt = (uint64_t)g.B * dim;
+          for (uint64_t i = 0; i < cnt; ++i) {
+            float x;
+            std::memcpy(&x, src + 4 * i, 4);
+            if (g.elem == 4) {
+              std::memcpy(dst + 4 * i, &x, 4);
+            } else {
+              const uint16_t hb = float_to_half_bits(x);
+              std::memcpy(dst + 2 * i, &hb, 2);
+            }
+          }
+        }
+        return TTKV_OK;
+      };
+      const uint64_t kwant = kb == 16 ? (uint64_t)g.B * dk * 4 : kbytes;
+      const uint64_t vwant = vb == 16 ? (uint64_t)g.B * dv * 4 : vbytes;
+      int rc = payload(kwant, kb, dk, rec.data(), "key");
+      if (rc) return rc;
+      rc = payload(vwant, vb, dv, rec.data() + g.rec.v_off, "value");
+      if (rc) return rc;
+      if (q.pos != q.n) return set_err(h, TTKV_EINTEGRITY, "deserialize: trailing bytes");
+      const uint64_t idx = (uint64_t)s * g.n_cap + b;
+      if (h->arena_host) std::memcpy(h->arena_host + idx * g.rec.stride, rec.data(), g.rec.stride);
+      else CU(h, cudaMemcpy(h->arena_dev + idx * g.rec.stride, rec.data(), g.rec.stride,
+                            cudaMemcpyHostToDevice));
+      if (pbytes)
+        CU(h, cudaMemcpy(h->params + idx * pbytes, rec.data() + g.rec.kp_off, pbytes,
+                         cudaMemcpyHostToDevice));
+      CU(h, cudaMemcpy(h->cent + idx * g.d_k, cent.data(), g.d_k * sizeof(float),
+                       cudaMemcpyHostToDevice));
+    }
+    if (r.pos != r.n) return set_err(h, TTKV_EINTEGRITY, "slow-tier file: trailing bytes");
+  }
+  h->n_slow = n_blocks;
+  h->appended = n_blocks * g.B;
+  h->fast_front = n_blocks * g.B;
+  return TTKV_OK;
+}
+
 int ttkv_gpu_read_fast(ttkv_gpu* h, uint32_t stream, float* keys, float* values,
                        uint64_t cap, uint64_t* n_tokens, uint64_t* first_position) {
   if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");

@@ -12,6 +12,7 @@ Everything runs in libttkv_gpu.so; there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import List, Optional
 
@@ -319,6 +320,45 @@ class MultiStreamEngine:
 
     def dump_slow_tier(self, stream: int, path: str):
         _check(self._lib.ttkv_gpu_dump_slow_tier(self._h, stream, str(path).encode()), self._h)
+
+    def restore_slow_tier(self, paths):
+        """Rebuild this (fresh) handle's slow tier from one TTKVTIER file per
+        stream (load_slow_tier, quantizer.cpp:344-365)."""
+        arr = (C.c_char_p * len(paths))(*[str(p).encode() for p in paths])
+        _check(self._lib.ttkv_gpu_restore_slow_tier(self._h, arr, len(paths)), self._h)
+
+    def append(self, keys, values):
+        """append_token for n tokens of every stream: keys [S, n, d_k]."""
+        k, dt = _kv(keys)
+        v, _ = _kv(values)
+        if v.dtype != k.dtype:
+            v = v.astype(k.dtype)
+        if k.ndim == 2:
+            k, v = k[:, None], v[:, None]
+        _check(self._lib.ttkv_gpu_append(self._h, _ptr(k), _ptr(v), k.shape[1], dt), self._h)
+
+    def checkpoint(self, directory):
+        """Checkpoint every stream: its slow tier in the reference's TTKVTIER
+        format (dump_slow_tier, byte-identical) plus the fast-tier rows."""
+        os.makedirs(directory, exist_ok=True)
+        ks, vs, first = [], [], 0
+        for s in range(self.S):
+            self.dump_slow_tier(s, os.path.join(directory, f"stream_{s:05d}.ttkvtier"))
+            k, v, first = self.read_fast(s)
+            ks.append(k)
+            vs.append(v)
+        np.savez(os.path.join(directory, "fast_tier.npz"), keys=np.stack(ks),
+                 values=np.stack(vs), first_position=first)
+
+    def restore(self, directory):
+        """Resume a fresh handle from checkpoint(): slow tier, then fast tier."""
+        self.restore_slow_tier([os.path.join(directory, f"stream_{s:05d}.ttkvtier")
+                                for s in range(self.S)])
+        ft = np.load(os.path.join(directory, "fast_tier.npz"))
+        if int(ft["first_position"]) != self.state()["appended"]:
+            raise IntegrityError("restore: fast tier does not continue the slow tier")
+        if ft["keys"].shape[1]:
+            self.append(ft["keys"], ft["values"])
 
     def read_fast(self, stream: int):
         n, first = C.c_uint64(), C.c_uint64()
