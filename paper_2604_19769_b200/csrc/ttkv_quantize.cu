@@ -51,20 +51,37 @@ __global__ void evict_quantize_kernel(EvictArgs a) {
     const uint32_t bits = is_k ? g.kb : g.vb;
     const T* ring = is_k ? ring_k : ring_v;
     const Tin* in = is_k ? in_k : in_v;
+    // A block never straddles the ring wrap (C and every eviction start are
+    // multiples of B), so its ring rows are slot0 .. slot0 + B - 1; rows at
+    // positions >= split_pos come from the staging input instead.
+    const T* ring_col = ring + (pos0 % g.C) * dim + ch;
+    const uint32_t n_ring = a.split_pos > pos0
+                                ? (uint32_t)(a.split_pos - pos0 < (uint64_t)g.B ? a.split_pos - pos0 : (uint64_t)g.B)
+                                : 0u;
+    const Tin* in_col = in + (pos0 + n_ring - a.split_pos) * dim + ch;  // row n_ring
     auto load = [&](uint32_t r) -> float {
-      const uint64_t p = pos0 + r;
-      if (p < a.split_pos) return to_f(ring[(p % g.C) * dim + ch]);
-      return through<T, Tin>(in[(p - a.split_pos) * dim + ch]);
+      if (r < n_ring) return to_f(ring_col[(size_t)r * dim]);
+      return through<T, Tin>(in_col[(size_t)(r - n_ring) * dim]);
     };
 
+    // rows are read kU at a time so kU loads are in flight per thread (the
+    // per-row dependence is only through lo/hi/sum, in row order as the
+    // reference walks them)
+    constexpr uint32_t kU = 8;
     float lo = __int_as_float(0x7f800000);   // +inf
     float hi = __int_as_float(0xff800000);   // -inf
     double sum = 0.0;
-    for (uint32_t r = 0; r < g.B; ++r) {
-      const float x = load(r);
-      lo = (x < lo) ? x : lo;   // std::min(lo, x)
-      hi = (hi < x) ? x : hi;   // std::max(hi, x)
-      if (is_k) sum = __dadd_rn(sum, (double)x);
+    for (uint32_t r0 = 0; r0 < g.B; r0 += kU) {
+      float x[kU];
+#pragma unroll
+      for (uint32_t u = 0; u < kU; ++u) x[u] = r0 + u < g.B ? load(r0 + u) : 0.0f;
+#pragma unroll
+      for (uint32_t u = 0; u < kU; ++u) {
+        if (r0 + u >= g.B) break;
+        lo = (x[u] < lo) ? x[u] : lo;   // std::min(lo, x)
+        hi = (hi < x[u]) ? x[u] : hi;   // std::max(hi, x)
+        if (is_k) sum = __dadd_rn(sum, (double)x[u]);
+      }
     }
     if (is_k)
       a.cent[((uint64_t)s * g.n_cap + blk) * g.d_k + ch] =
@@ -84,10 +101,26 @@ __global__ void evict_quantize_kernel(EvictArgs a) {
         const double levels = (double)((1u << bits) - 1u);
         scale = __double2float_rn(__ddiv_rn(__dsub_rn((double)hi, (double)lo), levels));
         const double dlo = (double)lo, dscale = (double)scale;
-        for (uint32_t r = 0; r < g.B; ++r) {
-          double q = round(__ddiv_rn(__dsub_rn((double)load(r), dlo), dscale));
-          q = q < 0.0 ? 0.0 : (levels < q ? levels : q);
-          cc[r * dkv] = (uint8_t)(uint32_t)q;
+        // code = round(a / scale) with a = x - lo.  The product with the
+        // rounded reciprocal is within a few ulp of the correctly rounded
+        // quotient, so the two round to the same integer unless the quotient
+        // sits within 2^-36 of a half-integer; those rare elements take the
+        // exact __ddiv_rn the reference uses (quantizer.cpp:80-84).
+        const double rcp = __drcp_rn(dscale);
+        for (uint32_t r0 = 0; r0 < g.B; r0 += kU) {
+          float x[kU];
+#pragma unroll
+          for (uint32_t u = 0; u < kU; ++u) x[u] = r0 + u < g.B ? load(r0 + u) : 0.0f;
+#pragma unroll
+          for (uint32_t u = 0; u < kU; ++u) {
+            if (r0 + u >= g.B) break;
+            const double a = __dsub_rn((double)x[u], dlo);
+            const double t = __dmul_rn(a, rcp);
+            const double fr = t - floor(t);
+            double q = fabs(fr - 0.5) > 0x1p-36 ? round(t) : round(__ddiv_rn(a, dscale));
+            q = q < 0.0 ? 0.0 : (levels < q ? levels : q);
+            cc[(r0 + u) * dkv] = (uint8_t)(uint32_t)q;
+          }
         }
       }
       float* par = reinterpret_cast<float*>(rec + (is_k ? g.rec.kp_off : g.rec.vp_off)) + 2 * ch;

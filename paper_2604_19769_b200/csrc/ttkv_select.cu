@@ -226,6 +226,40 @@ cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
 template <typename T, typename Tin>
 __global__ void append_kernel(Geometry g, T* ring_k, T* ring_v, const Tin* kn, const Tin* vn,
                               uint64_t slot0, uint64_t in_stride_tok, uint64_t n_tok) {
+  // one thread per 8-element group of a token row; K groups then V groups
+  const uint32_t gk = g.d_k / 8, gv = g.d_v / 8, gr = gk + gv;
+  const uint64_t total = (uint64_t)g.S * n_tok * gr;
+  const uint32_t slot_base = (uint32_t)(slot0 % g.C);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c8 = (uint32_t)(i % gr);
+    const uint64_t st = i / gr;
+    const uint32_t t = (uint32_t)(st % n_tok);
+    const uint32_t s = (uint32_t)(st / n_tok);
+    uint32_t slot = slot_base + t;
+    slot = slot >= g.C ? slot - (uint32_t)g.C * (slot / (uint32_t)g.C) : slot;
+    const bool is_k = c8 < gk;
+    const uint32_t dim = is_k ? g.d_k : g.d_v, c = 8 * (is_k ? c8 : c8 - gk);
+    const Tin* src = (is_k ? kn : vn) + ((uint64_t)s * in_stride_tok + t) * dim + c;
+    T* dst = (is_k ? ring_k : ring_v) + ((uint64_t)s * g.C + slot) * dim + c;
+    Tin x[8];
+#pragma unroll
+    for (int e = 0; e < 8; e += 16 / (int)sizeof(Tin))
+      *reinterpret_cast<uint4*>(x + e) = *reinterpret_cast<const uint4*>(src + e);
+    T o[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = from_f<T>(to_f(x[e]));
+#pragma unroll
+    for (int e = 0; e < 8; e += 16 / (int)sizeof(T) > 8 ? 8 : 16 / (int)sizeof(T))
+      *reinterpret_cast<uint4*>(dst + e) = *reinterpret_cast<const uint4*>(o + e);
+  }
+}
+
+// generic shape (a dimension not a multiple of 8): one thread per element
+template <typename T, typename Tin>
+__global__ void append_kernel_scalar(Geometry g, T* ring_k, T* ring_v, const Tin* kn,
+                                     const Tin* vn, uint64_t slot0, uint64_t in_stride_tok,
+                                     uint64_t n_tok) {
   const uint32_t dkv = g.d_k + g.d_v;
   const uint64_t total = (uint64_t)g.S * n_tok * dkv;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
@@ -242,31 +276,39 @@ __global__ void append_kernel(Geometry g, T* ring_k, T* ring_v, const Tin* kn, c
   }
 }
 
+template <typename T, typename Tin>
+static void launch_append_t(const Geometry& g, void* ring_k, void* ring_v, const void* k_new,
+                            const void* v_new, uint64_t slot, uint64_t in_stride_tok,
+                            uint64_t n_tok, cudaStream_t st) {
+  const bool vec = g.d_k % 8 == 0 && g.d_v % 8 == 0 &&
+                   ((reinterpret_cast<uintptr_t>(k_new) | reinterpret_cast<uintptr_t>(v_new)) & 15) == 0;
+  const uint64_t total = (uint64_t)g.S * n_tok * (vec ? (g.d_k + g.d_v) / 8 : g.d_k + g.d_v);
+  uint64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (vec)
+    append_kernel<T, Tin><<<(unsigned)blocks, 256, 0, st>>>(
+        g, (T*)ring_k, (T*)ring_v, (const Tin*)k_new, (const Tin*)v_new, slot, in_stride_tok,
+        n_tok);
+  else
+    append_kernel_scalar<T, Tin><<<(unsigned)blocks, 256, 0, st>>>(
+        g, (T*)ring_k, (T*)ring_v, (const Tin*)k_new, (const Tin*)v_new, slot, in_stride_tok,
+        n_tok);
+}
+
 cudaError_t launch_append(const Geometry& g, void* ring_k, void* ring_v, const void* k_new,
                           const void* v_new, int in_dtype, uint64_t slot, uint64_t in_stride_tok,
                           uint64_t n_tok, cudaStream_t st) {
   if (n_tok == 0) return cudaSuccess;
-  const uint64_t total = (uint64_t)g.S * n_tok * (g.d_k + g.d_v);
-  uint64_t blocks = (total + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
   if (g.elem == 2) {
     if (in_dtype == kInF16)
-      append_kernel<__half, __half><<<(unsigned)blocks, 256, 0, st>>>(
-          g, (__half*)ring_k, (__half*)ring_v, (const __half*)k_new, (const __half*)v_new, slot,
-          in_stride_tok, n_tok);
+      launch_append_t<__half, __half>(g, ring_k, ring_v, k_new, v_new, slot, in_stride_tok, n_tok, st);
     else
-      append_kernel<__half, float><<<(unsigned)blocks, 256, 0, st>>>(
-          g, (__half*)ring_k, (__half*)ring_v, (const float*)k_new, (const float*)v_new, slot,
-          in_stride_tok, n_tok);
+      launch_append_t<__half, float>(g, ring_k, ring_v, k_new, v_new, slot, in_stride_tok, n_tok, st);
   } else {
     if (in_dtype == kInF16)
-      append_kernel<float, __half><<<(unsigned)blocks, 256, 0, st>>>(
-          g, (float*)ring_k, (float*)ring_v, (const __half*)k_new, (const __half*)v_new, slot,
-          in_stride_tok, n_tok);
+      launch_append_t<float, __half>(g, ring_k, ring_v, k_new, v_new, slot, in_stride_tok, n_tok, st);
     else
-      append_kernel<float, float><<<(unsigned)blocks, 256, 0, st>>>(
-          g, (float*)ring_k, (float*)ring_v, (const float*)k_new, (const float*)v_new, slot,
-          in_stride_tok, n_tok);
+      launch_append_t<float, float>(g, ring_k, ring_v, k_new, v_new, slot, in_stride_tok, n_tok, st);
   }
   return cudaGetLastError();
 }

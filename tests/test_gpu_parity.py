@@ -108,6 +108,31 @@ def test_quantize_matches_oracle_bitexact(gpu, bits):
         assert cen.tobytes() == ocen.tobytes()
 
 
+@pytest.mark.parametrize("bits", [(8, 4), (4, 2), (3, 3)])
+def test_quantize_exact_half_ties(gpu, bits):
+    # (x - lo) / scale landing exactly on k + 0.5: quantizer.cpp:82 rounds half
+    # away from zero; the GPU takes its exact-division path for these elements
+    kb, vb = bits
+    rng = np.random.default_rng(kb + 17 * vb)
+    rows = 128
+
+    def tied(levels, dim):
+        step = np.float32(rng.choice([1.0, 0.5, 0.25, 2.0]))
+        x = (rng.integers(0, 2 * levels + 1, (rows, dim)).astype(np.float32) * np.float32(0.5)
+             * step)
+        x[0, :] = 0.0
+        x[1, :] = np.float32(levels) * step  # lo = 0, hi = levels * step -> scale = step
+        return x
+
+    k, v = tied((1 << kb) - 1, 64), tied((1 << vb) - 1, 48)
+    pk, pv, kp, vp, cen = gpu_quantize(gpu, k, v, kb, vb)
+    okp, opk = O.quantize_tensor(k, kb)
+    ovp, opv = O.quantize_tensor(v, vb)
+    assert pk.tobytes() == opk.tobytes()
+    assert pv.tobytes() == opv.tobytes()
+    assert kp.tobytes() == okp.tobytes() and vp.tobytes() == ovp.tobytes()
+
+
 # ---------------------------------------------------------------------------
 # engine parity
 # ---------------------------------------------------------------------------
