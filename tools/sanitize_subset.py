@@ -13,6 +13,9 @@ cases = [
     dict(S=1, G=4, d=128, B=128, l_fast=256, ctx=700, steps=2, slow_tier=1),  # TC slow (HBM)
     dict(S=1, G=2, d=64, B=64, l_fast=128, ctx=400, steps=2, literal=True),
     dict(S=1, G=2, d=16, B=32, l_fast=128, ctx=300, steps=2, elem=4),         # fp64 accumulation
+    # > 64 slow blocks: the selection sort's cross-warp (stride >= 64) passes
+    dict(S=2, G=4, d=128, B=128, l_fast=256, ctx=20000, steps=2, slow_tier=1),
+    dict(S=2, G=8, d=32, B=32, l_fast=128, ctx=9000, steps=2),
 ]
 for c in cases:
     P.run_parity(T, **c)
