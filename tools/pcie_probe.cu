@@ -41,6 +41,44 @@ __global__ void ldg_records(const uint8_t* base, const unsigned* order, unsigned
   if (acc == 0x123456789ull) *sink = acc;
 }
 
+// LDG.128 with the L2::256B sector-promotion hint (larger sysmem requests?)
+__global__ void ldg256_records(const uint8_t* base, const unsigned* order, unsigned n,
+                               unsigned long long* sink) {
+  unsigned long long acc = 0;
+  for (unsigned r = blockIdx.x; r < n; r += gridDim.x) {
+    const uint4* p = reinterpret_cast<const uint4*>(base + (size_t)order[r] * kRec);
+    for (unsigned j = threadIdx.x; j < kRec / 16; j += blockDim.x) {
+      uint4 v;
+      asm volatile("ld.global.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                   : "l"(p + j));
+      acc += v.x ^ v.y ^ v.z ^ v.w;
+    }
+  }
+  if (acc == 0x123456789ull) *sink = acc;
+}
+
+// bulk L2 prefetch of the next record (TMA unit), then LDG.128 of this one
+__global__ void prefetch_records(const uint8_t* base, const unsigned* order, unsigned n,
+                                 unsigned long long* sink) {
+  unsigned long long acc = 0;
+  if (threadIdx.x == 0 && blockIdx.x < n)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                     base + (size_t)order[blockIdx.x] * kRec), "r"((unsigned)kRec));
+  for (unsigned r = blockIdx.x; r < n; r += gridDim.x) {
+    const unsigned nx = r + gridDim.x;
+    if (threadIdx.x == 0 && nx < n)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                       base + (size_t)order[nx] * kRec), "r"((unsigned)kRec));
+    const uint4* p = reinterpret_cast<const uint4*>(base + (size_t)order[r] * kRec);
+    for (unsigned j = threadIdx.x; j < kRec / 16; j += blockDim.x) {
+      const uint4 v = p[j];
+      acc += v.x ^ v.y ^ v.z ^ v.w;
+    }
+  }
+  if (acc == 0x123456789ull) *sink = acc;
+}
+
 // cp.async.bulk of whole records into a 3-stage smem ring
 __global__ void bulk_records(const uint8_t* base, const unsigned* order, unsigned n,
                              unsigned long long* sink) {
@@ -250,6 +288,47 @@ int main(int argc, char** argv) {
     }
     std::printf("{\"path\": \"zero_copy_bulk\", \"grid\": %d, \"gbs\": %.2f}\n", grid,
                 bytes / ms / 1e6);
+  }
+  for (int grid_mult : {2, 4, 8}) {
+    const int grid = prop.multiProcessorCount * grid_mult;
+    ms = best([&] { ldg256_records<<<grid, 256>>>(hd, d_order, (unsigned)nrec, sink); }, 5);
+    CK(cudaGetLastError());
+    std::printf("{\"path\": \"zero_copy_ldg128_L2_256B\", \"grid\": %d, \"gbs\": %.2f}\n",
+                grid, bytes / ms / 1e6);
+    ms = best([&] { prefetch_records<<<grid, 256>>>(hd, d_order, (unsigned)nrec, sink); }, 5);
+    CK(cudaGetLastError());
+    std::printf("{\"path\": \"zero_copy_bulk_prefetch_L2\", \"grid\": %d, \"gbs\": %.2f}\n",
+                grid, bytes / ms / 1e6);
+  }
+  // zero-copy kernel over a share (1-f) of the records while the copy engine
+  // moves a contiguous share f of the same bytes on a second stream
+  {
+    cudaStream_t cs;
+    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaEvent_t e0, e1, e2;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventCreate(&e2);
+    for (double f : {0.1, 0.2, 0.3, 0.5}) {
+      const size_t nce = (size_t)(nrec * f), nzc = nrec - nce;
+      float bestms = 1e30f;
+      for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(e0, 0);
+        cudaStreamWaitEvent(cs, e0, 0);
+        cudaMemcpyAsync(d, h + nzc * kRec, nce * kRec, cudaMemcpyHostToDevice, cs);
+        cudaEventRecord(e1, cs);
+        ldg_records<<<prop.multiProcessorCount * 4, 256>>>(hd, d_order, (unsigned)nzc, sink);
+        cudaStreamWaitEvent(0, e1, 0);
+        cudaEventRecord(e2, 0);
+        cudaEventSynchronize(e2);
+        float t;
+        cudaEventElapsedTime(&t, e0, e2);
+        bestms = std::min(bestms, t);
+      }
+      std::printf("{\"path\": \"zero_copy_plus_copy_engine\", \"ce_share\": %.2f, \"gbs\": %.2f}\n",
+                  f, bytes / bestms / 1e6);
+    }
+    cudaStreamDestroy(cs);
   }
   // HBM reference for the same gather
   ms = best([&] { ldg_records<<<prop.multiProcessorCount * 8, 256>>>(d, d_order, (unsigned)nrec, sink); }, 5);
