@@ -15,6 +15,7 @@
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -22,6 +23,7 @@
 #include "ttkv/quantizer.hpp"
 #include "ttkv/reference.hpp"
 #include "ttkv/relevance.hpp"
+#include "ttkv/sim.hpp"
 #include "ttkv/tier_store.hpp"
 #include "ttkv/workload.hpp"
 #ifdef TTKV_REF_HAVE_HARNESS
@@ -237,6 +239,34 @@ int ref_dense_attention(const float* q, uint32_t d_k, const float* keys, const f
   const auto o = reference::dense_attention(std::span<const float>(q, d_k), h);
   std::copy(o.begin(), o.end(), out);
   return 0;
+}
+
+// ---- simulate_serial / simulate_pipelined (sim.hpp:50-58) --------------------
+// compute item i is labelled "c<i>"; transfer item j carries the label of
+// compute item t_of[j].
+int ref_simulate(int pipelined, uint64_t n_compute, const double* camount, uint64_t n_transfer,
+                 const double* tamount, const uint64_t* t_of, double bandwidth,
+                 double fixed_latency, double compute_rate, double* total, double* idle,
+                 double* stall, double* total_compute, double* total_transfer) {
+  try {
+    StepWorkload w;
+    for (uint64_t i = 0; i < n_compute; ++i)
+      w.compute_items.push_back({"c" + std::to_string(i), camount[i]});
+    for (uint64_t j = 0; j < n_transfer; ++j)
+      w.transfer_items.push_back({"c" + std::to_string(t_of[j]), tamount[j]});
+    LinkModel link{bandwidth, fixed_latency};
+    const PipelineTimeline tl = pipelined ? simulate_pipelined(w, link, compute_rate)
+                                          : simulate_serial(w, link, compute_rate);
+    *total = tl.total_latency;
+    *idle = tl.idle_fraction;
+    *stall = tl.mean_transfer_stall;
+    *total_compute = tl.total_compute;
+    *total_transfer = tl.total_transfer;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
 }
 
 // ---- Acceptance criterion 3 (acceptance.cpp:172-195) through run_benchmark --

@@ -538,6 +538,14 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
   uint32_t CH = 4;
   bool slow = n > 0 && k > 0;
   CU(h, cudaMemsetAsync(h->counters, 0, sizeof(unsigned long long) * 4, h->s0));
+  // HBM-resident slow tier: fork the (low-priority) fast tier before score +
+  // select so it fills the SMs they leave idle (cfg3 shape: 6.33 -> 5.66 ms
+  // per step).  With the slow tier in host DRAM the PCIe stream is the
+  // critical path and the fork stays after select.
+  const bool early_fork = h->opt.slow_tier == TTKV_SLOW_DEVICE && !h->opt.serial_schedule;
+  if (early_fork) {
+    if (int rcf = fork_fast()) return rcf;
+  }
   if (slow) {
     // union entries per CTA: ~4 waves of 2 CTAs/SM over the lower bound S*k
     const uint64_t est = (uint64_t)g.S * k;
@@ -571,7 +579,9 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       CU(h, launch_gather(g, h->arena_dev, h->stage_arena, h->uids, h->ucount,
                           (uint32_t)grid_chunks, CH, h->s0));
     }
-    if (int rcf = fork_fast()) return rcf;
+    if (!early_fork) {
+      if (int rcf = fork_fast()) return rcf;
+    }
     if (h->slow_tc) {
       SlowTcArgs& a = h->stc;
       a.g = g;
@@ -605,7 +615,7 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       KTimer t(h, K_SLOW, h->s0);
       CU(h, launch_slow(a, (uint32_t)grid_chunks, (int)h->copy_mode, h->s0));
     }
-  } else {
+  } else if (!early_fork) {
     if (int rcf = fork_fast()) return rcf;
   }
   CU(h, cudaStreamWaitEvent(h->s0, h->ev_join, 0));

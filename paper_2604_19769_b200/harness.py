@@ -188,6 +188,88 @@ def run_benchmark(tier: TierConfig, policy: SelectionPolicy, spec: WorkloadSpec,
     return rec
 
 
+# ---------------------------------------------------------------------------
+# The reference's two-lane timing model (sim.cpp:16-141), restated, and its
+# calibration against measured B200 kernel times.
+# ---------------------------------------------------------------------------
+@dataclass
+class LinkModel:
+    """sim.hpp:12-15"""
+    bandwidth: float = 3.2e10   # bytes/s
+    fixed_latency: float = 0.0  # s per transfer
+
+
+@dataclass
+class Timeline:
+    """PipelineTimeline (sim.hpp:35-46) without the per-event list."""
+    total_latency: float = 0.0
+    total_compute: float = 0.0
+    total_transfer: float = 0.0
+    idle_fraction: float = 0.0
+    mean_transfer_stall: float = 0.0
+
+
+def _sim(compute, transfers, link: LinkModel, rate: float, pipelined: bool) -> Timeline:
+    """simulate_serial / simulate_pipelined (sim.cpp:90-141).  compute: list of
+    amounts (elements) in schedule order; transfers: list of (compute index,
+    bytes) in transfer order."""
+    if link.bandwidth <= 0 or rate <= 0:
+        raise ValueError("simulate: bandwidth and compute_rate must be positive")
+    if link.fixed_latency < 0:
+        raise ValueError("simulate: fixed_latency must be non-negative")
+    tl = Timeline()
+    finish = {}
+    t = 0.0
+    for ci, amount in transfers:  # transfer_finish_map (sim.cpp:32-45)
+        t += link.fixed_latency + amount / link.bandwidth
+        finish[ci] = t
+    tl.total_transfer = t
+    starts, lane = [], (tl.total_transfer if not pipelined else 0.0)
+    for i, amount in enumerate(compute):
+        start = max(lane, finish[i]) if (pipelined and i in finish) else lane
+        dur = amount / rate
+        starts.append(start)
+        lane = start + dur
+        tl.total_compute += dur
+    tl.total_latency = max(lane, tl.total_transfer) if pipelined else lane
+    ideal, t = [], 0.0  # ideal_starts (sim.cpp:49-57)
+    for amount in compute:
+        ideal.append(t)
+        t += amount / rate
+    stalls = [starts[i] - ideal[i] for i in range(len(compute)) if i in finish]
+    tl.mean_transfer_stall = sum(stalls) / len(stalls) if stalls else 0.0
+    tl.idle_fraction = ((tl.total_latency - tl.total_compute) / tl.total_latency
+                        if tl.total_latency > 0 else 0.0)
+    return tl
+
+
+def simulate_serial(compute, transfers, link: LinkModel, rate: float) -> Timeline:
+    return _sim(compute, transfers, link, rate, False)
+
+
+def simulate_pipelined(compute, transfers, link: LinkModel, rate: float) -> Timeline:
+    return _sim(compute, transfers, link, rate, True)
+
+
+def calibrated_step(fast_s: float, n_records: int, record_compute_s: float,
+                    record_transfer_s: float) -> dict:
+    """The reference's model of one GPU decode step with measured B200 rates:
+    compute lane = the fast tier, then one item per streamed record; transfer
+    lane = one item per record.  Rates are expressed as 1 unit/s so each
+    item's amount is its measured duration (fast kernel time; slow-kernel time
+    per record in the serial schedule; gather time per record)."""
+    compute = [fast_s] + [record_compute_s] * n_records
+    transfers = [(i + 1, record_transfer_s) for i in range(n_records)]
+    link = LinkModel(bandwidth=1.0)
+    pipe = simulate_pipelined(compute, transfers, link, 1.0)
+    ser = simulate_serial(compute, transfers, link, 1.0)
+    return {"pipelined_ms": pipe.total_latency * 1e3, "serial_ms": ser.total_latency * 1e3,
+            "pipelined_idle_fraction": pipe.idle_fraction,
+            "serial_idle_fraction": ser.idle_fraction,
+            "pipelined_stall_ms": pipe.mean_transfer_stall * 1e3,
+            "serial_stall_ms": ser.mean_transfer_stall * 1e3}
+
+
 def run_sweep(tier, policy, spec, context_lengths=(), block_sizes=(), key_bits=(),
               value_bits=(), fetch_fractions=(), **kw) -> List[RunRecord]:
     """run_sweep (harness.cpp:173-208): deterministic grid order."""

@@ -7,6 +7,8 @@ by the GPU engine's accounting (acceptance.cpp:172-195 and 430-465).
 """
 import os
 
+import numpy as np
+
 import pytest
 
 from paper_2604_19769_b200 import harness as H
@@ -119,3 +121,45 @@ def test_dropin_workload_generator_matches_reference():
                                              d_k=64, d_v=1, seed=40001))
     want = O.generate_workload(1024, 2, 64, 1, 40001, needle=True)
     assert all(np.array_equal(a, b) for a, b in zip(got, want))
+
+
+# ---------------------------------------------------------------------------
+# the timing model restated in harness.py == the reference's sim.cpp (CPU)
+# ---------------------------------------------------------------------------
+def _ref_sim(pipelined, compute, transfers, bw, lat, rate):
+    import ctypes as C
+    import _oracle as O
+    lib = O.ref()
+    f = lib.ref_simulate
+    f.restype = C.c_int
+    ca = np.asarray(compute, np.float64)
+    ta = np.asarray([t for _, t in transfers] or [0.0], np.float64)
+    to = np.asarray([i for i, _ in transfers] or [0], np.uint64)
+    out = [C.c_double() for _ in range(5)]
+    rc = f(C.c_int(int(pipelined)), C.c_uint64(len(compute)), ca.ctypes.data_as(C.c_void_p),
+           C.c_uint64(len(transfers)), ta.ctypes.data_as(C.c_void_p),
+           to.ctypes.data_as(C.c_void_p), C.c_double(bw), C.c_double(lat), C.c_double(rate),
+           *[C.byref(o) for o in out])
+    assert rc == 0
+    return [o.value for o in out]
+
+
+@pytest.mark.skipif(not __import__("_oracle").ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("seed", range(6))
+def test_sim_matches_reference(seed):
+    from paper_2604_19769_b200 import harness as H
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 40))
+    compute = list(rng.uniform(1e3, 1e6, n))
+    idx = sorted(rng.choice(np.arange(1, n), size=min(n - 1, int(rng.integers(0, n))),
+                            replace=False).tolist()) if n > 1 else []
+    rng.shuffle(idx)  # transfer order = schedule order of the reference's report
+    transfers = [(int(i), float(rng.uniform(1e3, 1e5))) for i in idx]
+    bw, lat, rate = float(rng.uniform(1e9, 6e10)), float(rng.choice([0.0, 2e-6])), 1e9
+    for pipelined in (False, True):
+        fn = H.simulate_pipelined if pipelined else H.simulate_serial
+        tl = fn(compute, transfers, H.LinkModel(bw, lat), rate)
+        ref = _ref_sim(pipelined, compute, transfers, bw, lat, rate)
+        got = [tl.total_latency, tl.idle_fraction, tl.mean_transfer_stall, tl.total_compute,
+               tl.total_transfer]
+        assert np.allclose(got, ref, rtol=1e-12, atol=0), (pipelined, got, ref)
