@@ -437,3 +437,54 @@ def test_full_size_cfg1_sampled_streams(gpu):
     # every record streamed exactly once per step: union == k for G=1
     assert rep.union_blocks == S * 101
     eng.close()
+
+
+@pytest.mark.parametrize("slow_tier", [0, 1])
+def test_full_size_cfg2_sampled_streams(gpu, slow_tier):
+    """cfg2 at full size: 256 streams (32 layers x 8 KV heads) x 4 query heads,
+    128K ctx, 4K fp16 fast tier, K8/V4, 0.45 per query head (n = 992 blocks,
+    k = 447), slow tier in pinned DRAM (CUDA-core streaming kernel) or HBM
+    (tensor-core kernel).  KV is generated on device; two streams are
+    re-derived on the host from the read-back fast tier + records: all four
+    heads' selections identical in order, outputs within tolerance of an fp64
+    recomputation; the per-step union over all 1024 (stream, head) lists
+    equals the records the kernel streamed."""
+    T_ = gpu
+    S, G, d, B, lf, ctx = 256, 4, 128, 128, 4096, 131072
+    cfg = T_.TierConfig(hbm_budget_bytes=lf * 256 * 2, d_k=d, d_v=d, block_size=B)
+    eng = T_.MultiStreamEngine(cfg, n_streams=S, heads_per_stream=G, reserve_tokens=ctx + 256,
+                               slow_tier=slow_tier)
+    eng.prefill_synthetic(ctx, seed=23)
+    rng = np.random.default_rng(1)
+    q = rng.standard_normal((S, G, d)).astype(np.float32)
+    kn = O.fp16_round(rng.standard_normal((S, d)))
+    vn = O.fp16_round(rng.standard_normal((S, d)))
+    n = eng.state()["slow_blocks"]
+    assert n == 992
+    sampled = (7, S - 3)
+    before = {s: (eng.read_fast(s), [eng.read_block(s, b) for b in range(n)]) for s in sampled}
+    rep = eng.decode_step(q, kn, vn, fetched=True)
+    assert rep.blocks_scored == 992 and rep.blocks_fetched == 447
+    for s in sampled:
+        (fk, fv, _), blocks = before[s]
+        dk = [O.dequantize_tensor(b["packed_keys"], B, d, 8, b["key_params"]) for b in blocks]
+        dv = [O.dequantize_tensor(b["packed_values"], B, d, 4, b["value_params"]) for b in blocks]
+        for g in range(G):
+            scores = np.array([O.oracle().tko_score_block(q[s, g], b["key_centroid"], d)
+                               for b in blocks])
+            sel = np.zeros(447, np.uint64)
+            O.oracle().tko_select_top_k(scores, None, n, 447, sel)
+            assert np.array_equal(rep.fetched_blocks[s][g], sel), (s, g)
+            K = np.concatenate([fk.astype(np.float64), kn[s][None].astype(np.float64)] +
+                               [dk[int(b)] for b in sel])
+            V = np.concatenate([fv.astype(np.float64), vn[s][None].astype(np.float64)] +
+                               [dv[int(b)] for b in sel])
+            lg = K @ q[s, g].astype(np.float64) / np.sqrt(d)
+            w = np.exp(lg - lg.max())
+            ref = (w[:, None] * V).sum(0) / w.sum()
+            assert rel_err(rep.output[s, g], ref) < OUT_TOL
+    union = sum(len(set(np.concatenate([np.asarray(f, np.int64) for f in rep.fetched_blocks[s]])))
+                for s in range(S))
+    assert rep.union_blocks == union
+    assert rep.pcie_bytes == union * eng.state()["payload_bytes"]
+    eng.close()
