@@ -231,6 +231,13 @@ int ttkv_gpu_locate(struct ttkv_gpu* h, uint64_t position, int* where, uint64_t*
 /* ---- measurement ------------------------------------------------------------ */
 int ttkv_gpu_set_timing(struct ttkv_gpu* h, int enabled);
 int ttkv_gpu_kernel_times(struct ttkv_gpu* h, ttkv_kernel_times* t, int reset);
+/* Kernels of the last timed decode step (timing enabled): kind (0 append,
+ * 1 score, 2 select, 3 fast, 4 slow, 5 combine, 6 evict, 7 gather), start and
+ * end in ms from the step's start on the critical-path stream.  The measured
+ * counterpart of PipelineTimeline (sim.hpp:35-46) for write_run_timelines
+ * (harness.cpp:291-300).  *n = number of events (call with cap 0 to size). */
+int ttkv_gpu_read_timeline(struct ttkv_gpu* h, uint32_t* kinds, double* start_ms,
+                           double* end_ms, uint64_t cap, uint64_t* n);
 
 /* ---- stateless entry points --------------------------------------------------- */
 /* quantize_block on the GPU (bit-exact).  Host inputs keys[rows][d_k],

@@ -13,6 +13,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -267,6 +268,57 @@ int ref_simulate(int pipelined, uint64_t n_compute, const double* camount, uint6
     g_err = e.what();
     return 1;
   }
+}
+
+// ---- parse_config_file + apply_config_values (harness.hpp:90-96) ------------
+// u64[9]: seed, context_length, decode_steps, d_k, d_v, needle_block_position,
+//         hbm_budget_bytes, block_size, bytes_full_precision
+// u32[7]: kind, key_bits, value_bits, has_top_k, baseline, format, literal_merge
+// f64[7]: needle_strength, tier.fetch_fraction, policy.fetch_fraction,
+//         hbm_bandwidth, pcie_bandwidth, transfer_latency, compute_rate
+// u64 top_k; out_dir copied to out (cap bytes).  Returns 0, or 1 ConfigError,
+// 2 IoError, 3 other (message in ref_last_error).
+int ref_load_config(const char* path, uint64_t* u64s, uint32_t* u32s, double* f64s,
+                    uint64_t* top_k, char* out_dir, uint64_t cap) {
+#ifdef TTKV_REF_HAVE_HARNESS
+  try {
+    RunConfig cfg;
+    WorkloadSpec spec;
+    apply_config_values(parse_config_file(path), cfg, spec);
+    const uint64_t u[9] = {spec.seed, spec.context_length, spec.decode_steps, spec.d_k,
+                           spec.d_v, spec.needle_block_position, cfg.tier.hbm_budget_bytes,
+                           cfg.tier.block_size, cfg.tier.bytes_full_precision};
+    std::memcpy(u64s, u, sizeof(u));
+    u32s[0] = spec.kind == WorkloadSpec::Kind::PlantedNeedle ? 1u : 0u;
+    u32s[1] = cfg.tier.key_bits;
+    u32s[2] = cfg.tier.value_bits;
+    u32s[3] = cfg.policy.top_k.has_value() ? 1u : 0u;
+    u32s[4] = (uint32_t)cfg.baseline;
+    u32s[5] = (uint32_t)cfg.format;
+    u32s[6] = cfg.literal_merge ? 1u : 0u;
+    const double f[7] = {spec.needle_alignment_strength, cfg.tier.fetch_fraction,
+                         cfg.policy.fetch_fraction, cfg.tier.hbm_bandwidth,
+                         cfg.tier.pcie_bandwidth, cfg.tier.transfer_latency,
+                         cfg.tier.compute_rate};
+    std::memcpy(f64s, f, sizeof(f));
+    *top_k = cfg.policy.top_k.value_or(0);
+    std::snprintf(out_dir, cap, "%s", cfg.out_dir.c_str());
+    return 0;
+  } catch (const ConfigError& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const IoError& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 3;
+  }
+#else
+  (void)path; (void)u64s; (void)u32s; (void)f64s; (void)top_k; (void)out_dir; (void)cap;
+  g_err = "harness not built";
+  return 3;
+#endif
 }
 
 // ---- Acceptance criterion 3 (acceptance.cpp:172-195) through run_benchmark --

@@ -181,6 +181,11 @@ struct ttkv_gpu {
     cudaEvent_t a, b;
   };
   std::vector<Rec> recs;
+  struct TlEvent {
+    int kind;
+    double start, end;  // ms from the step's start
+  };
+  std::vector<TlEvent> timeline;  // kernels of the last timed step
   std::vector<cudaEvent_t> pool;
   double ms[K_N] = {};
   uint64_t cnt[K_N] = {};
@@ -226,8 +231,8 @@ struct KTimer {
   int kind;
   cudaStream_t st;
   cudaEvent_t a = nullptr;
-  KTimer(ttkv_gpu* hh, int k, cudaStream_t s) : h(hh), kind(k), st(s) {
-    h->launches++;
+  KTimer(ttkv_gpu* hh, int k, cudaStream_t s, int n_kernels = 1) : h(hh), kind(k), st(s) {
+    h->launches += n_kernels;
     if (h->timing) {
       a = take_event(h);
       cudaEventRecord(a, st);
@@ -243,13 +248,30 @@ struct KTimer {
 };
 
 void drain_timing(ttkv_gpu* h) {
-  for (auto& r : h->recs) {
+  // Kernel records of a step precede that step's K_STEP record (StepTimer
+  // closes last); the last step's kernels are kept as a timeline relative to
+  // the step's start event (write_run_timelines, harness.cpp:291-300).
+  size_t first = 0;
+  for (size_t i = 0; i < h->recs.size(); ++i) {
+    auto& r = h->recs[i];
     cudaEventSynchronize(r.b);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, r.a, r.b);
     h->ms[r.kind] += ms;
-    if (r.kind == K_STEP) h->last_step_ms = ms;
     h->cnt[r.kind] += 1;
+    if (r.kind == K_STEP) {
+      h->last_step_ms = ms;
+      h->timeline.clear();
+      for (size_t j = first; j < i; ++j) {
+        float t0 = 0.f, t1 = 0.f;
+        cudaEventElapsedTime(&t0, r.a, h->recs[j].a);
+        cudaEventElapsedTime(&t1, r.a, h->recs[j].b);
+        h->timeline.push_back({h->recs[j].kind, (double)t0, (double)t1});
+      }
+      first = i + 1;
+    }
+  }
+  for (auto& r : h->recs) {
     h->pool.push_back(r.a);
     h->pool.push_back(r.b);
   }
@@ -570,7 +592,7 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       a.counters = h->counters;
       a.n = (uint32_t)n;
       a.k = (uint32_t)k;
-      KTimer t(h, K_SELECT, h->s0);
+      KTimer t(h, K_SELECT, h->s0, 2);  // sort + union kernels
       CU(h, launch_select(a, h->s0));
     }
     if (h->opt.serial_schedule) {
@@ -1479,6 +1501,20 @@ int ttkv_gpu_kernel_times(ttkv_gpu* h, ttkv_kernel_times* t, int reset) {
     for (int i = 0; i < K_N; ++i) { h->ms[i] = 0; h->cnt[i] = 0; }
   }
   (void)kKernelNames;
+  return TTKV_OK;
+}
+
+int ttkv_gpu_read_timeline(ttkv_gpu* h, uint32_t* kinds, double* start_ms, double* end_ms,
+                           uint64_t cap, uint64_t* n) {
+  if (!h || !n) return set_err(h, TTKV_EINVAL, "null argument");
+  CU(h, cudaSetDevice(h->dev));
+  drain_timing(h);
+  *n = h->timeline.size();
+  for (uint64_t i = 0; i < h->timeline.size() && i < cap; ++i) {
+    if (kinds) kinds[i] = (uint32_t)h->timeline[i].kind;
+    if (start_ms) start_ms[i] = h->timeline[i].start;
+    if (end_ms) end_ms[i] = h->timeline[i].end;
+  }
   return TTKV_OK;
 }
 

@@ -379,6 +379,21 @@ class MultiStreamEngine:
     def set_timing(self, on: bool):
         _check(self._lib.ttkv_gpu_set_timing(self._h, int(on)), self._h)
 
+    KERNEL_NAMES = ("append", "score", "select", "fast", "slow", "combine", "evict", "gather")
+
+    def timeline(self):
+        """Kernels of the last timed step: [(name, start_ms, end_ms)] from the
+        step's start (ttkv_gpu_read_timeline)."""
+        n = C.c_uint64()
+        _check(self._lib.ttkv_gpu_read_timeline(self._h, None, None, None, 0, C.byref(n)),
+               self._h)
+        k = np.zeros(max(1, n.value), np.uint32)
+        a = np.zeros(max(1, n.value), np.float64)
+        b = np.zeros(max(1, n.value), np.float64)
+        _check(self._lib.ttkv_gpu_read_timeline(self._h, _ptr(k), _ptr(a), _ptr(b), n.value,
+                                                C.byref(n)), self._h)
+        return [(self.KERNEL_NAMES[int(k[i])], float(a[i]), float(b[i])) for i in range(n.value)]
+
     def kernel_times(self, reset=False) -> dict:
         t = L.KernelTimesC()
         _check(self._lib.ttkv_gpu_kernel_times(self._h, C.byref(t), int(reset)), self._h)

@@ -17,13 +17,15 @@ import ctypes as C
 import json
 import math
 import os
+import re
 from dataclasses import dataclass, field, replace
 from typing import List, Optional
 
 import numpy as np
 
 from . import _lib as L
-from .engine import MultiStreamEngine, SelectionPolicy, TierConfig, fast_capacity
+from .engine import (ConfigError, IoError, MultiStreamEngine, SelectionPolicy, TierConfig,
+                     fast_capacity)
 
 BASELINES = ("ttkv", "fp16_full_fetch", "uniform_quant_8_8", "no_pipeline", "single_tier")
 ABLATION_ORDER = ("fp16_full_fetch", "single_tier", "uniform_quant_8_8", "no_pipeline", "ttkv")
@@ -58,6 +60,7 @@ class RunRecord:
     evictions: List[bool] = field(default_factory=list)
     oracle_errors: List[float] = field(default_factory=list)
     needle_hits: int = 0
+    timelines: List[list] = field(default_factory=list)  # measured, per step
     summary: dict = field(default_factory=dict)
 
 
@@ -169,6 +172,7 @@ def run_benchmark(tier: TierConfig, policy: SelectionPolicy, spec: WorkloadSpec,
             r = eng.decode_step(dq[s][None, None], dk[s][None], dv[s][None], fetched=True)
             kt = eng.kernel_times(reset=True)
             rec.latency_ms.append(kt["last_step_ms"])
+            rec.timelines.append(eng.timeline())
             rec.step_bytes.append(r.bytes_transferred)
             rec.pcie_bytes.append(r.pcie_bytes)
             rec.blocks_scored.append(r.blocks_scored)
@@ -186,6 +190,134 @@ def run_benchmark(tier: TierConfig, policy: SelectionPolicy, spec: WorkloadSpec,
         eng.close()
     rec.summary = aggregate(rec)
     return rec
+
+
+# ---------------------------------------------------------------------------
+# RunConfig files (harness.cpp:324-413): `key = value` lines, `#` comments.
+# ---------------------------------------------------------------------------
+@dataclass
+class RunConfig:
+    """harness.hpp:33-40"""
+    tier: TierConfig = field(default_factory=TierConfig)
+    policy: SelectionPolicy = field(default_factory=SelectionPolicy)
+    baseline: str = "ttkv"
+    format: str = "csv"
+    out_dir: str = "."
+    literal_merge: bool = False
+
+
+_INT_RE = re.compile(r"\s*([+-]?)(\d+)")
+_FLT_RE = re.compile(r"\s*([+-]?(?:(?:\d+\.?\d*|\.\d+)(?:[eE][+-]?\d+)?|inf(?:inity)?|nan))",
+                     re.IGNORECASE)
+
+
+def _stoull(v: str) -> int:
+    """std::stoull: longest base-10 prefix after whitespace, a leading '-'
+    negates modulo 2^64; no digits -> invalid_argument; > 2^64-1 -> out_of_range."""
+    m = _INT_RE.match(v)
+    if not m:
+        raise ValueError("invalid")
+    x = int(m.group(2))
+    if x > 2 ** 64 - 1:
+        raise OverflowError("range")
+    return (2 ** 64 - x) % 2 ** 64 if m.group(1) == "-" else x
+
+
+def _stod(v: str) -> float:
+    """std::stod: longest decimal-float prefix; overflow -> out_of_range."""
+    m = _FLT_RE.match(v)
+    if not m:
+        raise ValueError("invalid")
+    x = float(m.group(1))
+    if math.isinf(x) and "inf" not in m.group(1).lower():
+        raise OverflowError("range")
+    return x
+
+
+def parse_config_file(path) -> dict:
+    """parse_config_file (harness.cpp:324-346)."""
+    try:
+        with open(path, "r", newline="") as f:
+            text = f.read()
+    except OSError:
+        raise IoError(f"cannot open config file {path}") from None
+    values = {}
+    lines = text.split("\n")
+    if lines and lines[-1] == "":
+        lines.pop()
+    for lineno, line in enumerate(lines, 1):
+        line = line.split("#", 1)[0].strip(" \t\r")
+        if not line:
+            continue
+        if "=" not in line:
+            raise ConfigError(f"{path}:{lineno}: expected key = value")
+        k, v = line.split("=", 1)
+        values[k.strip(" \t\r")] = v.strip(" \t\r")
+    return values
+
+
+def apply_config_values(values: dict, config: RunConfig, spec: WorkloadSpec) -> None:
+    """apply_config_values (harness.cpp:348-413); keys in std::map order."""
+    u32 = lambda x: x % 2 ** 32  # static_cast<unsigned>(std::stoul(value))  # noqa: E731
+    for key in sorted(values):
+        value = values[key]
+        try:
+            if key == "seed": spec.seed = _stoull(value)  # noqa: E701
+            elif key == "context_length": spec.context_length = _stoull(value)  # noqa: E701
+            elif key == "decode_steps": spec.decode_steps = _stoull(value)  # noqa: E701
+            elif key == "d_k": spec.d_k = _stoull(value)  # noqa: E701
+            elif key == "d_v": spec.d_v = _stoull(value)  # noqa: E701
+            elif key == "workload":
+                if value == "gaussian":
+                    spec.kind = "gaussian"
+                elif value == "planted_needle":
+                    spec.kind = "needle"
+                else:
+                    raise ConfigError("unknown workload kind: " + value)
+            elif key == "needle_block_position": spec.needle_block_position = _stoull(value)  # noqa
+            elif key == "needle_alignment_strength":
+                spec.needle_alignment_strength = _stod(value)
+            elif key == "hbm_budget_bytes": config.tier.hbm_budget_bytes = _stoull(value)  # noqa
+            elif key == "block_size": config.tier.block_size = _stoull(value)  # noqa: E701
+            elif key == "key_bits": config.tier.key_bits = u32(_stoull(value))  # noqa: E701
+            elif key == "value_bits": config.tier.value_bits = u32(_stoull(value))  # noqa: E701
+            elif key == "bytes_full_precision":
+                config.tier.bytes_full_precision = _stoull(value)
+            elif key == "fetch_fraction":
+                config.tier.fetch_fraction = _stod(value)
+                config.policy.fetch_fraction = _stod(value)
+            elif key == "top_k_blocks":
+                config.tier.top_k_blocks = _stoull(value)
+                config.policy.top_k = _stoull(value)
+            elif key == "hbm_bandwidth": config.tier.hbm_bandwidth = _stod(value)  # noqa: E701
+            elif key == "pcie_bandwidth": config.tier.pcie_bandwidth = _stod(value)  # noqa: E701
+            elif key == "transfer_latency": config.tier.transfer_latency = _stod(value)  # noqa
+            elif key == "compute_rate": config.tier.compute_rate = _stod(value)  # noqa: E701
+            elif key == "baseline":
+                if value not in BASELINES:
+                    raise ConfigError("unknown baseline: " + value)
+                config.baseline = value
+            elif key == "format":
+                if value not in ("csv", "json"):
+                    raise ConfigError("unknown format: " + value)
+                config.format = value
+            elif key == "out_dir": config.out_dir = value  # noqa: E701
+            elif key == "literal_merge": config.literal_merge = value in ("1", "true")  # noqa
+            else:
+                raise ConfigError("unknown config key: " + key)
+        except ValueError:
+            raise ConfigError(f"bad value for {key}: {value}") from None
+        except OverflowError:
+            raise ConfigError(f"value out of range for {key}: {value}") from None
+
+
+def load_run_config(path, config: Optional[RunConfig] = None,
+                    spec: Optional[WorkloadSpec] = None):
+    """Defaults < file (ttkv_bench.cpp:9): returns (RunConfig, WorkloadSpec)."""
+    config = config or RunConfig()
+    spec = spec or WorkloadSpec()
+    apply_config_values(parse_config_file(path), config, spec)
+    return config, spec
 
 
 # ---------------------------------------------------------------------------
@@ -344,6 +476,19 @@ def write_step_records(r: RunRecord) -> str:
                      f"{r.blocks_scored[i]},{r.blocks_fetched[i]},{int(r.evictions[i])},"
                      f"{_fmt(err)},{r.pcie_bytes[i]}")
     return "\n".join(lines) + "\n"
+
+
+def write_run_timelines(r: RunRecord) -> str:
+    """write_run_timelines (harness.cpp:291-300): `step lane label start finish`
+    (seconds), one line per event.  The events are the measured B200 kernels of
+    each step; the PCIe-streaming slow-tier kernel is the transfer lane, every
+    other kernel the compute lane."""
+    out = []
+    for i, tl in enumerate(r.timelines):
+        for name, a, b in tl:
+            lane = "transfer" if name in ("slow", "gather") else "compute"
+            out.append(f"{i}\t{lane}\t{name}\t{_fmt(a * 1e-3)}\t{_fmt(b * 1e-3)}")
+    return "\n".join(out) + ("\n" if out else "")
 
 
 def emit_report(records: List[RunRecord], out_dir: str, fmt: str = "csv") -> None:

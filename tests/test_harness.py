@@ -108,6 +108,26 @@ def test_emit_report_on_gpu(gpu, tmp_path):
     assert len(os.listdir(tmp_path)) == 5
 
 
+@pytest.mark.gpu
+def test_measured_timelines_on_gpu(gpu):
+    # write_run_timelines (harness.cpp:291-300) from measured kernel events
+    spec = H.WorkloadSpec(context_length=6000, decode_steps=4, d_k=64, d_v=64, seed=5)
+    rec = H.run_benchmark(TierConfig(d_k=64, d_v=64, block_size=128,
+                                     hbm_budget_bytes=1024 * 128 * 2),
+                          SelectionPolicy(None, 0.45), spec)
+    assert len(rec.timelines) == 4
+    for tl, lat in zip(rec.timelines, rec.latency_ms):
+        names = [n for n, _, _ in tl]
+        assert {"append", "score", "select", "fast", "slow", "combine"} <= set(names)
+        for _, a, b in tl:
+            assert -1e-3 <= a <= b <= lat + 1e-3
+    tsv = H.write_run_timelines(rec).splitlines()
+    assert len(tsv) == sum(len(t) for t in rec.timelines)
+    f = tsv[0].split("\t")
+    assert f[0] == "0" and f[1] in ("compute", "transfer") and len(f) == 5
+    assert any(line.split("\t")[1:3] == ["transfer", "slow"] for line in tsv)
+
+
 def test_dropin_workload_generator_matches_reference():
     # libttkv.so's generate_workload (C entry in include/ttkv_dropin_c.h) is the
     # reference generator (workload.cpp:42-95), pinned against the oracle port
@@ -163,3 +183,77 @@ def test_sim_matches_reference(seed):
         got = [tl.total_latency, tl.idle_fraction, tl.mean_transfer_stall, tl.total_compute,
                tl.total_transfer]
         assert np.allclose(got, ref, rtol=1e-12, atol=0), (pipelined, got, ref)
+
+
+# ---------------------------------------------------------------------------
+# RunConfig files (harness.cpp:324-413) vs the reference's own parser (CPU)
+# ---------------------------------------------------------------------------
+CONFIG_CASES = [
+    "",
+    "# only a comment\n\n   \n",
+    "seed = 7\ncontext_length=16384\ndecode_steps = 8 # trailing comment\nd_k=128\nd_v = 96\n",
+    "workload = planted_needle\nneedle_block_position = 3\nneedle_alignment_strength = 2.5\n",
+    "hbm_budget_bytes = 524288\nblock_size = 64\nkey_bits = 6\nvalue_bits = 3\n"
+    "bytes_full_precision = 4\nfetch_fraction = 0.3\ntop_k_blocks = 12\n",
+    "hbm_bandwidth = 8e12\npcie_bandwidth=5.5e10\ntransfer_latency = 2e-6\ncompute_rate = 1e13\n",
+    "baseline = no_pipeline\nformat = json\nout_dir = /tmp/x y\nliteral_merge = true\r\n",
+    "seed = 12abc\nkey_bits = 4294967304\n",            # prefix parse, unsigned wrap
+    "seed = -1\n",                                       # stoull negation wraps
+    "fetch_fraction = .5e1x\n",
+    "seed = abc\n",                                      # bad value
+    "seed = 99999999999999999999999\n",                  # out of range
+    "compute_rate = 1e999\n",                            # out of range
+    "workload = uniform\n",                              # unknown kind
+    "baseline = fastest\n",                              # unknown baseline
+    "format = xml\n",                                    # unknown format
+    "colour = blue\n",                                   # unknown key
+    "seed 7\n",                                          # expected key = value
+    "seed = 1\nseed = 2\n",                              # last wins
+]
+
+
+def _ref_load(path):
+    import ctypes as C
+    import _oracle as O
+    f = O.ref().ref_load_config
+    f.restype = C.c_int
+    u64 = np.zeros(9, np.uint64)
+    u32 = np.zeros(7, np.uint32)
+    f64 = np.zeros(7, np.float64)
+    tk = C.c_uint64()
+    out = C.create_string_buffer(256)
+    rc = f(str(path).encode(), u64.ctypes.data_as(C.c_void_p), u32.ctypes.data_as(C.c_void_p),
+           f64.ctypes.data_as(C.c_void_p), C.byref(tk), out, C.c_uint64(256))
+    return rc, O.ref().ref_last_error().decode(), u64, u32, f64, tk.value, out.value.decode()
+
+
+@pytest.mark.skipif(not __import__("_oracle").ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("i", range(len(CONFIG_CASES)))
+def test_config_file_matches_reference(tmp_path, i):
+    from paper_2604_19769_b200.engine import ConfigError as CE
+    path = tmp_path / "run.cfg"
+    path.write_bytes(CONFIG_CASES[i].encode())
+    rc, msg, u64, u32, f64, top_k, out_dir = _ref_load(path)
+    if rc != 0:
+        assert rc == 1, msg
+        with pytest.raises(CE) as e:
+            H.load_run_config(path)
+        assert str(e.value) == msg
+        return
+    cfg, spec = H.load_run_config(path)
+    t = cfg.tier
+    assert [spec.seed, spec.context_length, spec.decode_steps, spec.d_k, spec.d_v,
+            spec.needle_block_position, t.hbm_budget_bytes, t.block_size,
+            t.bytes_full_precision] == [int(x) for x in u64]
+    assert [int(spec.kind == "needle"), t.key_bits, t.value_bits,
+            int(cfg.policy.top_k is not None), H.BASELINES.index(cfg.baseline),
+            ["csv", "json"].index(cfg.format), int(cfg.literal_merge)] == [int(x) for x in u32]
+    assert [spec.needle_alignment_strength, t.fetch_fraction, cfg.policy.fetch_fraction,
+            t.hbm_bandwidth, t.pcie_bandwidth, t.transfer_latency, t.compute_rate] == list(f64)
+    assert (cfg.policy.top_k or 0) == top_k and cfg.out_dir == out_dir
+
+
+def test_config_file_missing_is_io_error(tmp_path):
+    from paper_2604_19769_b200.engine import IoError
+    with pytest.raises(IoError, match="cannot open config file"):
+        H.load_run_config(tmp_path / "nope.cfg")
