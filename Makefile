@@ -36,8 +36,8 @@ CXX      ?= g++
 REF      ?= /root/reference
 dropin: $(LIBDIR)/libttkv.so
 
-$(LIBDIR)/libttkv.so: $(PKG)/cpp/ttkv_dropin.cpp include/ttkv/gpu_dropin.hpp include/ttkv_gpu.h $(LIBDIR)/libttkv_gpu.so
-	$(CXX) -std=c++20 -O2 -fPIC -shared -Iinclude -o $@ $(PKG)/cpp/ttkv_dropin.cpp \
+$(LIBDIR)/libttkv.so: $(PKG)/cpp/ttkv_dropin.cpp $(PKG)/cpp/ttkv_sim.cpp include/ttkv/gpu_dropin.hpp include/ttkv_gpu.h $(LIBDIR)/libttkv_gpu.so
+	$(CXX) -std=c++20 -O2 -fPIC -shared -Iinclude -o $@ $(PKG)/cpp/ttkv_dropin.cpp $(PKG)/cpp/ttkv_sim.cpp \
 	  -L$(LIBDIR) -lttkv_gpu -Wl,-rpath,'$$ORIGIN'
 
 # The reference's own unit tests, compiled UNMODIFIED (in place, read-only)
@@ -56,4 +56,22 @@ build/ref_unit_tests_on_gpu:
 	@echo "reference tree absent: keeping prebuilt $@ (if any)"
 endif
 
-.PHONY: dropin reftests
+# The reference's acceptance gate (tests/acceptance.cpp, criteria 1-9) compiled
+# UNMODIFIED against the drop-in; the reference harness.cpp (run_benchmark,
+# sweeps, reports, config parsing) is compiled in place next to it and drives
+# the GPU engine through libttkv.so, whose ttkv_sim.cpp supplies the timing
+# model.  No other reference source is linked.
+NLOHMANN ?= $(shell python -c "import os,sys; p=os.path.join(sys.prefix,'lib','python3.12','site-packages','include','cudnn_frontend','thirdparty'); print(p)")
+refacceptance: build/ref_acceptance_on_gpu
+ifneq ($(wildcard $(REF)/proj/tests/acceptance.cpp),)
+build/ref_acceptance_on_gpu: $(LIBDIR)/libttkv.so
+	@mkdir -p build
+	$(CXX) -std=c++20 -O2 -Iinclude -I$(REF)/proj/core/include -I$(NLOHMANN) \
+	  -o $@ $(REF)/proj/tests/acceptance.cpp $(REF)/proj/core/src/harness.cpp \
+	  -L$(LIBDIR) -lttkv -lttkv_gpu -Wl,-rpath,'$$ORIGIN/../$(LIBDIR)'
+else
+build/ref_acceptance_on_gpu:
+	@echo "reference tree absent: keeping prebuilt $@ (if any)"
+endif
+
+.PHONY: dropin reftests refacceptance

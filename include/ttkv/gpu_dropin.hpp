@@ -23,6 +23,7 @@
 #include <cstdint>
 #include <deque>
 #include <filesystem>
+#include <iosfwd>
 #include <limits>
 #include <optional>
 #include <random>
@@ -301,15 +302,60 @@ class TierStore {
   mutable std::vector<QuantizedBlock> slow_view_;  // append-only cache
 };
 
-// ---- simulator-facing step description (reference sim.hpp subset) -------------------
+// ---- two-lane timing model (reference sim.hpp; implemented in ttkv_sim.cpp) --------
+// One decode step as the simulator sees it: compute items (the fast chunk, then
+// one per fetched block) and transfer items (one per fetched block), both in
+// prefetch-schedule order, matched by label.
 struct WorkItem {
   std::string label;
-  double amount = 0.0;
+  double amount = 0.0;  // attention elements (compute) or bytes (transfer)
 };
 struct StepWorkload {
   std::vector<WorkItem> compute_items;
   std::vector<WorkItem> transfer_items;
 };
+struct LinkModel {
+  double bandwidth = 3.2e10;   // bytes/s
+  double fixed_latency = 0.0;  // s per transfer
+};
+struct TimelineEvent {
+  enum class Lane { Transfer, Compute };
+  Lane lane = Lane::Compute;
+  std::string label;
+  double start = 0.0;
+  double finish = 0.0;
+};
+struct PipelineTimeline {
+  std::vector<TimelineEvent> events;
+  double total_latency = 0.0;
+  double total_compute = 0.0;
+  double total_transfer = 0.0;
+  double idle_fraction = 0.0;        // compute-lane idle time / total latency
+  double mean_transfer_stall = 0.0;  // mean delay of fetched blocks' compute starts
+};
+// All transfers first, then all compute.
+PipelineTimeline simulate_serial(const StepWorkload& workload, const LinkModel& link,
+                                 double compute_rate);
+// Transfers back to back; each block's compute waits for its own transfer.
+PipelineTimeline simulate_pipelined(const StepWorkload& workload, const LinkModel& link,
+                                    double compute_rate);
+struct TrafficLedger {
+  std::vector<double> step_bytes;
+  std::vector<double> baseline_step_bytes;
+  double total_bytes() const;
+  double total_baseline_bytes() const;
+};
+struct RunSummary {
+  std::size_t steps = 0;
+  double p95_latency = 0.0;
+  double mean_latency = 0.0;
+  double tokens_per_second = 0.0;
+  double total_h2g_bytes = 0.0;
+  double traffic_reduction_vs_baseline = 0.0;
+};
+RunSummary aggregate_run(const std::vector<PipelineTimeline>& timelines,
+                         const TrafficLedger& ledger);
+void dump_timeline(std::ostream& os, const PipelineTimeline& timeline);
 
 // ---- workload generator (reference workload.hpp) --------------------------------------
 inline constexpr std::size_t kNeedleSpanTokens = 128;

@@ -16,6 +16,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -100,6 +103,61 @@ int resolve_k(const ttkv_selection_policy& p, uint64_t n, uint64_t& k, std::stri
   const uint64_t kk = (uint64_t)std::ceil(p.fetch_fraction * (double)n);
   k = std::min<uint64_t>(kk, n);
   return TTKV_OK;
+}
+
+// Process-wide cache of pinned, mapped host blocks.  Pinning costs ~3 ms per
+// MB-scale arena (measured on the GPU box), and handles are created per
+// request when serving and per trial in the reference's acceptance gate, so
+// freed blocks are kept (up to kPinnedCacheMax bytes) and reused for any
+// request they cover within 2x.  Leaked at exit on purpose (process lifetime).
+struct PinnedCache {
+  std::mutex mu;
+  std::multimap<size_t, void*> idle;     // size -> block
+  std::unordered_map<void*, size_t> size_of;  // every block handed out or idle
+  size_t idle_bytes = 0;
+};
+constexpr size_t kPinnedCacheMax = 8ull << 30;
+PinnedCache& pinned_cache() {
+  static PinnedCache* c = new PinnedCache;
+  return *c;
+}
+cudaError_t pinned_alloc(void** p, size_t bytes) {
+  PinnedCache& c = pinned_cache();
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.idle.lower_bound(bytes);
+    if (it != c.idle.end() && it->first <= 2 * bytes + (1u << 20)) {
+      *p = it->second;
+      c.idle_bytes -= it->first;
+      c.idle.erase(it);
+      return cudaSuccess;
+    }
+  }
+  cudaError_t e = cudaHostAlloc(p, bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.size_of[*p] = bytes;
+  }
+  return e;
+}
+void pinned_free(void* p) {
+  if (!p) return;
+  PinnedCache& c = pinned_cache();
+  std::unique_lock<std::mutex> lk(c.mu);
+  const auto it = c.size_of.find(p);
+  if (it == c.size_of.end()) {  // not ours
+    lk.unlock();
+    cudaFreeHost(p);
+    return;
+  }
+  if (c.idle_bytes + it->second <= kPinnedCacheMax) {
+    c.idle.emplace(it->second, p);
+    c.idle_bytes += it->second;
+    return;
+  }
+  c.size_of.erase(it);
+  lk.unlock();
+  cudaFreeHost(p);
 }
 
 uint32_t align_up(uint64_t x, uint64_t a) { return (uint32_t)((x + a - 1) / a * a); }
@@ -285,12 +343,12 @@ void free_all(ttkv_gpu* h) {
   F(h->ring_k); F(h->ring_v); F(h->cent); F(h->params); F(h->scores); F(h->sel); F(h->mask); F(h->uids);
   F(h->umask); F(h->ucount); F(h->counters); F(h->fpart); F(h->spart); F(h->q_dev);
   F(h->out_dev); F(h->kn_dev); F(h->vn_dev); F(h->stg_k); F(h->stg_v); F(h->stage_arena);
-  if (h->arena_host) cudaFreeHost(h->arena_host);
+  if (h->arena_host) pinned_free(h->arena_host);
   else if (h->arena_dev) cudaFree(h->arena_dev);
-  if (h->h_q) cudaFreeHost(h->h_q);
-  if (h->h_out) cudaFreeHost(h->h_out);
-  if (h->h_k) cudaFreeHost(h->h_k);
-  if (h->h_v) cudaFreeHost(h->h_v);
+  pinned_free(h->h_q);
+  pinned_free(h->h_out);
+  pinned_free(h->h_k);
+  pinned_free(h->h_v);
   for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : h->pool) cudaEventDestroy(e);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
@@ -316,7 +374,7 @@ int ensure_blocks(ttkv_gpu* h, uint64_t need) {
   uint8_t *nh = nullptr, *nd = nullptr;
   const size_t arena_bytes = S * cap * stride;
   if (h->opt.slow_tier == TTKV_SLOW_PINNED_HOST) {
-    CU(h, cudaHostAlloc((void**)&nh, arena_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    CU(h, pinned_alloc((void**)&nh, arena_bytes));
     CU(h, cudaHostGetDevicePointer((void**)&nd, nh, 0));
   } else {
     CU(h, cudaMalloc((void**)&nd, arena_bytes));
@@ -341,7 +399,7 @@ int ensure_blocks(ttkv_gpu* h, uint64_t need) {
     CU(h, cudaMemcpy2D(ncent, cap * h->g.d_k * 4, h->cent, old_cap * h->g.d_k * 4,
                        h->n_slow * h->g.d_k * 4, S, cudaMemcpyDeviceToDevice));
   }
-  if (h->arena_host) cudaFreeHost(h->arena_host);
+  if (h->arena_host) pinned_free(h->arena_host);
   else if (h->arena_dev) cudaFree(h->arena_dev);
   if (h->cent) cudaFree(h->cent);
   if (h->params) cudaFree(h->params);
@@ -864,10 +922,10 @@ int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* po
   CREATE_CU(cudaMalloc((void**)&h->out_dev, S * g.G * g.d_v * sizeof(double)));
   CREATE_CU(cudaMalloc(&h->kn_dev, S * g.d_k * 4));
   CREATE_CU(cudaMalloc(&h->vn_dev, S * g.d_v * 4));
-  CREATE_CU(cudaHostAlloc((void**)&h->h_q, S * g.G * g.d_k * sizeof(float), cudaHostAllocPortable));
-  CREATE_CU(cudaHostAlloc((void**)&h->h_out, S * g.G * g.d_v * sizeof(double), cudaHostAllocPortable));
-  CREATE_CU(cudaHostAlloc(&h->h_k, S * g.d_k * 4, cudaHostAllocPortable));
-  CREATE_CU(cudaHostAlloc(&h->h_v, S * g.d_v * 4, cudaHostAllocPortable));
+  CREATE_CU(pinned_alloc((void**)&h->h_q, S * g.G * g.d_k * sizeof(float)));
+  CREATE_CU(pinned_alloc((void**)&h->h_out, S * g.G * g.d_v * sizeof(double)));
+  CREATE_CU(pinned_alloc(&h->h_k, S * g.d_k * 4));
+  CREATE_CU(pinned_alloc(&h->h_v, S * g.d_v * 4));
   const uint64_t reserve_blocks =
       std::max<uint64_t>(16, (opt->reserve_tokens + g.B - 1) / g.B + 2);
   rc = ensure_blocks(h, std::min<uint64_t>(reserve_blocks, select_max_blocks()));

@@ -4,6 +4,10 @@ criteria reproduced on the GPU path.
 * build/ref_unit_tests_on_gpu is the reference's own doctest unit suite
   (proj/tests/test_{quantizer,relevance,attention,tier_store,engine}.cpp),
   compiled UNMODIFIED against include/ttkv/ (Makefile target `reftests`).
+* build/ref_acceptance_on_gpu is the reference's acceptance gate
+  (proj/tests/acceptance.cpp, criteria 1-9) compiled UNMODIFIED against the
+  drop-in, with the reference's harness.cpp compiled in place next to it
+  (Makefile target `refacceptance`): all nine criteria must pass on B200.
 * Criterion 7 (acceptance.cpp:376-426) planted-needle selection runs as one
   multi-stream GPU decode (one stream per seed) and must reproduce the
   reference's per-seed hit pattern (tests/golden/needle.json).
@@ -28,6 +32,19 @@ def test_reference_unit_suite_on_dropin(gpu):
     print(r.stdout[-4000:])
     assert r.returncode == 0, r.stdout[-4000:]
     assert "27 test cases, 0 failed" in r.stdout
+
+
+ACC = os.path.join(ROOT, "build", "ref_acceptance_on_gpu")
+
+
+@pytest.mark.skipif(not os.path.exists(ACC), reason="reference acceptance gate not built")
+def test_reference_acceptance_gate_on_dropin(gpu, tmp_path):
+    r = subprocess.run([ACC], capture_output=True, text=True, timeout=1500, cwd=tmp_path)
+    print(r.stdout[-4000:])
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    passed = [ln for ln in r.stdout.splitlines() if ln.startswith("[PASS]")]
+    assert len(passed) == 9, r.stdout[-4000:]
+    assert "5.639x" in r.stdout and "recall 0.998 at block 128, 0.972 at block 256" in r.stdout
 
 
 @pytest.mark.parametrize("B", [128, 256])
