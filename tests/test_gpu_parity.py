@@ -203,6 +203,14 @@ def run_parity(T_, *, S=2, G=1, d=32, dv=None, B=32, l_fast=128, kb=8, vb=4, ele
     return worst
 
 
+@pytest.mark.parametrize("ctx", [70000, 140000])
+def test_engine_many_blocks_selection(gpu, ctx):
+    # n = 4371 / 8746 slow blocks per stream: the selection sort runs with
+    # N2 = 8192 / 16384 and several compare-exchange pairs per thread, the
+    # regime of cfg5's 256K context (n = 2016) and beyond
+    run_parity(gpu, S=2, G=2, d=16, B=16, l_fast=64, ctx=ctx, steps=2, check_blocks=False)
+
+
 def test_engine_reference_unit_config(gpu):
     # test_engine.cpp:18-37 shape: d=16, B=32, 128-token fast tier, 512 ctx
     run_parity(gpu, S=1, G=1, d=16, B=32, l_fast=128, ctx=512, steps=6, seed=13)
