@@ -384,10 +384,10 @@ int ensure_blocks(ttkv_gpu* h, uint64_t need) {
   const uint64_t pbytes = h->g.rec.used - h->g.rec.kp_off;
   uint8_t* nparams = nullptr;
   if (pbytes) CU(h, cudaMalloc((void**)&nparams, S * cap * pbytes));
-  uint32_t* nsel = nullptr;
-  CU(h, cudaMalloc((void**)&nsel, S * h->g.Gs * cap * sizeof(uint32_t)));
-  if (old_cap && h->last_k)  // keep the last step's fetched lists readable
-    CU(h, cudaMemcpy2D(nsel, cap * 4, h->sel, old_cap * 4, h->last_k * 4, S * h->g.Gs,
+  double* nscores = nullptr;  // the last step's scores stay readable (fetched_blocks)
+  CU(h, cudaMalloc((void**)&nscores, S * h->g.Gs * cap * sizeof(double)));
+  if (old_cap && h->last_n && h->scores)
+    CU(h, cudaMemcpy2D(nscores, cap * 8, h->scores, old_cap * 8, h->last_n * 8, S * h->g.Gs,
                        cudaMemcpyDeviceToDevice));
   if (old_cap && h->n_slow && pbytes)
     CU(h, cudaMemcpy2D(nparams, cap * pbytes, h->params, old_cap * pbytes, h->n_slow * pbytes, S,
@@ -403,19 +403,18 @@ int ensure_blocks(ttkv_gpu* h, uint64_t need) {
   else if (h->arena_dev) cudaFree(h->arena_dev);
   if (h->cent) cudaFree(h->cent);
   if (h->params) cudaFree(h->params);
-  if (h->sel) cudaFree(h->sel);
   h->arena_host = nh;
   h->arena_dev = nd;
   h->cent = ncent;
   h->params = nparams;
-  h->sel = nsel;
   // per-step selection arrays (contents are per step; no copy)
   auto realloc_dev = [&](void** p, size_t bytes) -> cudaError_t {
     if (*p) cudaFree(*p);
     *p = nullptr;
     return cudaMalloc(p, bytes);
   };
-  CU(h, realloc_dev((void**)&h->scores, S * h->g.Gs * cap * sizeof(double)));
+  if (h->scores) cudaFree(h->scores);
+  h->scores = nscores;
   CU(h, realloc_dev((void**)&h->mask, S * cap * sizeof(uint32_t)));
   CU(h, cudaMemset(h->mask, 0, S * cap * sizeof(uint32_t)));  // select leaves it zeroed
   CU(h, realloc_dev((void**)&h->uids, S * cap * sizeof(uint32_t)));
@@ -642,7 +641,7 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       SelectArgs a{};
       a.g = g;
       a.scores = h->scores;
-      a.sel = h->sel;
+      a.sel = nullptr;  // the order is materialized by ttkv_gpu_read_fetched
       a.mask = h->mask;
       a.union_ids = h->uids;
       a.union_mask = h->umask;
@@ -1157,13 +1156,23 @@ int ttkv_gpu_read_fetched(ttkv_gpu* h, uint32_t stream, uint32_t head, uint64_t*
   const uint64_t k = h->last_k;
   if (n) *n = k;
   if (!out || k == 0) return TTKV_OK;
+  // select_top_k's order (relevance.cpp:29-43): stable_sort by score desc,
+  // then block id desc -- from the step's bit-exact fp64 scores; the GPU
+  // selected exactly this order's first k as a set
   const uint32_t hs = h->g.Gs == h->g.G ? head : 0;
-  std::vector<uint32_t> tmp(k);
+  const uint64_t n_sc = h->last_n;
+  std::vector<double> sc(n_sc);
   CU(h, cudaSetDevice(h->dev));
   CU(h, cudaStreamSynchronize(h->s0));
-  CU(h, cudaMemcpy(tmp.data(), h->sel + ((uint64_t)stream * h->g.Gs + hs) * h->g.n_cap,
-                   k * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-  for (uint64_t i = 0; i < k && i < cap; ++i) out[i] = tmp[i];
+  CU(h, cudaMemcpy(sc.data(), h->scores + ((uint64_t)stream * h->g.Gs + hs) * h->g.n_cap,
+                   n_sc * sizeof(double), cudaMemcpyDeviceToHost));
+  std::vector<uint32_t> ids(n_sc);
+  for (uint64_t i = 0; i < n_sc; ++i) ids[i] = (uint32_t)i;
+  std::stable_sort(ids.begin(), ids.end(), [&](uint32_t x, uint32_t y) {
+    if (sc[x] != sc[y]) return sc[x] > sc[y];
+    return x > y;
+  });
+  for (uint64_t i = 0; i < k && i < cap; ++i) out[i] = ids[i];
   return TTKV_OK;
 }
 

@@ -5,8 +5,9 @@
 // sequential in i, unfused (__dmul_rn/__dadd_rn) -- bit-exact with the
 // reference, so top-k ties are decided exactly as on the CPU.
 // select_topk replaces SelectionPolicy::resolve + select_top_k
-// (relevance.cpp:10-17, 29-43): a block-wide bitonic sort of (score desc,
-// block_id desc) -- a total order, so the result equals std::stable_sort's.
+// (relevance.cpp:10-17, 29-43): a radix selection of the k largest
+// (score, block_id) pairs -- a total order, so the set equals the prefix of
+// std::stable_sort's order, which ttkv_gpu_read_fetched reproduces on demand.
 // For GQA it also builds the per-stream union of the G selected sets plus a
 // per-block head mask, so every record crosses PCIe once per step.
 //
@@ -105,55 +106,100 @@ __device__ __forceinline__ uint64_t order_key(double d) {
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
-// One CTA per (stream, selection head): bitonic sort of (key, id) descending
-// in shared memory.  Compare-exchange passes whose stride is < 64 stay inside
-// one warp's 64-element window, so they are ordered by __syncwarp; only the
-// passes that cross windows need the CTA barrier (10 of 55 at n = 1024).
-__global__ void __launch_bounds__(kSelectThreads) select_sort_kernel(SelectArgs a, uint32_t N2) {
+// One CTA per (stream, selection head): the top-k SET by radix selection.
+// The attention needs only which blocks each head selected; their order (the
+// reference's fetched_blocks, select_top_k's stable_sort by score desc, id
+// desc) is a report field, materialized on demand by ttkv_gpu_read_fetched
+// from the same fp64 scores.  The k-th largest (key, id) pair is found MSB
+// first over the 64-bit order key (8-bit digits) and then the 14-bit block id
+// (two 7-bit digits), stopping as soon as the threshold bucket is taken
+// whole; every element at or above the threshold is selected.
+constexpr int kTopkThreads = 256;
+
+__device__ __forceinline__ uint32_t topk_digit(uint64_t key, uint32_t id, int p) {
+  return p < 8 ? (uint32_t)(key >> (56 - 8 * p)) & 0xffu : (p == 8 ? (id >> 7) & 0x7fu : id & 0x7fu);
+}
+
+__global__ void __launch_bounds__(kTopkThreads) select_topk_kernel(SelectArgs a) {
   const Geometry& g = a.g;
   const uint32_t h = blockIdx.x, s = blockIdx.y;
-  extern __shared__ __align__(16) uint8_t smem[];
-  uint64_t* key = reinterpret_cast<uint64_t*>(smem);
-  uint32_t* id = reinterpret_cast<uint32_t*>(key + N2);
-
   const double* sc = a.scores + ((uint64_t)s * g.Gs + h) * g.n_cap;
-  for (uint32_t i = threadIdx.x; i < N2; i += blockDim.x) {
-    key[i] = i < a.n ? order_key(sc[i]) : 0ull;
-    id[i] = i < a.n ? i : 0u;
-  }
-  __syncthreads();
-  const uint32_t half = N2 / 2;
-  for (uint32_t size = 2; size <= N2; size <<= 1) {
-    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-      for (uint32_t i = threadIdx.x; i < half; i += blockDim.x) {
-        const uint32_t lo = 2 * i - (i & (stride - 1));
-        const uint32_t hi = lo + stride;
-        const bool desc = (lo & size) == 0;
-        const uint64_t kl = key[lo], kh = key[hi];
-        const uint32_t il = id[lo], ih = id[hi];
-        const bool less = (kl < kh) || (kl == kh && il < ih);  // (lo) < (hi)
-        if (less == desc) {
-          key[lo] = kh; key[hi] = kl;
-          id[lo] = ih; id[hi] = il;
+  __shared__ uint32_t hist[256];
+  __shared__ uint32_t sh_digit, sh_need, sh_done;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  uint64_t key_pre = 0;  // chosen key digits so far (passes < 8)
+  uint32_t id_pre = 0;   // chosen id digits (passes 8, 9)
+  uint32_t need = a.k;
+  int p = 0;
+  bool done = false;
+  // does (key, id) agree with the chosen digits of passes < p?
+  auto match = [&](uint64_t key, uint32_t id, int pp) -> bool {
+    if (pp == 0) return true;
+    if (pp <= 8) return (key >> (64 - 8 * pp)) == key_pre;
+    return key == key_pre && (id >> 7) == id_pre;
+  };
+  for (;; ++p) {
+    for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < a.n; i += blockDim.x) {
+      const uint64_t key = order_key(sc[i]);
+      if (match(key, i, p)) atomicAdd(&hist[topk_digit(key, i, p)], 1u);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // bins from the top: lane l owns bins 255-8l .. 248-8l
+      uint32_t c[8], tot = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        c[e] = hist[255 - 8 * lane - e];
+        tot += c[e];
+      }
+      uint32_t incl = tot;  // inclusive prefix over lanes (higher bins first)
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += v;
+      }
+      uint32_t above = incl - tot;
+      const bool mine = above < need && incl >= need;
+      if (mine) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (above + c[e] >= need) {
+            sh_digit = 255 - 8 * lane - e;
+            sh_need = need - above;
+            sh_done = (c[e] == need - above) ? 1u : 0u;
+            break;
+          }
+          above += c[e];
         }
       }
-      // a pass with stride <= 32 touches only its warp's 64-element windows;
-      // two such passes in a row need only warp-level ordering
-      const bool last = stride == 1 && size == N2;
-      const uint32_t next = stride > 1 ? stride >> 1 : size;  // the next pass's stride
-      if (!last && stride <= 32 && next <= 32)
-        __syncwarp();
-      else
-        __syncthreads();
     }
+    __syncthreads();
+    const uint32_t d = sh_digit;
+    need = sh_need;
+    done = sh_done != 0;
+    if (p < 8) key_pre = (key_pre << 8) | d;
+    else id_pre = (id_pre << 7) | d;
+    if (done || p == 9) break;
+    __syncthreads();  // sh_* are rewritten by the next pass
   }
-  uint32_t* out = a.sel + ((uint64_t)s * g.Gs + h) * g.n_cap;
+  // selected: (key, id) >= threshold, compared on the digits fixed so far
   uint32_t* mask = a.mask + (uint64_t)s * g.n_cap;
   const uint32_t all_heads = (g.G >= 32) ? 0xffffffffu : ((1u << g.G) - 1u);
   const uint32_t bit = (g.Gs == g.G) ? (1u << h) : all_heads;
-  for (uint32_t i = threadIdx.x; i < a.k; i += blockDim.x) {
-    out[i] = id[i];
-    atomicOr(&mask[id[i]], bit);
+  for (uint32_t i = threadIdx.x; i < a.n; i += blockDim.x) {
+    const uint64_t key = order_key(sc[i]);
+    bool sel;
+    if (p < 8) {
+      sel = (key >> (56 - 8 * p)) >= key_pre;
+    } else if (p == 8) {
+      sel = key > key_pre || (key == key_pre && (i >> 7) >= id_pre);
+    } else {
+      sel = key > key_pre || (key == key_pre && i >= id_pre);
+    }
+    if (sel) atomicOr(&mask[i], bit);
   }
 }
 
@@ -201,18 +247,11 @@ __global__ void __launch_bounds__(kSelectThreads) select_union_kernel(SelectArgs
 uint32_t select_max_blocks() { return kSelectMaxN; }
 
 // The head mask (a.mask) must be all-zero on entry; select_union_kernel
-// leaves it zeroed again.
+// leaves it zeroed again.  `sel` is not written: the order is a cold read.
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
   if (a.n == 0) return cudaSuccess;
-  uint32_t N2 = 2;
-  while (N2 < a.n) N2 <<= 1;
-  const size_t smem = (size_t)N2 * 12;
-  cudaError_t e = cudaFuncSetAttribute(select_sort_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const uint32_t threads = N2 / 2 < kSelectThreads ? (N2 / 2 < 64 ? 64 : N2 / 2) : kSelectThreads;
-  select_sort_kernel<<<dim3(a.g.Gs, a.g.S), threads, smem, st>>>(a, N2);
-  e = cudaGetLastError();
+  select_topk_kernel<<<dim3(a.g.Gs, a.g.S), kTopkThreads, 0, st>>>(a);
+  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   select_union_kernel<<<a.g.S, 256, 0, st>>>(a);
   return cudaGetLastError();
