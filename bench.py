@@ -9,7 +9,8 @@ tier in pinned host DRAM, fetch fraction 0.45, per-query-head selection
 (one generated token per request).
 N>1 (configs[3], cfg4): the same request head-sharded over N GPUs -- rank r
 owns KV heads [8r/N, 8(r+1)/N) of every layer, streams its records over its
-own PCIe link, and the per-head outputs are all-gathered over NVLink (NCCL).
+own PCIe link, and the combine kernel writes every head's output into every rank over
+NVLink peer memory (the all-gather fused into the combine; NCCL as fallback).
 --workload cfg1|cfg3|cfg5 selects the other BASELINE configs (cfg3 shards
 by request at N>1, no collective).
 
@@ -281,6 +282,21 @@ def allreduce_max(t):
     return c.to(t.device)
 
 
+def setup_gather(eng, plan):
+    """N>1 with heads sharded: the combine kernel writes every rank's rows over
+    peer memory (PeerGather, no separate collective); NCCL all_gather if the
+    IPC mapping is unavailable or TTKV_GATHER=nccl."""
+    if not plan.needs_gather:
+        return None, "none"
+    if os.environ.get("TTKV_GATHER", "peer") == "peer":
+        from paper_2604_19769_b200.sharding import PeerGather
+        try:
+            return PeerGather(eng, plan), "combine fused with the all-gather over peer memory"
+        except Exception as e:  # noqa: BLE001
+            print(f"peer gather unavailable ({e}); using NCCL all_gather", file=sys.stderr)
+    return None, "NCCL all_gather"
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -320,10 +336,12 @@ def run_ours(args):
     vs = [torch.randn(S, D, device=dev, generator=gen).half() for _ in range(NPOOL)]
     out = torch.empty(S, G, D, device=dev, dtype=torch.float64)
 
+    pg, gather_kind = setup_gather(eng, plan)
+
     def step(i):
         eng.decode_step_device(qs[i % NPOOL].data_ptr(), ks[i % NPOOL].data_ptr(),
                                vs[i % NPOOL].data_ptr(), out.data_ptr(), dtype=1)
-        if plan.needs_gather:  # per-head outputs -> every rank (NVLink, NCCL)
+        if plan.needs_gather and pg is None:  # per-head outputs -> every rank (NCCL)
             gather_outputs(out, plan)
 
     def barrier():
@@ -363,7 +381,9 @@ def run_ours(args):
     t_e2e0 = time.perf_counter()
     for i in range(args.steps):
         r = eng.decode_step(hq[i % NPOOL], hk[i % NPOOL], hv[i % NPOOL])
-        if plan.needs_gather:
+        if pg is not None:
+            _ = pg.host()
+        elif plan.needs_gather:
             _ = gather_outputs(torch.from_numpy(r.output).to(dev), plan).cpu()
     barrier()
     e2e_ms = (time.perf_counter() - t_e2e0) * 1000.0 / args.steps
@@ -422,9 +442,9 @@ def run_ours(args):
         "dtype": "f32",
         "data": "synthetic (device N(0,1) KV rounded to fp16, random queries)",
         "config": {
-            "workload": w["desc"] + (f", head-sharded over {world} GPUs + NCCL all-gather"
-                                     if plan.needs_gather else
+            "workload": w["desc"] + (f", head-sharded over {world} GPUs" if plan.needs_gather else
                                      (f", request-sharded over {world} GPUs" if world > 1 else "")),
+            "output_gather": gather_kind,
             "ctx": ctx, "streams_per_gpu": S, "heads_per_stream": G, "batch": batch, "d": D,
             "block": B, "l_fast": L_FAST, "bits": "K8/V4", "fetch_fraction": FRAC,
             "selection": "group-shared" if args.group_select else "per-query-head (reference)",
@@ -531,6 +551,7 @@ def run_growth(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    pg, gather_kind = setup_gather(eng, plan)
     curve, non_ev, evict_ms, launches, prefill_s = [], [], [], 0, 0.0
     kt_tot = {}
     pcie_last = union_last = 0
@@ -556,7 +577,7 @@ def run_growth(args):
             for i in range(K):
                 rep = eng.decode_step_device(qs[i % NPOOL].data_ptr(), ks[i % NPOOL].data_ptr(),
                                              vs[i % NPOOL].data_ptr(), out.data_ptr(), dtype=1)
-                if plan.needs_gather:
+                if plan.needs_gather and pg is None:
                     gather_outputs(out, plan)
                 evs[i + 1].record()
                 ev_flags.append(bool(rep.eviction_occurred))
@@ -606,7 +627,9 @@ def run_growth(args):
     t_e2e0 = time.perf_counter()
     for i in range(n_e2e):
         r = eng.decode_step(hq[i % NPOOL], hk[i % NPOOL], hv[i % NPOOL])
-        if plan.needs_gather:
+        if pg is not None:
+            _ = pg.host()
+        elif plan.needs_gather:
             _ = gather_outputs(torch.from_numpy(r.output).to(dev), plan).cpu()
     barrier()
     e2e_ms = (time.perf_counter() - t_e2e0) * 1000.0 / n_e2e
@@ -632,8 +655,9 @@ def run_growth(args):
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (device N(0,1) KV rounded to fp16, random queries)",
         "config": {
-            "workload": w["desc"] + (f", head-sharded over {world} GPUs + NCCL all-gather"
-                                     if plan.needs_gather else ""),
+            "workload": w["desc"] + (f", head-sharded over {world} GPUs" if plan.needs_gather
+                                     else ""),
+            "output_gather": gather_kind,
             "growth_points": list(points), "steps_per_point": K,
             "timing": ("per point: one eviction period (B consecutive steps) timed with CUDA "
                        "events; value = 131072 tokens / trapezoid integral of ms/step over "

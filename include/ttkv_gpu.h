@@ -239,6 +239,24 @@ int ttkv_gpu_kernel_times(struct ttkv_gpu* h, ttkv_kernel_times* t, int reset);
 int ttkv_gpu_read_timeline(struct ttkv_gpu* h, uint32_t* kinds, double* start_ms,
                            double* end_ms, uint64_t cap, uint64_t* n);
 
+/* ---- multi-GPU: combine fused with the all-gather over peer memory ----------
+ * With streams sharded over n_ranks GPUs (one handle per rank), every rank
+ * needs every head's output.  init allocates this rank's gathered buffer
+ * [s_global][G][d_v] f64 (+ arrival counters), takes gidx[s] = the global
+ * index of local stream s, and returns its CUDA IPC handle (64 bytes) for the
+ * caller to exchange; open maps the other ranks' buffers (handles: n_ranks x 64
+ * bytes, rank order).  From then on every decode step's combine kernel also
+ * stores its rows into every rank's buffer over NVLink and the step waits
+ * until all ranks' rows have arrived (no separate collective); the buffer is
+ * double-buffered by step parity, so the rows of step t stay valid until this
+ * handle's step t+2 is enqueued.  output returns the device pointer of the
+ * last completed step's gathered rows and, if timed_out is non-null,
+ * synchronizes and reports whether any rank failed to arrive within ~4 s. */
+int ttkv_gpu_peer_gather_init(struct ttkv_gpu* h, uint32_t n_ranks, uint32_t my_rank,
+                              uint64_t s_global, const uint32_t* gidx, void* ipc_handle);
+int ttkv_gpu_peer_gather_open(struct ttkv_gpu* h, const void* handles);
+int ttkv_gpu_peer_gather_output(struct ttkv_gpu* h, double** device_rows, int* timed_out);
+
 /* ---- stateless entry points --------------------------------------------------- */
 /* quantize_block on the GPU (bit-exact).  Host inputs keys[rows][d_k],
  * values[rows][d_v] f32; outputs in the reference layout. */

@@ -657,7 +657,46 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
       for (uint32_t i = 0; i < nsc_used; ++i)
         if (sp[i * pitch + g.d_v + 1] > 0) o += sp[i * pitch + c];
     a.out[(uint64_t)idx * g.d_v + c] = (double)o;
+    if (a.n_peers) {
+      const uint64_t gi = ((uint64_t)a.gidx[s] * g.G + (idx - s * g.G)) * g.d_v + c;
+      for (uint32_t r = 0; r < a.n_peers; ++r) a.peer_out[r][gi] = (double)o;
+    }
   }
+  if (a.n_peers) {  // this CTA's row is in every rank's buffer: publish it
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (uint32_t r = 0; r < a.n_peers; ++r)
+        asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(a.peer_flags[r] + a.my_rank)
+                     : "memory");
+    }
+  }
+}
+
+__global__ void peer_wait_kernel(const unsigned long long* flags, uint32_t n_ranks,
+                                 unsigned long long target, int* status) {
+  const uint32_t r = threadIdx.x;
+  if (r >= n_ranks) return;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + r) : "memory");
+    if (v >= target) return;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 4000000000ull) {  // a rank never arrived: fail instead of hanging
+      atomicExch(status, 1);
+      return;
+    }
+    __nanosleep(256);
+  }
+}
+
+cudaError_t launch_peer_wait(const unsigned long long* flags, uint32_t n_ranks,
+                             unsigned long long target, int* status, cudaStream_t st) {
+  peer_wait_kernel<<<1, 32, 0, st>>>(flags, n_ranks, target, status);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {

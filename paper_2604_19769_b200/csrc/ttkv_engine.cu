@@ -185,6 +185,18 @@ enum Kind { K_APPEND = 0, K_SCORE, K_SELECT, K_FAST, K_SLOW, K_COMBINE, K_EVICT,
 void ttkv_dev::set_last_error(const char* msg) { g_last_error = msg ? msg : ""; }
 
 struct ttkv_gpu {
+  // fused combine + all-gather over peer memory (ttkv_gpu_peer_gather_*)
+  struct PeerGather {
+    uint32_t n_ranks = 0, my_rank = 0;
+    uint64_t s_global = 0;
+    uint8_t* base = nullptr;  // own [2][S_global][G][d_v] f64 rows + [8] u64 counters
+    size_t out_bytes = 0;
+    uint32_t* gidx = nullptr;  // device [S_local]
+    int* status = nullptr;     // device
+    void* peer_base[ttkv_dev::kMaxPeers] = {};  // IPC-opened peers (null for self)
+    unsigned long long epoch = 0;
+    bool active = false;
+  } pg;
   ttkv_tier_config cfg{};
   ttkv_selection_policy pol{};
   ttkv_gpu_options opt{};
@@ -336,7 +348,20 @@ void drain_timing(ttkv_gpu* h) {
   h->recs.clear();
 }
 
+void free_peer_gather(ttkv_gpu* h) {
+  for (auto& p : h->pg.peer_base)
+    if (p) {
+      cudaIpcCloseMemHandle(p);
+      p = nullptr;
+    }
+  if (h->pg.base) cudaFree(h->pg.base);
+  if (h->pg.gidx) cudaFree(h->pg.gidx);
+  if (h->pg.status) cudaFree(h->pg.status);
+  h->pg = ttkv_gpu::PeerGather{};
+}
+
 void free_all(ttkv_gpu* h) {
+  free_peer_gather(h);
   auto F = [](void* p) {
     if (p) cudaFree(p);
   };
@@ -709,8 +734,28 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
     a.union_count = slow ? h->ucount : nullptr;
     a.out = out;
     a.literal = h->opt.literal_additive_merge ? 1u : 0u;
-    KTimer t(h, K_COMBINE, h->s0);
+    if (h->pg.active) {
+      // double-buffered by step parity: a rank one step ahead never
+      // overwrites rows another rank may still be consuming
+      const size_t half = (size_t)((h->pg.epoch + 1) & 1) * h->pg.out_bytes;
+      a.n_peers = h->pg.n_ranks;
+      a.my_rank = h->pg.my_rank;
+      a.gidx = h->pg.gidx;
+      for (uint32_t r = 0; r < h->pg.n_ranks; ++r) {
+        uint8_t* b = r == h->pg.my_rank ? h->pg.base : static_cast<uint8_t*>(h->pg.peer_base[r]);
+        a.peer_out[r] = reinterpret_cast<double*>(b + half);
+        a.peer_flags[r] = reinterpret_cast<unsigned long long*>(b + 2 * h->pg.out_bytes);
+      }
+    }
+    KTimer t(h, K_COMBINE, h->s0, h->pg.active ? 2 : 1);
     CU(h, launch_combine(a, h->s0));
+    if (h->pg.active) {  // every rank's rows of this step have landed here
+      h->pg.epoch += 1;
+      CU(h, launch_peer_wait(
+                reinterpret_cast<const unsigned long long*>(h->pg.base + 2 * h->pg.out_bytes),
+                h->pg.n_ranks, h->pg.epoch * (unsigned long long)g.S * g.G, h->pg.status,
+                h->s0));
+    }
   }
   h->last_k = slow ? k : 0;
   h->last_n = n;
@@ -1568,6 +1613,70 @@ int ttkv_gpu_kernel_times(ttkv_gpu* h, ttkv_kernel_times* t, int reset) {
     for (int i = 0; i < K_N; ++i) { h->ms[i] = 0; h->cnt[i] = 0; }
   }
   (void)kKernelNames;
+  return TTKV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Fused combine + all-gather over peer memory.  With heads (or requests)
+// sharded over N ranks, every rank needs every head's output; instead of a
+// combine kernel followed by an NCCL all-gather, the combine kernel stores
+// each (stream, head) row straight into every rank's gathered buffer over
+// NVLink (CUDA IPC mappings) and publishes it with a system-scope counter;
+// a one-warp wait kernel on the step's stream holds the next step until all
+// ranks' rows of this step have arrived.
+// ---------------------------------------------------------------------------
+int ttkv_gpu_peer_gather_init(ttkv_gpu* h, uint32_t n_ranks, uint32_t my_rank,
+                              uint64_t s_global, const uint32_t* gidx, void* ipc_handle) {
+  if (!h || !gidx || !ipc_handle) return set_err(h, TTKV_EINVAL, "null argument");
+  if (n_ranks < 1 || n_ranks > (uint32_t)kMaxPeers || my_rank >= n_ranks)
+    return set_err(h, TTKV_ECONFIG, "peer gather: 1..8 ranks");
+  for (uint32_t i = 0; i < h->g.S; ++i)
+    if (gidx[i] >= s_global) return set_err(h, TTKV_ESHAPE, "peer gather: stream index out of range");
+  CU(h, cudaSetDevice(h->dev));
+  free_peer_gather(h);
+  auto& p = h->pg;
+  p.n_ranks = n_ranks;
+  p.my_rank = my_rank;
+  p.s_global = s_global;
+  p.out_bytes = (size_t)s_global * h->g.G * h->g.d_v * sizeof(double);
+  const size_t total = 2 * p.out_bytes + (size_t)kMaxPeers * sizeof(unsigned long long);
+  CU(h, cudaMalloc((void**)&p.base, total));
+  CU(h, cudaMemset(p.base, 0, total));
+  CU(h, cudaMalloc((void**)&p.gidx, h->g.S * sizeof(uint32_t)));
+  CU(h, cudaMemcpy(p.gidx, gidx, h->g.S * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  CU(h, cudaMalloc((void**)&p.status, sizeof(int)));
+  CU(h, cudaMemset(p.status, 0, sizeof(int)));
+  cudaIpcMemHandle_t mh;
+  CU(h, cudaIpcGetMemHandle(&mh, p.base));
+  std::memcpy(ipc_handle, &mh, sizeof(mh));
+  return TTKV_OK;
+}
+
+int ttkv_gpu_peer_gather_open(ttkv_gpu* h, const void* handles) {
+  if (!h || !handles) return set_err(h, TTKV_EINVAL, "null argument");
+  auto& p = h->pg;
+  if (!p.base) return set_err(h, TTKV_EERROR, "peer gather: call ttkv_gpu_peer_gather_init first");
+  CU(h, cudaSetDevice(h->dev));
+  for (uint32_t r = 0; r < p.n_ranks; ++r) {
+    if (r == p.my_rank) continue;
+    cudaIpcMemHandle_t mh;
+    std::memcpy(&mh, static_cast<const uint8_t*>(handles) + (size_t)r * sizeof(mh), sizeof(mh));
+    CU(h, cudaIpcOpenMemHandle(&p.peer_base[r], mh, cudaIpcMemLazyEnablePeerAccess));
+  }
+  p.active = true;
+  return TTKV_OK;
+}
+
+int ttkv_gpu_peer_gather_output(ttkv_gpu* h, double** device_rows, int* timed_out) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  if (!h->pg.active) return set_err(h, TTKV_EERROR, "peer gather not active");
+  if (device_rows)  // the half written by the last completed step
+    *device_rows = reinterpret_cast<double*>(h->pg.base + (h->pg.epoch & 1) * h->pg.out_bytes);
+  if (timed_out) {
+    CU(h, cudaSetDevice(h->dev));
+    CU(h, cudaStreamSynchronize(h->s0));
+    CU(h, cudaMemcpy(timed_out, h->pg.status, sizeof(int), cudaMemcpyDeviceToHost));
+  }
   return TTKV_OK;
 }
 

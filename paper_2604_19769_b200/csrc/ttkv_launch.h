@@ -9,6 +9,7 @@
 namespace ttkv_dev {
 
 constexpr int kInF32 = 0;
+constexpr int kMaxPeers = 8;
 constexpr int kInF16 = 1;
 
 // thread-local message behind ttkv_last_error() (defined in ttkv_engine.cu)
@@ -153,7 +154,20 @@ struct CombineArgs {
   const uint32_t* union_count;  // null when no slow work this step
   double* out;                  // [S][G][d_v] (reference output is double)
   uint32_t literal;
+  // Fused all-gather over peer memory (multi-GPU sharding): each CTA also
+  // stores its (stream, head) row into every rank's gathered buffer
+  // [S_global][G][d_v] at global stream gidx[s], then bumps that rank's
+  // arrival counter for this rank (system-scope release).
+  uint32_t n_peers;  // 0: off
+  uint32_t my_rank;
+  const uint32_t* gidx;
+  double* peer_out[kMaxPeers];
+  unsigned long long* peer_flags[kMaxPeers];  // rank r's counters [n_ranks]
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);
+// Blocks the stream until every rank's arrival counter in `flags` reaches
+// `target` (acquire, system scope); gives up after ~4 s and sets *status = 1.
+cudaError_t launch_peer_wait(const unsigned long long* flags, uint32_t n_ranks,
+                             unsigned long long target, int* status, cudaStream_t st);
 
 }  // namespace ttkv_dev

@@ -185,6 +185,7 @@ class MultiStreamEngine:
         self.config = config
         self.policy = policy or SelectionPolicy(config.top_k_blocks, config.fetch_fraction)
         self.S, self.G = n_streams, heads_per_stream
+        self.device = device
         self._lib = L.lib()
         self._c_cfg = config.to_c()
         self._c_pol = self.policy.to_c()

@@ -76,3 +76,73 @@ def gather_outputs(local_out, plan: ShardPlan, group=None):
     else:
         x = gathered.view(N, R // N, L, H, G, d)
     return x.reshape(R * L * H, G, d)
+
+
+class PeerGather:
+    """Combine fused with the all-gather over peer memory
+    (ttkv_gpu_peer_gather_*, include/ttkv_gpu.h): every rank's combine kernel
+    stores its (stream, head) rows straight into every rank's gathered buffer
+    over NVLink (CUDA IPC mappings exchanged once through torch.distributed),
+    so a decode step needs no separate collective.  Rows are in global stream
+    order, like gather_outputs."""
+
+    def __init__(self, engine, plan: ShardPlan, group=None):
+        import ctypes as C
+
+        import numpy as np
+        import torch.distributed as dist
+
+        from .engine import _check
+
+        self.engine, self.plan = engine, plan
+        self.S = plan.layers * plan.kv_heads * plan.requests
+        self.shape = (self.S, engine.G, engine.config.d_v)
+        lib = engine._lib
+        gidx = np.ascontiguousarray(plan.local_streams(), np.uint32)
+        if gidx.size != engine.S:
+            raise ValueError("peer gather: the engine's streams do not match the shard plan")
+        handle = (C.c_uint8 * 64)()
+        _check(lib.ttkv_gpu_peer_gather_init(engine.handle, plan.world, plan.rank, self.S,
+                                             gidx.ctypes.data_as(C.c_void_p), handle),
+               engine.handle)
+        handles = [None] * plan.world
+        dist.all_gather_object(handles, bytes(handle), group=group)
+        blob = b"".join(handles)
+        _check(lib.ttkv_gpu_peer_gather_open(engine.handle, blob), engine.handle)
+        self._C, self._np = C, np
+
+    def device_ptr(self) -> int:
+        C = self._C
+        p = C.c_void_p()
+        from .engine import _check
+        _check(self.engine._lib.ttkv_gpu_peer_gather_output(self.engine.handle, C.byref(p), None),
+               self.engine.handle)
+        return p.value
+
+    def host(self):
+        """The last step's gathered rows [S][G][d_v] (float64) on the host;
+        raises if a rank failed to arrive."""
+        C, np = self._C, self._np
+        from .engine import Error, _check
+        p, t = C.c_void_p(), C.c_int()
+        lib = self.engine._lib
+        _check(lib.ttkv_gpu_peer_gather_output(self.engine.handle, C.byref(p), C.byref(t)),
+               self.engine.handle)
+        if t.value:
+            raise Error("peer gather: a rank did not deliver its rows")
+        return self._view(p.value).cpu().numpy()
+
+    def tensor(self):
+        """Zero-copy torch view of the last step's gathered rows on the device."""
+        return self._view(self.device_ptr())
+
+    def _view(self, ptr):
+        import torch
+
+        class _Rows:
+            pass
+
+        rows = _Rows()
+        rows.__cuda_array_interface__ = {"shape": self.shape, "typestr": "<f8",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+        return torch.as_tensor(rows, device=torch.device("cuda", self.engine.device))

@@ -106,3 +106,49 @@ def test_sharded_decode_matches_single_handle(gpu, mode):
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}, res
+
+
+def _peer_worker(rank, world, port, q):
+    # the fused combine + all-gather over peer memory (CUDA IPC between the two
+    # rank processes; on this one-GPU box both map the same device)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2604_19769_b200 as T
+        from paper_2604_19769_b200.sharding import PeerGather, ShardPlan
+        plan = ShardPlan(rank, world, L_, H, 1, "heads")
+        pk, pv, steps = _inputs(1)
+        idx = np.asarray(plan.local_streams())
+        cfg = T.TierConfig(hbm_budget_bytes=LF * 2 * D * 2, d_k=D, d_v=D, block_size=B)
+        eng = T.MultiStreamEngine(cfg, n_streams=len(idx), heads_per_stream=G)
+        eng.prefill(pk[idx], pv[idx])
+        pg = PeerGather(eng, plan)
+        gathered = []
+        for qq, k, v in steps:
+            eng.decode_step(qq[idx], k[idx], v[idx])
+            gathered.append(pg.host())
+        eng.close()
+        ok = True
+        if rank == 0:
+            ref_outs, _ = _run(T, list(range(L_ * H)), pk, pv, steps)
+            for a, b in zip(gathered, ref_outs):
+                ok &= bool(np.array_equal(a, b))
+        q.put((rank, ok))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_memory_gather_matches_single_handle(gpu):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}, res
