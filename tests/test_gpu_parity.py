@@ -276,6 +276,7 @@ def test_engine_hot_shape_small(gpu):
 
 
 @pytest.mark.parametrize("G,mode,literal", [(4, 0, False), (4, 1, False), (1, 0, False), (2, 0, False),
+                                            (3, 0, False), (6, 0, False), (5, 1, False),
                                             (8, 0, False), (4, 0, True)])
 def test_engine_hbm_resident_slow_tier(gpu, G, mode, literal):
     # slow tier in HBM: the tensor-core slow kernel (TMA tensor maps, mma.sync
