@@ -117,6 +117,11 @@ def ref_sample(ctx, steps, G, engines=None, threads=None):
     return ms, pre.value, engines, threads
 
 
+def scale_note(engines, total):
+    return ("all engines, not extrapolated" if engines >= total else
+            f"extrapolated x{total / engines:g} to {total} engines")
+
+
 def cpu_throughput(ms_step, engines, total_engines, tokens_per_step):
     """tokens/s of the full workload, extrapolated linearly from the sample:
     a full step needs total_engines/engines sample steps."""
@@ -132,13 +137,15 @@ def run_reference(args):
     S = w["layers"] * w["kv_heads"] * w["batch"]
     total_engines = S * w["G"]  # one reference Engine per (stream, q-head)
     n = args.warmup + args.steps
-    ms, pre_s, engines, threads = ref_sample(w["ctx"], n, w["G"])
+    # small workloads (cfg1: 32 Engines) run in full; larger ones are sampled
+    ms, pre_s, engines, threads = ref_sample(w["ctx"], n, w["G"],
+                                             engines=total_engines if total_engines <= 64 else None)
     timed = ms[args.warmup:]
     vals = [cpu_throughput(m, engines, total_engines, w["batch"]) for m in timed]
     value = statistics.mean(vals)
     sample = (f"{engines} reference Engines (1 per stream x q-head) at {w['ctx']} ctx on "
               f"{threads} threads, {args.steps} timed decode steps after {args.warmup} warm-up; "
-              f"extrapolated x{total_engines / engines:g} to {total_engines} engines")
+              f"{scale_note(engines, total_engines)}")
     line = {
         "impl": "reference", "metric": metric_for(args.workload), "value": value, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -485,15 +492,15 @@ def run_ours(args):
         line["clocks"] = clk.summary()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            ms, _, engines, threads = ref_sample(ctx, 2, G)
             total = S * G
+            ms, _, engines, threads = ref_sample(ctx, 2, G,
+                                                 engines=total if total <= 64 else None)
             cv = cpu_throughput(float(ms[-1]), engines, total, tokens_per_step)
             line["cpu_baseline"] = {
                 "value": cv, "unit": UNIT, "cores": threads, "kind": "reference",
                 "sample": (f"{engines} unmodified reference Engines at {ctx} ctx, "
                            f"2 decode steps on {threads} threads (last timed: "
-                           f"{ms[-1]:.0f} ms), extrapolated x{total / engines:g} to "
-                           f"{total} engines")}
+                           f"{ms[-1]:.0f} ms), {scale_note(engines, total)}")}
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": host_cores(),
                                     "kind": "reference", "sample": f"unavailable: {e}"}
@@ -706,15 +713,16 @@ def run_growth(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             ctx = points[-1]
-            ms, _, engines, threads = ref_sample(ctx, 2, G)
             total = S * G
+            ms, _, engines, threads = ref_sample(ctx, 2, G,
+                                                 engines=total if total <= 64 else None)
             line["cpu_baseline"] = {
                 "value": cpu_throughput(float(ms[-1]), engines, total, 1), "unit": UNIT,
                 "cores": threads, "kind": "reference",
                 "sample": (f"{engines} unmodified reference Engines at {ctx} ctx (the end of the "
                            f"growth; upper bound on its sustained rate), 2 decode steps on "
-                           f"{threads} threads (last timed: {ms[-1]:.0f} ms), extrapolated "
-                           f"x{total / engines:g} to {total} engines")}
+                           f"{threads} threads (last timed: {ms[-1]:.0f} ms), "
+                           f"{scale_note(engines, total)}")}
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": host_cores(),
                                     "kind": "reference", "sample": f"unavailable: {e}"}
