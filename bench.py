@@ -70,6 +70,8 @@ def parse():
                    help="one selection per KV head (q' = sum_g q_g) instead of per query head")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--slow-tier", default="host", choices=["host", "device"])
+    p.add_argument("--layer-sequential", action="store_true",
+                   help="one dependent decode call per layer (one handle per layer)")
     a = p.parse_args()
     a.steps_given = a.steps is not None
     if a.steps is None:
@@ -733,12 +735,99 @@ def run_growth(args):
         dist.destroy_process_group()
 
 
+def run_layer_sequential(args):
+    """Layer-sequential decode (--layer-sequential): a model's layers attend one
+    after another (layer l+1's query depends on layer l's output), so one
+    token is `layers` dependent decode calls, each over that layer's
+    kv_heads x batch streams, on one CUDA stream.  One handle per layer; same
+    data, metric and roofline as the batched step.  N = 1 only."""
+    import numpy as np
+    import torch
+    import paper_2604_19769_b200 as T
+
+    w = args.w
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    Lyr, G, ctx = w["layers"], w["G"], w["ctx"]
+    S = w["kv_heads"] * w["batch"]
+    cfg = T.TierConfig(hbm_budget_bytes=L_FAST * 2 * D * 2, d_k=D, d_v=D, bytes_full_precision=2,
+                       block_size=B, key_bits=8, value_bits=4, fetch_fraction=FRAC)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    engs = []
+    for layer in range(Lyr):
+        e = T.MultiStreamEngine(cfg, T.SelectionPolicy(None, FRAC), n_streams=S,
+                                heads_per_stream=G, device=0,
+                                reserve_tokens=ctx + args.warmup + args.steps + 2 * B,
+                                slow_tier=0 if args.slow_tier == "host" else 1)
+        e.set_stream(stream.cuda_stream)
+        e.prefill_synthetic(ctx, seed=7000 + layer)
+        engs.append(e)
+    h2d_peak = measure_h2d_peak(torch, dev)
+    gen = torch.Generator(device=dev).manual_seed(0)
+    qs = [torch.randn(S, G, D, device=dev, generator=gen) for _ in range(Lyr)]
+    ks = [torch.randn(S, D, device=dev, generator=gen).half() for _ in range(Lyr)]
+    vs = [torch.randn(S, D, device=dev, generator=gen).half() for _ in range(Lyr)]
+    outs = [torch.empty(S, G, D, device=dev, dtype=torch.float64) for _ in range(Lyr)]
+
+    def token():
+        for layer, e in enumerate(engs):
+            e.decode_step_device(qs[layer].data_ptr(), ks[layer].data_ptr(), vs[layer].data_ptr(),
+                                 outs[layer].data_ptr(), dtype=1)
+
+    for _ in range(args.warmup):
+        token()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(0) as clk:
+        torch.cuda.synchronize()
+        ev0.record()
+        for _ in range(args.steps):
+            token()
+        ev1.record()
+        torch.cuda.synchronize()
+    ms_step = ev0.elapsed_time(ev1) / args.steps
+    union = sum(e.step_counters()[0] for e in engs)
+    st = engs[0].state()
+    pcie = union * st["payload_bytes"]
+    host_tier = args.slow_tier == "host"
+    hbm = sum(S * st["fast_tokens"] * 2 * D * 2 + S * st["slow_blocks"] * D * 4 for _ in engs) + \
+        union * (st["record_bytes"] - st["payload_bytes"]) + (0 if host_tier else pcie)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:  # noqa: BLE001
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    t_roof = max(hbm / (hbm_peak * 1e9), (pcie / (h2d_peak * 1e9)) if host_tier else 0.0) * 1e3
+    line = {
+        "metric": metric_for(args.workload) + ", layer-sequential", "value": w["batch"] * 1e3 / ms_step,
+        "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (device N(0,1) KV rounded to fp16, random queries)",
+        "config": {"workload": w["desc"] + f", layer-sequential: {Lyr} dependent calls per token",
+                   "ctx": ctx, "streams_per_layer": S, "heads_per_stream": G,
+                   "slow_tier": "pinned host DRAM, zero-copy PCIe" if host_tier else "HBM"},
+        "ms_per_layer": ms_step / Lyr,
+        "roofline": {"tier_roofline_ms": t_roof, "tier_frac": t_roof / ms_step,
+                     "pcie_gbs": pcie / (ms_step * 1e-3) / 1e9 if host_tier else None,
+                     "pcie_peak": h2d_peak},
+        "clocks": clk.summary(),
+    }
+    for e in engs:
+        e.close()
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.layer_sequential:
+        run_layer_sequential(args)
     elif args.workload == "cfg5":
         run_growth(args)
     else:

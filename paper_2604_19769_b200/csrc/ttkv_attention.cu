@@ -649,9 +649,58 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = L;
   __syncthreads();
   const Acc inv = Acc(1) / (red[0] + red[1] + red[2] + red[3]);
-  for (uint32_t c = threadIdx.x; c < g.d_v; c += blockDim.x) {
-    Acc A = 0;
-    for (uint32_t i = 0; i < np; ++i) A += w[i] * part(i)[c];
+  // the weighted sum over partials for this CTA's channel slice
+  // [c_lo, c_hi) (blockIdx.y; several slices when S*G is small): warp w takes
+  // partials w, w+4, ..., lane l channels c_lo + l + 32j (coalesced segments
+  // of each partial row), two partials in flight; warps meet in smem
+  const uint32_t cw = (g.d_v + gridDim.y - 1) / gridDim.y;
+  const uint32_t c_lo = blockIdx.y * cw, c_hi = min(g.d_v, c_lo + cw);
+  __shared__ Acc red2[4][kMaxD];
+  {
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // 8 partial rows in flight per lane (the rows come from L2 or DRAM)
+    constexpr int kU = 8;
+    Acc acc[kU][4];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[u][j] = 0;
+    uint32_t i = warp;
+    for (; i + 4 * (kU - 1) < np; i += 4 * kU) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const Acc* pu = part(i + 4 * u);
+        const Acc wu = w[i + 4 * u];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t c = c_lo + lane + 32 * j;
+          if (c < c_hi) acc[u][j] += wu * pu[c];
+        }
+      }
+    }
+    for (; i < np; i += 4) {
+      const Acc* p0 = part(i);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t c = c_lo + lane + 32 * j;
+        if (c < c_hi) acc[0][j] += w[i] * p0[c];
+      }
+    }
+    Acc a0[4], a1[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      a0[j] = ((acc[0][j] + acc[1][j]) + (acc[2][j] + acc[3][j]));
+      a1[j] = ((acc[4][j] + acc[5][j]) + (acc[6][j] + acc[7][j]));
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t c = c_lo + lane + 32 * j;
+      if (c < c_hi) red2[warp][c] = a0[j] + a1[j];
+    }
+  }
+  __syncthreads();
+  for (uint32_t c = c_lo + threadIdx.x; c < c_hi; c += blockDim.x) {
+    const Acc A = (red2[0][c] + red2[1][c]) + (red2[2][c] + red2[3][c]);
     Acc o = A * inv;
     if (a.literal)
       for (uint32_t i = 0; i < nsc_used; ++i)
@@ -699,10 +748,18 @@ cudaError_t launch_peer_wait(const unsigned long long* flags, uint32_t n_ranks,
   return cudaGetLastError();
 }
 
+// channel slices per (stream, head): enough CTAs to keep the combine from
+// being latency-bound when S*G is small (one layer of a layer-sequential step)
+uint32_t combine_slices(const Geometry& g) {
+  const uint32_t rows = g.S * g.G;
+  if (rows >= 256 || g.d_v <= 32) return 1;
+  return (g.d_v + 31) / 32;
+}
+
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
   const size_t acc = a.g.elem == 4 ? 8 : 4;
   const size_t smem = (size_t)(a.nfc + a.nsc + 1) * acc;
-  const uint32_t grid = a.g.S * a.g.G;
+  const dim3 grid(a.g.S * a.g.G, combine_slices(a.g));
   if (a.g.elem == 4) {
     cudaFuncSetAttribute(combine_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);

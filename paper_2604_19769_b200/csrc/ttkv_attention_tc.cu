@@ -313,12 +313,21 @@ constexpr int kScPitch = 132;  // score row pitch (floats): conflict-free C-frag
 __device__ __forceinline__ uint32_t swz64(uint32_t off) {  // TMA SWIZZLE_64B
   return off ^ (((off >> 7) & 3u) << 4);
 }
+// Records are streamed exactly once per step: their TMA loads carry an
+// L2 evict-first policy so they do not push the step's partials and
+// selection arrays (re-read by the combine) out of L2.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
-                                            uint64_t* bar) {
+                                            uint64_t* bar, uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)),
+      "l"(policy)
       : "memory");
 }
 // D += A(16x16) * B(16x8), f16 in, f32 accumulate
@@ -430,14 +439,15 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
 
   if (warp == 0) {
     if (lane == 0) {
+      const uint64_t evict_first = l2_evict_first_policy();
       for (uint32_t i = 0; i < nb; ++i) {
         const uint32_t st = i % ST;
         if (i >= ST) mbar_wait_sleep(&empty[st], ((i / ST) - 1) & 1);
         const int rec = (int)((uint64_t)s * g.n_cap + uids[i]);
         uint8_t* dst = base + st * kSlowStage;
         mbar_arrive_expect_tx(&full[st], kSlowStage);
-        tma_load_3d(dst, &a.tk, 0, 0, rec, &full[st]);
-        tma_load_3d(dst + kKBox, &a.tv, 0, 0, rec, &full[st]);
+        tma_load_3d(dst, &a.tk, 0, 0, rec, &full[st], evict_first);
+        tma_load_3d(dst + kKBox, &a.tv, 0, 0, rec, &full[st], evict_first);
         bulk_g2s(dst + kKBox + kVBox, a.params + (uint64_t)rec * kPBytes, kPBytes, &full[st]);
       }
     }

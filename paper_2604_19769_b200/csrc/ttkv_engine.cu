@@ -753,7 +753,8 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       h->pg.epoch += 1;
       CU(h, launch_peer_wait(
                 reinterpret_cast<const unsigned long long*>(h->pg.base + 2 * h->pg.out_bytes),
-                h->pg.n_ranks, h->pg.epoch * (unsigned long long)g.S * g.G, h->pg.status,
+                h->pg.n_ranks, h->pg.epoch * (unsigned long long)g.S * g.G * combine_slices(g),
+                h->pg.status,
                 h->s0));
     }
   }

@@ -165,6 +165,7 @@ struct CombineArgs {
   unsigned long long* peer_flags[kMaxPeers];  // rank r's counters [n_ranks]
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);
+uint32_t combine_slices(const Geometry& g);  // CTAs per (stream, head) row
 // Blocks the stream until every rank's arrival counter in `flags` reaches
 // `target` (acquire, system scope); gives up after ~4 s and sets *status = 1.
 cudaError_t launch_peer_wait(const unsigned long long* flags, uint32_t n_ranks,
