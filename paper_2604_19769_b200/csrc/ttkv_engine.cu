@@ -204,7 +204,7 @@ struct ttkv_gpu {
   int dev = 0;
   cudaStream_t s0 = nullptr, s1 = nullptr;
   bool own_s0 = true;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_start = nullptr;
   Geometry g{};
   uint64_t l_fast = 0;
   uint32_t copy_mode = 1;
@@ -377,6 +377,7 @@ void free_all(ttkv_gpu* h) {
   for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : h->pool) cudaEventDestroy(e);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_start) cudaEventDestroy(h->ev_start);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->s1) cudaStreamDestroy(h->s1);
   if (h->s0 && h->own_s0) cudaStreamDestroy(h->s0);
@@ -577,10 +578,14 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
   if (pos - h->fast_front + 1 > g.C)
     return set_err(h, TTKV_EERROR,
                    "decode_step: fast tier would exceed its ring; settle pending evictions");
-  // append_kv: the new token attends to itself
+  // append_kv: the new token attends to itself.  Only the fast
+  // tier reads the ring, so the append runs on s1 ahead of the fast kernel and
+  // stays off the critical path score -> select -> slow on s0.
+  CU(h, cudaEventRecord(h->ev_start, h->s0));
+  CU(h, cudaStreamWaitEvent(h->s1, h->ev_start, 0));
   {
-    KTimer t(h, K_APPEND, h->s0);
-    CU(h, launch_append(g, h->ring_k, h->ring_v, kn, vn, dtype, pos % g.C, 1, 1, h->s0));
+    KTimer t(h, K_APPEND, h->s1);
+    CU(h, launch_append(g, h->ring_k, h->ring_v, kn, vn, dtype, pos % g.C, 1, 1, h->s1));
   }
   h->appended = pos + 1;
   const uint64_t F = h->appended - h->fast_front;
@@ -949,6 +954,7 @@ int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* po
     CREATE_CU(cudaStreamCreateWithPriority(&h->s1, cudaStreamNonBlocking, lo));
   }
   CREATE_CU(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+  CREATE_CU(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming));
   CREATE_CU(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   const size_t S = g.S;
   CREATE_CU(cudaMalloc(&h->ring_k, S * g.C * g.d_k * g.elem));
