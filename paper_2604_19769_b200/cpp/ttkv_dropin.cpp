@@ -401,7 +401,10 @@ ttkv_gpu* open_store(const TierConfig& cfg, const SelectionPolicy& pol, bool lit
   o.device = device_ordinal();
   o.n_streams = 1;
   o.heads_per_stream = 1;
-  o.slow_tier = TTKV_SLOW_PINNED_HOST;
+  // TTKV_SLOW_TIER=hbm keeps the slow tier resident in HBM (tensor-core
+  // consumer); the default is the reference's pinned host DRAM tier
+  const char* tier = std::getenv("TTKV_SLOW_TIER");
+  o.slow_tier = (tier && std::strcmp(tier, "hbm") == 0) ? TTKV_SLOW_DEVICE : TTKV_SLOW_PINNED_HOST;
   o.literal_additive_merge = literal ? 1u : 0u;
   // The reference keeps float32 tokens whatever bytes_full_precision accounts
   // for (kv_types.hpp:14-15): default to an fp32 ring (fp64 accumulation).
