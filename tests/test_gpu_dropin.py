@@ -27,8 +27,10 @@ BIN = os.path.join(ROOT, "build", "ref_unit_tests_on_gpu")
 
 
 @pytest.mark.skipif(not os.path.exists(BIN), reason="reference unit tests not built")
-def test_reference_unit_suite_on_dropin(gpu):
-    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+@pytest.mark.parametrize("slow_tier", ["host", "hbm"])
+def test_reference_unit_suite_on_dropin(gpu, slow_tier):
+    env = dict(os.environ, TTKV_SLOW_TIER=slow_tier)
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600, env=env)
     print(r.stdout[-4000:])
     assert r.returncode == 0, r.stdout[-4000:]
     assert "27 test cases, 0 failed" in r.stdout
