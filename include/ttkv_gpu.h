@@ -256,6 +256,8 @@ int ttkv_gpu_peer_gather_init(struct ttkv_gpu* h, uint32_t n_ranks, uint32_t my_
                               uint64_t s_global, const uint32_t* gidx, void* ipc_handle);
 int ttkv_gpu_peer_gather_open(struct ttkv_gpu* h, const void* handles);
 int ttkv_gpu_peer_gather_output(struct ttkv_gpu* h, double** device_rows, int* timed_out);
+/* Unmaps the peers and frees the gathered buffer (steps stop publishing). */
+int ttkv_gpu_peer_gather_close(struct ttkv_gpu* h);
 
 /* ---- stateless entry points --------------------------------------------------- */
 /* quantize_block on the GPU (bit-exact).  Host inputs keys[rows][d_k],

@@ -70,7 +70,8 @@ EXPORTS = [
     "ttkv_gpu_state", "ttkv_gpu_read_fetched", "ttkv_gpu_read_block", "ttkv_gpu_serialize_block",
     "ttkv_gpu_dump_slow_tier", "ttkv_gpu_restore_slow_tier", "ttkv_gpu_read_fast", "ttkv_gpu_locate", "ttkv_gpu_set_timing",
     "ttkv_gpu_kernel_times", "ttkv_gpu_read_timeline", "ttkv_gpu_peer_gather_init",
-    "ttkv_gpu_peer_gather_open", "ttkv_gpu_peer_gather_output", "ttkv_gpu_quantize_block",
+    "ttkv_gpu_peer_gather_open", "ttkv_gpu_peer_gather_output", "ttkv_gpu_peer_gather_close",
+    "ttkv_gpu_quantize_block",
     "ttkv_gpu_append", "ttkv_gpu_evict",
     "ttkv_gpu_eviction_pending", "ttkv_gpu_dequantize_block", "ttkv_gpu_score_blocks",
     "ttkv_gpu_select_top_k", "ttkv_fast_capacity",
@@ -121,6 +122,7 @@ def lib():
         "ttkv_gpu_peer_gather_init": (i32, [vp, u32, u32, u64, vp, vp]),
         "ttkv_gpu_peer_gather_open": (i32, [vp, vp]),
         "ttkv_gpu_peer_gather_output": (i32, [vp, P(vp), P(i32)]),
+        "ttkv_gpu_peer_gather_close": (i32, [vp]),
         "ttkv_gpu_quantize_block": (i32, [i32, vp, vp, u64, u32, u32, u32, u32, vp, vp, vp, vp,
                                           vp]),
         "ttkv_gpu_append": (i32, [vp, vp, vp, u64, i32]),

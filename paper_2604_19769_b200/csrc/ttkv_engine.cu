@@ -1674,6 +1674,14 @@ int ttkv_gpu_peer_gather_open(ttkv_gpu* h, const void* handles) {
   return TTKV_OK;
 }
 
+int ttkv_gpu_peer_gather_close(ttkv_gpu* h) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  CU(h, cudaSetDevice(h->dev));
+  CU(h, cudaStreamSynchronize(h->s0));
+  free_peer_gather(h);
+  return TTKV_OK;
+}
+
 int ttkv_gpu_peer_gather_output(ttkv_gpu* h, double** device_rows, int* timed_out) {
   if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
   if (!h->pg.active) return set_err(h, TTKV_EERROR, "peer gather not active");

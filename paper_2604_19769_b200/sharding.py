@@ -108,7 +108,15 @@ class PeerGather:
         handles = [None] * plan.world
         dist.all_gather_object(handles, bytes(handle), group=group)
         blob = b"".join(handles)
-        _check(lib.ttkv_gpu_peer_gather_open(engine.handle, blob), engine.handle)
+        rc = lib.ttkv_gpu_peer_gather_open(engine.handle, blob)
+        # every rank must map every peer, or none may publish (a rank on the
+        # NCCL fallback would leave the others waiting for its rows)
+        oks = [None] * plan.world
+        dist.all_gather_object(oks, rc == 0, group=group)
+        if not all(oks):
+            lib.ttkv_gpu_peer_gather_close(engine.handle)
+            _check(rc, engine.handle)
+            raise RuntimeError("peer gather: a peer could not map the IPC buffers")
         self._C, self._np = C, np
 
     def device_ptr(self) -> int:
