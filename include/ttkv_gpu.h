@@ -204,7 +204,8 @@ int ttkv_gpu_eviction_pending(struct ttkv_gpu* h, int* pending);
 
 /* ---- state / cold path ------------------------------------------------------ */
 int ttkv_gpu_state(struct ttkv_gpu* h, ttkv_state* st);
-/* fetched_blocks of the last step for (stream, head), schedule order. */
+/* fetched_blocks of the last step for (stream, head), in select_top_k's
+ * schedule order (score desc, block id desc), from the step's fp64 scores. */
 int ttkv_gpu_read_fetched(struct ttkv_gpu* h, uint32_t stream, uint32_t head, uint64_t* out,
                           uint64_t cap, uint64_t* n);
 /* Slow block in the reference's QuantizedBlock layout (16-bit payloads as

@@ -227,7 +227,7 @@ struct ttkv_gpu {
   float* cent = nullptr;
   uint8_t* params = nullptr;  // HBM mirror of record params
   double* scores = nullptr;
-  uint32_t *sel = nullptr, *mask = nullptr, *uids = nullptr, *umask = nullptr, *ucount = nullptr;
+  uint32_t *mask = nullptr, *uids = nullptr, *umask = nullptr, *ucount = nullptr;
   unsigned long long* counters = nullptr;
   void* fpart = nullptr;
   void* spart = nullptr;
@@ -365,7 +365,7 @@ void free_all(ttkv_gpu* h) {
   auto F = [](void* p) {
     if (p) cudaFree(p);
   };
-  F(h->ring_k); F(h->ring_v); F(h->cent); F(h->params); F(h->scores); F(h->sel); F(h->mask); F(h->uids);
+  F(h->ring_k); F(h->ring_v); F(h->cent); F(h->params); F(h->scores); F(h->mask); F(h->uids);
   F(h->umask); F(h->ucount); F(h->counters); F(h->fpart); F(h->spart); F(h->q_dev);
   F(h->out_dev); F(h->kn_dev); F(h->vn_dev); F(h->stg_k); F(h->stg_v); F(h->stage_arena);
   if (h->arena_host) pinned_free(h->arena_host);
@@ -671,7 +671,6 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       SelectArgs a{};
       a.g = g;
       a.scores = h->scores;
-      a.sel = nullptr;  // the order is materialized by ttkv_gpu_read_fetched
       a.mask = h->mask;
       a.union_ids = h->uids;
       a.union_mask = h->umask;

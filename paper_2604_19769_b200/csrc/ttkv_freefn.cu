@@ -2,7 +2,7 @@
 // (the cold-path API surface of the drop-in; the hot path fuses these):
 //   dequantize_block  quantizer.cpp:90-113, 157-170  (bit-exact fp64 affine)
 //   score_block       relevance.cpp:19-27            (bit-exact fp64, unfused)
-//   select_top_k      relevance.cpp:29-43            (bitonic, total order)
+//   select_top_k      relevance.cpp:29-43            (bitonic sort, total order)
 #include <cuda_runtime.h>
 
 #include <algorithm>

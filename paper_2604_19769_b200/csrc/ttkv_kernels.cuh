@@ -10,7 +10,8 @@
 //           (quantizer.cpp:22-32), so a record is serialize_block's payload
 //           verbatim.  K8/V4, d=128, B=128: 16384+8192+1024+1024 = 26,624 B.
 //   params  [S][n_cap][used - kp_off] u8  HBM mirror of each record's params
-//   scores  [S][Gs][n_cap] f64, sel [S][Gs][n_cap] u32 (schedule order),
+//   scores  [S][Gs][n_cap] f64 (bit-exact; the fetched_blocks order is
+//           materialized from them on demand),
 //   union_ids / union_mask [S][n_cap] u32, union_count [S]
 //   partials [S][G][chunks][d_v + 2] f32  (acc[d_v], m (log2 units), l)
 #pragma once

@@ -52,7 +52,6 @@ cudaError_t launch_score(const ScoreArgs& a, cudaStream_t st);
 struct SelectArgs {
   Geometry g;
   const double* scores;
-  uint32_t* sel;          // [S][Gs][n_cap]
   uint32_t* mask;         // [S][n_cap] scratch
   uint32_t* union_ids;    // [S][n_cap]
   uint32_t* union_mask;   // [S][n_cap]
