@@ -174,6 +174,10 @@ int ttkv_gpu_prefill(struct ttkv_gpu* h, const void* keys, const void* values,
                      uint64_t n_tokens, int dtype);
 /* Device-generated N(0,1) tokens rounded to the ring type (perf runs). */
 int ttkv_gpu_prefill_synthetic(struct ttkv_gpu* h, uint64_t n_tokens, uint64_t seed);
+/* Engine::prefill (engine.cpp:15-20) from DEVICE memory: keys [S][n][d_k],
+ * values [S][n][d_v] (f32 or f16) read in place on the handle's stream. */
+int ttkv_gpu_prefill_device(struct ttkv_gpu* h, const void* keys, const void* values,
+                            uint64_t n_tokens, int dtype);
 
 /* Host buffers, synchronous: q[S][G][d_k] f32, k_new[S][d_k], v_new[S][d_v]
  * (dtype), out[S][G][d_v] f64 (DecodeStepReport::output is double; values are

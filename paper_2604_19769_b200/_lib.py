@@ -66,6 +66,7 @@ EXPORTS = [
     "ttkv_gpu_create", "ttkv_gpu_destroy", "ttkv_gpu_last_error", "ttkv_last_error",
     "ttkv_abi_version", "ttkv_device_count", "ttkv_gpu_set_stream", "ttkv_gpu_get_stream",
     "ttkv_gpu_synchronize", "ttkv_gpu_prefill", "ttkv_gpu_prefill_synthetic",
+    "ttkv_gpu_prefill_device",
     "ttkv_gpu_decode_step", "ttkv_gpu_decode_step_device", "ttkv_gpu_read_step_counters",
     "ttkv_gpu_state", "ttkv_gpu_read_fetched", "ttkv_gpu_read_block", "ttkv_gpu_serialize_block",
     "ttkv_gpu_dump_slow_tier", "ttkv_gpu_restore_slow_tier", "ttkv_gpu_read_fast", "ttkv_gpu_locate", "ttkv_gpu_set_timing",
@@ -105,6 +106,7 @@ def lib():
         "ttkv_gpu_synchronize": (i32, [vp]),
         "ttkv_gpu_prefill": (i32, [vp, vp, vp, u64, i32]),
         "ttkv_gpu_prefill_synthetic": (i32, [vp, u64, u64]),
+        "ttkv_gpu_prefill_device": (i32, [vp, vp, vp, u64, i32]),
         "ttkv_gpu_decode_step": (i32, [vp, vp, vp, vp, i32, vp, P(StepReportC)]),
         "ttkv_gpu_decode_step_device": (i32, [vp, vp, vp, vp, i32, vp, P(StepReportC)]),
         "ttkv_gpu_read_step_counters": (i32, [vp, P(u64), P(u64)]),

@@ -507,7 +507,9 @@ int settle_evictions(ttkv_gpu* h, bool* evicted) {
 }
 
 // Bulk prefill of P tokens already on the device (staging layout [S][P][d]).
-int prefill_chunk(ttkv_gpu* h, const void* in_k, const void* in_v, int in_dtype, uint64_t P) {
+int prefill_chunk(ttkv_gpu* h, const void* in_k, const void* in_v, int in_dtype, uint64_t P,
+                  uint64_t stride = 0) {
+  if (!stride) stride = P;  // tokens between consecutive streams' rows
   const uint64_t A = h->appended, total = A + P, B = h->g.B;
   uint64_t nb_after = h->n_slow;
   if (total > h->l_fast) nb_after = std::max<uint64_t>(nb_after, (total - h->l_fast - 1) / B + 1);
@@ -520,7 +522,7 @@ int prefill_chunk(ttkv_gpu* h, const void* in_k, const void* in_v, int in_dtype,
     a.ring_v = h->ring_v;
     a.in_k = in_k;
     a.in_v = in_v;
-    a.in_tokens = P;
+    a.in_tokens = stride;
     a.split_pos = A;
     a.first_block = h->n_slow;
     a.arena = h->arena_dev;
@@ -535,7 +537,7 @@ int prefill_chunk(ttkv_gpu* h, const void* in_k, const void* in_v, int in_dtype,
     const uint8_t* kb = static_cast<const uint8_t*>(in_k) + (start - A) * h->g.d_k * esz;
     const uint8_t* vb = static_cast<const uint8_t*>(in_v) + (start - A) * h->g.d_v * esz;
     KTimer t(h, K_APPEND, h->s0);
-    CU(h, launch_append(h->g, h->ring_k, h->ring_v, kb, vb, in_dtype, start, P, total - start,
+    CU(h, launch_append(h->g, h->ring_k, h->ring_v, kb, vb, in_dtype, start, stride, total - start,
                         h->s0));
   }
   h->appended = total;
@@ -1046,6 +1048,34 @@ int ttkv_gpu_prefill(ttkv_gpu* h, const void* keys, const void* values, uint64_t
                             static_cast<const uint8_t*>(values) + t0 * g.d_v * esz,
                             n * g.d_v * esz, m * g.d_v * esz, g.S, cudaMemcpyHostToDevice, h->s0));
     rc = prefill_chunk(h, h->stg_k, h->stg_v, dtype == TTKV_DTYPE_F16 ? kInF16 : kInF32, m);
+    if (rc) return rc;
+  }
+  CU(h, cudaStreamSynchronize(h->s0));
+  return TTKV_OK;
+}
+
+// Engine::prefill from device memory (the model's prefill leaves K/V on the
+// GPU): keys/values [S][n][d] of the ring or f32 type, read in place -- no
+// staging copy; records are quantized straight from the caller's rows.
+// Enqueued on the handle's stream; returns after it completes.
+int ttkv_gpu_prefill_device(ttkv_gpu* h, const void* keys, const void* values, uint64_t n,
+                            int dtype) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  if (n == 0) return TTKV_OK;
+  if (!keys || !values) return set_err(h, TTKV_EINVAL, "null key/value pointer");
+  if (dtype != TTKV_DTYPE_F32 && dtype != TTKV_DTYPE_F16)
+    return set_err(h, TTKV_ESHAPE, "prefill: unknown dtype");
+  CU(h, cudaSetDevice(h->dev));
+  const int in_dt = dtype == TTKV_DTYPE_F16 ? kInF16 : kInF32;
+  // one chunk of the caller's tokens at a time keeps each launch's grid and
+  // the ring tail bounded; rows are addressed with the caller's stride n
+  const uint64_t P = std::max<uint64_t>(prefill_chunk_tokens(h), h->g.B);
+  const size_t esz = dtype == TTKV_DTYPE_F16 ? 2 : 4;
+  for (uint64_t t0 = 0; t0 < n; t0 += P) {
+    const uint64_t m = std::min<uint64_t>(P, n - t0);
+    int rc = prefill_chunk(h, static_cast<const uint8_t*>(keys) + t0 * h->g.d_k * esz,
+                           static_cast<const uint8_t*>(values) + t0 * h->g.d_v * esz, in_dt, m,
+                           n);
     if (rc) return rc;
   }
   CU(h, cudaStreamSynchronize(h->s0));

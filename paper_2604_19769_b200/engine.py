@@ -231,6 +231,11 @@ class MultiStreamEngine:
             raise ShapeError("prefill: key/value dimension mismatch")
         _check(self._lib.ttkv_gpu_prefill(self._h, _ptr(k), _ptr(v), k.shape[1], dt), self._h)
 
+    def prefill_device(self, k_ptr: int, v_ptr: int, n_tokens: int, dtype: int = L.DTYPE_F16):
+        """Prefill from device rows [S][n][d] (e.g. torch tensors' data_ptr())."""
+        _check(self._lib.ttkv_gpu_prefill_device(self._h, C.c_void_p(k_ptr), C.c_void_p(v_ptr),
+                                                 n_tokens, dtype), self._h)
+
     def prefill_synthetic(self, n_tokens: int, seed: int = 0):
         _check(self._lib.ttkv_gpu_prefill_synthetic(self._h, n_tokens, seed), self._h)
 

@@ -497,3 +497,34 @@ def test_full_size_cfg2_sampled_streams(gpu, slow_tier):
     assert rep.union_blocks == union
     assert rep.pcie_bytes == union * eng.state()["payload_bytes"]
     eng.close()
+
+
+@pytest.mark.parametrize("dtype", ["f16", "f32"])
+def test_prefill_from_device_memory(gpu, dtype):
+    # ttkv_gpu_prefill_device reads the caller's [S][n][d] device rows in
+    # place; records, fast tier and the next decode equal a host prefill's
+    import torch
+    T_ = gpu
+    S, G, d, B, lf, ctx = 3, 2, 128, 128, 512, 5000
+    cfg = T_.TierConfig(hbm_budget_bytes=lf * 2 * d * 2, d_k=d, d_v=d, block_size=B)
+    rng = np.random.default_rng(4)
+    pk = O.fp16_round(rng.standard_normal((S, ctx, d)))
+    pv = O.fp16_round(rng.standard_normal((S, ctx, d)))
+    host = T_.MultiStreamEngine(cfg, n_streams=S, heads_per_stream=G)
+    host.prefill(pk, pv)
+    dev = T_.MultiStreamEngine(cfg, n_streams=S, heads_per_stream=G)
+    tdt = torch.float16 if dtype == "f16" else torch.float32
+    tk = torch.from_numpy(pk).to("cuda", tdt).contiguous()
+    tv = torch.from_numpy(pv).to("cuda", tdt).contiguous()
+    dev.prefill_device(tk.data_ptr(), tv.data_ptr(), ctx, 1 if dtype == "f16" else 0)
+    assert dev.state()["slow_blocks"] == host.state()["slow_blocks"]
+    assert dev.state()["fast_tokens"] == host.state()["fast_tokens"]
+    for s in range(S):
+        for b in range(host.state()["slow_blocks"]):
+            assert dev.serialize_block(s, b) == host.serialize_block(s, b)
+    q = rng.standard_normal((S, G, d)).astype(np.float32)
+    kn = O.fp16_round(rng.standard_normal((S, d)))
+    vn = O.fp16_round(rng.standard_normal((S, d)))
+    assert np.array_equal(dev.decode_step(q, kn, vn).output, host.decode_step(q, kn, vn).output)
+    host.close()
+    dev.close()
