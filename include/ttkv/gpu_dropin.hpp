@@ -286,11 +286,19 @@ class TierStore {
   std::size_t appended_count() const;
   std::size_t l_fast_capacity() const { return l_fast_; }
 
-  ttkv_gpu* handle() const { return h_; }
+  // the device handle, with every buffered append applied
+  ttkv_gpu* handle() const {
+    flush();
+    return h_;
+  }
   void note_decode_step(std::size_t evicted_blocks);  // Engine bookkeeping
 
  private:
-  ttkv_state state() const;
+  ttkv_state state() const;  // applies buffered appends first
+  // device bookkeeping + buffered appends, without touching the device
+  std::size_t appended_now() const;
+  std::size_t fast_now() const;
+  void flush() const;
   void invalidate() { fast_valid_ = false; }
 
   TierConfig config_;
@@ -300,6 +308,11 @@ class TierStore {
   mutable std::deque<TokenKV> fast_view_;
   mutable bool fast_valid_ = false;
   mutable std::vector<QuantizedBlock> slow_view_;  // append-only cache
+  // append_token buffers tokens on the host and hands them to the device in
+  // one ttkv_gpu_append when something reads the ring (a GPU round trip per
+  // token otherwise dominates token-at-a-time callers)
+  mutable std::vector<float> pend_k_, pend_v_;
+  mutable std::size_t pend_n_ = 0;
 };
 
 // ---- two-lane timing model (reference sim.hpp; implemented in ttkv_sim.cpp) --------

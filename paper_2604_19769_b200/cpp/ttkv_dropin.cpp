@@ -431,8 +431,10 @@ TierStore::~TierStore() {
 TierStore::TierStore(TierStore&& o) noexcept
     : config_(std::move(o.config_)), l_fast_(o.l_fast_), h_(o.h_), index_(std::move(o.index_)),
       fast_view_(std::move(o.fast_view_)), fast_valid_(o.fast_valid_),
-      slow_view_(std::move(o.slow_view_)) {
+      slow_view_(std::move(o.slow_view_)), pend_k_(std::move(o.pend_k_)),
+      pend_v_(std::move(o.pend_v_)), pend_n_(o.pend_n_) {
   o.h_ = nullptr;
+  o.pend_n_ = 0;
 }
 
 TierStore& TierStore::operator=(TierStore&& o) noexcept {
@@ -445,42 +447,74 @@ TierStore& TierStore::operator=(TierStore&& o) noexcept {
     fast_view_ = std::move(o.fast_view_);
     fast_valid_ = o.fast_valid_;
     slow_view_ = std::move(o.slow_view_);
+    pend_k_ = std::move(o.pend_k_);
+    pend_v_ = std::move(o.pend_v_);
+    pend_n_ = o.pend_n_;
     o.h_ = nullptr;
+    o.pend_n_ = 0;
   }
   return *this;
 }
 
+void TierStore::flush() const {
+  if (!pend_n_) return;
+  const std::size_t n = pend_n_;
+  pend_n_ = 0;  // the device owns the tokens now (or the append failed and threw)
+  check(ttkv_gpu_append(h_, pend_k_.data(), pend_v_.data(), n, TTKV_DTYPE_F32), h_);
+  pend_k_.clear();
+  pend_v_.clear();
+}
+
+std::size_t TierStore::appended_now() const {
+  ttkv_state st{};
+  check(ttkv_gpu_state(h_, &st), h_);  // host-side bookkeeping, no device work
+  return st.appended + pend_n_;
+}
+
+std::size_t TierStore::fast_now() const {
+  ttkv_state st{};
+  check(ttkv_gpu_state(h_, &st), h_);
+  return st.fast_tokens + pend_n_;
+}
+
 ttkv_state TierStore::state() const {
+  flush();
   ttkv_state st{};
   check(ttkv_gpu_state(h_, &st), h_);
   return st;
 }
 
 std::vector<CacheEvent> TierStore::append_token(TokenKV kv) {
-  const ttkv_state st = state();
-  if (kv.position != st.appended)
-    throw SequencingError("append_token: expected position " + std::to_string(st.appended) +
+  const std::size_t appended = appended_now(), fast_before = fast_now();
+  if (kv.position != appended)
+    throw SequencingError("append_token: expected position " + std::to_string(appended) +
                           ", got " + std::to_string(kv.position));
   if (kv.key.size() != config_.d_k || kv.value.size() != config_.d_v)
     throw ShapeError("append_token: key/value dimension mismatch");
-  check(ttkv_gpu_append(h_, kv.key.data(), kv.value.data(), 1, TTKV_DTYPE_F32), h_);
+  if (fast_before + 1 > l_fast_ + config_.block_size || pend_n_ >= 4096) {
+    // the ring bound (or a full buffer): hand over now, so an overflow is
+    // reported by this append as before
+    flush();
+    check(ttkv_gpu_append(h_, kv.key.data(), kv.value.data(), 1, TTKV_DTYPE_F32), h_);
+  } else {
+    pend_k_.insert(pend_k_.end(), kv.key.begin(), kv.key.end());
+    pend_v_.insert(pend_v_.end(), kv.value.begin(), kv.value.end());
+    ++pend_n_;
+  }
   invalidate();
   std::vector<CacheEvent> events;
-  const std::size_t fast = st.fast_tokens + 1;
+  const std::size_t fast = fast_before + 1;
   if (fast > l_fast_) {
-    const Position first = st.appended + 1 - fast;
+    const Position first = appended + 1 - fast;
     events.push_back({CacheEvent::Type::EvictBlock, first, first + config_.block_size - 1});
   }
   return events;
 }
 
-bool TierStore::eviction_pending() const {
-  int p = 0;
-  check(ttkv_gpu_eviction_pending(h_, &p), h_);
-  return p != 0;
-}
+bool TierStore::eviction_pending() const { return fast_now() > l_fast_; }
 
 BlockId TierStore::evict_and_compress() {
+  flush();
   std::uint64_t id = 0;
   check(ttkv_gpu_evict(h_, &id), h_);
   index_.append_block(id, id * config_.block_size, id * config_.block_size + config_.block_size - 1);
@@ -497,9 +531,9 @@ void TierStore::note_decode_step(std::size_t) {
 }
 
 Location TierStore::locate(Position p) const {
-  const ttkv_state st = state();
-  if (p >= st.appended) return Location::absent();
-  if (st.fast_tokens > 0 && p >= st.appended - st.fast_tokens) return Location::fast();
+  const std::size_t appended = appended_now(), fast = fast_now();
+  if (p >= appended) return Location::absent();
+  if (fast > 0 && p >= appended - fast) return Location::fast();
   if (auto id = index_.find(p)) return Location::slow(*id);
   return Location::absent();
 }
@@ -559,11 +593,13 @@ const std::vector<QuantizedBlock>& TierStore::slow_blocks() const {
   return slow_view_;
 }
 
-std::size_t TierStore::fast_token_count() const { return state().fast_tokens; }
+std::size_t TierStore::fast_token_count() const { return fast_now(); }
 std::size_t TierStore::slow_token_count() const {
-  return state().slow_blocks * config_.block_size;
+  ttkv_state st{};
+  check(ttkv_gpu_state(h_, &st), h_);
+  return st.slow_blocks * config_.block_size;
 }
-std::size_t TierStore::appended_count() const { return state().appended; }
+std::size_t TierStore::appended_count() const { return appended_now(); }
 
 // ---- workload generator ------------------------------------------------------------------
 double detail::GaussianSource::next() {

@@ -1760,12 +1760,7 @@ int ttkv_gpu_quantize_block(int device, const float* keys, const float* values, 
   if (e != cudaSuccess) return set_err(nullptr, TTKV_ECUDA, cudaGetErrorString(e));
   float *dk = nullptr, *dv = nullptr, *dc = nullptr;
   uint8_t* dr = nullptr;
-  auto cleanup = [&]() {
-    if (dk) cudaFree(dk);
-    if (dv) cudaFree(dv);
-    if (dc) cudaFree(dc);
-    if (dr) cudaFree(dr);
-  };
+  auto cleanup = [&]() {};  // scratch slots persist (ttkv_dev::scratch)
 #define QCU(call)                                                          \
   do {                                                                     \
     cudaError_t e__ = (call);                                              \
@@ -1774,10 +1769,14 @@ int ttkv_gpu_quantize_block(int device, const float* keys, const float* values, 
       return set_err(nullptr, TTKV_ECUDA, cudaGetErrorString(e__));        \
     }                                                                      \
   } while (0)
-  QCU(cudaMalloc((void**)&dk, rows * d_k * 4));
-  QCU(cudaMalloc((void**)&dv, rows * d_v * 4));
-  QCU(cudaMalloc((void**)&dc, d_k * 4));
-  QCU(cudaMalloc((void**)&dr, g.rec.stride));
+  {
+    cudaError_t se = cudaSuccess;
+    dk = static_cast<float*>(scratch(0, rows * d_k * 4, &se));
+    if (se == cudaSuccess) dv = static_cast<float*>(scratch(1, rows * d_v * 4, &se));
+    if (se == cudaSuccess) dc = static_cast<float*>(scratch(2, d_k * 4, &se));
+    if (se == cudaSuccess) dr = static_cast<uint8_t*>(scratch(3, g.rec.stride, &se));
+    QCU(se);
+  }
   QCU(cudaMemcpy(dk, keys, rows * d_k * 4, cudaMemcpyHostToDevice));
   QCU(cudaMemcpy(dv, values, rows * d_v * 4, cudaMemcpyHostToDevice));
   EvictArgs a{};

@@ -80,17 +80,51 @@ __global__ void topk_free_kernel(const double* scores, const uint64_t* ids, uint
   for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) out[i] = id[i];
 }
 
+// Thread-local, grow-only device scratch for the stateless entry points:
+// token-at-a-time callers (10^4 quantize_block / dequantize_block calls in the
+// reference's acceptance gate) were dominated by a cudaMalloc + cudaFree pair
+// per buffer per call, each free an implicit device synchronization.  Slots
+// are reused across calls (every entry point is synchronous) and live for the
+// thread.
+void* scratch(int slot, size_t bytes, cudaError_t* err) {
+  struct Pool {
+    int dev = -1;
+    void* p[8] = {};
+    size_t cap[8] = {};
+  };
+  thread_local Pool pool;
+  int dev = 0;
+  *err = cudaGetDevice(&dev);
+  if (*err != cudaSuccess) return nullptr;
+  if (pool.dev != dev) pool = Pool{dev};  // another device: start over (old blocks stay)
+  bytes = bytes ? bytes : 16;
+  if (pool.cap[slot] < bytes) {
+    const size_t want = std::max(bytes, 2 * pool.cap[slot]);
+    if (pool.p[slot]) cudaFree(pool.p[slot]);
+    pool.p[slot] = nullptr;
+    pool.cap[slot] = 0;
+    *err = cudaMalloc(&pool.p[slot], want);
+    if (*err != cudaSuccess) return nullptr;
+    pool.cap[slot] = want;
+  }
+  return pool.p[slot];
+}
+
 }  // namespace ttkv_dev
 
 namespace {
 
 
+// A slot of the thread-local scratch pool (ttkv_dev::scratch).
 struct DevBuf {
+  int slot;
   void* p = nullptr;
-  ~DevBuf() {
-    if (p) cudaFree(p);
+  explicit DevBuf(int s) : slot(s) {}
+  cudaError_t alloc(size_t n) {
+    cudaError_t e = cudaSuccess;
+    p = ttkv_dev::scratch(slot, n, &e);
+    return e;
   }
-  cudaError_t alloc(size_t n) { return cudaMalloc(&p, n ? n : 16); }
 };
 
 int fail(cudaError_t e) {
@@ -124,7 +158,7 @@ int ttkv_gpu_dequantize_block(int device, const uint8_t* packed_k, const uint8_t
     const uint32_t dim = t ? d_v : d_k, bits = t ? vb : kb;
     float* out = t ? values : keys;
     if (!out || rows * dim == 0) continue;
-    DevBuf dp, dpar, dout;
+    DevBuf dp(0), dpar(1), dout(2);
     const size_t nb = bytes(rows * dim, bits);
     FCU(dp.alloc(nb + 8));
     FCU(cudaMemset(dp.p, 0, nb + 8));
@@ -146,7 +180,7 @@ int ttkv_gpu_score_blocks(int device, const float* query, const float* centroids
   if (n == 0) return TTKV_OK;
   if (!query || !centroids || !scores) return TTKV_EINVAL;
   FCU(cudaSetDevice(device));
-  DevBuf dq, dc, ds;
+  DevBuf dq(0), dc(1), ds(2);
   FCU(dq.alloc(d * 4));
   FCU(dc.alloc(n * d * 4));
   FCU(ds.alloc(n * 8));
@@ -171,7 +205,7 @@ int ttkv_gpu_select_top_k(int device, const double* scores, const uint64_t* ids,
   FCU(cudaSetDevice(device));
   uint32_t N2 = 2;
   while (N2 < n) N2 <<= 1;
-  DevBuf ds, di, dout;
+  DevBuf ds(0), di(1), dout(2);
   FCU(ds.alloc(n * 8));
   FCU(di.alloc(n * 8));
   FCU(dout.alloc(k * 8));

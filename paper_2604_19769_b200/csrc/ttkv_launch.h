@@ -14,6 +14,8 @@ constexpr int kInF16 = 1;
 
 // thread-local message behind ttkv_last_error() (defined in ttkv_engine.cu)
 void set_last_error(const char* msg);
+// thread-local grow-only device scratch, slot < 8 (ttkv_freefn.cu)
+void* scratch(int slot, size_t bytes, cudaError_t* err);
 
 struct EvictArgs {
   Geometry g;
