@@ -450,7 +450,9 @@ int ensure_blocks(ttkv_gpu* h, uint64_t need) {
     CU(h, realloc_dev((void**)&h->stage_arena, arena_bytes));
   }
   uint8_t* attn_arena = h->opt.serial_schedule ? h->stage_arena : h->arena_dev;
-  if (h->slow_tc && make_arena_tmaps(h->g, attn_arena, h->stc) != cudaSuccess)
+  // TMA record coordinates are int32: very large handles use the CUDA-core tier
+  if (h->slow_tc && (S * cap >= (1ull << 31) ||
+                     make_arena_tmaps(h->g, attn_arena, h->stc) != cudaSuccess))
     h->slow_tc = false;  // fall back to the CUDA-core slow tier
   return TTKV_OK;
 }
@@ -921,7 +923,8 @@ int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* po
   h->acc = g.elem == 4 ? 8 : 4;
   {
     const char* tc_env = std::getenv("TTKV_FAST_TC");
-    h->fast_tc = fast_tc_supported(g) && !(tc_env && tc_env[0] == '0');
+    h->fast_tc = fast_tc_supported(g) && !(tc_env && tc_env[0] == '0') &&
+                 (uint64_t)g.S * g.C < (1ull << 31);  // int32 TMA row coordinates
     // tensor-core slow tier: HBM-resident records (the CUDA-core consumer has
     // 3x headroom over the PCIe link); TTKV_SLOW_TC=1/0 forces it on/off
     const char* stc_env = std::getenv("TTKV_SLOW_TC");
