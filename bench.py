@@ -516,6 +516,18 @@ def run_ours(args):
 GROWTH_POINTS = (131072, 163840, 196608, 229376, 262144)
 
 
+def growth_ms_per_step(curve):
+    """Mean ms/step of generating every token between the first and the last
+    sampled context: the trapezoid integral of ms/step over the context
+    divided by the tokens generated (one point: its own ms/step)."""
+    if len(curve) == 1:
+        return curve[0]["ms_per_step"]
+    xs = [c["ctx_start"] for c in curve]
+    ys = [c["ms_per_step"] for c in curve]
+    total_ms = sum((xs[i + 1] - xs[i]) * (ys[i] + ys[i + 1]) / 2 for i in range(len(xs) - 1))
+    return total_ms / (xs[-1] - xs[0])
+
+
 def run_growth(args):
     """cfg5 (BASELINE configs[4]): sustained generation 128K -> 256K.
 
@@ -622,14 +634,7 @@ def run_growth(args):
                           "slow_kernel_ms": kt["ms_slow"] / max(1, kt["n_slow"]),
                           "union_blocks": union_last})
 
-    # sustained rate over the growth: integrate ms/step(ctx) (trapezoid)
-    if len(curve) > 1:
-        xs = [c["ctx_start"] for c in curve]
-        ys = [c["ms_per_step"] for c in curve]
-        total_ms = sum((xs[i + 1] - xs[i]) * (ys[i] + ys[i + 1]) / 2 for i in range(len(xs) - 1))
-        ms_step = total_ms / (xs[-1] - xs[0])
-    else:
-        ms_step = curve[0]["ms_per_step"]
+    ms_step = growth_ms_per_step(curve)
     value = 1000.0 / ms_step
 
     # e2e through the C ABI with host buffers, at the last (256K) point
