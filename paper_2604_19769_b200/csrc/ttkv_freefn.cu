@@ -39,9 +39,9 @@ __global__ void score_free_kernel(const float* q, const float* cent, uint64_t n,
                                   double* out) {
   for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < n;
        b += (uint64_t)gridDim.x * blockDim.x) {
+    // exact products of float-valued doubles: one fma == mul + add (see score_kernel)
     double acc = 0.0;
-    for (uint32_t i = 0; i < d; ++i)
-      acc = __dadd_rn(acc, __dmul_rn((double)q[i], (double)cent[b * d + i]));
+    for (uint32_t i = 0; i < d; ++i) acc = __fma_rn((double)q[i], (double)cent[b * d + i], acc);
     out[b] = acc;
   }
 }

@@ -29,8 +29,11 @@ __global__ void __launch_bounds__(128) score_kernel(ScoreArgs a) {
   const uint32_t b0 = blockIdx.x * kScoreTile;
   extern __shared__ __align__(16) uint8_t smem[];
   double* qs = reinterpret_cast<double*>(smem);                 // [Gs][d_k]
-  float* ct = reinterpret_cast<float*>(qs + g.Gs * g.d_k);      // [tile][d_k + 1]
-  const uint32_t pitch = g.d_k + 1;
+  float* ct = reinterpret_cast<float*>(qs + g.Gs * g.d_k);      // [tile][pitch]
+  // d_k % 4 == 0: 16-byte rows (pitch d_k + 4 keeps 8-lane phases on distinct
+  // banks); otherwise d_k + 1
+  const bool vec = (g.d_k & 3u) == 0;
+  const uint32_t pitch = vec ? g.d_k + 4 : g.d_k + 1;
 
   for (uint32_t i = threadIdx.x; i < g.Gs * g.d_k; i += blockDim.x) {
     const uint32_t h = i / g.d_k, c = i % g.d_k;
@@ -63,8 +66,7 @@ __global__ void __launch_bounds__(128) score_kernel(ScoreArgs a) {
         const uint32_t i = i0 + u * blockDim.x;
         if (i < n4) {
           const uint32_t r = 4 * i / g.d_k, c = 4 * i % g.d_k;
-          float* d = ct + r * pitch + c;
-          d[0] = v[u].x; d[1] = v[u].y; d[2] = v[u].z; d[3] = v[u].w;
+          *reinterpret_cast<float4*>(ct + r * pitch + c) = v[u];
         }
       }
     }
@@ -81,15 +83,31 @@ __global__ void __launch_bounds__(128) score_kernel(ScoreArgs a) {
     if (b0 + r >= a.n) continue;
     const double* qh = qs + h * g.d_k;
     const float* cr = ct + r * pitch;
+    // s += double(q_i) * c_i, sequential in i (relevance.cpp:23-26).  The
+    // product of two float-valued doubles has <= 48 significant bits, so the
+    // reference's separate multiply is exact and RN(s + q_i c_i) is exactly
+    // one fused multiply-add: bit-identical, half the fp64 instructions.
     double acc = 0.0;
-    for (uint32_t c = 0; c < g.d_k; ++c) acc = __dadd_rn(acc, __dmul_rn(qh[c], (double)cr[c]));
+    if (vec) {
+      for (uint32_t c = 0; c < g.d_k; c += 4) {
+        const float4 cv = *reinterpret_cast<const float4*>(cr + c);
+        const double2 q01 = *reinterpret_cast<const double2*>(qh + c);
+        const double2 q23 = *reinterpret_cast<const double2*>(qh + c + 2);
+        acc = __fma_rn(q01.x, (double)cv.x, acc);
+        acc = __fma_rn(q01.y, (double)cv.y, acc);
+        acc = __fma_rn(q23.x, (double)cv.z, acc);
+        acc = __fma_rn(q23.y, (double)cv.w, acc);
+      }
+    } else {
+      for (uint32_t c = 0; c < g.d_k; ++c) acc = __fma_rn(qh[c], (double)cr[c], acc);
+    }
     a.scores[((uint64_t)s * g.Gs + h) * g.n_cap + b0 + r] = acc;
   }
 }
 
 cudaError_t launch_score(const ScoreArgs& a, cudaStream_t st) {
   if (a.n == 0) return cudaSuccess;
-  const size_t smem = (size_t)a.g.Gs * a.g.d_k * 8 + (size_t)kScoreTile * (a.g.d_k + 1) * 4;
+  const size_t smem = (size_t)a.g.Gs * a.g.d_k * 8 + (size_t)kScoreTile * (a.g.d_k + 4) * 4;
   cudaError_t e = cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
