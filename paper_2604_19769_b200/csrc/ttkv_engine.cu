@@ -651,11 +651,16 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
   uint32_t CH = 4;
   bool slow = n > 0 && k > 0;
   CU(h, cudaMemsetAsync(h->counters, 0, sizeof(unsigned long long) * 4, h->s0));
-  // HBM-resident slow tier: fork the (low-priority) fast tier before score +
-  // select so it fills the SMs they leave idle (cfg3 shape: 6.33 -> 5.66 ms
-  // per step).  With the slow tier in host DRAM the PCIe stream is the
-  // critical path and the fork stays after select.
-  const bool early_fork = h->opt.slow_tier == TTKV_SLOW_DEVICE && !h->opt.serial_schedule;
+  // The fast tier (low priority, s1) is forked after select: score and
+  // select are short, latency-bound kernels that should not wait for SM slots
+  // held by long fast-tier CTAs, and the PCIe stream (host tier) or the record
+  // stream (HBM tier) is the critical path after them (HBM cfg2: 1.289 ms/step
+  // forked late vs 1.338 forked at the step start; cfg3 equal).
+  static const int fork_env = [] {  // TTKV_FORK=early|late overrides (measurement)
+    const char* e = std::getenv("TTKV_FORK");
+    return e ? (std::strcmp(e, "early") == 0 ? 1 : 0) + (std::strcmp(e, "late") == 0 ? 2 : 0) : 0;
+  }();
+  const bool early_fork = fork_env == 1;
   if (early_fork) {
     if (int rcf = fork_fast()) return rcf;
   }
