@@ -528,3 +528,10 @@ def test_prefill_from_device_memory(gpu, dtype):
     assert np.array_equal(dev.decode_step(q, kn, vn).output, host.decode_step(q, kn, vn).output)
     host.close()
     dev.close()
+
+
+@pytest.mark.parametrize("slow_tier", [0, 1])
+def test_engine_d64_tensor_core_fast_tier(gpu, slow_tier):
+    # d = 64, B = 64: the tensor-core fast tier with one 64-channel box (ND = 1);
+    # the slow tier takes the CUDA-core kernel (host DRAM or HBM)
+    run_parity(gpu, S=3, G=4, d=64, B=64, l_fast=256, ctx=3000, steps=4, slow_tier=slow_tier)
