@@ -228,7 +228,7 @@ struct ttkv_gpu {
   uint8_t* params = nullptr;  // HBM mirror of record params
   double* scores = nullptr;
   uint32_t *mask = nullptr, *uids = nullptr, *umask = nullptr, *ucount = nullptr;
-  unsigned long long* counters = nullptr;
+  uint32_t* h_ucount = nullptr;  // pinned copy of union_count for the step report
   void* fpart = nullptr;
   void* spart = nullptr;
   uint64_t spart_chunks = 0;
@@ -366,7 +366,7 @@ void free_all(ttkv_gpu* h) {
     if (p) cudaFree(p);
   };
   F(h->ring_k); F(h->ring_v); F(h->cent); F(h->params); F(h->scores); F(h->mask); F(h->uids);
-  F(h->umask); F(h->ucount); F(h->counters); F(h->fpart); F(h->spart); F(h->q_dev);
+  F(h->umask); F(h->ucount); F(h->fpart); F(h->spart); F(h->q_dev);
   F(h->out_dev); F(h->kn_dev); F(h->vn_dev); F(h->stg_k); F(h->stg_v); F(h->stage_arena);
   if (h->arena_host) pinned_free(h->arena_host);
   else if (h->arena_dev) cudaFree(h->arena_dev);
@@ -374,6 +374,7 @@ void free_all(ttkv_gpu* h) {
   pinned_free(h->h_out);
   pinned_free(h->h_k);
   pinned_free(h->h_v);
+  pinned_free(h->h_ucount);
   for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : h->pool) cudaEventDestroy(e);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
@@ -650,7 +651,6 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
 
   uint32_t CH = 4;
   bool slow = n > 0 && k > 0;
-  CU(h, cudaMemsetAsync(h->counters, 0, sizeof(unsigned long long) * 4, h->s0));
   // The fast tier (low priority, s1) is forked after select: score and
   // select are short, latency-bound kernels that should not wait for SM slots
   // held by long fast-tier CTAs, and the PCIe stream (host tier) or the record
@@ -684,7 +684,6 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       a.union_ids = h->uids;
       a.union_mask = h->umask;
       a.union_count = h->ucount;
-      a.counters = h->counters;
       a.n = (uint32_t)n;
       a.k = (uint32_t)k;
       KTimer t(h, K_SELECT, h->s0, 2);  // sort + union kernels
@@ -976,7 +975,7 @@ int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* po
   }
   CREATE_CU(cudaMalloc((void**)&h->ucount, S * sizeof(uint32_t)));
   CREATE_CU(cudaMemset(h->ucount, 0, S * sizeof(uint32_t)));
-  CREATE_CU(cudaMalloc((void**)&h->counters, 4 * sizeof(unsigned long long)));
+  CREATE_CU(pinned_alloc((void**)&h->h_ucount, S * sizeof(uint32_t)));
   CREATE_CU(cudaMalloc((void**)&h->fpart, S * g.G * h->nfc_cap * (g.d_v + 2) * h->acc));
   CREATE_CU(cudaMalloc((void**)&h->q_dev, S * g.G * g.d_k * sizeof(float)));
   CREATE_CU(cudaMalloc((void**)&h->out_dev, S * g.G * g.d_v * sizeof(double)));
@@ -1200,25 +1199,35 @@ int ttkv_gpu_decode_step(ttkv_gpu* h, const float* q, const void* kn, const void
                        dtype == TTKV_DTYPE_F16 ? kInF16 : kInF32, h->out_dev, rep);
   if (rc) return rc;
   CU(h, cudaMemcpyAsync(h->h_out, h->out_dev, ob, cudaMemcpyDeviceToHost, h->s0));
-  unsigned long long ctr[4] = {};
-  CU(h, cudaMemcpyAsync(ctr, h->counters, sizeof(ctr), cudaMemcpyDeviceToHost, h->s0));
+  if (h->last_k)
+    CU(h, cudaMemcpyAsync(h->h_ucount, h->ucount, g.S * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                          h->s0));
   CU(h, cudaStreamSynchronize(h->s0));
   std::memcpy(out, h->h_out, ob);
   if (rep) {
-    rep->union_blocks = ctr[0];
-    rep->pcie_bytes = ctr[0] * (uint64_t)h->g.rec.kp_off;
+    uint64_t u = 0;
+    if (h->last_k)
+      for (uint32_t i = 0; i < g.S; ++i) u += h->h_ucount[i];
+    rep->union_blocks = u;
+    rep->pcie_bytes = u * (uint64_t)h->g.rec.kp_off;
   }
   return TTKV_OK;
 }
 
+// Records streamed by the last step: the sum of the per-stream union sizes
+// (read on demand; the hot path keeps no global counter).
 int ttkv_gpu_read_step_counters(ttkv_gpu* h, uint64_t* union_blocks, uint64_t* pcie_bytes) {
   if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
-  unsigned long long ctr[4] = {};
-  CU(h, cudaSetDevice(h->dev));
-  CU(h, cudaMemcpyAsync(ctr, h->counters, sizeof(ctr), cudaMemcpyDeviceToHost, h->s0));
-  CU(h, cudaStreamSynchronize(h->s0));
-  if (union_blocks) *union_blocks = ctr[0];
-  if (pcie_bytes) *pcie_bytes = ctr[0] * (uint64_t)h->g.rec.kp_off;
+  uint64_t u = 0;
+  if (h->last_k) {
+    CU(h, cudaSetDevice(h->dev));
+    CU(h, cudaMemcpyAsync(h->h_ucount, h->ucount, h->g.S * sizeof(uint32_t),
+                          cudaMemcpyDeviceToHost, h->s0));
+    CU(h, cudaStreamSynchronize(h->s0));
+    for (uint32_t i = 0; i < h->g.S; ++i) u += h->h_ucount[i];
+  }
+  if (union_blocks) *union_blocks = u;
+  if (pcie_bytes) *pcie_bytes = u * (uint64_t)h->g.rec.kp_off;
   return TTKV_OK;
 }
 

@@ -58,7 +58,6 @@ struct SelectArgs {
   uint32_t* union_ids;    // [S][n_cap]
   uint32_t* union_mask;   // [S][n_cap]
   uint32_t* union_count;  // [S]
-  unsigned long long* counters;  // [0] += union blocks
   uint32_t n, k;
 };
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t st);

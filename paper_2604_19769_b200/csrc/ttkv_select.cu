@@ -256,10 +256,7 @@ __global__ void __launch_bounds__(kSelectThreads) select_union_kernel(SelectArgs
     if (threadIdx.x == 0) base_sh += total;
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    a.union_count[s] = base_sh;
-    atomicAdd(&a.counters[0], (unsigned long long)base_sh);
-  }
+  if (threadIdx.x == 0) a.union_count[s] = base_sh;
 }
 
 uint32_t select_max_blocks() { return kSelectMaxN; }
