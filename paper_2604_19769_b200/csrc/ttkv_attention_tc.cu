@@ -339,35 +339,27 @@ __device__ __forceinline__ void mma_a4(float (&d)[4], uint32_t a0, uint32_t a1, 
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
-// 4 u8 codes -> two half2 {c0,c1}, {c2,c3} (exact: 1024 + c minus 1024)
+// Codes enter the tensor cores as fp16 SUBNORMALS: a half whose exponent
+// field is 0 and mantissa is the integer n is exactly n * 2^-24, so a byte
+// or nibble lands in an A fragment with one mask / byte-permute and no float
+// op; the 2^24 (2^20 for a high nibble) comes back in the fp32 epilogue, an
+// exact power-of-two scaling.
+constexpr float kSub24 = 16777216.0f, kSub20 = 1048576.0f;
+// 4 u8 codes -> two half2 {c0,c1} * 2^-24, {c2,c3} * 2^-24 (exact)
 __device__ __forceinline__ void codes_to_h2(uint32_t w, uint32_t& lo, uint32_t& hi) {
-  const uint32_t a = __byte_perm(w, 0x64646464u, 0x5140u);
-  const uint32_t b = __byte_perm(w, 0x64646464u, 0x7362u);
-  const __half2 off = __floats2half2_rn(1024.f, 1024.f);
-  __half2 ha = __hsub2(*reinterpret_cast<const __half2*>(&a), off);
-  __half2 hb = __hsub2(*reinterpret_cast<const __half2*>(&b), off);
-  lo = *reinterpret_cast<uint32_t*>(&ha);
-  hi = *reinterpret_cast<uint32_t*>(&hb);
+  lo = __byte_perm(w, 0u, 0x4140u);
+  hi = __byte_perm(w, 0u, 0x4342u);
 }
 // x = [t.b0, t.b1, t'.b0, t'.b1] (two tokens' 4 LSB-first nibbles = channels
-// c..c+3) -> half2 {v[t][c+i], v[t'][c+i]} for i = 0..3, exact integers.
+// c..c+3) -> half2 {v[t][c+i], v[t'][c+i]} * 2^-24 for i = 0, 2 and * 2^-20
+// for i = 1, 3 (exact subnormals)
 __device__ __forceinline__ void nibbles_to_h2(uint32_t x, uint32_t& c0, uint32_t& c1,
                                               uint32_t& c2, uint32_t& c3) {
   const uint32_t y = x >> 8;
-  const uint32_t e0 = (x & 0x000F000Fu) | 0x64006400u;  // 1024 + n
-  const uint32_t o0 = (x & 0x00F000F0u) | 0x64006400u;  // 1024 + 16 n
-  const uint32_t e1 = (y & 0x000F000Fu) | 0x64006400u;
-  const uint32_t o1 = (y & 0x00F000F0u) | 0x64006400u;
-  const __half2 k1024 = __floats2half2_rn(1024.f, 1024.f);
-  const __half2 k16 = __floats2half2_rn(0.0625f, 0.0625f), k64 = __floats2half2_rn(-64.f, -64.f);
-  __half2 r0 = __hsub2(*reinterpret_cast<const __half2*>(&e0), k1024);
-  __half2 r1 = __hfma2(*reinterpret_cast<const __half2*>(&o0), k16, k64);
-  __half2 r2 = __hsub2(*reinterpret_cast<const __half2*>(&e1), k1024);
-  __half2 r3 = __hfma2(*reinterpret_cast<const __half2*>(&o1), k16, k64);
-  c0 = *reinterpret_cast<uint32_t*>(&r0);
-  c1 = *reinterpret_cast<uint32_t*>(&r1);
-  c2 = *reinterpret_cast<uint32_t*>(&r2);
-  c3 = *reinterpret_cast<uint32_t*>(&r3);
+  c0 = x & 0x000F000Fu;
+  c1 = x & 0x00F000F0u;
+  c2 = y & 0x000F000Fu;
+  c3 = y & 0x00F000F0u;
 }
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   // try_wait with a suspend-time hint: the producer sleeps in hardware until
@@ -551,7 +543,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
         for (int e = 0; e < 4; ++e) {
           const uint32_t h = 2 * qq + (e & 1);
           const uint32_t t = 32 * cw + 16 * mt + gq + 8 * (e >> 1);
-          if (h < G) sc[h * kScPitch + t] = c[mt][0][e] + c[mt][1][e];
+          if (h < G) sc[h * kScPitch + t] = (c[mt][0][e] + c[mt][1][e]) * kSub24;
         }
     }
     named_bar(1, nthreads_c);
@@ -632,7 +624,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
       // affine epilogue: acc = acc * alpha + s_c * (P . code) + z_c * sum(P)
       const float4 sz01 = *reinterpret_cast<const float4*>(vp + 2 * c0);
       const float4 sz23 = *reinterpret_cast<const float4*>(vp + 2 * c0 + 4);
-      const float vs[4] = {sz01.x, sz01.z, sz23.x, sz23.z};
+      const float vs[4] = {sz01.x * kSub24, sz01.z * kSub20, sz23.x * kSub24, sz23.z * kSub20};
       const float vz[4] = {sz01.y, sz01.w, sz23.y, sz23.w};
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
