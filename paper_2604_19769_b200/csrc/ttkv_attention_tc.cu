@@ -342,8 +342,12 @@ __device__ __forceinline__ void mma_a4(float (&d)[4], uint32_t a0, uint32_t a1, 
 // Codes enter the tensor cores as fp16 SUBNORMALS: a half whose exponent
 // field is 0 and mantissa is the integer n is exactly n * 2^-24, so a byte
 // or nibble lands in an A fragment with one mask / byte-permute and no float
-// op; the 2^24 (2^20 for a high nibble) comes back in the fp32 epilogue, an
-// exact power-of-two scaling.
+// op; the 2^24 (2^20 for a nibble) comes back in the fp32 epilogue, an exact
+// power-of-two scaling.  The MMA keeps every subnormal product exactly but
+// aligns its sum at the subnormal's nominal exponent, so a value with many
+// leading zero mantissa bits loses that many bits of the sum
+// (tools/mma_subnormal_probe.cu): nibbles therefore sit in mantissa bits 4-7
+// (measured output error unchanged vs. the 1024 + n encoding, tools/err_probe.py).
 constexpr float kSub24 = 16777216.0f, kSub20 = 1048576.0f;
 // 4 u8 codes -> two half2 {c0,c1} * 2^-24, {c2,c3} * 2^-24 (exact)
 __device__ __forceinline__ void codes_to_h2(uint32_t w, uint32_t& lo, uint32_t& hi) {
@@ -351,15 +355,14 @@ __device__ __forceinline__ void codes_to_h2(uint32_t w, uint32_t& lo, uint32_t& 
   hi = __byte_perm(w, 0u, 0x4342u);
 }
 // x = [t.b0, t.b1, t'.b0, t'.b1] (two tokens' 4 LSB-first nibbles = channels
-// c..c+3) -> half2 {v[t][c+i], v[t'][c+i]} * 2^-24 for i = 0, 2 and * 2^-20
-// for i = 1, 3 (exact subnormals)
+// c..c+3) -> half2 {v[t][c+i], v[t'][c+i]} * 2^-20 (exact subnormals with the
+// nibble in mantissa bits 4-7)
 __device__ __forceinline__ void nibbles_to_h2(uint32_t x, uint32_t& c0, uint32_t& c1,
                                               uint32_t& c2, uint32_t& c3) {
-  const uint32_t y = x >> 8;
-  c0 = x & 0x000F000Fu;
+  c0 = (x << 4) & 0x00F000F0u;
   c1 = x & 0x00F000F0u;
-  c2 = y & 0x000F000Fu;
-  c3 = y & 0x00F000F0u;
+  c2 = (x >> 4) & 0x00F000F0u;
+  c3 = (x >> 8) & 0x00F000F0u;
 }
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   // try_wait with a suspend-time hint: the producer sleeps in hardware until
@@ -624,7 +627,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
       // affine epilogue: acc = acc * alpha + s_c * (P . code) + z_c * sum(P)
       const float4 sz01 = *reinterpret_cast<const float4*>(vp + 2 * c0);
       const float4 sz23 = *reinterpret_cast<const float4*>(vp + 2 * c0 + 4);
-      const float vs[4] = {sz01.x * kSub24, sz01.z * kSub20, sz23.x * kSub24, sz23.z * kSub20};
+      const float vs[4] = {sz01.x * kSub20, sz01.z * kSub20, sz23.x * kSub20, sz23.z * kSub20};
       const float vz[4] = {sz01.y, sz01.w, sz23.y, sz23.w};
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
