@@ -57,6 +57,17 @@ __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a2
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
 }
+// Power-of-two normalization ahead of an fp16 hi/lo split: returns 2^-k with
+// k chosen so the largest magnitude m lands in [2^14, 2^15) -- the hi part
+// cannot overflow fp16 (queries of any size, keys near the fp16 range, scales
+// of restored records) and the lo part stays a normal fp16 -- and sets
+// *unscale = 2^(extra + k) to restore the fp32 result exactly.
+__device__ __forceinline__ float pow2_normalizer(float m, int extra, float* unscale) {
+  int k = 0;
+  if (m > 0.f) k = max(-100, min(100, (int)((__float_as_uint(m) >> 23) & 0xffu) - 127 - 14));
+  *unscale = __uint_as_float((uint32_t)(127 + extra + k) << 23);
+  return __uint_as_float((uint32_t)(127 - k) << 23);
+}
 __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
   const __half2 h = __floats2half2_rn(x0, x1);
   const float2 hf = __half22float2(h);
@@ -139,14 +150,26 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
   const bool head_ok = gq < g.G;
   // A fragments of q (scaled into log2 units), hi + lo
   uint32_t aqh[KSTEPS][2], aql[KSTEPS][2];
+  float qunscale;  // scores = MMA result * qunscale (see pow2_normalizer)
   {
     const float* qr = a.q + ((uint64_t)s * g.G + (head_ok ? gq : 0)) * D;
     const float sl = (float)a.scale_log2;
+    float m = 0.f;  // max |q| of this head: 32 values here, x4 lanes (qq)
 #pragma unroll
     for (int ks = 0; ks < KSTEPS; ++ks) {
       const int c = 16 * ks + 2 * qq;
-      const float x0 = head_ok ? qr[c] * sl : 0.f, x1 = head_ok ? qr[c + 1] * sl : 0.f;
-      const float x8 = head_ok ? qr[c + 8] * sl : 0.f, x9 = head_ok ? qr[c + 9] * sl : 0.f;
+      if (head_ok)
+        m = fmaxf(m, fmaxf(fmaxf(fabsf(qr[c]), fabsf(qr[c + 1])),
+                           fmaxf(fabsf(qr[c + 8]), fabsf(qr[c + 9]))));
+    }
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+    const float f = pow2_normalizer(m * fabsf(sl), 0, &qunscale) * sl;
+#pragma unroll
+    for (int ks = 0; ks < KSTEPS; ++ks) {
+      const int c = 16 * ks + 2 * qq;
+      const float x0 = head_ok ? qr[c] * f : 0.f, x1 = head_ok ? qr[c + 1] * f : 0.f;
+      const float x8 = head_ok ? qr[c + 8] * f : 0.f, x9 = head_ok ? qr[c + 9] * f : 0.f;
       split2(x0, x1, aqh[ks][0], aql[ks][0]);
       split2(x8, x9, aqh[ks][1], aql[ks][1]);
     }
@@ -196,8 +219,9 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const uint32_t tA = 8 * (2 * cw + h) + 2 * qq;
-          scb[gq * kTT + tA] = tA < rows ? c[h][0][0] + c[h][1][0] : -INFINITY;
-          scb[gq * kTT + tA + 1] = tA + 1 < rows ? c[h][0][1] + c[h][1][1] : -INFINITY;
+          scb[gq * kTT + tA] = tA < rows ? (c[h][0][0] + c[h][1][0]) * qunscale : -INFINITY;
+          scb[gq * kTT + tA + 1] =
+              tA + 1 < rows ? (c[h][0][1] + c[h][1][1]) * qunscale : -INFINITY;
         }
       }
     }
@@ -348,7 +372,7 @@ __device__ __forceinline__ void mma_a4(float (&d)[4], uint32_t a0, uint32_t a1, 
 // leading zero mantissa bits loses that many bits of the sum
 // (tools/mma_subnormal_probe.cu): nibbles therefore sit in mantissa bits 4-7
 // (measured output error unchanged vs. the 1024 + n encoding, tools/err_probe.py).
-constexpr float kSub24 = 16777216.0f, kSub20 = 1048576.0f;
+constexpr float kSub20 = 1048576.0f;
 // 4 u8 codes -> two half2 {c0,c1} * 2^-24, {c2,c3} * 2^-24 (exact)
 __device__ __forceinline__ void codes_to_h2(uint32_t w, uint32_t& lo, uint32_t& hi) {
   lo = __byte_perm(w, 0u, 0x4140u);
@@ -377,8 +401,8 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
 }
 template <int GT>
 constexpr size_t slow_tc_tail_bytes() {
-  // qsf + phl (2 x 256 uint4) | sc [GT][kScPitch] | qsm [GT][128] | 5 x 8 stats
-  return 2 * 256 * 16 + (size_t)GT * kScPitch * 4 + (size_t)GT * 128 * 4 + 5 * 8 * 4;
+  // qsf + phl (2 x 256 uint4) | sc [GT][kScPitch] | qsm [GT][128] | 6 x 8 stats
+  return 2 * 256 * 16 + (size_t)GT * kScPitch * 4 + (size_t)GT * 128 * 4 + 6 * 8 * 4;
 }
 }  // namespace
 
@@ -406,7 +430,8 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
   float* ast = lst + 8;
   float* pst = ast + 8;  // sum_t p of the current block
   float* bst = pst + 8;  // beta = q . z of the current block
-  uint64_t* full = reinterpret_cast<uint64_t*>(bst + 8);
+  float* usc = bst + 8;  // per-head score unscale (pow2_normalizer), then max |q|
+  uint64_t* full = reinterpret_cast<uint64_t*>(usc + 8);
   uint64_t* empty = full + ST;
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -418,15 +443,32 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
     fence_mbar_init();
   }
   for (uint32_t i = threadIdx.x; i < 512; i += blockDim.x) qsf[i] = make_uint4(0, 0, 0, 0);
+  // q in log2 units, normalized per head by a power of two so that
+  // |q_c s_c| <= |q|max * kTcKeyScaleBound lands below 2^15: the fp16 hi part
+  // of q * s cannot overflow for any query or record (ttkv_launch.h)
+  if (threadIdx.x < 8) usc[threadIdx.x] = 0.f;
+  __syncthreads();
+  const float* qb = a.q + (uint64_t)s * G * 128;
+  const float sl = (float)a.scale_log2;
+  for (uint32_t i = threadIdx.x; i < G * 128; i += blockDim.x)
+    atomicMax(reinterpret_cast<uint32_t*>(usc) + i / 128, __float_as_uint(fabsf(qb[i] * sl)));
+  __syncthreads();
+  {
+    float f = 1.f, uns = 1.f;
+    if (threadIdx.x < 8) f = pow2_normalizer(usc[threadIdx.x] * kTcKeyScaleBound, 24, &uns);
+    __syncthreads();
+    if (threadIdx.x < 8) {
+      usc[threadIdx.x] = uns;  // 2^24: the subnormal K codes
+      mst[threadIdx.x] = f;    // scratch until the stats are initialized below
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < GT * 128; i += blockDim.x)
+    qsm[i] = (i / 128 < G) ? (qb[i] * sl) * mst[i / 128] : 0.f;
+  __syncthreads();
   if (threadIdx.x < 8) {
     mst[threadIdx.x] = -INFINITY;
     lst[threadIdx.x] = 0.0f;
-  }
-  {
-    const float* qb = a.q + (uint64_t)s * G * 128;
-    const float sl = (float)a.scale_log2;
-    for (uint32_t i = threadIdx.x; i < GT * 128; i += blockDim.x)
-      qsm[i] = (i / 128 < G) ? qb[i] * sl : 0.f;
   }
   __syncthreads();
   const uint32_t* uids = a.union_ids + (uint64_t)s * g.n_cap + i0;
@@ -458,6 +500,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
 #pragma unroll
   for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.f;
   uint32_t seen = 0;
+  const float uns0 = usc[2 * qq], uns1 = usc[2 * qq + 1];  // score unscale of this lane's heads
   // Swizzle-folded shared-memory offsets (loop-invariant):
   //  K (128B swizzle): ldmatrix row address of matrix m = lane / 8 -- token
   //  32cw + 16mt + 8(m&1) + (lane&7), 16-byte chunk 2jp + (m>>1); the XOR
@@ -536,7 +579,8 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
       for (int rep = 0; rep < 2; ++rep) {
         const uint32_t h = cw + rep * kSlowConsumerWarps;
         if (h < G) {  // warp-uniform
-          const float beta = warp_sum(bpart[rep]);
+          // qsm carries the pow2 normalizer 2^-k; usc[h] = 2^(24 + k)
+          const float beta = warp_sum(bpart[rep]) * (usc[h] * (1.0f / 16777216.0f));
           if (lane == 0) bst[h] = beta;
         }
       }
@@ -546,7 +590,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
         for (int e = 0; e < 4; ++e) {
           const uint32_t h = 2 * qq + (e & 1);
           const uint32_t t = 32 * cw + 16 * mt + gq + 8 * (e >> 1);
-          if (h < G) sc[h * kScPitch + t] = (c[mt][0][e] + c[mt][1][e]) * kSub24;
+          if (h < G) sc[h * kScPitch + t] = (c[mt][0][e] + c[mt][1][e]) * ((e & 1) ? uns1 : uns0);
         }
     }
     named_bar(1, nthreads_c);

@@ -1488,6 +1488,7 @@ int ttkv_gpu_restore_slow_tier(ttkv_gpu* h, const char* const* paths, uint32_t n
   const uint64_t vbytes = packed_bytes_u((uint64_t)g.B * g.d_v, g.vb);
   const uint64_t pbytes = g.rec.used - g.rec.kp_off;
   uint64_t n_blocks = 0;
+  bool wide_scales = false;
   std::vector<uint8_t> rec(g.rec.stride), all;
   std::vector<float> cent(g.d_k);
   for (uint32_t s = 0; s < g.S; ++s) {
@@ -1538,6 +1539,8 @@ int ttkv_gpu_restore_slow_tier(ttkv_gpu* h, const char* const* paths, uint32_t n
       float* kp = reinterpret_cast<float*>(rec.data() + g.rec.kp_off);
       float* vp = reinterpret_cast<float*>(rec.data() + g.rec.vp_off);
       for (uint32_t c = 0; c < (kb == 16 ? 0u : dk); ++c) { kp[2 * c] = q.f32(); kp[2 * c + 1] = q.f32(); }
+      for (uint32_t c = 0; c < (kb == 16 ? 0u : dk); ++c)  // see kTcKeyScaleBound
+        if (!(std::fabs(kp[2 * c]) <= kTcKeyScaleBound)) wide_scales = true;
       for (uint32_t c = 0; c < (vb == 16 ? 0u : dv); ++c) { vp[2 * c] = q.f32(); vp[2 * c + 1] = q.f32(); }
       for (uint32_t c = 0; c < dk; ++c) cent[c] = q.f32();
       auto payload = [&](uint64_t want, uint32_t bits, uint32_t dim, uint8_t* dst,
@@ -1588,6 +1591,9 @@ int ttkv_gpu_restore_slow_tier(ttkv_gpu* h, const char* const* paths, uint32_t n
   h->n_slow = n_blocks;
   h->appended = n_blocks * g.B;
   h->fast_front = n_blocks * g.B;
+  // key scales no fp16 ring can produce (a dump from an fp32 engine): the
+  // tensor-core slow kernel's fp16 operand bound no longer holds
+  if (wide_scales) h->slow_tc = false;
   return TTKV_OK;
 }
 

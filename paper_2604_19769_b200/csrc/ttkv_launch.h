@@ -110,6 +110,12 @@ struct alignas(64) SlowTcArgs {
   double scale_log2;
 };
 bool slow_tc_supported(const Geometry& g);
+// Largest |key scale| the tensor-core slow kernel accepts: records quantized
+// from an fp16 ring have s = (max - min) / 255 <= 2 * 65504 / 255 < 514, and
+// the kernel normalizes q by a power of two against this bound so that the
+// fp16 hi part of q * s cannot overflow.  Restored records beyond it send the
+// handle to the CUDA-core slow kernel.
+constexpr float kTcKeyScaleBound = 514.0f;
 cudaError_t make_arena_tmaps(const Geometry& g, uint8_t* arena, SlowTcArgs& a);
 cudaError_t launch_slow_tc(const SlowTcArgs& a, uint32_t grid_chunks, cudaStream_t st);
 

@@ -157,7 +157,7 @@ def make_inputs(S, ctx, T, dk, dv, G, seed, fp16):
 
 def run_parity(T_, *, S=2, G=1, d=32, dv=None, B=32, l_fast=128, kb=8, vb=4, elem=2, ctx=600,
                steps=6, frac=0.45, top_k=None, mode=0, seed=100, prefill_chunks=1,
-               check_blocks=True, literal=False, slow_tier=0):
+               check_blocks=True, literal=False, slow_tier=0, q_mul=1.0, kv_mul=1.0):
     dv = dv or d
     cfg = T_.TierConfig(hbm_budget_bytes=l_fast * (d + dv) * elem, d_k=d, d_v=dv,
                         bytes_full_precision=elem, block_size=B, key_bits=kb, value_bits=vb,
@@ -165,6 +165,11 @@ def run_parity(T_, *, S=2, G=1, d=32, dv=None, B=32, l_fast=128, kb=8, vb=4, ele
     pol = T_.SelectionPolicy(top_k, frac)
     assert T_.fast_capacity(cfg) == l_fast
     pk, pv, dk_, dv_, dq = make_inputs(S, ctx, steps, d, dv, G, seed, fp16=(elem == 2))
+    if q_mul != 1.0 or kv_mul != 1.0:
+        dq = (dq * q_mul).astype(np.float32)
+        pk, pv, dk_, dv_ = ((x * kv_mul).astype(np.float32) for x in (pk, pv, dk_, dv_))
+        if elem == 2:
+            pk, pv, dk_, dv_ = map(O.fp16_round, (pk, pv, dk_, dv_))
     eng = T_.MultiStreamEngine(cfg, pol, n_streams=S, heads_per_stream=G, group_select=bool(mode),
                                literal_additive_merge=literal, slow_tier=slow_tier)
     orc = [O.OracleEngine(d, dv, B, l_fast, kb, vb, top_k, frac) for _ in range(S)]
@@ -283,6 +288,16 @@ def test_engine_hbm_resident_slow_tier(gpu, G, mode, literal):
     # on raw codes) for K8/V4, d = B = 128; records still bit-exact
     run_parity(gpu, S=3, G=G, d=128, B=128, l_fast=512, ctx=5000, steps=4, mode=mode,
                literal=literal, slow_tier=1)
+
+
+@pytest.mark.parametrize("slow_tier", [0, 1])
+@pytest.mark.parametrize("q_mul,kv_mul", [(3e4, 1.0), (1.0, 2e3), (50.0, 2e3), (1e-6, 1e-3), (1e7, 1.0), (3e3, 5e3)])
+def test_engine_extreme_magnitudes(gpu, slow_tier, q_mul, kv_mul):
+    # hot-path shape with queries / KV far from N(0, 1): the tensor-core
+    # kernels' fp16 operand splits must neither overflow (scores of 1e4+ in
+    # log2 units, keys near the fp16 range) nor lose the small end
+    run_parity(gpu, S=2, G=4, d=128, B=128, l_fast=512, ctx=3000, steps=3, slow_tier=slow_tier,
+               q_mul=q_mul, kv_mul=kv_mul)
 
 
 def test_engine_hbm_resident_generic_shape(gpu):

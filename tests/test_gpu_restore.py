@@ -161,3 +161,43 @@ def test_restore_errors(gpu, tmp_path):
     with pytest.raises(T.IoError):
         fresh().restore_slow_tier([p0, tmp_path / "missing"])
     src.close()
+
+
+def test_restore_wide_key_scales_hbm_tier(gpu, tmp_path):
+    # A dump from an fp32 engine can carry key scales no fp16 ring produces
+    # (|s| > kTcKeyScaleBound, ttkv_launch.h); restored into an HBM-tier
+    # handle at the tensor-core shape, the engine must stay exact (it moves to
+    # the CUDA-core slow kernel instead of overflowing the fp16 q * s split).
+    T = gpu
+    S, d, B, lf, ctx, steps = 2, 128, 128, 512, 1500, 3
+    rng = np.random.default_rng(5)
+    pk = (rng.standard_normal((S, ctx, d)) * 3e4).astype(np.float32)  # fp32 range
+    pv = O.fp16_round(rng.standard_normal((S, ctx, d)))
+    refs, paths = [], []
+    for s in range(S):
+        r = O.RefEngine(lf * 2 * d * 2, d, d, B)
+        r.prefill(pk[s], pv[s])
+        refs.append(r)
+        p = tmp_path / f"w{s}.ttkvtier"
+        p.write_bytes(tier_file([r.serialize_block(b) for b in range(r.slow_blocks())]))
+        paths.append(p)
+    n = refs[0].slow_blocks()
+    cfg = T.TierConfig(hbm_budget_bytes=lf * 2 * d * 2, d_k=d, d_v=d, block_size=B)
+    eng = T.MultiStreamEngine(cfg, n_streams=S, slow_tier=1)
+    eng.restore_slow_tier(paths)
+    tail_k = O.fp16_round(pk[:, n * B:] / 3e4)  # the fast tier resumes at fp16 scale
+    eng.append(tail_k, pv[:, n * B:])
+    for s in range(S):
+        refs[s] = O.RefEngine(lf * 2 * d * 2, d, d, B)
+        refs[s].prefill(np.concatenate([pk[s, :n * B], tail_k[s]]), pv[s])
+    for t in range(steps):
+        q = rng.standard_normal((S, 1, d)).astype(np.float32)
+        kn = O.fp16_round(rng.standard_normal((S, d)))
+        vn = O.fp16_round(rng.standard_normal((S, d)))
+        rep = eng.decode_step(q, kn, vn, fetched=True)
+        for s in range(S):
+            o = refs[s].decode_step(q[s, 0], kn[s], vn[s])
+            assert np.array_equal(rep.fetched_blocks[s][0], o["fetched"]), (t, s)
+            assert np.all(np.isfinite(rep.output[s, 0]))
+            assert rel_err(rep.output[s, 0], o["output"]) < 1e-3
+    eng.close()
