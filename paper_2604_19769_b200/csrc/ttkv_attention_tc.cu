@@ -721,6 +721,8 @@ static int slow_tc_stages() {
   return (e && e[0] == '3') ? 3 : 2;
 }
 
+uint32_t slow_tc_ctas_per_sm() { return slow_tc_stages() == 3 ? 2u : 3u; }
+
 template <int GT, int ST>
 static size_t slow_tc_smem() {
   return 1024 + (size_t)ST * kSlowStage + slow_tc_tail_bytes<GT>() + 2 * ST * 8;

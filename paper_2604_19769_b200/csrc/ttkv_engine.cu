@@ -217,6 +217,7 @@ struct ttkv_gpu {
   bool fast_tc = false;      // tensor-core fast tier (TMA tensor maps)
   FastTcArgs tc{};           // ring tensor maps, encoded once at create
   bool slow_tc = false;      // tensor-core slow tier (arena tensor maps)
+  int sms = 148;             // SM count of the device
   SlowTcArgs stc{};          // re-encoded whenever the arena is reallocated
   uint8_t* stage_arena = nullptr;  // serial schedule: HBM copy of selected records
   double last_step_ms = 0.0;
@@ -665,9 +666,25 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
     if (int rcf = fork_fast()) return rcf;
   }
   if (slow) {
-    // union entries per CTA: ~4 waves of 2 CTAs/SM over the lower bound S*k
-    const uint64_t est = (uint64_t)g.S * k;
-    CH = (uint32_t)std::min<uint64_t>(64, std::max<uint64_t>(4, (est + 1183) / 1184));
+    if (h->slow_tc) {
+      // HBM records: every CTA pays a prologue and a pipeline fill, so the
+      // smallest chunk that fits the union's upper bound S * min(n, Gs * k)
+      // into ONE wave of resident CTAs (layer-sequential cfg2, S = 8: 308 ->
+      // 379 tok/s vs 4-record chunks; a second partial wave costs ~15 %)
+      const uint64_t ub = (uint64_t)g.S * std::min<uint64_t>(n, (uint64_t)g.Gs * k);
+      const uint64_t slots = (uint64_t)h->sms * slow_tc_ctas_per_sm();
+      CH = (uint32_t)std::min<uint64_t>(64, std::max<uint64_t>(4, (ub + slots - 1) / slots));
+    } else {
+      // host records: union entries per CTA ~4 waves of 2 CTAs/SM over the
+      // lower bound S * k (more zero-copy streams in flight)
+      const uint64_t est = (uint64_t)g.S * k;
+      CH = (uint32_t)std::min<uint64_t>(64, std::max<uint64_t>(4, (est + 1183) / 1184));
+    }
+    static const uint32_t ch_env = [] {  // TTKV_SLOW_CH=n overrides (measurement)
+      const char* e = std::getenv("TTKV_SLOW_CH");
+      return e ? (uint32_t)std::max(1, std::min(256, std::atoi(e))) : 0u;
+    }();
+    if (ch_env) CH = ch_env;
     const uint64_t grid_chunks = (n + CH - 1) / CH;
     int rc = ensure_spart(h, grid_chunks);
     if (rc) return rc;
@@ -894,6 +911,7 @@ int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* po
   h->pol = *pol;
   h->opt = *opt;
   h->dev = opt->device;
+  cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->dev);
   h->l_fast = l_fast;
   Geometry& g = h->g;
   g.S = opt->n_streams;

@@ -110,6 +110,7 @@ struct alignas(64) SlowTcArgs {
   double scale_log2;
 };
 bool slow_tc_supported(const Geometry& g);
+uint32_t slow_tc_ctas_per_sm();  // resident CTAs per SM of the slow tensor-core kernel
 // Largest |key scale| the tensor-core slow kernel accepts: records quantized
 // from an fp16 ring have s = (max - min) / 255 <= 2 * 65504 / 255 < 514, and
 // the kernel normalizes q by a power of two against this bound so that the
