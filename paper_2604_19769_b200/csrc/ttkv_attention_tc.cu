@@ -409,6 +409,7 @@ constexpr size_t slow_tc_tail_bytes() {
 template <int GT, int ST>
 __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
     slow_attn_tc_kernel(const __grid_constant__ SlowTcArgs a) {
+  pdl_wait();  // the union lists (launched chained behind the selection)
   const Geometry& g = a.g;
   const uint32_t G = g.G;
   const uint32_t s = blockIdx.y, chunk = blockIdx.x;
@@ -736,8 +737,7 @@ static cudaError_t launch_slow_tc_t(const SlowTcArgs& a, uint32_t grid_chunks, c
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid(grid_chunks, a.g.S);
-  kern<<<grid, 32 + kSlowConsumerWarps * 32, smem, st>>>(a);
-  return cudaGetLastError();
+  return launch_chained(kern, grid, dim3(32 + kSlowConsumerWarps * 32), smem, st, a);
 }
 
 template <int ST>

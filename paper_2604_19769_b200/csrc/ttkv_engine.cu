@@ -183,6 +183,13 @@ enum Kind { K_APPEND = 0, K_SCORE, K_SELECT, K_FAST, K_SLOW, K_COMBINE, K_EVICT,
 }  // namespace
 
 void ttkv_dev::set_last_error(const char* msg) { g_last_error = msg ? msg : ""; }
+bool ttkv_dev::pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TTKV_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 struct ttkv_gpu {
   // fused combine + all-gather over peer memory (ttkv_gpu_peer_gather_*)

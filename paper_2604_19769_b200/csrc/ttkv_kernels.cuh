@@ -82,6 +82,16 @@ __device__ __forceinline__ float warp_max(float v) {
 
 // warp-wide fp32 max in one instruction (CREDUX.MAX.F32, sm_100a; NaN-ignoring
 // like fmaxf)
+// Programmatic dependent launch: a kernel started by launch_chained() may run
+// while its predecessor on the stream drains, so it calls pdl_wait() before
+// touching anything the predecessor writes (griddepcontrol.wait returns once
+// that grid has completed and its memory is visible; a no-op for a normal
+// launch).  pdl_trigger() lets the successor's CTAs be scheduled early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ float warp_max_redux(float v) {
   float r;
   asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));

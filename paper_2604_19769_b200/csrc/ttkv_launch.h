@@ -12,6 +12,26 @@ constexpr int kInF32 = 0;
 constexpr int kMaxPeers = 8;
 constexpr int kInF16 = 1;
 
+// Launch with programmatic stream serialization (PDL, see pdl_wait in
+// ttkv_kernels.cuh): the kernel's CTAs launch while the previous kernel on
+// the stream finishes.  TTKV_PDL=0 turns it off (measurement).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_chained(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                           cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // thread-local message behind ttkv_last_error() (defined in ttkv_engine.cu)
 void set_last_error(const char* msg);
 // thread-local grow-only device scratch, slot < 8 (ttkv_freefn.cu)

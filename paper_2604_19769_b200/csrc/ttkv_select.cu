@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(128) score_kernel(ScoreArgs a) {
     }
     a.scores[((uint64_t)s * g.Gs + h) * g.n_cap + b0 + r] = acc;
   }
+  pdl_trigger();  // the selection kernels may launch as the last tiles drain
 }
 
 cudaError_t launch_score(const ScoreArgs& a, cudaStream_t st) {
@@ -139,6 +140,8 @@ __device__ __forceinline__ uint32_t topk_digit(uint64_t key, uint32_t id, int p)
 }
 
 __global__ void __launch_bounds__(kTopkThreads) select_topk_kernel(SelectArgs a) {
+  pdl_trigger();  // few CTAs: let the union kernel's CTAs get resident
+  pdl_wait();     // the scores
   const Geometry& g = a.g;
   const uint32_t h = blockIdx.x, s = blockIdx.y;
   const double* sc = a.scores + ((uint64_t)s * g.Gs + h) * g.n_cap;
@@ -225,6 +228,8 @@ __global__ void __launch_bounds__(kTopkThreads) select_topk_kernel(SelectArgs a)
 // (records are then read in arena order; the merge is order-independent,
 // SPEC.md:287) and clear the head mask for the next step.
 __global__ void __launch_bounds__(kSelectThreads) select_union_kernel(SelectArgs a) {
+  pdl_trigger();
+  pdl_wait();  // the per-head selection masks
   const Geometry& g = a.g;
   const uint32_t s = blockIdx.x;
   __shared__ uint32_t warp_tot[kSelectThreads / 32];
@@ -265,11 +270,10 @@ uint32_t select_max_blocks() { return kSelectMaxN; }
 // leaves it zeroed again.  `sel` is not written: the order is a cold read.
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
   if (a.n == 0) return cudaSuccess;
-  select_topk_kernel<<<dim3(a.g.Gs, a.g.S), kTopkThreads, 0, st>>>(a);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_chained(select_topk_kernel, dim3(a.g.Gs, a.g.S), dim3(kTopkThreads), 0,
+                                 st, a);
   if (e != cudaSuccess) return e;
-  select_union_kernel<<<a.g.S, 256, 0, st>>>(a);
-  return cudaGetLastError();
+  return launch_chained(select_union_kernel, dim3(a.g.S), dim3(256), 0, st, a);
 }
 
 // ---------------------------------------------------------------------------
