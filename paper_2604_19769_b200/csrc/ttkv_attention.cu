@@ -612,6 +612,7 @@ cudaError_t launch_fast(const FastArgs& a, cudaStream_t st) {
 // are computed once into smem, then each thread reduces one output channel.
 template <typename Acc>
 __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
+  pdl_wait();  // the slow partials (the fast tier joins through an event)
   const Geometry& g = a.g;
   const uint32_t idx = blockIdx.x;  // s * G + head
   const uint32_t s = idx / g.G;
@@ -763,13 +764,12 @@ cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
   if (a.g.elem == 4) {
     cudaFuncSetAttribute(combine_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    combine_kernel<double><<<grid, 128, smem, st>>>(a);
+    return launch_chained(combine_kernel<double>, grid, dim3(128), smem, st, a);
   } else {
     cudaFuncSetAttribute(combine_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    combine_kernel<float><<<grid, 128, smem, st>>>(a);
+    return launch_chained(combine_kernel<float>, grid, dim3(128), smem, st, a);
   }
-  return cudaGetLastError();
 }
 
 }  // namespace ttkv_dev

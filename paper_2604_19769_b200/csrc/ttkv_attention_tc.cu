@@ -692,6 +692,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
     if (lane == 0) mbar_arrive(&empty[st]);
   }
 
+  pdl_trigger();  // the combine's CTAs may get resident while partials drain
   // ---- emit the (acc, m, l) partial of every head ----
   named_bar(1, nthreads_c);
   const uint32_t pitch = 128 + 2;

@@ -24,6 +24,7 @@ constexpr int kSelectThreads = 1024;
 constexpr uint32_t kSelectMaxN = 16384;  // blocks per stream (2M tokens at B=128)
 
 __global__ void __launch_bounds__(128) score_kernel(ScoreArgs a) {
+  pdl_wait();  // the query / centroids when the previous kernel produced them
   const Geometry& g = a.g;
   const uint32_t s = blockIdx.y;
   const uint32_t b0 = blockIdx.x * kScoreTile;
@@ -113,8 +114,7 @@ cudaError_t launch_score(const ScoreArgs& a, cudaStream_t st) {
                                        (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((a.n + kScoreTile - 1) / kScoreTile, a.g.S);
-  score_kernel<<<grid, 128, smem, st>>>(a);
-  return cudaGetLastError();
+  return launch_chained(score_kernel, grid, dim3(128), smem, st, a);
 }
 
 // orderable key: ascending u64 == ascending double; -0.0 folded onto +0.0

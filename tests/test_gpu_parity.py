@@ -300,6 +300,15 @@ def test_engine_extreme_magnitudes(gpu, slow_tier, q_mul, kv_mul):
                q_mul=q_mul, kv_mul=kv_mul)
 
 
+@pytest.mark.parametrize("slow_tier", [0, 1])
+def test_engine_long_fast_tier_short_slow(gpu, slow_tier):
+    # a long fast tier (second stream) against a one-record slow tier: the
+    # combine, launched chained behind the short slow kernel, must still wait
+    # for the fast tier's event (programmatic launch must not bypass it)
+    run_parity(gpu, S=4, G=4, d=128, B=128, l_fast=16384, ctx=16384 + 200, steps=4,
+               slow_tier=slow_tier, check_blocks=False)
+
+
 def test_engine_hbm_resident_generic_shape(gpu):
     # a shape the tensor-core kernel does not cover -> CUDA-core slow kernel on HBM
     run_parity(gpu, S=2, G=2, d=32, B=32, l_fast=128, ctx=900, steps=4, slow_tier=1)
