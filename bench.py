@@ -783,6 +783,7 @@ def run_layer_sequential(args):
     for _ in range(args.warmup):
         token()
     torch.cuda.synchronize()
+    launches0 = sum(e.state()["launches"] for e in engs)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(0) as clk:
         torch.cuda.synchronize()
@@ -792,6 +793,7 @@ def run_layer_sequential(args):
         ev1.record()
         torch.cuda.synchronize()
     ms_step = ev0.elapsed_time(ev1) / args.steps
+    launches = sum(e.state()["launches"] for e in engs) - launches0
     union = sum(e.step_counters()[0] for e in engs)
     st = engs[0].state()
     pcie = union * st["payload_bytes"]
@@ -819,6 +821,7 @@ def run_layer_sequential(args):
                      "pcie_gbs": pcie / (ms_step * 1e-3) / 1e9 if host_tier else None,
                      "pcie_peak": h2d_peak},
         "clocks": clk.summary(),
+        "gpu_launches": launches,
     }
     for e in engs:
         e.close()

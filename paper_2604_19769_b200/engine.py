@@ -250,7 +250,7 @@ class MultiStreamEngine:
             raise ShapeError("decode_step: query dimension mismatch")
         if k.size != self.S * self.config.d_k or v.size != self.S * self.config.d_v:
             raise ShapeError("append_token: key/value dimension mismatch")
-        out = np.zeros((self.S, self.G, self.config.d_v), np.float64)
+        out = np.empty((self.S, self.G, self.config.d_v), np.float64)  # fully written by the call
         rep = L.StepReportC()
         _check(self._lib.ttkv_gpu_decode_step(self._h, _ptr(q), _ptr(k), _ptr(v), dt, _ptr(out),
                                               C.byref(rep)), self._h)
