@@ -16,6 +16,8 @@ cases = [
     # > 64 slow blocks: the selection sort's cross-warp (stride >= 64) passes
     dict(S=2, G=4, d=128, B=128, l_fast=256, ctx=20000, steps=2, slow_tier=1),
     dict(S=2, G=8, d=32, B=32, l_fast=128, ctx=9000, steps=2),
+    # power-of-two q normalization at query magnitudes that overflow fp16
+    dict(S=1, G=4, d=128, B=128, l_fast=256, ctx=700, steps=2, slow_tier=1, q_mul=1e7),
 ]
 for c in cases:
     P.run_parity(T, **c)
