@@ -610,8 +610,9 @@ cudaError_t launch_fast(const FastArgs& a, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // One CTA per (stream, head): weights w_i = exp2(m_i - M) of every partial
 // are computed once into smem, then each thread reduces one output channel.
+constexpr int kCombineWarps = 8;
 template <typename Acc>
-__global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
+__global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs a) {
   pdl_wait();  // the slow partials (the fast tier joins through an event)
   const Geometry& g = a.g;
   const uint32_t idx = blockIdx.x;  // s * G + head
@@ -626,7 +627,7 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
   const uint32_t np = a.nfc + nlse;
   extern __shared__ __align__(16) uint8_t csm[];
   Acc* w = reinterpret_cast<Acc*>(csm);  // [np]
-  __shared__ Acc red[4];
+  __shared__ Acc red[kCombineWarps];
   auto part = [&](uint32_t i) { return i < a.nfc ? fp + i * pitch : sp + (i - a.nfc) * pitch; };
 
   Acc M = -INFINITY;
@@ -637,7 +638,9 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
   M = wmax(M);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = M;
   __syncthreads();
-  M = fmax(fmax(red[0], red[1]), fmax(red[2], red[3]));
+  M = red[0];
+#pragma unroll
+  for (int k = 1; k < kCombineWarps; ++k) M = fmax(M, red[k]);
   __syncthreads();
   Acc L = 0;
   for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
@@ -649,14 +652,17 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
   L = wsum(L);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = L;
   __syncthreads();
-  const Acc inv = Acc(1) / (red[0] + red[1] + red[2] + red[3]);
+  Acc Lt = 0;
+#pragma unroll
+  for (int k = 0; k < kCombineWarps; ++k) Lt += red[k];
+  const Acc inv = Acc(1) / Lt;
   // the weighted sum over partials for this CTA's channel slice
   // [c_lo, c_hi) (blockIdx.y; several slices when S*G is small): warp w takes
   // partials w, w+4, ..., lane l channels c_lo + l + 32j (coalesced segments
   // of each partial row), two partials in flight; warps meet in smem
   const uint32_t cw = (g.d_v + gridDim.y - 1) / gridDim.y;
   const uint32_t c_lo = blockIdx.y * cw, c_hi = min(g.d_v, c_lo + cw);
-  __shared__ Acc red2[4][kMaxD];
+  __shared__ Acc red2[kCombineWarps][kMaxD];
   {
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // 8 partial rows in flight per lane (the rows come from L2 or DRAM)
@@ -667,11 +673,11 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[u][j] = 0;
     uint32_t i = warp;
-    for (; i + 4 * (kU - 1) < np; i += 4 * kU) {
+    for (; i + kCombineWarps * (kU - 1) < np; i += kCombineWarps * kU) {
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        const Acc* pu = part(i + 4 * u);
-        const Acc wu = w[i + 4 * u];
+        const Acc* pu = part(i + kCombineWarps * u);
+        const Acc wu = w[i + kCombineWarps * u];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const uint32_t c = c_lo + lane + 32 * j;
@@ -679,7 +685,7 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
         }
       }
     }
-    for (; i < np; i += 4) {
+    for (; i < np; i += kCombineWarps) {
       const Acc* p0 = part(i);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -701,7 +707,9 @@ __global__ void __launch_bounds__(128) combine_kernel(CombineArgs a) {
   }
   __syncthreads();
   for (uint32_t c = c_lo + threadIdx.x; c < c_hi; c += blockDim.x) {
-    const Acc A = (red2[0][c] + red2[1][c]) + (red2[2][c] + red2[3][c]);
+    Acc A = 0;
+#pragma unroll
+    for (int k = 0; k < kCombineWarps; ++k) A += red2[k][c];
     Acc o = A * inv;
     if (a.literal)
       for (uint32_t i = 0; i < nsc_used; ++i)
@@ -764,11 +772,11 @@ cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
   if (a.g.elem == 4) {
     cudaFuncSetAttribute(combine_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    return launch_chained(combine_kernel<double>, grid, dim3(128), smem, st, a);
+    return launch_chained(combine_kernel<double>, grid, dim3(kCombineWarps * 32), smem, st, a);
   } else {
     cudaFuncSetAttribute(combine_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    return launch_chained(combine_kernel<float>, grid, dim3(128), smem, st, a);
+    return launch_chained(combine_kernel<float>, grid, dim3(kCombineWarps * 32), smem, st, a);
   }
 }
 
