@@ -134,6 +134,7 @@ __device__ __forceinline__ uint64_t order_key(double d) {
 // (two 7-bit digits), stopping as soon as the threshold bucket is taken
 // whole; every element at or above the threshold is selected.
 constexpr int kTopkThreads = 256;
+constexpr uint32_t kTopkSmemKeys = 5632;  // order keys cached in smem (44 KB) up to this n
 
 __device__ __forceinline__ uint32_t topk_digit(uint64_t key, uint32_t id, int p) {
   return p < 8 ? (uint32_t)(key >> (56 - 8 * p)) & 0xffu : (p == 8 ? (id >> 7) & 0x7fu : id & 0x7fu);
@@ -148,6 +149,19 @@ __global__ void __launch_bounds__(kTopkThreads) select_topk_kernel(SelectArgs a)
   __shared__ uint32_t hist[256];
   __shared__ uint32_t sh_digit, sh_need, sh_done;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // the order keys are computed once (pass 0) and re-read from shared memory
+  // by the later passes and the final marking, not from L2 each time
+  extern __shared__ uint64_t keys_sm[];
+  const bool cached = a.n <= kTopkSmemKeys;
+  auto key_of = [&](uint32_t i, int pass) -> uint64_t {
+    if (!cached) return order_key(sc[i]);
+    if (pass == 0) {
+      const uint64_t k = order_key(sc[i]);
+      keys_sm[i] = k;
+      return k;
+    }
+    return keys_sm[i];
+  };
 
   uint64_t key_pre = 0;  // chosen key digits so far (passes < 8)
   uint32_t id_pre = 0;   // chosen id digits (passes 8, 9)
@@ -164,7 +178,7 @@ __global__ void __launch_bounds__(kTopkThreads) select_topk_kernel(SelectArgs a)
     for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < a.n; i += blockDim.x) {
-      const uint64_t key = order_key(sc[i]);
+      const uint64_t key = key_of(i, p);
       if (match(key, i, p)) atomicAdd(&hist[topk_digit(key, i, p)], 1u);
     }
     __syncthreads();
@@ -211,7 +225,7 @@ __global__ void __launch_bounds__(kTopkThreads) select_topk_kernel(SelectArgs a)
   const uint32_t all_heads = (g.G >= 32) ? 0xffffffffu : ((1u << g.G) - 1u);
   const uint32_t bit = (g.Gs == g.G) ? (1u << h) : all_heads;
   for (uint32_t i = threadIdx.x; i < a.n; i += blockDim.x) {
-    const uint64_t key = order_key(sc[i]);
+    const uint64_t key = key_of(i, 1);  // each thread re-reads only its own keys
     bool sel;
     if (p < 8) {
       sel = (key >> (56 - 8 * p)) >= key_pre;
@@ -270,8 +284,9 @@ uint32_t select_max_blocks() { return kSelectMaxN; }
 // leaves it zeroed again.  `sel` is not written: the order is a cold read.
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
   if (a.n == 0) return cudaSuccess;
-  cudaError_t e = launch_chained(select_topk_kernel, dim3(a.g.Gs, a.g.S), dim3(kTopkThreads), 0,
-                                 st, a);
+  const size_t smem = a.n <= kTopkSmemKeys ? (size_t)a.n * 8 : 0;
+  cudaError_t e = launch_chained(select_topk_kernel, dim3(a.g.Gs, a.g.S), dim3(kTopkThreads),
+                                 smem, st, a);
   if (e != cudaSuccess) return e;
   return launch_chained(select_union_kernel, dim3(a.g.S), dim3(256), 0, st, a);
 }
