@@ -615,7 +615,16 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
   // Fast tier on s1 (low priority), overlapped with the PCIe-bound slow
   // stream on s0.  It is forked after select so it never competes with the
   // critical path append -> score -> select for SM slots.
-  const uint32_t nfc = (uint32_t)((F + h->FC - 1) / h->FC);
+  // With slow work in the step the fast tier runs hidden under it, so it is
+  // cut into at most ~16 chunks per stream: fewer partial rows for the
+  // combine, which is on the critical path (small S only; large S already
+  // has long chunks).  Without slow work it keeps the GPU-filling split.
+  uint32_t FCs = h->FC;
+  if (n > 0 && k > 0) {
+    const uint64_t want = ((h->l_fast + g.B + 15) / 16 + h->TT - 1) / h->TT * h->TT;
+    FCs = (uint32_t)std::max<uint64_t>(FCs, want);
+  }
+  const uint32_t nfc = (uint32_t)((F + FCs - 1) / FCs);
   auto fork_fast = [&]() -> int {
     CU(h, cudaEventRecord(h->ev_fork, h->s0));
     CU(h, cudaStreamWaitEvent(h->s1, h->ev_fork, 0));
@@ -626,7 +635,7 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       a.part = h->fpart;
       a.front = h->fast_front;
       a.F = (uint32_t)F;
-      a.FC = h->FC;
+      a.FC = FCs;
       a.nfc = nfc;
       a.scale_log2 = scale_log2;
       {
@@ -644,7 +653,7 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
     a.part = h->fpart;
     a.front = h->fast_front;
     a.F = (uint32_t)F;
-    a.FC = h->FC;
+    a.FC = FCs;
     a.nfc = nfc;
     a.TT = h->TT;
     a.stages = kFastStages;
