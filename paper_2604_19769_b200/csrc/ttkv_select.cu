@@ -253,27 +253,46 @@ __global__ void __launch_bounds__(kSelectThreads) select_union_kernel(SelectArgs
   const uint32_t nwarps = blockDim.x >> 5;
   if (threadIdx.x == 0) base_sh = 0;
   __syncthreads();
-  for (uint32_t base = 0; base < a.n; base += blockDim.x) {
-    const uint32_t b = base + threadIdx.x;
-    const uint32_t m = b < a.n ? mask[b] : 0u;
-    if (b < a.n) mask[b] = 0u;
-    const uint32_t ballot = __ballot_sync(0xffffffffu, m != 0u);
-    if (lane == 0) warp_tot[warp] = __popc(ballot);
-    __syncthreads();
-    uint32_t before = 0, total = 0;
-    for (uint32_t w = 0; w < nwarps; ++w) {
-      const uint32_t t = warp_tot[w];
-      before += (w < warp) ? t : 0u;
-      total += t;
+  // the mask words of kPre consecutive tiles are loaded together (one L2
+  // round trip), then compacted tile by tile from registers
+  constexpr int kPre = 8;
+  for (uint32_t base0 = 0; base0 < a.n; base0 += kPre * blockDim.x) {
+    uint32_t mv[kPre];
+#pragma unroll
+    for (int u = 0; u < kPre; ++u) {
+      const uint32_t b = base0 + u * blockDim.x + threadIdx.x;
+      mv[u] = b < a.n ? mask[b] : 0u;
     }
-    if (m != 0u) {
-      const uint32_t pos = base_sh + before + __popc(ballot & ((1u << lane) - 1u));
-      a.union_ids[(uint64_t)s * g.n_cap + pos] = b;
-      a.union_mask[(uint64_t)s * g.n_cap + pos] = m;
+#pragma unroll
+    for (int u = 0; u < kPre; ++u) {
+      const uint32_t b = base0 + u * blockDim.x + threadIdx.x;
+      if (b < a.n) mask[b] = 0u;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) base_sh += total;
-    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kPre; ++u) {
+      const uint32_t base = base0 + u * blockDim.x;
+      if (base < a.n) {  // CTA-uniform
+        const uint32_t b = base + threadIdx.x;
+        const uint32_t m = mv[u];
+        const uint32_t ballot = __ballot_sync(0xffffffffu, m != 0u);
+        if (lane == 0) warp_tot[warp] = __popc(ballot);
+        __syncthreads();
+        uint32_t before = 0, total = 0;
+        for (uint32_t w = 0; w < nwarps; ++w) {
+          const uint32_t t = warp_tot[w];
+          before += (w < warp) ? t : 0u;
+          total += t;
+        }
+        if (m != 0u) {
+          const uint32_t pos = base_sh + before + __popc(ballot & ((1u << lane) - 1u));
+          a.union_ids[(uint64_t)s * g.n_cap + pos] = b;
+          a.union_mask[(uint64_t)s * g.n_cap + pos] = m;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) base_sh += total;
+        __syncthreads();
+      }
+    }
   }
   if (threadIdx.x == 0) a.union_count[s] = base_sh;
 }
