@@ -443,39 +443,12 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
     }
     fence_mbar_init();
   }
-  for (uint32_t i = threadIdx.x; i < 512; i += blockDim.x) qsf[i] = make_uint4(0, 0, 0, 0);
-  // q in log2 units, normalized per head by a power of two so that
-  // |q_c s_c| <= |q|max * kTcKeyScaleBound lands below 2^15: the fp16 hi part
-  // of q * s cannot overflow for any query or record (ttkv_launch.h)
-  if (threadIdx.x < 8) usc[threadIdx.x] = 0.f;
-  __syncthreads();
-  const float* qb = a.q + (uint64_t)s * G * 128;
-  const float sl = (float)a.scale_log2;
-  for (uint32_t i = threadIdx.x; i < G * 128; i += blockDim.x)
-    atomicMax(reinterpret_cast<uint32_t*>(usc) + i / 128, __float_as_uint(fabsf(qb[i] * sl)));
-  __syncthreads();
-  {
-    float f = 1.f, uns = 1.f;
-    if (threadIdx.x < 8) f = pow2_normalizer(usc[threadIdx.x] * kTcKeyScaleBound, 24, &uns);
-    __syncthreads();
-    if (threadIdx.x < 8) {
-      usc[threadIdx.x] = uns;  // 2^24: the subnormal K codes
-      mst[threadIdx.x] = f;    // scratch until the stats are initialized below
-    }
-  }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < GT * 128; i += blockDim.x)
-    qsm[i] = (i / 128 < G) ? (qb[i] * sl) * mst[i / 128] : 0.f;
-  __syncthreads();
-  if (threadIdx.x < 8) {
-    mst[threadIdx.x] = -INFINITY;
-    lst[threadIdx.x] = 0.0f;
-  }
-  __syncthreads();
+  __syncthreads();  // the barriers are initialized: the producer may start
   const uint32_t* uids = a.union_ids + (uint64_t)s * g.n_cap + i0;
   const uint32_t* umask = a.union_mask + (uint64_t)s * g.n_cap + i0;
 
   if (warp == 0) {
+    // the first records are in flight while the consumers stage q below
     if (lane == 0) {
       const uint64_t evict_first = l2_evict_first_policy();
       for (uint32_t i = 0; i < nb; ++i) {
@@ -492,9 +465,41 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
     return;
   }
 
-  const uint32_t cw = warp - 1, ct = threadIdx.x - 32;
-  const uint32_t gq = lane >> 2, qq = lane & 3;  // fragment row group / thread in group
+  // ---- consumer prologue (named barrier 1 over the consumer warps only) ----
   const int nthreads_c = kSlowConsumerWarps * 32;
+  const uint32_t ct = threadIdx.x - 32;
+  for (uint32_t i = ct; i < 512; i += nthreads_c) qsf[i] = make_uint4(0, 0, 0, 0);
+  // q in log2 units, normalized per head by a power of two so that
+  // |q_c s_c| <= |q|max * kTcKeyScaleBound lands below 2^15: the fp16 hi part
+  // of q * s cannot overflow for any query or record (ttkv_launch.h)
+  if (ct < 8) usc[ct] = 0.f;
+  named_bar(1, nthreads_c);
+  const float* qb = a.q + (uint64_t)s * G * 128;
+  const float sl = (float)a.scale_log2;
+  for (uint32_t i = ct; i < G * 128; i += nthreads_c)
+    atomicMax(reinterpret_cast<uint32_t*>(usc) + i / 128, __float_as_uint(fabsf(qb[i] * sl)));
+  named_bar(1, nthreads_c);
+  {
+    float f = 1.f, uns = 1.f;
+    if (ct < 8) f = pow2_normalizer(usc[ct] * kTcKeyScaleBound, 24, &uns);
+    named_bar(1, nthreads_c);
+    if (ct < 8) {
+      usc[ct] = uns;  // 2^24: the subnormal K codes
+      mst[ct] = f;    // scratch until the stats are initialized below
+    }
+  }
+  named_bar(1, nthreads_c);
+  for (uint32_t i = ct; i < GT * 128; i += nthreads_c)
+    qsm[i] = (i / 128 < G) ? (qb[i] * sl) * mst[i / 128] : 0.f;
+  named_bar(1, nthreads_c);
+  if (ct < 8) {
+    mst[ct] = -INFINITY;
+    lst[ct] = 0.0f;
+  }
+  named_bar(1, nthreads_c);
+
+  const uint32_t cw = warp - 1;
+  const uint32_t gq = lane >> 2, qq = lane & 3;  // fragment row group / thread in group
   // PV ownership: channels c0 .. c0 + 3, heads 2qq, 2qq + 1
   const uint32_t c0 = 32 * cw + 4 * gq;
   float acc[4][2];
