@@ -208,10 +208,31 @@ int ttkv_gpu_eviction_pending(struct ttkv_gpu* h, int* pending);
 
 /* ---- state / cold path ------------------------------------------------------ */
 int ttkv_gpu_state(struct ttkv_gpu* h, ttkv_state* st);
-/* fetched_blocks of the last step for (stream, head), in select_top_k's
- * schedule order (score desc, block id desc), from the step's fp64 scores. */
+/* fetched_blocks of the last step for (stream, head) (engine.hpp:29,
+ * engine.cpp:58): the set the GPU selected and streamed (the head's bits of
+ * the per-stream union, as ttkv_gpu_read_selected returns it), put in
+ * select_top_k's order (relevance.cpp:29-43: score desc, block id desc) by
+ * the step's fp64 scores.  TTKV_EERROR if the GPU's set does not hold
+ * exactly resolve(n) blocks. */
 int ttkv_gpu_read_fetched(struct ttkv_gpu* h, uint32_t stream, uint32_t head, uint64_t* out,
                           uint64_t cap, uint64_t* n);
+/* The block ids the last step's slow kernel streamed for (stream, head), in
+ * ascending block id: select_topk_kernel's radix-selected set as the union
+ * compaction recorded it.  No reference counterpart (it is the set of
+ * fetched_blocks, relevance.cpp:40-42); exposed so callers and tests can check
+ * the GPU's own selection. */
+int ttkv_gpu_read_selected(struct ttkv_gpu* h, uint32_t stream, uint32_t head, uint32_t* out,
+                           uint64_t cap, uint64_t* n);
+/* The last step's per-stream union: ascending block ids and, per id, the
+ * bitmask of the query heads that selected it (each record crosses PCIe once
+ * per step).  *n = union size. */
+int ttkv_gpu_read_union(struct ttkv_gpu* h, uint32_t stream, uint32_t* ids, uint32_t* head_masks,
+                        uint64_t cap, uint64_t* n);
+/* The last step's fp64 block scores for (stream, head) (score_block,
+ * relevance.cpp:19-27, one per slow block); *n = 0 when the step fetched
+ * nothing (scoring is skipped then). */
+int ttkv_gpu_read_scores(struct ttkv_gpu* h, uint32_t stream, uint32_t head, double* out,
+                         uint64_t cap, uint64_t* n);
 /* Slow block in the reference's QuantizedBlock layout (16-bit payloads as
  * float32).  Any output pointer may be NULL.  Sizes: packed_k
  * packed_bytes(B*d_k, key_bits), params 2*d floats, centroid d_k floats. */
@@ -282,7 +303,8 @@ int ttkv_gpu_dequantize_block(int device, const uint8_t* packed_k, const uint8_t
 int ttkv_gpu_score_blocks(int device, const float* query, const float* centroids, uint64_t n,
                           uint32_t d, double* scores);
 /* select_top_k (relevance.cpp:29-43): the k ids ordered by (score desc, id
- * desc).  n <= 8192. */
+ * desc).  Any n < 2^31: one shared-memory bitonic CTA up to 8192 scores, a
+ * global-memory bitonic network above. */
 int ttkv_gpu_select_top_k(int device, const double* scores, const uint64_t* ids, uint64_t n,
                           uint64_t k, uint64_t* out);
 uint64_t ttkv_fast_capacity(const ttkv_tier_config* cfg); /* 0 + last_error on error */

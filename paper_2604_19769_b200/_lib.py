@@ -68,7 +68,8 @@ EXPORTS = [
     "ttkv_gpu_synchronize", "ttkv_gpu_prefill", "ttkv_gpu_prefill_synthetic",
     "ttkv_gpu_prefill_device",
     "ttkv_gpu_decode_step", "ttkv_gpu_decode_step_device", "ttkv_gpu_read_step_counters",
-    "ttkv_gpu_state", "ttkv_gpu_read_fetched", "ttkv_gpu_read_block", "ttkv_gpu_serialize_block",
+    "ttkv_gpu_state", "ttkv_gpu_read_fetched", "ttkv_gpu_read_selected", "ttkv_gpu_read_union",
+    "ttkv_gpu_read_scores", "ttkv_gpu_read_block", "ttkv_gpu_serialize_block",
     "ttkv_gpu_dump_slow_tier", "ttkv_gpu_restore_slow_tier", "ttkv_gpu_read_fast", "ttkv_gpu_locate", "ttkv_gpu_set_timing",
     "ttkv_gpu_kernel_times", "ttkv_gpu_read_timeline", "ttkv_gpu_peer_gather_init",
     "ttkv_gpu_peer_gather_open", "ttkv_gpu_peer_gather_output", "ttkv_gpu_peer_gather_close",
@@ -112,6 +113,9 @@ def lib():
         "ttkv_gpu_read_step_counters": (i32, [vp, P(u64), P(u64)]),
         "ttkv_gpu_state": (i32, [vp, P(StateC)]),
         "ttkv_gpu_read_fetched": (i32, [vp, u32, u32, vp, u64, P(u64)]),
+        "ttkv_gpu_read_selected": (i32, [vp, u32, u32, vp, u64, P(u64)]),
+        "ttkv_gpu_read_union": (i32, [vp, u32, vp, vp, u64, P(u64)]),
+        "ttkv_gpu_read_scores": (i32, [vp, u32, u32, vp, u64, P(u64)]),
         "ttkv_gpu_read_block": (i32, [vp, u32, u64, vp, vp, vp, vp, vp, P(u64)]),
         "ttkv_gpu_serialize_block": (i32, [vp, u32, u64, vp, u64, P(u64)]),
         "ttkv_gpu_dump_slow_tier": (i32, [vp, u32, C.c_char_p]),

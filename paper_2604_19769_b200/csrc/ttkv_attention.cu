@@ -657,9 +657,10 @@ __global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs
   for (int k = 0; k < kCombineWarps; ++k) Lt += red[k];
   const Acc inv = Acc(1) / Lt;
   // the weighted sum over partials for this CTA's channel slice
-  // [c_lo, c_hi) (blockIdx.y; several slices when S*G is small): warp w takes
-  // partials w, w+4, ..., lane l channels c_lo + l + 32j (coalesced segments
-  // of each partial row), two partials in flight; warps meet in smem
+  // [c_lo, c_hi) (blockIdx.y; several slices when S*G is small): warp w of
+  // the kCombineWarps takes partials w, w + kCombineWarps, ..., lane l
+  // channels c_lo + l + 32j (coalesced segments of each partial row), kU = 8
+  // partial rows in flight; warps meet in smem
   const uint32_t cw = (g.d_v + gridDim.y - 1) / gridDim.y;
   const uint32_t c_lo = blockIdx.y * cw, c_hi = min(g.d_v, c_lo + cw);
   __shared__ Acc red2[kCombineWarps][kMaxD];

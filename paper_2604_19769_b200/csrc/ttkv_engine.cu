@@ -452,8 +452,21 @@ int ensure_blocks(ttkv_gpu* h, uint64_t need) {
   h->scores = nscores;
   CU(h, realloc_dev((void**)&h->mask, S * cap * sizeof(uint32_t)));
   CU(h, cudaMemset(h->mask, 0, S * cap * sizeof(uint32_t)));  // select leaves it zeroed
-  CU(h, realloc_dev((void**)&h->uids, S * cap * sizeof(uint32_t)));
-  CU(h, realloc_dev((void**)&h->umask, S * cap * sizeof(uint32_t)));
+  // the last step's union (the records it streamed) stays readable too
+  // (ttkv_gpu_read_selected / read_fetched)
+  uint32_t *nuids = nullptr, *numask = nullptr;
+  CU(h, cudaMalloc((void**)&nuids, S * cap * sizeof(uint32_t)));
+  CU(h, cudaMalloc((void**)&numask, S * cap * sizeof(uint32_t)));
+  if (old_cap && h->last_k && h->uids) {
+    CU(h, cudaMemcpy2D(nuids, cap * 4, h->uids, old_cap * 4, old_cap * 4, S,
+                       cudaMemcpyDeviceToDevice));
+    CU(h, cudaMemcpy2D(numask, cap * 4, h->umask, old_cap * 4, old_cap * 4, S,
+                       cudaMemcpyDeviceToDevice));
+  }
+  if (h->uids) cudaFree(h->uids);
+  if (h->umask) cudaFree(h->umask);
+  h->uids = nuids;
+  h->umask = numask;
   h->g.n_cap = cap;
   if (h->opt.serial_schedule) {
     CU(h, realloc_dev((void**)&h->stage_arena, arena_bytes));
@@ -1281,6 +1294,75 @@ int ttkv_gpu_state(ttkv_gpu* h, ttkv_state* st) {
   return TTKV_OK;
 }
 
+namespace {
+// The records the last step's slow kernel streamed for (stream, head): the
+// per-stream union (select_union_kernel, ascending block id) filtered by the
+// head's bit of the union mask.  Cold path.
+int selected_of(ttkv_gpu* h, uint32_t stream, uint32_t head, std::vector<uint32_t>& ids) {
+  ids.clear();
+  if (h->last_k == 0) return TTKV_OK;
+  CU(h, cudaSetDevice(h->dev));
+  CU(h, cudaStreamSynchronize(h->s0));
+  uint32_t cnt = 0;
+  CU(h, cudaMemcpy(&cnt, h->ucount + stream, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  if (cnt > h->last_n)
+    return set_err(h, TTKV_EERROR, "selection: union larger than the slow tier");
+  std::vector<uint32_t> u(cnt), m(cnt);
+  const uint64_t off = (uint64_t)stream * h->g.n_cap;
+  if (cnt) {
+    CU(h, cudaMemcpy(u.data(), h->uids + off, cnt * 4ull, cudaMemcpyDeviceToHost));
+    CU(h, cudaMemcpy(m.data(), h->umask + off, cnt * 4ull, cudaMemcpyDeviceToHost));
+  }
+  for (uint32_t i = 0; i < cnt; ++i)
+    if (m[i] >> head & 1u) ids.push_back(u[i]);
+  return TTKV_OK;
+}
+}  // namespace
+
+int ttkv_gpu_read_selected(ttkv_gpu* h, uint32_t stream, uint32_t head, uint32_t* out,
+                           uint64_t cap, uint64_t* n) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  if (stream >= h->g.S || head >= h->g.G) return set_err(h, TTKV_ESHAPE, "stream/head out of range");
+  std::vector<uint32_t> ids;
+  if (int rc = selected_of(h, stream, head, ids)) return rc;
+  if (n) *n = ids.size();
+  if (out)
+    for (uint64_t i = 0; i < ids.size() && i < cap; ++i) out[i] = ids[i];
+  return TTKV_OK;
+}
+
+int ttkv_gpu_read_union(ttkv_gpu* h, uint32_t stream, uint32_t* ids, uint32_t* head_masks,
+                        uint64_t cap, uint64_t* n) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  if (stream >= h->g.S) return set_err(h, TTKV_ESHAPE, "stream out of range");
+  if (n) *n = 0;
+  if (h->last_k == 0) return TTKV_OK;
+  CU(h, cudaSetDevice(h->dev));
+  CU(h, cudaStreamSynchronize(h->s0));
+  uint32_t cnt = 0;
+  CU(h, cudaMemcpy(&cnt, h->ucount + stream, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  if (n) *n = cnt;
+  const uint64_t off = (uint64_t)stream * h->g.n_cap, m = std::min<uint64_t>(cnt, cap);
+  if (ids && m) CU(h, cudaMemcpy(ids, h->uids + off, m * 4, cudaMemcpyDeviceToHost));
+  if (head_masks && m) CU(h, cudaMemcpy(head_masks, h->umask + off, m * 4, cudaMemcpyDeviceToHost));
+  return TTKV_OK;
+}
+
+int ttkv_gpu_read_scores(ttkv_gpu* h, uint32_t stream, uint32_t head, double* out, uint64_t cap,
+                         uint64_t* n) {
+  if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
+  if (stream >= h->g.S || head >= h->g.G) return set_err(h, TTKV_ESHAPE, "stream/head out of range");
+  const uint64_t n_sc = h->last_k ? h->last_n : 0;  // scoring runs only when a fetch does
+  if (n) *n = n_sc;
+  if (!out || n_sc == 0) return TTKV_OK;
+  const uint32_t hs = h->g.Gs == h->g.G ? head : 0;
+  CU(h, cudaSetDevice(h->dev));
+  CU(h, cudaStreamSynchronize(h->s0));
+  CU(h, cudaMemcpy(out, h->scores + ((uint64_t)stream * h->g.Gs + hs) * h->g.n_cap,
+                   std::min(n_sc, cap) * sizeof(double), cudaMemcpyDeviceToHost));
+  return TTKV_OK;
+}
+
 int ttkv_gpu_read_fetched(ttkv_gpu* h, uint32_t stream, uint32_t head, uint64_t* out,
                           uint64_t cap, uint64_t* n) {
   if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
@@ -1288,19 +1370,23 @@ int ttkv_gpu_read_fetched(ttkv_gpu* h, uint32_t stream, uint32_t head, uint64_t*
   const uint64_t k = h->last_k;
   if (n) *n = k;
   if (!out || k == 0) return TTKV_OK;
-  // select_top_k's order (relevance.cpp:29-43): stable_sort by score desc,
-  // then block id desc -- from the step's bit-exact fp64 scores; the GPU
-  // selected exactly this order's first k as a set
+  // fetched_blocks = the set the GPU selected and streamed (the union row of
+  // this head), put in select_top_k's order (relevance.cpp:29-43: score desc,
+  // then block id desc) by the step's bit-exact fp64 scores.  A strict total
+  // order, so sorting the top-k set alone gives the prefix of the
+  // reference's stable_sort over all n.
+  std::vector<uint32_t> ids;
+  if (int rc = selected_of(h, stream, head, ids)) return rc;
+  if (ids.size() != k)
+    return set_err(h, TTKV_EERROR,
+                   "selection: the GPU streamed " + std::to_string(ids.size()) +
+                       " blocks for stream " + std::to_string(stream) + " head " +
+                       std::to_string(head) + ", expected " + std::to_string(k));
   const uint32_t hs = h->g.Gs == h->g.G ? head : 0;
-  const uint64_t n_sc = h->last_n;
-  std::vector<double> sc(n_sc);
-  CU(h, cudaSetDevice(h->dev));
-  CU(h, cudaStreamSynchronize(h->s0));
+  std::vector<double> sc(h->last_n);
   CU(h, cudaMemcpy(sc.data(), h->scores + ((uint64_t)stream * h->g.Gs + hs) * h->g.n_cap,
-                   n_sc * sizeof(double), cudaMemcpyDeviceToHost));
-  std::vector<uint32_t> ids(n_sc);
-  for (uint64_t i = 0; i < n_sc; ++i) ids[i] = (uint32_t)i;
-  std::stable_sort(ids.begin(), ids.end(), [&](uint32_t x, uint32_t y) {
+                   h->last_n * sizeof(double), cudaMemcpyDeviceToHost));
+  std::sort(ids.begin(), ids.end(), [&](uint32_t x, uint32_t y) {
     if (sc[x] != sc[y]) return sc[x] > sc[y];
     return x > y;
   });

@@ -1,8 +1,10 @@
 // ttkv_freefn.cu -- the reference's stateless numeric free functions on the GPU
 // (the cold-path API surface of the drop-in; the hot path fuses these):
 //   dequantize_block  quantizer.cpp:90-113, 157-170  (bit-exact fp64 affine)
-//   score_block       relevance.cpp:19-27            (bit-exact fp64, unfused)
-//   select_top_k      relevance.cpp:29-43            (bitonic sort, total order)
+//   score_block       relevance.cpp:19-27            (bit-exact fp64, one exact fma per term)
+//   select_top_k      relevance.cpp:29-43            (bitonic sort, total order: one CTA
+//                                                     in shared memory up to 8192 scores,
+//                                                     a global-memory network above)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -80,6 +82,29 @@ __global__ void topk_free_kernel(const double* scores, const uint64_t* ids, uint
   for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) out[i] = id[i];
 }
 
+// Global-memory bitonic network for select_top_k above the shared-memory
+// kernel's 8192 scores: one launch per (size, stride) stage, one thread per
+// compare-exchange pair, the same order as topk_free_kernel.
+__global__ void topk_keys_kernel(const double* scores, uint64_t* key, uint32_t n, uint32_t N2) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < N2; i += gridDim.x * blockDim.x)
+    key[i] = i < n ? order_key_free(scores[i]) : 0ull;
+}
+
+__global__ void bitonic_stage_kernel(uint64_t* key, uint64_t* id, uint32_t N2, uint32_t size,
+                                     uint32_t stride) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < N2 / 2;
+       i += gridDim.x * blockDim.x) {
+    const uint32_t lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+    const bool desc = (lo & size) == 0;
+    const uint64_t kl = key[lo], kh = key[hi], il = id[lo], ih = id[hi];
+    const bool less = (kl < kh) || (kl == kh && il < ih);
+    if (less == desc) {
+      key[lo] = kh; key[hi] = kl;
+      id[lo] = ih; id[hi] = il;
+    }
+  }
+}
+
 // Thread-local, grow-only device scratch for the stateless entry points:
 // token-at-a-time callers (10^4 quantize_block / dequantize_block calls in the
 // reference's acceptance gate) were dominated by a cudaMalloc + cudaFree pair
@@ -88,15 +113,20 @@ __global__ void topk_free_kernel(const double* scores, const uint64_t* ids, uint
 // thread.
 void* scratch(int slot, size_t bytes, cudaError_t* err) {
   struct Pool {
-    int dev = -1;
     void* p[8] = {};
     size_t cap[8] = {};
   };
-  thread_local Pool pool;
+  constexpr int kMaxDev = 64;
+  thread_local Pool pools[kMaxDev];  // one pool per device: a thread that
+                                     // alternates devices keeps (and reuses) both
   int dev = 0;
   *err = cudaGetDevice(&dev);
   if (*err != cudaSuccess) return nullptr;
-  if (pool.dev != dev) pool = Pool{dev};  // another device: start over (old blocks stay)
+  if (dev < 0 || dev >= kMaxDev) {
+    *err = cudaErrorInvalidDevice;
+    return nullptr;
+  }
+  Pool& pool = pools[dev];
   bytes = bytes ? bytes : 16;
   if (pool.cap[slot] < bytes) {
     const size_t want = std::max(bytes, 2 * pool.cap[slot]);
@@ -198,19 +228,35 @@ int ttkv_gpu_select_top_k(int device, const double* scores, const uint64_t* ids,
                           uint64_t k, uint64_t* out) {
   if (k > n) k = n;
   if (n == 0 || k == 0) return TTKV_OK;
-  if (n > 8192) {
-    ttkv_dev::set_last_error("select_top_k: more than 8192 blocks");
+  if (n > (1ull << 31)) {
+    ttkv_dev::set_last_error("select_top_k: more than 2^31 blocks");
     return TTKV_ECONFIG;
   }
   FCU(cudaSetDevice(device));
-  uint32_t N2 = 2;
+  uint64_t N2 = 2;
   while (N2 < n) N2 <<= 1;
   DevBuf ds(0), di(1), dout(2);
   FCU(ds.alloc(n * 8));
-  FCU(di.alloc(n * 8));
+  FCU(di.alloc(N2 * 8));
   FCU(dout.alloc(k * 8));
   FCU(cudaMemcpy(ds.p, scores, n * 8, cudaMemcpyHostToDevice));
   FCU(cudaMemcpy(di.p, ids, n * 8, cudaMemcpyHostToDevice));
+  if (N2 > 8192) {
+    DevBuf dk(3);
+    FCU(dk.alloc(N2 * 8));
+    FCU(cudaMemset((uint64_t*)di.p + n, 0, (N2 - n) * 8));
+    const unsigned grid = (unsigned)std::min<uint64_t>((N2 / 2 + 255) / 256, 148 * 16);
+    ttkv_dev::topk_keys_kernel<<<grid, 256>>>((const double*)ds.p, (uint64_t*)dk.p, (uint32_t)n,
+                                               (uint32_t)N2);
+    for (uint64_t size = 2; size <= N2; size <<= 1)
+      for (uint64_t stride = size >> 1; stride > 0; stride >>= 1)
+        ttkv_dev::bitonic_stage_kernel<<<grid, 256>>>((uint64_t*)dk.p, (uint64_t*)di.p,
+                                                       (uint32_t)N2, (uint32_t)size,
+                                                       (uint32_t)stride);
+    FCU(cudaGetLastError());
+    FCU(cudaMemcpy(out, di.p, k * 8, cudaMemcpyDeviceToHost));
+    return TTKV_OK;
+  }
   const size_t smem = (size_t)N2 * 16;
   FCU(cudaFuncSetAttribute(ttkv_dev::topk_free_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem));

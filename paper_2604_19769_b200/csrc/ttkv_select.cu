@@ -2,12 +2,14 @@
 //
 // score_blocks replaces the engine's scoring loop (engine.cpp:51-56) over
 // score_block (relevance.cpp:19-27): s = sum_i double(q_i) * double(c_i),
-// sequential in i, unfused (__dmul_rn/__dadd_rn) -- bit-exact with the
-// reference, so top-k ties are decided exactly as on the CPU.
+// sequential in i, one __fma_rn per term (the product of two float-valued
+// doubles is exact, so this equals the reference's separate multiply + add) --
+// bit-exact with the reference, so top-k ties are decided exactly as on the CPU.
 // select_topk replaces SelectionPolicy::resolve + select_top_k
 // (relevance.cpp:10-17, 29-43): a radix selection of the k largest
 // (score, block_id) pairs -- a total order, so the set equals the prefix of
-// std::stable_sort's order, which ttkv_gpu_read_fetched reproduces on demand.
+// std::stable_sort's order.  ttkv_gpu_read_fetched reads this set back (the
+// union row below) and orders it by the same scores on demand.
 // For GQA it also builds the per-stream union of the G selected sets plus a
 // per-block head mask, so every record crosses PCIe once per step.
 //
@@ -128,8 +130,8 @@ __device__ __forceinline__ uint64_t order_key(double d) {
 // One CTA per (stream, selection head): the top-k SET by radix selection.
 // The attention needs only which blocks each head selected; their order (the
 // reference's fetched_blocks, select_top_k's stable_sort by score desc, id
-// desc) is a report field, materialized on demand by ttkv_gpu_read_fetched
-// from the same fp64 scores.  The k-th largest (key, id) pair is found MSB
+// desc) is a report field: ttkv_gpu_read_fetched reads this kernel's set back
+// from the union row and sorts it by the same fp64 scores.  The k-th largest (key, id) pair is found MSB
 // first over the 64-bit order key (8-bit digits) and then the 14-bit block id
 // (two 7-bit digits), stopping as soon as the threshold bucket is taken
 // whole; every element at or above the threshold is selected.

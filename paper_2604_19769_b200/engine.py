@@ -300,6 +300,36 @@ class MultiStreamEngine:
                                                C.byref(n)), self._h)
         return out[:n.value]
 
+    def read_selected(self, stream: int, head: int = 0) -> np.ndarray:
+        """The block ids the last step's slow kernel streamed for (stream,
+        head), ascending (the GPU's own top-k set)."""
+        n = C.c_uint64()
+        _check(self._lib.ttkv_gpu_read_selected(self._h, stream, head, None, 0, C.byref(n)),
+               self._h)
+        out = np.zeros(max(1, n.value), np.uint32)
+        _check(self._lib.ttkv_gpu_read_selected(self._h, stream, head, _ptr(out), n.value,
+                                                C.byref(n)), self._h)
+        return out[:n.value]
+
+    def read_union(self, stream: int):
+        """(ids, head_masks) of the last step's per-stream union, ascending."""
+        n = C.c_uint64()
+        _check(self._lib.ttkv_gpu_read_union(self._h, stream, None, None, 0, C.byref(n)), self._h)
+        ids = np.zeros(max(1, n.value), np.uint32)
+        masks = np.zeros(max(1, n.value), np.uint32)
+        _check(self._lib.ttkv_gpu_read_union(self._h, stream, _ptr(ids), _ptr(masks), n.value,
+                                             C.byref(n)), self._h)
+        return ids[:n.value], masks[:n.value]
+
+    def read_scores(self, stream: int, head: int = 0) -> np.ndarray:
+        """The last step's fp64 block scores for (stream, head)."""
+        n = C.c_uint64()
+        _check(self._lib.ttkv_gpu_read_scores(self._h, stream, head, None, 0, C.byref(n)), self._h)
+        out = np.zeros(max(1, n.value), np.float64)
+        _check(self._lib.ttkv_gpu_read_scores(self._h, stream, head, _ptr(out), n.value,
+                                              C.byref(n)), self._h)
+        return out[:n.value]
+
     def read_block(self, stream: int, block_id: int) -> dict:
         cfg = self.config
         B = cfg.block_size

@@ -155,6 +155,43 @@ def make_inputs(S, ctx, T, dk, dv, G, seed, fp16):
     return pk, pv, dkk, dvv, dq  # dq: [S, T, G, dk]
 
 
+def check_streamed_sets(eng, s, expected, G):
+    """The GPU's own selection (ttkv_gpu_read_selected / read_union: the
+    records the slow kernel streamed) equals `expected[g]` as a set for every
+    head, and the per-stream union is exactly their union with the right head
+    bits (relevance.cpp:29-43; each record streamed once)."""
+    want = {}
+    for g in range(G):
+        exp = np.sort(np.asarray(expected[g], np.int64))
+        got = eng.read_selected(s, g).astype(np.int64)
+        assert np.array_equal(got, exp), (s, g, len(got), len(exp))
+        for b in exp:
+            want[int(b)] = want.get(int(b), 0) | (1 << g)
+    ids, masks = eng.read_union(s)
+    assert list(ids) == sorted(want), s
+    assert [int(m) for m in masks] == [want[int(b)] for b in ids], s
+
+
+def host_top_k(scores, k):
+    """select_top_k (relevance.cpp:29-43) on the host: score desc, id desc."""
+    ids = np.arange(len(scores), dtype=np.int64)
+    order = np.lexsort((-ids, -np.asarray(scores, np.float64)))
+    return order[:k]
+
+
+def check_every_list(eng, S, G, k):
+    """Every (stream, head) list the GPU streamed equals the top-k of the
+    step's bit-exact device scores taken on the host; returns the union size."""
+    union = 0
+    for s in range(S):
+        exp = [host_top_k(eng.read_scores(s, g), k) for g in range(G)]
+        for g in range(G):
+            assert np.array_equal(eng.read_fetched(s, g).astype(np.int64), exp[g]), (s, g)
+        check_streamed_sets(eng, s, exp, G)
+        union += len(set(np.concatenate(exp).tolist()))
+    return union
+
+
 def run_parity(T_, *, S=2, G=1, d=32, dv=None, B=32, l_fast=128, kb=8, vb=4, elem=2, ctx=600,
                steps=6, frac=0.45, top_k=None, mode=0, seed=100, prefill_chunks=1,
                check_blocks=True, literal=False, slow_tier=0, q_mul=1.0, kv_mul=1.0):
@@ -191,6 +228,7 @@ def run_parity(T_, *, S=2, G=1, d=32, dv=None, B=32, l_fast=128, kb=8, vb=4, ele
             assert rep.blocks_scored == o["blocks_scored"]
             assert rep.eviction_occurred == o["eviction_occurred"]
             assert rep.bytes_transferred == o["bytes_transferred"]
+            check_streamed_sets(eng, s, o["fetched"], G)
             for g in range(G):
                 assert np.array_equal(rep.fetched_blocks[s][g], o["fetched"][g]), (t, s, g)
                 e = rel_err(rep.output[s, g], o["output"][g])
@@ -210,10 +248,19 @@ def run_parity(T_, *, S=2, G=1, d=32, dv=None, B=32, l_fast=128, kb=8, vb=4, ele
 
 @pytest.mark.parametrize("ctx", [70000, 140000])
 def test_engine_many_blocks_selection(gpu, ctx):
-    # n = 4371 / 8746 slow blocks per stream: the selection sort runs with
-    # N2 = 8192 / 16384 and several compare-exchange pairs per thread, the
-    # regime of cfg5's 256K context (n = 2016) and beyond
+    # n = 4371 / 8746 slow blocks per stream: the radix select with its order
+    # keys cached in shared memory (n <= 5632) and uncached (re-read from L2
+    # every pass); the streamed sets are read back and compared exactly
     run_parity(gpu, S=2, G=2, d=16, B=16, l_fast=64, ctx=ctx, steps=2, check_blocks=False)
+
+
+@pytest.mark.parametrize("elem", [4, 2])
+def test_engine_uncached_radix_select_d128(gpu, elem):
+    # d = 128 with n = 6234 > kTopkSmemKeys (5632): the uncached radix path at
+    # the hot head dimension; fp32 ring -> outputs to 1e-9, so one wrongly
+    # streamed block could not hide under the tolerance either
+    run_parity(gpu, S=2, G=4, d=128, B=16, l_fast=256, ctx=100000, steps=2, elem=elem,
+               check_blocks=False)
 
 
 def test_engine_reference_unit_config(gpu):
@@ -429,44 +476,81 @@ def test_gpu_vs_reference_engine_fp32_ring(gpu):
 # ---------------------------------------------------------------------------
 # full-size properties (cfg1 shape) with device-generated KV
 # ---------------------------------------------------------------------------
+def full_size_step(eng, q, kn, vn, sampled, k, B, d, kb=8, vb=4):
+    """One decode step at a full BASELINE shape, checked three ways
+    (engine.cpp:22-93):
+      * sampled streams re-derived on the host from the read-back fast tier +
+        records: fp64 scores bit-equal to the device's, every head's fetched
+        list identical in order to select_top_k's, the output within 1e-3 of an
+        fp64 recomputation over exactly the selected blocks;
+      * the record evicted at the end of the step equals the oracle's
+        quantize_block of the fast-tier rows it came from (bit-exact);
+      * every (stream, head) set the slow kernel streamed equals the host
+        top-k of that head's device scores, and the per-step union matches the
+        reported union / PCIe bytes."""
+    S, G = q.shape[0], q.shape[1]
+    st0 = eng.state()
+    n = st0["slow_blocks"]
+    before = {s: (eng.read_fast(s), [eng.read_block(s, b) for b in range(n)]) for s in sampled}
+    rep = eng.decode_step(q, kn, vn, fetched=True)
+    assert rep.blocks_scored == n and rep.blocks_fetched == k
+    for s in sampled:
+        (fk, fv, first), blocks = before[s]
+        dk = [O.dequantize_tensor(b["packed_keys"], B, d, kb, b["key_params"]) for b in blocks]
+        dv = [O.dequantize_tensor(b["packed_values"], B, d, vb, b["value_params"]) for b in blocks]
+        for g in range(G):
+            scores = np.array([O.oracle().tko_score_block(q[s, g], b["key_centroid"], d)
+                               for b in blocks])
+            assert np.array_equal(eng.read_scores(s, g), scores), (s, g)
+            sel = np.zeros(k, np.uint64)
+            O.oracle().tko_select_top_k(scores, None, n, k, sel)
+            assert np.array_equal(rep.fetched_blocks[s][g], sel), (s, g)
+            assert np.array_equal(eng.read_selected(s, g), np.sort(sel)), (s, g)
+            K = np.concatenate([fk.astype(np.float64), kn[s][None].astype(np.float64)] +
+                               [dk[int(b)] for b in sel])
+            V = np.concatenate([fv.astype(np.float64), vn[s][None].astype(np.float64)] +
+                               [dv[int(b)] for b in sel])
+            lg = K @ q[s, g].astype(np.float64) / np.sqrt(d)
+            w = np.exp(lg - lg.max())
+            ref = (w[:, None] * V).sum(0) / w.sum()
+            assert rel_err(rep.output[s, g], ref) < OUT_TOL, (s, g)
+        if rep.eviction_occurred:
+            # tier_store.cpp:71-98: the oldest B fast tokens become block n
+            blk = eng.read_block(s, n)
+            assert blk["first_position"] == first
+            okp, opk = O.quantize_tensor(fk[:B], kb)
+            ovp, opv = O.quantize_tensor(fv[:B], vb)
+            ocen = np.zeros(d, np.float32)
+            O.oracle().tko_centroid(np.ascontiguousarray(fk[:B]).reshape(-1), B, d, ocen)
+            assert blk["packed_keys"].tobytes() == opk.tobytes(), s
+            assert blk["packed_values"].tobytes() == opv.tobytes(), s
+            assert blk["key_params"].tobytes() == okp.tobytes(), s
+            assert blk["value_params"].tobytes() == ovp.tobytes(), s
+            assert blk["key_centroid"].tobytes() == ocen.tobytes(), s
+    union = check_every_list(eng, S, G, k)
+    assert rep.union_blocks == union
+    assert rep.pcie_bytes == union * eng.state()["payload_bytes"]
+    return rep
+
+
+def step_inputs(rng, S, G, d):
+    q = rng.standard_normal((S, G, d)).astype(np.float32)
+    kn = O.fp16_round(rng.standard_normal((S, d)))
+    vn = O.fp16_round(rng.standard_normal((S, d)))
+    return q, kn, vn
+
+
 def test_full_size_cfg1_sampled_streams(gpu):
-    """cfg1: 32 MHA streams, 32K ctx, 4K fp16 fast tier, K8/V4, 0.45.  KV is
-    generated on device; two streams are re-derived on the host from the
-    read-back fast tier + records: selection must be identical and the output
-    within tolerance of an fp64 recomputation."""
+    """cfg1: 32 MHA streams, 32K ctx, 4K fp16 fast tier, K8/V4, 0.45 (n = 224,
+    k = 101).  KV is generated on device; the step evicts one block per stream."""
     T_ = gpu
     S, d, B, lf, ctx = 32, 128, 128, 4096, 32768
     cfg = T_.TierConfig(hbm_budget_bytes=lf * 256 * 2, d_k=d, d_v=d, block_size=B)
     eng = T_.MultiStreamEngine(cfg, n_streams=S, heads_per_stream=1, reserve_tokens=ctx + 256)
     eng.prefill_synthetic(ctx, seed=11)
-    rng = np.random.default_rng(0)
-    q = rng.standard_normal((S, 1, d)).astype(np.float32)
-    kn = O.fp16_round(rng.standard_normal((S, d)))
-    vn = O.fp16_round(rng.standard_normal((S, d)))
-    n = eng.state()["slow_blocks"]
-    assert n == 224
-    before = {s: (eng.read_fast(s), [eng.read_block(s, b) for b in range(n)]) for s in (0, S - 1)}
-    rep = eng.decode_step(q, kn, vn, fetched=True)
-    assert rep.blocks_scored == 224 and rep.blocks_fetched == 101 and rep.eviction_occurred
-    for s in (0, S - 1):
-        (fk, fv, _), blocks = before[s]
-        scores = np.array([O.oracle().tko_score_block(q[s, 0], b["key_centroid"], d)
-                           for b in blocks])
-        sel = np.zeros(101, np.uint64)
-        O.oracle().tko_select_top_k(scores, None, n, 101, sel)
-        assert np.array_equal(rep.fetched_blocks[s][0], sel)
-        keys = [fk.astype(np.float64), kn[s][None].astype(np.float64)]
-        vals = [fv.astype(np.float64), vn[s][None].astype(np.float64)]
-        for b in sel:
-            blk = blocks[int(b)]
-            keys.append(O.dequantize_tensor(blk["packed_keys"], B, d, 8, blk["key_params"]))
-            vals.append(O.dequantize_tensor(blk["packed_values"], B, d, 4, blk["value_params"]))
-        K = np.concatenate(keys)
-        V = np.concatenate(vals)
-        lg = K @ q[s, 0].astype(np.float64) / np.sqrt(d)
-        w = np.exp(lg - lg.max())
-        ref = (w[:, None] * V).sum(0) / w.sum()
-        assert rel_err(rep.output[s, 0], ref) < OUT_TOL
+    assert eng.state()["slow_blocks"] == 224
+    rep = full_size_step(eng, *step_inputs(np.random.default_rng(0), S, 1, d), (0, S - 1), 101, B, d)
+    assert rep.eviction_occurred
     # every record streamed exactly once per step: union == k for G=1
     assert rep.union_blocks == S * 101
     eng.close()
@@ -477,49 +561,64 @@ def test_full_size_cfg2_sampled_streams(gpu, slow_tier):
     """cfg2 at full size: 256 streams (32 layers x 8 KV heads) x 4 query heads,
     128K ctx, 4K fp16 fast tier, K8/V4, 0.45 per query head (n = 992 blocks,
     k = 447), slow tier in pinned DRAM (CUDA-core streaming kernel) or HBM
-    (tensor-core kernel).  KV is generated on device; two streams are
-    re-derived on the host from the read-back fast tier + records: all four
-    heads' selections identical in order, outputs within tolerance of an fp64
-    recomputation; the per-step union over all 1024 (stream, head) lists
-    equals the records the kernel streamed."""
+    (tensor-core kernel); all 1024 streamed sets checked."""
     T_ = gpu
     S, G, d, B, lf, ctx = 256, 4, 128, 128, 4096, 131072
     cfg = T_.TierConfig(hbm_budget_bytes=lf * 256 * 2, d_k=d, d_v=d, block_size=B)
     eng = T_.MultiStreamEngine(cfg, n_streams=S, heads_per_stream=G, reserve_tokens=ctx + 256,
                                slow_tier=slow_tier)
     eng.prefill_synthetic(ctx, seed=23)
-    rng = np.random.default_rng(1)
-    q = rng.standard_normal((S, G, d)).astype(np.float32)
-    kn = O.fp16_round(rng.standard_normal((S, d)))
-    vn = O.fp16_round(rng.standard_normal((S, d)))
-    n = eng.state()["slow_blocks"]
-    assert n == 992
-    sampled = (7, S - 3)
-    before = {s: (eng.read_fast(s), [eng.read_block(s, b) for b in range(n)]) for s in sampled}
-    rep = eng.decode_step(q, kn, vn, fetched=True)
-    assert rep.blocks_scored == 992 and rep.blocks_fetched == 447
-    for s in sampled:
-        (fk, fv, _), blocks = before[s]
-        dk = [O.dequantize_tensor(b["packed_keys"], B, d, 8, b["key_params"]) for b in blocks]
-        dv = [O.dequantize_tensor(b["packed_values"], B, d, 4, b["value_params"]) for b in blocks]
-        for g in range(G):
-            scores = np.array([O.oracle().tko_score_block(q[s, g], b["key_centroid"], d)
-                               for b in blocks])
-            sel = np.zeros(447, np.uint64)
-            O.oracle().tko_select_top_k(scores, None, n, 447, sel)
-            assert np.array_equal(rep.fetched_blocks[s][g], sel), (s, g)
-            K = np.concatenate([fk.astype(np.float64), kn[s][None].astype(np.float64)] +
-                               [dk[int(b)] for b in sel])
-            V = np.concatenate([fv.astype(np.float64), vn[s][None].astype(np.float64)] +
-                               [dv[int(b)] for b in sel])
-            lg = K @ q[s, g].astype(np.float64) / np.sqrt(d)
-            w = np.exp(lg - lg.max())
-            ref = (w[:, None] * V).sum(0) / w.sum()
-            assert rel_err(rep.output[s, g], ref) < OUT_TOL
-    union = sum(len(set(np.concatenate([np.asarray(f, np.int64) for f in rep.fetched_blocks[s]])))
-                for s in range(S))
-    assert rep.union_blocks == union
-    assert rep.pcie_bytes == union * eng.state()["payload_bytes"]
+    assert eng.state()["slow_blocks"] == 992
+    rep = full_size_step(eng, *step_inputs(np.random.default_rng(1), S, G, d), (7, S - 3), 447,
+                         B, d)
+    assert rep.eviction_occurred
+    eng.close()
+
+
+@pytest.mark.parametrize("slow_tier", [0, 1])
+def test_full_size_cfg3_batch16(gpu, slow_tier):
+    """cfg3 at full size: LLaMA-3-8B GQA at 32K ctx, batch 16 -> 4096 streams
+    (32 layers x 8 KV heads x 16 requests) x 4 query heads (n = 224, k = 101):
+    24 GB of records in pinned DRAM or HBM; all 16,384 streamed sets checked,
+    three sampled streams (first request, middle, last) re-derived."""
+    T_ = gpu
+    S, G, d, B, lf, ctx = 4096, 4, 128, 128, 4096, 32768
+    cfg = T_.TierConfig(hbm_budget_bytes=lf * 256 * 2, d_k=d, d_v=d, block_size=B)
+    eng = T_.MultiStreamEngine(cfg, n_streams=S, heads_per_stream=G, reserve_tokens=ctx + 256,
+                               slow_tier=slow_tier)
+    eng.prefill_synthetic(ctx, seed=31)
+    assert eng.state()["slow_blocks"] == 224
+    rep = full_size_step(eng, *step_inputs(np.random.default_rng(3), S, G, d), (0, 2053, S - 1),
+                         101, B, d)
+    assert rep.eviction_occurred
+    eng.close()
+
+
+@pytest.mark.parametrize("slow_tier", [0, 1])
+def test_full_size_cfg5_256k_after_eviction_period(gpu, slow_tier):
+    """cfg5 hot shape: 256 streams x 4 heads grown to 256K ctx through one full
+    eviction period of decode (128 steps, the first evicting a block per
+    stream into the slow tier), then the 128th step checked in full at
+    n = 2016, k = 908 -- the scored slow tier includes the decode-time
+    eviction's records."""
+    T_ = gpu
+    S, G, d, B, lf = 256, 4, 128, 128, 4096
+    ctx0 = 262144 - 128
+    cfg = T_.TierConfig(hbm_budget_bytes=lf * 256 * 2, d_k=d, d_v=d, block_size=B)
+    eng = T_.MultiStreamEngine(cfg, n_streams=S, heads_per_stream=G, reserve_tokens=262144 + 256,
+                               slow_tier=slow_tier)
+    eng.prefill_synthetic(ctx0, seed=47)
+    assert eng.state()["slow_blocks"] == 2015
+    rng = np.random.default_rng(5)
+    # the first step evicts block 2015 from the fast tier: check it bit-exact
+    rep = full_size_step(eng, *step_inputs(rng, S, G, d), (11,), 907, B, d)
+    assert rep.eviction_occurred and eng.state()["slow_blocks"] == 2016
+    for _ in range(126):
+        rep = eng.decode_step(*step_inputs(rng, S, G, d))
+        assert not rep.eviction_occurred and rep.blocks_fetched == 908
+    assert eng.state()["appended"] == 262143
+    rep = full_size_step(eng, *step_inputs(rng, S, G, d), (11, S - 1), 908, B, d)
+    assert not rep.eviction_occurred and eng.state()["fast_tokens"] == 4096
     eng.close()
 
 
@@ -559,3 +658,23 @@ def test_engine_d64_tensor_core_fast_tier(gpu, slow_tier):
     # d = 64, B = 64: the tensor-core fast tier with one 64-channel box (ND = 1);
     # the slow tier takes the CUDA-core kernel (host DRAM or HBM)
     run_parity(gpu, S=3, G=4, d=64, B=64, l_fast=256, ctx=3000, steps=4, slow_tier=slow_tier)
+
+
+@pytest.mark.parametrize("n", [1, 37, 8192, 8193, 20000, 70001])
+def test_free_select_top_k_any_n(gpu, n):
+    # the stateless select_top_k (relevance.cpp:29-43) on arbitrary ids and
+    # heavily tied scores: shared-memory bitonic CTA up to 8192, global-memory
+    # network above; order = score desc, id desc, for every k
+    import ctypes as C
+    from paper_2604_19769_b200 import _lib as L
+    rng = np.random.default_rng(n)
+    scores = np.round(rng.standard_normal(n) * 4) / 4  # many exact ties
+    scores[rng.integers(0, n, max(1, n // 50))] = -0.0
+    ids = rng.permutation(3 * n)[:n].astype(np.uint64)
+    order = np.lexsort((-ids.astype(np.int64), -scores))
+    p = lambda a: a.ctypes.data_as(C.c_void_p)
+    for k in sorted({1, n // 3, n}):
+        out = np.zeros(max(1, k), np.uint64)
+        rc = L.lib().ttkv_gpu_select_top_k(0, p(scores), p(ids), n, k, p(out))
+        assert rc == 0, L.lib().ttkv_last_error()
+        assert np.array_equal(out[:k], ids[order[:k]]), (n, k)
