@@ -51,10 +51,39 @@ WORKLOADS = {
 }
 
 
-def metric_for(w):
-    if w == "cfg2":
-        return "decode tokens/s at 128K ctx (LLaMA-3-8B GQA, all layers, batch 1)"
-    return f"decode tokens/s ({WORKLOADS[w]['desc']})"
+def ctx_label(ctx):
+    return f"{ctx // 1024}K" if ctx % 1024 == 0 else str(ctx)
+
+
+def desc_for(name, ctx):
+    """The workload description at the effective context (--ctx overrides)."""
+    d = WORKLOADS[name]["desc"]
+    base = ctx_label(WORKLOADS[name]["ctx"])
+    return d if ctx == WORKLOADS[name]["ctx"] else d.replace(f"{base} ctx", f"{ctx_label(ctx)} ctx")
+
+
+def metric_for(name, ctx):
+    if name == "cfg2":
+        return (f"decode tokens/s at {ctx_label(ctx)} ctx "
+                "(LLaMA-3-8B GQA, all layers, batch 1)")
+    return f"decode tokens/s ({desc_for(name, ctx)})"
+
+
+def make_config(args, world, S):
+    """The `config` object, identical in both arms for the same command line."""
+    w = args.w
+    mode = "heads" if w["batch"] == 1 else "requests"
+    return {
+        "workload": desc_for(args.workload, w["ctx"]) + (
+            f", {mode}-sharded over {world} GPUs" if world > 1 else ""),
+        "ctx": w["ctx"], "streams": w["layers"] * w["kv_heads"] * w["batch"],
+        "streams_per_gpu": S, "heads_per_stream": w["G"], "batch": w["batch"], "d": D,
+        "block": B, "l_fast": L_FAST, "bits": "K8/V4", "fetch_fraction": FRAC,
+        "selection": "group-shared" if args.group_select else "per-query-head (reference)",
+        "slow_tier": "pinned host DRAM, zero-copy PCIe" if args.slow_tier == "host" else "HBM",
+        "parallelism": f"{mode}-shard{world}" if world > 1 else "single",
+        "l2": "inputs larger than L2 (fp16 ring + slow tier far above 126 MB)",
+    }
 
 
 def parse():
@@ -79,7 +108,42 @@ def parse():
     a.w = dict(WORKLOADS[a.workload])
     if a.ctx:
         a.w["ctx"] = a.ctx
+    if a.gpus < 1:
+        p.error("--gpus must be >= 1")
     return a
+
+
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def self_launch(args):
+    """`bench.py --gpus N` outside torchrun: launch N ranks (one process per
+    GPU) under torch.distributed.run and exit with its status.  Fails loudly
+    when fewer than N devices are visible (TTKV_SHARE_DEVICE=1 runs every rank
+    on cuda:0 -- the test mode of the N>1 path on a one-GPU box)."""
+    if args.impl == "ours" and os.environ.get("TTKV_SHARE_DEVICE") != "1":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible",
+                  file=sys.stderr, flush=True)
+            sys.exit(2)
+    env = dict(os.environ)
+    if os.environ.get("TTKV_DIST_BACKEND", "nccl") == "nccl":
+        # communicator init on every rank stays visible in the log
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    print("self-launch: " + " ".join(cmd), file=sys.stderr, flush=True)
+    sys.exit(subprocess.call(cmd, env=env))
 
 
 def dist_env():
@@ -132,9 +196,16 @@ def cpu_throughput(ms_step, engines, total_engines, tokens_per_step):
 
 
 def run_reference(args):
+    """The reference arm: the unmodified reference engine (oracle/_ref) on the
+    host cores.  Each step is a bounded sample -- `engines` of the workload's
+    S x G reference Engines (one per (stream, query head)) decoding once on
+    all host threads; the full step is that sample time x `factor`
+    (total / sampled Engines, the Engines are independent).  `ms_per_step` and
+    `steps` are what actually ran; `value` is the extrapolated throughput."""
     rank, _, world = dist_env()
     if rank != 0:
         return
+    world = max(world, args.gpus)
     w = args.w
     S = w["layers"] * w["kv_heads"] * w["batch"]
     total_engines = S * w["G"]  # one reference Engine per (stream, q-head)
@@ -143,20 +214,24 @@ def run_reference(args):
     ms, pre_s, engines, threads = ref_sample(w["ctx"], n, w["G"],
                                              engines=total_engines if total_engines <= 64 else None)
     timed = ms[args.warmup:]
-    vals = [cpu_throughput(m, engines, total_engines, w["batch"]) for m in timed]
-    value = statistics.mean(vals)
+    factor = total_engines / engines
+    sample_ms = float(statistics.mean(timed))
+    value = cpu_throughput(sample_ms, engines, total_engines, w["batch"])
     sample = (f"{engines} reference Engines (1 per stream x q-head) at {w['ctx']} ctx on "
               f"{threads} threads, {args.steps} timed decode steps after {args.warmup} warm-up; "
               f"{scale_note(engines, total_engines)}")
     line = {
-        "impl": "reference", "metric": metric_for(args.workload), "value": value, "unit": UNIT,
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": w["batch"] * 1000.0 / value, "higher_is_better": True,
+        "impl": "reference", "metric": metric_for(args.workload, w["ctx"]), "value": value,
+        "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sample_ms, "higher_is_better": True,
         "scaling": "strong" if world > 1 and w["batch"] == 1 else "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (reference GaussianSource)",
-        "config": {"workload": w["desc"], "ctx": w["ctx"], "streams": S,
-                   "heads_per_stream": w["G"], "d": D, "block": B, "l_fast": L_FAST,
-                   "bits": "K8/V4", "fetch_fraction": FRAC},
+        "config": make_config(args, world, S // world),
+        "extrapolation": {
+            "engines_sampled": engines, "engines_total": total_engines, "factor": factor,
+            "sample_ms_per_step": sample_ms, "full_step_ms": sample_ms * factor,
+            "note": "ms_per_step is the sample's wall time per step; value = tokens per full "
+                    "step / (sample ms x factor)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -170,50 +245,110 @@ def run_reference(args):
 # clocks during the timed region
 # ---------------------------------------------------------------------------
 class Clocks:
+    """SM clocks and throttle reasons sampled DURING the timed region: an NVML
+    read when the region opens and closes plus a 10 ms sampler thread in
+    between (nvidia-smi -lms 100 when NVML is unavailable).  A region shorter
+    than ~50 ms cannot give 5 samples; `admissible` says whether it did."""
+    REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20),
+               ("hw_thermal_slowdown", 0x40), ("sw_power_cap", 0x4))
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device):
         self.device = device
+        self.samples = []  # (sm_mhz, max_mhz, reason bits)
         self.proc = None
-        self.lines = []
+        self.nvml = None
+        self.source = None
+
+    def _read(self):
+        n = self.nvml
+        sm = n.nvmlDeviceGetClockInfo(self.h, n.NVML_CLOCK_SM)
+        mx = n.nvmlDeviceGetMaxClockInfo(self.h, n.NVML_CLOCK_SM)
+        try:
+            rs = n.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:  # noqa: BLE001 -- older bindings
+            rs = n.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        self.samples.append((float(sm), float(mx), int(rs)))
+
+    def _loop(self):
+        while not self._stop.wait(0.01):
+            try:
+                self._read()
+            except Exception:  # noqa: BLE001
+                return
 
     def __enter__(self):
+        import threading
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except Exception:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            try:
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(_bus_id(self.device).encode())
+            except Exception:  # noqa: BLE001
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self._read()
+            self._stop = threading.Event()
+            self.th = threading.Thread(target=self._loop, daemon=True)
+            self.th.start()
+            self.source = "nvml 10 ms + region open/close"
+        except Exception:  # noqa: BLE001
+            self.nvml = None
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits", "-lms", "100"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.source = "nvidia-smi -lms 100"
+            except Exception:  # noqa: BLE001
+                self.proc = None
         return self
 
     def __exit__(self, *a):
+        if self.nvml is not None:
+            self._stop.set()
+            self.th.join(timeout=1)
+            try:
+                self._read()
+            except Exception:  # noqa: BLE001
+                pass
         if self.proc:
             self.proc.terminate()
             try:
                 out, _ = self.proc.communicate(timeout=5)
-            except Exception:
+            except Exception:  # noqa: BLE001
                 self.proc.kill()
                 out = ""
-            self.lines = [l for l in out.splitlines() if l.strip()]
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            bits = dict(self.REASONS)
+            for l in out.splitlines():
+                f = [x.strip() for x in l.split(",")]
+                try:
+                    sm, mx = float(f[1]), float(f[2])
+                except (ValueError, IndexError):
+                    continue
+                rs = sum(bits[n] for n, v in zip(names, f[5:9]) if v.lower().startswith("active"))
+                self.samples.append((sm, mx, rs))
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in self.lines:
-            f = [x.strip() for x in l.split(",")]
-            try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
-            except (ValueError, IndexError):
-                continue
-            for n, v in zip(names, f[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
+        sm = [x[0] for x in self.samples]
+        mx = max((x[1] for x in self.samples), default=None)
+        reasons = sorted({n for _, _, r in self.samples for n, b in self.REASONS if r & b})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "sm_mhz_min": min(sm) if sm else None, "reasons": reasons,
+                "samples": len(sm), "admissible": len(sm) >= 5, "source": self.source}
+
+
+def _bus_id(device):
+    """PCI bus id of a CUDA ordinal (the NVML handle of the same GPU)."""
+    import ctypes as C_
+    from paper_2604_19769_b200 import _lib as L
+    buf = C_.create_string_buffer(32)
+    if L.lib().ttkv_pci_bus_id(device, buf, 32) != 0:
+        raise RuntimeError("pci bus id unavailable")
+    return buf.value.decode()
 
 
 # ---------------------------------------------------------------------------
@@ -243,22 +378,48 @@ def load_traffic():
         return None
 
 
+def numa_nodes():
+    try:
+        return sorted(int(d[4:]) for d in os.listdir("/sys/devices/system/node")
+                      if d.startswith("node") and d[4:].isdigit())
+    except OSError:
+        return [0]
+
+
 def bind_numa(device):
     """Pin this rank to the CPUs of its GPU's NUMA node before the pinned
     slow-tier arena is allocated, so cudaHostAlloc's pages land on the node
     whose memory controller sits next to that GPU's PCIe root port (8-GPU
-    boxes have two sockets; each rank streams ~51 GB/s from host DRAM)."""
+    boxes have two sockets; each rank streams ~51 GB/s from host DRAM).
+    Returns what happened; on a multi-node host a failed binding is an error
+    (the per-GPU PCIe numbers would mix remote-socket traffic)."""
+    info = {"numa_nodes": len(numa_nodes()), "bound": False}
     try:
+        bus = _bus_id(device).lower()
+        info["bus_id"] = bus
+        try:
+            with open(f"/sys/bus/pci/devices/{bus}/numa_node") as f:
+                info["gpu_numa_node"] = int(f.read().strip())
+        except (OSError, ValueError):
+            info["gpu_numa_node"] = None
         import pynvml
         pynvml.nvmlInit()
-        h = pynvml.nvmlDeviceGetHandleByIndex(device)
+        try:
+            h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:  # noqa: BLE001
+            h = pynvml.nvmlDeviceGetHandleByIndex(device)
         words = pynvml.nvmlDeviceGetCpuAffinity(h, 16)
         cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1}
         cpus &= os.sched_getaffinity(0)
         if cpus:
             os.sched_setaffinity(0, cpus)
-    except Exception:  # noqa: BLE001 -- affinity is an optimisation only
-        pass
+            info["bound"] = True
+            info["cpus"] = len(cpus)
+    except Exception as e:  # noqa: BLE001
+        info["error"] = repr(e)
+        if info["numa_nodes"] > 1:
+            raise RuntimeError(f"bind_numa: multi-socket host and the binding failed: {e!r}")
+    return info
 
 
 def init_dist(torch, dist, local, world):
@@ -266,8 +427,10 @@ def init_dist(torch, dist, local, world):
     TTKV_SHARE_DEVICE=1 runs every rank on cuda:0 (exercises the N>1 path on a
     1-GPU box; the NVLink numbers need NCCL and one GPU per rank)."""
     share = os.environ.get("TTKV_SHARE_DEVICE") == "1"
+    if world > 1 and not share and torch.cuda.device_count() < world:
+        raise RuntimeError(f"{world} ranks but only {torch.cuda.device_count()} CUDA devices")
     dev = torch.device("cuda", 0 if share else local)
-    bind_numa(dev.index)
+    numa = bind_numa(dev.index)
     torch.cuda.set_device(dev)
     if world > 1:
         backend = os.environ.get("TTKV_DIST_BACKEND", "nccl")
@@ -275,7 +438,7 @@ def init_dist(torch, dist, local, world):
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-    return dev
+    return dev, numa
 
 
 def allreduce_max(t):
@@ -300,10 +463,77 @@ def setup_gather(eng, plan):
     if os.environ.get("TTKV_GATHER", "peer") == "peer":
         from paper_2604_19769_b200.sharding import PeerGather
         try:
-            return PeerGather(eng, plan), "combine fused with the all-gather over peer memory"
+            pg = PeerGather(eng, plan)
+            return pg, ("combine fused with the all-gather over peer memory "
+                        f"(P2P probe OK for all {plan.world} ranks)")
         except Exception as e:  # noqa: BLE001
-            print(f"peer gather unavailable ({e}); using NCCL all_gather", file=sys.stderr)
-    return None, "NCCL all_gather"
+            print(f"peer gather unavailable ({e}); using NCCL all_gather", file=sys.stderr,
+                  flush=True)
+            return None, f"NCCL all_gather (peer gather unavailable: {e})"
+    return None, "NCCL all_gather (TTKV_GATHER=nccl)"
+
+
+def traffic_for(kernel, workload):
+    """DRAM (and PCIe sysmem) traffic per launch of the dominant kernel from
+    its committed `ncu --set full` capture (profiles/traffic.json, written by
+    tools/stamp_traffic.py), reported only while the loaded kernel's SASS
+    signature equals the measured one; otherwise null with fresh=false."""
+    t = (load_traffic() or {}).get(f"{kernel}@{workload}")
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import kernel_sig
+        cur = kernel_sig.kernel_sig(kernel)
+    except Exception as e:  # noqa: BLE001 -- cuobjdump missing: cannot prove freshness
+        cur = f"unavailable: {e}"
+    if not t:
+        return None, None, {"source": None, "fresh": False, "loaded_sig": cur}
+    fresh = t.get("sig") is not None and t.get("sig") == cur
+    meta = {"source": t.get("source"), "git": t.get("git"), "sig": t.get("sig"),
+            "loaded_sig": cur, "fresh": fresh}
+    if not fresh:
+        return None, None, meta
+    return t.get("dram_bytes_per_launch"), t.get("sysmem_read_bytes_per_launch"), meta
+
+
+def read_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:  # noqa: BLE001
+        return {}
+
+
+def fast_tier_solo(T, cfg, S, G, dev, stream, args, torch):
+    """The fast-tier kernel timed alone (no slow work on the GPU beside it): a
+    second handle with the same S x L_FAST fp16 ring and no slow tier yet."""
+    n_kt = 5
+    e = T.MultiStreamEngine(cfg, T.SelectionPolicy(None, FRAC), n_streams=S, heads_per_stream=G,
+                            device=dev.index, reserve_tokens=L_FAST + 2 * B)
+    e.set_stream(stream.cuda_stream)
+    e.prefill_synthetic(L_FAST - 3 - n_kt, seed=99)
+    gen = torch.Generator(device=dev).manual_seed(123)
+    q = torch.randn(S, G, D, device=dev, generator=gen)
+    k = torch.randn(S, D, device=dev, generator=gen).half()
+    v = torch.randn(S, D, device=dev, generator=gen).half()
+    o = torch.empty(S, G, D, device=dev, dtype=torch.float64)
+    for _ in range(2):
+        e.decode_step_device(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), dtype=1)
+    torch.cuda.synchronize()
+    f0 = e.state()["fast_tokens"]
+    e.kernel_times(reset=True)
+    e.set_timing(True)
+    for _ in range(n_kt):
+        e.decode_step_device(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), dtype=1)
+    torch.cuda.synchronize()
+    e.set_timing(False)
+    kt = e.kernel_times(reset=True)
+    assert e.state()["slow_blocks"] == 0
+    e.close()
+    ms = kt["ms_fast"] / max(1, kt["n_fast"])
+    F = f0 + (n_kt + 1) / 2.0  # mean fast-tier length over the timed steps
+    byts = S * F * 2 * D * 2
+    return {"ms": ms, "tokens": F, "bytes": byts, "hbm_gbs": byts / (ms * 1e-3) / 1e9,
+            "note": "fast_attn timed alone: a handle with the same S x L_FAST ring, no slow tier"}
 
 
 def run_ours(args):
@@ -314,20 +544,22 @@ def run_ours(args):
     from paper_2604_19769_b200.sharding import ShardPlan, gather_outputs
 
     rank, local, world = dist_env()
-    dev = init_dist(torch, dist, local, world)
+    dev, numa = init_dist(torch, dist, local, world)
     w = args.w
     G, ctx, batch = w["G"], w["ctx"], w["batch"]
     mode = "heads" if batch == 1 else "requests"
     plan = ShardPlan(rank, world, w["layers"], w["kv_heads"], batch, mode)
     S = plan.n_local  # streams on this rank
+    host_tier = args.slow_tier == "host"
 
     cfg = T.TierConfig(hbm_budget_bytes=L_FAST * 2 * D * 2, d_k=D, d_v=D, bytes_full_precision=2,
                        block_size=B, key_bits=8, value_bits=4, fetch_fraction=FRAC)
-    n_steps_total = args.warmup + 2 * args.steps + 8  # timed + kernel-breakdown + e2e steps
+    max_steps = args.steps if args.steps_given else 2000
+    n_steps_total = args.warmup + 2 * max_steps + 16  # timed + kernel-breakdown + e2e steps
     eng = T.MultiStreamEngine(cfg, T.SelectionPolicy(None, FRAC), n_streams=S,
                               heads_per_stream=G, group_select=args.group_select, device=dev.index,
                               reserve_tokens=ctx + n_steps_total + B,
-                              slow_tier=0 if args.slow_tier == "host" else 1)
+                              slow_tier=0 if host_tier else 1)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
     eng.set_stream(stream.cuda_stream)
@@ -361,13 +593,24 @@ def run_ours(args):
     for i in range(args.warmup):
         step(i)
     barrier()
+    if not args.steps_given:
+        # default K: at least 10 steps and >= ~1 s of timed region (clock samples)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        step(args.warmup)
+        e1.record()
+        barrier()
+        one = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+        one = float(allreduce_max(one)[0]) if world > 1 else float(one[0])
+        args.steps = int(min(max_steps, max(10, -(-1000.0 // max(one, 1e-3)))))
+    base = args.warmup + 1
     st0 = eng.state()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(dev.index) as clk:
         barrier()
         ev0.record()
         for i in range(args.steps):
-            step(args.warmup + i)
+            step(base + i)
         ev1.record()
         barrier()
     ms_total = ev0.elapsed_time(ev1)
@@ -380,7 +623,7 @@ def run_ours(args):
     eng.kernel_times(reset=True)
     eng.set_timing(True)
     for i in range(n_kt):
-        step(args.warmup + args.steps + i)
+        step(base + args.steps + i)
     barrier()
     eng.set_timing(False)
     kt = eng.kernel_times(reset=True)
@@ -403,114 +646,118 @@ def run_ours(args):
     barrier()
     e2e_ms = (time.perf_counter() - t_e2e0) * 1000.0 / args.steps
 
-    # --- max over ranks ---------------------------------------------------------
-    vals = torch.tensor([ms_total, e2e_ms], device=dev, dtype=torch.float64)
+    # --- roofline of the dominant kernel ----------------------------------------
+    rec = st1["record_bytes"]
+    payload = st1["payload_bytes"]  # params are staged from the HBM mirror
+    slow_ms = kt["ms_slow"] / max(1, kt["n_slow"])
+    pcie_bytes_launch = union_last * payload
+    achieved = pcie_bytes_launch / (slow_ms * 1e-3) / 1e9 if slow_ms > 0 else 0.0
+    F = st1["fast_tokens"]
+    fast_bytes = S * F * 2 * D * 2
+    fast_conc_ms = kt["ms_fast"] / max(1, kt["n_fast"])
+    hbm_peak = read_peaks().get("hbm_gbs", 6650.0)
+    hbm_bytes_step = fast_bytes + S * st1["slow_blocks"] * D * 4 + union_last * (rec - payload)
+    fast_solo = fast_tier_solo(T, cfg, S, G, dev, stream, args, torch)
+    fast_solo.update({"hbm_peak": hbm_peak, "frac": fast_solo["hbm_gbs"] / hbm_peak,
+                      "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                      "concurrent_ms": fast_conc_ms,
+                      "concurrent_note": "wall time on the low-priority stream beside the slow "
+                                         "kernel (hidden under it), not an HBM rate"})
+
+    # --- per-rank facts and the max over ranks ----------------------------------
+    me = {"rank": rank, "device": dev.index, "numa": numa, "h2d_peak_gbs": h2d_peak,
+          "union_blocks": union_last, "pcie_bytes": pcie_bytes_launch if host_tier else 0,
+          "slow_kernel_ms": slow_ms, "pcie_gbs": achieved if host_tier else None,
+          "ms_timed": ms_total, "e2e_ms": e2e_ms}
+    ranks = [me]
     if world > 1:
-        vals = allreduce_max(vals)
-    ms_total, e2e_ms = float(vals[0]), float(vals[1])
+        ranks = [None] * world
+        dist.all_gather_object(ranks, me)
+    ms_total = max(r_["ms_timed"] for r_ in ranks)
+    e2e_ms = max(r_["e2e_ms"] for r_ in ranks)
     ms_step = ms_total / args.steps
     tokens_per_step = batch  # one generated token per request per step
     value = tokens_per_step * 1000.0 / ms_step
+    pcie_all = sum(r_["pcie_bytes"] for r_ in ranks)
 
-    # --- roofline of the dominant kernel (slow_stream_attn, PCIe-bound) ---------
-    rec = st1["record_bytes"]
-    payload = st1["payload_bytes"]  # params are staged from the HBM mirror
-    n_slow = kt["n_slow"] or 1
-    slow_ms = kt["ms_slow"] / n_slow
-    pcie_bytes_launch = union_last * payload
-    achieved = pcie_bytes_launch / (slow_ms * 1e-3) / 1e9 if slow_ms > 0 else 0.0
-    fast_ms = kt["ms_fast"] / max(1, kt["n_fast"])
-    F = st1["fast_tokens"]
-    fast_bytes = S * F * 2 * D * 2
-    peaks = {}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peaks = json.load(f)
-    except Exception:
-        pass
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    hbm_bytes_step = fast_bytes + S * st1["slow_blocks"] * D * 4 + union_last * (rec - payload)
-    host_tier = args.slow_tier == "host"
     if host_tier:  # records cross PCIe (zero-copy); params + centroids + fast tier from HBM
         t_roof_ms = max(hbm_bytes_step / (hbm_peak * 1e9),
                         pcie_bytes_launch / (h2d_peak * 1e9)) * 1e3
-        roof = {"bound": "pcie_h2d", "kernel": "slow_stream_attn", "achieved": achieved,
+        traffic, pcie_traffic, tmeta = traffic_for("slow_attn_kernel", args.workload)
+        roof = {"bound": "pcie_h2d", "kernel": "slow_attn_kernel", "achieved": achieved,
                 "peak": h2d_peak, "unit": "GB/s", "frac": achieved / h2d_peak,
                 "peak_source": "pinned cudaMemcpy H2D 256 MiB best of 10, measured in this run" +
-                               (", all ranks concurrently" if world > 1 else "")}
+                               (", all ranks concurrently" if world > 1 else ""),
+                "traffic": traffic, "pcie_traffic": pcie_traffic,
+                "algorithmic_bytes_per_launch": pcie_bytes_launch}
     else:  # HBM-resident slow tier: every byte of the step is an HBM byte
         hbm_bytes_step += pcie_bytes_launch
         t_roof_ms = hbm_bytes_step / (hbm_peak * 1e9) * 1e3
         slow_bytes = union_last * rec  # payload from the arena + params from the mirror
         ach = slow_bytes / (slow_ms * 1e-3) / 1e9 if slow_ms > 0 else 0.0
-        roof = {"bound": "hbm", "kernel": "slow_attn_tc", "achieved": ach, "peak": hbm_peak,
-                "unit": "GB/s", "frac": ach / hbm_peak,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"}
+        traffic, _, tmeta = traffic_for("slow_attn_tc_kernel", args.workload)
+        roof = {"bound": "hbm", "kernel": "slow_attn_tc_kernel", "achieved": ach,
+                "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)", "traffic": traffic,
+                "algorithmic_bytes_per_launch": slow_bytes}
         pcie_bytes_launch = 0
-    traffic = load_traffic() if args.workload == "cfg2" else None
 
     line = {
-        "metric": metric_for(args.workload), "value": value, "unit": UNIT, "n_gpus": world,
+        "metric": metric_for(args.workload, ctx), "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": True,
         "scaling": "strong" if world > 1 and mode == "heads" else "weak", "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (device N(0,1) KV rounded to fp16, random queries)",
-        "config": {
-            "workload": w["desc"] + (f", head-sharded over {world} GPUs" if plan.needs_gather else
-                                     (f", request-sharded over {world} GPUs" if world > 1 else "")),
-            "output_gather": gather_kind,
-            "ctx": ctx, "streams_per_gpu": S, "heads_per_stream": G, "batch": batch, "d": D,
-            "block": B, "l_fast": L_FAST, "bits": "K8/V4", "fetch_fraction": FRAC,
-            "selection": "group-shared" if args.group_select else "per-query-head (reference)",
-            "slow_tier": "pinned host DRAM, zero-copy PCIe" if args.slow_tier == "host" else "HBM",
-            "storage": "fp16 ring, u8 keys / u4 values, f32 params",
-            "parallelism": f"{mode}-shard{world}" if world > 1 else "single",
-            "l2": "inputs larger than L2 (fp16 ring + slow tier far above 126 MB)",
-        },
+        "config": make_config(args, world, S),
+        "output_gather": gather_kind,
+        "storage": "fp16 ring, u8 keys / u4 values, f32 params",
         "roofline": {
-            **roof,
-            "traffic": (traffic.get("slow_dram_bytes_per_launch") if host_tier
-                        else traffic.get("slow_tc_hbm_dram_bytes_per_launch")) if traffic else None,
-            "pcie_traffic": (traffic.get("slow_sysmem_read_bytes_per_launch")
-                             if traffic and host_tier else None),
-            "algorithmic_bytes_per_launch": pcie_bytes_launch if host_tier else union_last * rec,
+            **roof, "traffic_source": tmeta,
             "launch_ms": slow_ms,
             "tier_roofline_ms": t_roof_ms, "tier_frac": t_roof_ms / ms_step,
-            "fast_attn": {"ms": fast_ms, "hbm_gbs": fast_bytes / (fast_ms * 1e-3) / 1e9
-                          if fast_ms > 0 else None,
-                          "hbm_peak": hbm_peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-                          "note": "timed concurrently with slow_stream_attn on a second stream"},
+            "fast_attn": fast_solo,
         },
-        "pcie_bytes_per_token": pcie_bytes_launch * world / tokens_per_step,
-        "union_blocks_per_step": union_last,
+        "pcie_bytes_per_token": pcie_all / tokens_per_step,
+        "union_blocks_per_step": sum(r_["union_blocks"] for r_ in ranks),
         "kernel_ms_per_step": {k[3:]: v / n_kt for k, v in kt.items() if k.startswith("ms_")},
         "gpu_launches": launches,
         "e2e": {"value": tokens_per_step * 1000.0 / e2e_ms, "unit": UNIT,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "prefill_s": round(prefill_s, 2),
     }
+    if world > 1:
+        line["ranks"] = ranks
+    else:
+        line["numa"] = numa
     if rank == 0:
         line["clocks"] = clk.summary()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            total = S * G
-            ms, _, engines, threads = ref_sample(ctx, 2, G,
-                                                 engines=total if total <= 64 else None)
-            cv = cpu_throughput(float(ms[-1]), engines, total, tokens_per_step)
-            line["cpu_baseline"] = {
-                "value": cv, "unit": UNIT, "cores": threads, "kind": "reference",
-                "sample": (f"{engines} unmodified reference Engines at {ctx} ctx, "
-                           f"2 decode steps on {threads} threads (last timed: "
-                           f"{ms[-1]:.0f} ms), {scale_note(engines, total)}")}
-        except Exception as e:  # noqa: BLE001
-            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": host_cores(),
-                                    "kind": "reference", "sample": f"unavailable: {e}"}
+        line["cpu_baseline"] = cpu_baseline_line(ctx, G, S * G, tokens_per_step)
     eng.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def cpu_baseline_line(ctx, G, total, tokens_per_step, warm=2, timed=5, note=""):
+    """The unmodified reference engine on this box's host cores: `timed`
+    decode steps after `warm` of a bounded sample of Engines, extrapolated."""
+    try:
+        ms, _, engines, threads = ref_sample(ctx, warm + timed, G,
+                                             engines=total if total <= 64 else None)
+        m = float(statistics.mean(ms[warm:]))
+        return {
+            "value": cpu_throughput(m, engines, total, tokens_per_step), "unit": UNIT,
+            "cores": threads, "kind": "reference",
+            "sample": (f"{engines} unmodified reference Engines at {ctx} ctx{note}, {timed} "
+                       f"decode steps timed after {warm} on {threads} threads (mean {m:.0f} ms), "
+                       f"{scale_note(engines, total)}"),
+            "sample_ms_per_step": [round(float(x), 1) for x in ms[warm:]]}
+    except Exception as e:  # noqa: BLE001
+        return {"value": None, "unit": UNIT, "cores": host_cores(), "kind": "reference",
+                "sample": f"unavailable: {e}"}
 
 
 GROWTH_POINTS = (131072, 163840, 196608, 229376, 262144)
@@ -547,7 +794,7 @@ def run_growth(args):
     from paper_2604_19769_b200.sharding import ShardPlan, gather_outputs
 
     rank, local, world = dist_env()
-    dev = init_dist(torch, dist, local, world)
+    dev, numa = init_dist(torch, dist, local, world)
     w = args.w
     G = w["G"]
     plan = ShardPlan(rank, world, w["layers"], w["kv_heads"], w["batch"], "heads")
@@ -666,28 +913,22 @@ def run_growth(args):
     slow_ms = curve[-1]["slow_kernel_ms"]
     achieved = union_last * payload / (slow_ms * 1e-3) / 1e9 if slow_ms > 0 else 0.0
     evict_bytes = S * rec  # one record per stream per eviction step
+    growth_traffic = traffic_for("slow_attn_kernel", "cfg5")
     ek = [c["evict_kernel_ms"] for c in curve if c["eviction_steps"]]
     evict_kernel_ms = statistics.mean(ek) if ek else None
     line = {
-        "metric": metric_for(args.workload), "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": K * len(points), "warmup": args.warmup, "ms_per_step": ms_step,
+        "metric": metric_for(args.workload, points[-1]), "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": K * len(points), "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (device N(0,1) KV rounded to fp16, random queries)",
+        "output_gather": gather_kind,
         "config": {
-            "workload": w["desc"] + (f", head-sharded over {world} GPUs" if plan.needs_gather
-                                     else ""),
-            "output_gather": gather_kind,
+            **make_config(args, world, S),
             "growth_points": list(points), "steps_per_point": K,
             "timing": ("per point: one eviction period (B consecutive steps) timed with CUDA "
                        "events; value = 131072 tokens / trapezoid integral of ms/step over "
                        "the sampled 128K->256K curve"),
-            "streams_per_gpu": S, "heads_per_stream": G, "batch": 1, "d": D, "block": B,
-            "l_fast": L_FAST, "bits": "K8/V4", "fetch_fraction": FRAC,
-            "selection": "group-shared" if args.group_select else "per-query-head (reference)",
-            "slow_tier": "pinned host DRAM, zero-copy PCIe" if args.slow_tier == "host" else "HBM",
-            "parallelism": f"heads-shard{world}" if world > 1 else "single",
-            "l2": "inputs larger than L2 (slow tier 6.8-13.7 GB)",
         },
         "growth_curve": curve,
         "eviction": {"steps": len(evict_ms),
@@ -702,7 +943,9 @@ def run_growth(args):
             "achieved": achieved, "peak": h2d_peak, "unit": "GB/s", "frac": achieved / h2d_peak,
             "peak_source": "pinned cudaMemcpy H2D 256 MiB best of 10, measured in this run" +
                            (", all ranks concurrently" if world > 1 else ""),
-            "traffic": None, "algorithmic_bytes_per_launch": union_last * payload,
+            "traffic": growth_traffic[0], "pcie_traffic": growth_traffic[1],
+            "traffic_source": growth_traffic[2],
+            "algorithmic_bytes_per_launch": union_last * payload,
             "launch_ms": slow_ms},
         "kernel_ms_per_step": {k[3:]: v / (K * len(points)) for k, v in kt_tot.items()
                                if k.startswith("ms_")},
@@ -718,21 +961,9 @@ def run_growth(args):
     if rank == 0:
         line["clocks"] = clk.summary()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            ctx = points[-1]
-            total = S * G
-            ms, _, engines, threads = ref_sample(ctx, 2, G,
-                                                 engines=total if total <= 64 else None)
-            line["cpu_baseline"] = {
-                "value": cpu_throughput(float(ms[-1]), engines, total, 1), "unit": UNIT,
-                "cores": threads, "kind": "reference",
-                "sample": (f"{engines} unmodified reference Engines at {ctx} ctx (the end of the "
-                           f"growth; upper bound on its sustained rate), 2 decode steps on "
-                           f"{threads} threads (last timed: {ms[-1]:.0f} ms), "
-                           f"{scale_note(engines, total)}")}
-        except Exception as e:  # noqa: BLE001
-            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": host_cores(),
-                                    "kind": "reference", "sample": f"unavailable: {e}"}
+        line["cpu_baseline"] = cpu_baseline_line(
+            points[-1], G, S * G, 1,
+            note=" (the end of the growth; upper bound on its sustained rate)")
     eng.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -753,6 +984,7 @@ def run_layer_sequential(args):
     w = args.w
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
+    args.max_auto = args.steps if args.steps_given else 2000
     Lyr, G, ctx = w["layers"], w["G"], w["ctx"]
     S = w["kv_heads"] * w["batch"]
     cfg = T.TierConfig(hbm_budget_bytes=L_FAST * 2 * D * 2, d_k=D, d_v=D, bytes_full_precision=2,
@@ -763,7 +995,7 @@ def run_layer_sequential(args):
     for layer in range(Lyr):
         e = T.MultiStreamEngine(cfg, T.SelectionPolicy(None, FRAC), n_streams=S,
                                 heads_per_stream=G, device=0,
-                                reserve_tokens=ctx + args.warmup + args.steps + 2 * B,
+                                reserve_tokens=ctx + args.warmup + args.max_auto + 2 * B,
                                 slow_tier=0 if args.slow_tier == "host" else 1)
         e.set_stream(stream.cuda_stream)
         e.prefill_synthetic(ctx, seed=7000 + layer)
@@ -783,6 +1015,13 @@ def run_layer_sequential(args):
     for _ in range(args.warmup):
         token()
     torch.cuda.synchronize()
+    if not args.steps_given:  # >= 10 tokens and >= ~1 s of timed region
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        token()
+        e1.record()
+        torch.cuda.synchronize()
+        args.steps = int(min(args.max_auto, max(10, -(-1000.0 // max(e0.elapsed_time(e1), 1e-3)))))
     launches0 = sum(e.state()["launches"] for e in engs)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(0) as clk:
@@ -800,16 +1039,11 @@ def run_layer_sequential(args):
     host_tier = args.slow_tier == "host"
     hbm = sum(S * st["fast_tokens"] * 2 * D * 2 + S * st["slow_blocks"] * D * 4 for _ in engs) + \
         union * (st["record_bytes"] - st["payload_bytes"]) + (0 if host_tier else pcie)
-    peaks = {}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peaks = json.load(f)
-    except Exception:  # noqa: BLE001
-        pass
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_peak = read_peaks().get("hbm_gbs", 6650.0)
     t_roof = max(hbm / (hbm_peak * 1e9), (pcie / (h2d_peak * 1e9)) if host_tier else 0.0) * 1e3
     line = {
-        "metric": metric_for(args.workload) + ", layer-sequential", "value": w["batch"] * 1e3 / ms_step,
+        "metric": metric_for(args.workload, ctx) + ", layer-sequential",
+        "value": w["batch"] * 1e3 / ms_step,
         "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (device N(0,1) KV rounded to fp16, random queries)",
@@ -832,6 +1066,12 @@ def main():
     args = parse()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        if args.layer_sequential:
+            sys.exit("--layer-sequential runs on one GPU")
+        self_launch(args)
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}")
     if args.impl == "reference":
         run_reference(args)
     elif args.layer_sequential:

@@ -284,6 +284,14 @@ int ttkv_gpu_peer_gather_open(struct ttkv_gpu* h, const void* handles);
 int ttkv_gpu_peer_gather_output(struct ttkv_gpu* h, double** device_rows, int* timed_out);
 /* Unmaps the peers and frees the gathered buffer (steps stop publishing). */
 int ttkv_gpu_peer_gather_close(struct ttkv_gpu* h);
+/* Peer-access probe that must pass for every pair before _open: the PCI bus
+ * id of a device ("dddd:bb:dd.f", cudaDeviceGetPCIBusId), and whether
+ * `device` can load/store the memory of the GPU with bus id `peer_bus_id`
+ * (the same GPU -> 1; a GPU this process cannot see -> 0; otherwise
+ * cudaDeviceCanAccessPeer).  Callers exchange bus ids, probe every peer and
+ * fall back to an NCCL all-gather unless every rank reports 1. */
+int ttkv_pci_bus_id(int device, char* out, int len);
+int ttkv_peer_probe(int device, const char* peer_bus_id, int* can_access);
 
 /* ---- stateless entry points --------------------------------------------------- */
 /* quantize_block on the GPU (bit-exact).  Host inputs keys[rows][d_k],

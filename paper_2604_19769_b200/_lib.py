@@ -78,7 +78,7 @@ EXPORTS = [
     "ttkv_gpu_eviction_pending", "ttkv_gpu_dequantize_block", "ttkv_gpu_score_blocks",
     "ttkv_gpu_select_top_k", "ttkv_fast_capacity",
     "ttkv_modeled_block_bytes", "ttkv_packed_bytes", "ttkv_resolve", "ttkv_validate_config",
-    "ttkv_default_config",
+    "ttkv_default_config", "ttkv_pci_bus_id", "ttkv_peer_probe",
 ]
 
 _lib = None
@@ -144,6 +144,8 @@ def lib():
         "ttkv_resolve": (u64, [P(SelectionPolicyC), u64]),
         "ttkv_validate_config": (i32, [P(TierConfigC)]),
         "ttkv_default_config": (None, [P(TierConfigC)]),
+        "ttkv_pci_bus_id": (i32, [i32, C.c_char_p, i32]),
+        "ttkv_peer_probe": (i32, [i32, C.c_char_p, P(i32)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -1831,6 +1831,32 @@ int ttkv_gpu_peer_gather_init(ttkv_gpu* h, uint32_t n_ranks, uint32_t my_rank,
   return TTKV_OK;
 }
 
+int ttkv_pci_bus_id(int device, char* out, int len) {
+  if (!out || len < 13) return set_err(nullptr, TTKV_EINVAL, "pci bus id: buffer too small");
+  cudaError_t e = cudaDeviceGetPCIBusId(out, len, device);
+  if (e != cudaSuccess)
+    return set_err(nullptr, TTKV_ECUDA, std::string("cudaDeviceGetPCIBusId: ") + cudaGetErrorString(e));
+  return TTKV_OK;
+}
+
+int ttkv_peer_probe(int device, const char* peer_bus_id, int* can_access) {
+  if (!peer_bus_id || !can_access) return set_err(nullptr, TTKV_EINVAL, "null argument");
+  *can_access = 0;
+  int peer = -1;
+  if (cudaDeviceGetByPCIBusId(&peer, peer_bus_id) != cudaSuccess) {
+    cudaGetLastError();  // not visible to this process: no peer path
+    return TTKV_OK;
+  }
+  if (peer == device) {
+    *can_access = 1;
+    return TTKV_OK;
+  }
+  cudaError_t e = cudaDeviceCanAccessPeer(can_access, device, peer);
+  if (e != cudaSuccess)
+    return set_err(nullptr, TTKV_ECUDA, std::string("cudaDeviceCanAccessPeer: ") + cudaGetErrorString(e));
+  return TTKV_OK;
+}
+
 int ttkv_gpu_peer_gather_open(ttkv_gpu* h, const void* handles) {
   if (!h || !handles) return set_err(h, TTKV_EINVAL, "null argument");
   auto& p = h->pg;

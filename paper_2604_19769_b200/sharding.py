@@ -78,6 +78,43 @@ def gather_outputs(local_out, plan: ShardPlan, group=None):
     return x.reshape(R * L * H, G, d)
 
 
+class PeerUnavailable(RuntimeError):
+    """Some pair of ranks cannot map each other's memory (no P2P path)."""
+
+
+def probe_peers(device: int, group=None) -> dict:
+    """Exchange every rank's PCI bus id and check, on every rank, that its
+    device can access every other rank's GPU (ttkv_peer_probe:
+    cudaDeviceGetByPCIBusId + cudaDeviceCanAccessPeer).  Returns
+    {"bus_ids": [...], "ok": bool, "failed": [(rank, peer), ...]}, identical on
+    every rank."""
+    import ctypes as C
+
+    import torch.distributed as dist
+
+    from . import _lib as L
+
+    lib = L.lib()
+    buf = C.create_string_buffer(32)
+    from .engine import _check
+    _check(lib.ttkv_pci_bus_id(device, buf, 32))
+    me = buf.value.decode()
+    world = dist.get_world_size(group)
+    bus = [None] * world
+    dist.all_gather_object(bus, me, group=group)
+    rank = dist.get_rank(group)
+    mine = []
+    for r, b in enumerate(bus):
+        ok = C.c_int(0)
+        _check(lib.ttkv_peer_probe(device, b.encode(), C.byref(ok)))
+        if not ok.value:
+            mine.append((rank, r))
+    failed = [None] * world
+    dist.all_gather_object(failed, mine, group=group)
+    failed = [p for f in failed for p in f]
+    return {"bus_ids": bus, "ok": not failed, "failed": failed}
+
+
 class PeerGather:
     """Combine fused with the all-gather over peer memory
     (ttkv_gpu_peer_gather_*, include/ttkv_gpu.h): every rank's combine kernel
@@ -95,6 +132,11 @@ class PeerGather:
         from .engine import _check
 
         self.engine, self.plan = engine, plan
+        # every pair must have a P2P path before any rank maps or publishes
+        self.probe = probe_peers(engine.device, group)
+        if not self.probe["ok"]:
+            raise PeerUnavailable(f"no peer access between ranks {self.probe['failed']} "
+                                  f"(bus ids {self.probe['bus_ids']})")
         self.S = plan.layers * plan.kv_heads * plan.requests
         self.shape = (self.S, engine.G, engine.config.d_v)
         lib = engine._lib

@@ -152,3 +152,69 @@ def test_peer_memory_gather_matches_single_handle(gpu):
     for p in procs:
         p.join(timeout=60)
     assert res == {0: True, 1: True}, res
+
+
+def _two_gpu_worker(rank, world, port, q):
+    # one rank per physical GPU, NCCL: the fused peer gather (over NVLink)
+    # against NCCL's all_gather and against one handle holding every stream
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    try:
+        import paper_2604_19769_b200 as T
+        from paper_2604_19769_b200.sharding import PeerGather, ShardPlan, gather_outputs
+        plan = ShardPlan(rank, world, L_, H, 1, "heads")
+        pk, pv, steps = _inputs(1)
+        idx = np.asarray(plan.local_streams())
+        cfg = T.TierConfig(hbm_budget_bytes=LF * 2 * D * 2, d_k=D, d_v=D, block_size=B)
+        eng = T.MultiStreamEngine(cfg, n_streams=len(idx), heads_per_stream=G, device=rank)
+        eng.prefill(pk[idx], pv[idx])
+        pg = PeerGather(eng, plan)
+        assert pg.probe["ok"] and len(set(pg.probe["bus_ids"])) == world
+        ok = True
+        peer_rows, nccl_rows = [], []
+        for qq, k, v in steps:
+            r = eng.decode_step(qq[idx], k[idx], v[idx])
+            peer_rows.append(pg.host())
+            nccl_rows.append(gather_outputs(torch.from_numpy(r.output).cuda(rank), plan)
+                             .cpu().numpy())
+        eng.close()
+        for a, b in zip(peer_rows, nccl_rows):
+            ok &= bool(np.array_equal(a, b))
+        if rank == 0:
+            ref_outs, _ = _run(T, list(range(L_ * H)), pk, pv, steps)
+            for a, b in zip(peer_rows, ref_outs):
+                ok &= bool(np.array_equal(a, b))
+        q.put((rank, ok))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two physical GPUs")
+def test_peer_gather_two_physical_gpus(gpu):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_two_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}, res
+
+
+def test_peer_probe_same_device(gpu):
+    # the probe's own contract on one GPU: a device reaches itself; a bus id
+    # that is not visible to this process has no peer path
+    import ctypes as C
+    from paper_2604_19769_b200 import _lib as L
+    buf = C.create_string_buffer(32)
+    assert L.lib().ttkv_pci_bus_id(0, buf, 32) == 0
+    ok = C.c_int(-1)
+    assert L.lib().ttkv_peer_probe(0, buf.value, C.byref(ok)) == 0 and ok.value == 1
+    assert L.lib().ttkv_peer_probe(0, b"ffff:ff:1f.7", C.byref(ok)) == 0 and ok.value == 0
