@@ -325,7 +325,14 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
 //   V nibbles are decoded straight into A fragments (token pairs per channel)
 //   with the 0x6400 magic-number trick -- no fp16 V tile in shared memory;
 // * the contraction index of QK is permuted identically in A and B (exact in
-//   real arithmetic), and each thread owns 4 consecutive channels of PV.
+//   real arithmetic), and each thread owns 4 consecutive channels of PV;
+// * G <= 4 (PK): the hi and lo parts share ONE MMA through the N dimension --
+//   column n = 2h + part carries head h's hi (part 0) or lo (part 1) operand,
+//   so a thread's accumulator pair (n = 2qq, 2qq + 1) is one head's hi + lo and
+//   is summed in registers: half the HMMAs of the two-chain form (G = 8 keeps
+//   it, all 8 columns being heads);
+// * the head mask of each record reaches the consumers through shared memory
+//   (written by the producer with the stage), not a global load per record.
 // ---------------------------------------------------------------------------
 namespace {
 constexpr uint32_t kKBox = 128 * 128;  // K codes
@@ -402,13 +409,15 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
 template <int GT>
 constexpr size_t slow_tc_tail_bytes() {
   // qsf + phl (2 x 256 uint4) | sc [GT][kScPitch] | qsm [GT][128] | 6 x 8 stats
-  return 2 * 256 * 16 + (size_t)GT * kScPitch * 4 + (size_t)GT * 128 * 4 + 6 * 8 * 4;
+  // | head mask per stage (4 words)
+  return 2 * 256 * 16 + (size_t)GT * kScPitch * 4 + (size_t)GT * 128 * 4 + 6 * 8 * 4 + 16;
 }
 }  // namespace
 
 template <int GT, int ST>
 __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
     slow_attn_tc_kernel(const __grid_constant__ SlowTcArgs a) {
+  constexpr bool PK = GT <= 4;  // hi/lo packed into the N dimension
   pdl_wait();  // the union lists (launched chained behind the selection)
   const Geometry& g = a.g;
   const uint32_t G = g.G;
@@ -432,7 +441,8 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
   float* pst = ast + 8;  // sum_t p of the current block
   float* bst = pst + 8;  // beta = q . z of the current block
   float* usc = bst + 8;  // per-head score unscale (pow2_normalizer), then max |q|
-  uint64_t* full = reinterpret_cast<uint64_t*>(usc + 8);
+  uint32_t* hms = reinterpret_cast<uint32_t*>(usc + 8);  // head mask of each stage
+  uint64_t* full = reinterpret_cast<uint64_t*>(hms + 4);
   uint64_t* empty = full + ST;
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -456,6 +466,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
         if (i >= ST) mbar_wait_sleep(&empty[st], ((i / ST) - 1) & 1);
         const int rec = (int)((uint64_t)s * g.n_cap + uids[i]);
         uint8_t* dst = base + st * kSlowStage;
+        hms[st] = umask[i];  // published by the arrive below (release.cta)
         mbar_arrive_expect_tx(&full[st], kSlowStage);
         tma_load_3d(dst, &a.tk, 0, 0, rec, &full[st], evict_first);
         tma_load_3d(dst + kKBox, &a.tv, 0, 0, rec, &full[st], evict_first);
@@ -506,7 +517,8 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
 #pragma unroll
   for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.f;
   uint32_t seen = 0;
-  const float uns0 = usc[2 * qq], uns1 = usc[2 * qq + 1];  // score unscale of this lane's heads
+  // score unscale of this lane's heads (PK: head qq; otherwise 2qq, 2qq + 1)
+  const float uns0 = usc[PK ? qq : 2 * qq], uns1 = usc[2 * qq + 1];
   // Swizzle-folded shared-memory offsets (loop-invariant):
   //  K (128B swizzle): ldmatrix row address of matrix m = lane / 8 -- token
   //  32cw + 16mt + 8(m&1) + (lane&7), 16-byte chunk 2jp + (m>>1); the XOR
@@ -530,7 +542,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
     const uint8_t* vn = stg + kKBox;
     const float* kp = reinterpret_cast<const float*>(stg + kKBox + kVBox);  // {s,z} x 128
     const float* vp = kp + 2 * 128;
-    const uint32_t hm = umask[i];
+    const uint32_t hm = hms[st];
     seen |= hm;
 
     // ---- (q * s) B fragments (hi/lo) and this lane's share of beta = q . z
@@ -548,14 +560,64 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
       uint32_t h01, l01, h23, l23;
       split2(qv.x * sz0.x, qv.y * sz0.z, h01, l01);
       split2(qv.z * sz1.x, qv.w * sz1.z, h23, l23);
-      qsf[(j * 8 + h) * 4 + q4] = make_uint4(h01, h23, l01, l23);
+      if constexpr (PK) {  // column 2h: hi, 2h + 1: lo
+        uint2* qsf2 = reinterpret_cast<uint2*>(qsf);
+        qsf2[(j * 8 + 2 * h) * 4 + q4] = make_uint2(h01, h23);
+        qsf2[(j * 8 + 2 * h + 1) * 4 + q4] = make_uint2(l01, l23);
+      } else {
+        qsf[(j * 8 + h) * 4 + q4] = make_uint4(h01, h23, l01, l23);
+      }
       bpart[rep] = qv.x * sz0.y + qv.y * sz0.w + qv.z * sz1.y + qv.w * sz1.w;
     }
     named_bar(1, nthreads_c);
 
     // ---- QK^T: warp cw -> tokens [32cw, 32cw + 32) = 2 m-tiles; hi and lo
-    // accumulate in independent chains ----
-    {
+    // accumulate in independent chains (PK: one chain per k-half, hi and lo
+    // in adjacent columns) ----
+    if constexpr (PK) {
+      const uint2* qsf2 = reinterpret_cast<const uint2*>(qsf);
+      float c[2][2][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) c[mt][0][e] = c[mt][1][e] = 0.f;
+#pragma unroll
+      for (int jp = 0; jp < 4; ++jp) {
+        const uint2 b0 = qsf2[((2 * jp) * 8 + gq) * 4 + qq];
+        const uint2 b1 = qsf2[((2 * jp + 1) * 8 + gq) * 4 + qq];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const uint32_t addr = kb + koff[jp] + mt * 16 * 128;
+          uint32_t r0, r1, r2, r3, a0, a1, a2, a3;
+          ldsm_x4(addr, r0, r1, r2, r3);
+          codes_to_h2(r0, a0, a2);
+          codes_to_h2(r1, a1, a3);
+          mma_a4(c[mt][0], a0, a1, a2, a3, b0.x, b0.y);
+          codes_to_h2(r2, a0, a2);
+          codes_to_h2(r3, a1, a3);
+          mma_a4(c[mt][1], a0, a1, a2, a3, b1.x, b1.y);
+        }
+      }
+#pragma unroll
+      for (int rep = 0; rep < 2; ++rep) {
+        const uint32_t h = cw + rep * kSlowConsumerWarps;
+        if (h < G) {  // warp-uniform
+          const float beta = warp_sum(bpart[rep]) * (usc[h] * (1.0f / 16777216.0f));
+          if (lane == 0) bst[h] = beta;
+        }
+      }
+      // thread (gq, qq): columns 2qq (hi) and 2qq + 1 (lo) of head qq
+      if (qq < G) {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int e = 0; e < 4; e += 2) {
+            const uint32_t t = 32 * cw + 16 * mt + gq + 4 * e;
+            sc[qq * kScPitch + t] =
+                ((c[mt][0][e] + c[mt][0][e + 1]) + (c[mt][1][e] + c[mt][1][e + 1])) * uns0;
+          }
+      }
+    } else {
       float c[2][2][4];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
@@ -606,8 +668,15 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
     for (uint32_t h = cw; h < G; h += kSlowConsumerWarps) {
       const uint32_t ks = lane >> 2, q4 = lane & 3;
       uint4* dst = phl + (ks * 8 + h) * 4 + q4;
+      uint2* dhi = reinterpret_cast<uint2*>(phl) + (ks * 8 + 2 * h) * 4 + q4;  // PK columns
+      uint2* dlo = dhi + 4;
       if (!((hm >> h) & 1u)) {  // head did not select this block
-        *dst = make_uint4(0, 0, 0, 0);
+        if constexpr (PK) {
+          *dhi = make_uint2(0, 0);
+          *dlo = make_uint2(0, 0);
+        } else {
+          *dst = make_uint4(0, 0, 0, 0);
+        }
         if (lane == 0) {
           ast[h] = 1.0f;
           pst[h] = 0.0f;
@@ -632,7 +701,12 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
       uint32_t h01, l01, h89, l89;
       split2(p0, p1, h01, l01);
       split2(p8, p9, h89, l89);
-      *dst = make_uint4(h01, h89, l01, l89);
+      if constexpr (PK) {
+        *dhi = make_uint2(h01, h89);
+        *dlo = make_uint2(l01, l89);
+      } else {
+        *dst = make_uint4(h01, h89, l01, l89);
+      }
       __syncwarp();  // all lanes have read mst[h] before lane 0 rewrites it
       if (lane == 0) {
         if (a.literal) {
@@ -652,7 +726,42 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
     // ---- PV^T: warp cw -> channels [32cw, 32cw + 32) as 2 m-tiles; thread
     // rows gq / gq + 8 of m-tile 0 = channels c0, c0 + 1, of m-tile 1 =
     // c0 + 2, c0 + 3 (one u16 of V nibbles per token) ----
-    {
+    if constexpr (PK) {  // columns 2qq, 2qq + 1 = head qq hi, lo; chains by ks parity
+      const uint2* phl2 = reinterpret_cast<const uint2*>(phl);
+      float cf[2][2][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) cf[mt][0][e] = cf[mt][1][e] = 0.f;
+      const uint8_t* vt = vn + voff;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const uint32_t u0 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024);
+        const uint32_t u1 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 64);
+        const uint32_t u8 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 512);
+        const uint32_t u9 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 576);
+        uint32_t x0, x1, x2, x3, y0, y1, y2, y3;
+        nibbles_to_h2(__byte_perm(u0, u1, 0x5410u), x0, x1, x2, x3);
+        nibbles_to_h2(__byte_perm(u8, u9, 0x5410u), y0, y1, y2, y3);
+        const uint2 pb = phl2[(ks * 8 + gq) * 4 + qq];
+        mma_a4(cf[0][ks & 1], x0, x1, y0, y1, pb.x, pb.y);
+        mma_a4(cf[1][ks & 1], x2, x3, y2, y3, pb.x, pb.y);
+      }
+      const uint32_t h = qq;
+      if (h < G && ((hm >> h) & 1u)) {
+        const float4 sz01 = *reinterpret_cast<const float4*>(vp + 2 * c0);
+        const float4 sz23 = *reinterpret_cast<const float4*>(vp + 2 * c0 + 4);
+        const float vs[4] = {sz01.x * kSub20, sz01.z * kSub20, sz23.x * kSub20, sz23.z * kSub20};
+        const float vz[4] = {sz01.y, sz01.w, sz23.y, sz23.w};
+        const float alpha = ast[h], psum = pst[h];
+#pragma unroll
+        for (int ci = 0; ci < 4; ++ci) {
+          const int mt = ci >> 1, e = 2 * (ci & 1);
+          const float o = (cf[mt][0][e] + cf[mt][0][e + 1]) + (cf[mt][1][e] + cf[mt][1][e + 1]);
+          acc[ci][0] = acc[ci][0] * alpha + vs[ci] * o + vz[ci] * psum;
+        }
+      }
+    } else {
       float cf[2][2][4];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
@@ -702,8 +811,8 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
   named_bar(1, nthreads_c);
   const uint32_t pitch = 128 + 2;
 #pragma unroll
-  for (int hh = 0; hh < 2; ++hh) {
-    const uint32_t h = 2 * qq + hh;
+  for (int hh = 0; hh < (PK ? 1 : 2); ++hh) {
+    const uint32_t h = PK ? qq : 2 * qq + hh;
     if (h >= G) continue;
     float* p = reinterpret_cast<float*>(a.part) + (((uint64_t)s * G + h) * a.nsc + chunk) * pitch;
     const bool any = (seen >> h) & 1u;
