@@ -139,6 +139,9 @@ typedef struct {
   uint64_t launches;        /* kernels launched by this handle so far */
   uint64_t payload_bytes;   /* bytes of each record streamed over PCIe (codes);
                                the per-channel params are staged from HBM */
+  uint64_t graph_replays;   /* decode steps launched as a replay of the captured
+                               step graph (TTKV_GRAPH=0: none) */
+  uint64_t graph_captures;  /* step graphs captured (one per eviction period) */
 } ttkv_state;
 
 /* Kernel timing (enabled by ttkv_gpu_set_timing); milliseconds summed over

@@ -48,7 +48,7 @@ class StateC(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "appended", "fast_tokens", "slow_blocks", "l_fast", "record_bytes",
         "modeled_block_bytes", "n_streams", "heads_per_stream", "block_capacity", "launches",
-        "payload_bytes")]
+        "payload_bytes", "graph_replays", "graph_captures")]
 
 
 class KernelTimesC(C.Structure):

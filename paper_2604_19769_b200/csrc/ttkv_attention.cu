@@ -419,8 +419,9 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32) fast_attn_kernel
   using Acc = AccOf<T>;
   const Geometry& g = a.g;
   const uint32_t s = blockIdx.y, f = blockIdx.x;
+  const uint32_t F = a.pos ? (uint32_t)(*a.pos + 1 - a.front) : a.F;
   const uint32_t t0 = f * a.FC;
-  const uint32_t t1 = min(t0 + a.FC, a.F);
+  const uint32_t t1 = min(t0 + a.FC, F);
   const uint32_t ntiles = t1 > t0 ? (t1 - t0 + a.TT - 1) / a.TT : 0;
   const uint32_t NS = a.stages;
   const uint32_t kbytes_row = g.d_k * sizeof(T), vbytes_row = g.d_v * sizeof(T);
@@ -585,8 +586,7 @@ static cudaError_t launch_fast_t(const FastArgs& a, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid(a.nfc, g.S);
-  kern<<<grid, 32 + kSlowConsumerWarps * 32, smem, st>>>(b);
-  return cudaGetLastError();
+  return launch_background(kern, grid, dim3(32 + kSlowConsumerWarps * 32), smem, st, b);
 }
 
 template <typename T, int COPY>
@@ -721,6 +721,9 @@ __global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs
       for (uint32_t r = 0; r < a.n_peers; ++r) a.peer_out[r][gi] = (double)o;
     }
   }
+  // the step is combined: advance the device step position (nothing in this
+  // kernel reads it; the next step's append and fast tier do)
+  if (a.pos_inc && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *a.pos_inc += 1;
   if (a.n_peers) {  // this CTA's row is in every rank's buffer: publish it
     __syncthreads();
     if (threadIdx.x == 0) {

@@ -96,8 +96,9 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
   constexpr uint32_t STAGE = 2 * ND * kBox;
   const Geometry& g = a.g;
   const uint32_t s = blockIdx.y, f = blockIdx.x;
+  const uint32_t F = a.pos ? (uint32_t)(*a.pos + 1 - a.front) : a.F;
   const uint32_t t0 = f * a.FC;
-  const uint32_t t1 = min(t0 + a.FC, a.F);
+  const uint32_t t1 = min(t0 + a.FC, F);
   const uint32_t ntiles = t1 > t0 ? (t1 - t0 + kTT - 1) / kTT : 0;
 
   extern __shared__ uint8_t smem_raw[];
@@ -918,8 +919,7 @@ static cudaError_t launch_fast_tc_t(const FastTcArgs& a, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid(a.nfc, a.g.S);
-  kern<<<grid, 32 + kSlowConsumerWarps * 32, smem, st>>>(a);
-  return cudaGetLastError();
+  return launch_background(kern, grid, dim3(32 + kSlowConsumerWarps * 32), smem, st, a);
 }
 
 template <int ND>

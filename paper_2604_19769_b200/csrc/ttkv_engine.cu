@@ -183,6 +183,16 @@ enum Kind { K_APPEND = 0, K_SCORE, K_SELECT, K_FAST, K_SLOW, K_COMBINE, K_EVICT,
 }  // namespace
 
 void ttkv_dev::set_last_error(const char* msg) { g_last_error = msg ? msg : ""; }
+int ttkv_dev::launch_priority(bool critical) {
+  static int least = 1, greatest = 1;  // 1: not queried yet (valid values are <= 0)
+  if (least == 1) {
+    int lo = 0, hi = 0;
+    if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) lo = hi = 0;
+    greatest = hi;
+    least = lo;
+  }
+  return critical ? greatest : least;
+}
 bool ttkv_dev::pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("TTKV_PDL");
@@ -268,6 +278,31 @@ struct ttkv_gpu {
   double ms[K_N] = {};
   uint64_t cnt[K_N] = {};
   uint64_t launches = 0;
+  // Device step position (= `appended` before the step): the append slot and
+  // the fast tier's length are read from it on the device and the combine
+  // advances it, so a decode step's launches do not change from one step to
+  // the next within an eviction period and replay as one CUDA graph.
+  uint64_t* pos_dev = nullptr;
+  bool pos_synced = false;  // pos_dev == appended (host-side appends clear it)
+  uint64_t gen = 0;         // bumped whenever a buffer a captured step uses moves
+  struct GraphKey {
+    const void *q, *kn, *vn, *out;
+    cudaStream_t s0;
+    uint64_t n, k, front, gen, grid_chunks;
+    uint32_t nfc, CH, dtype, host_io;
+  };
+  struct StepGraph {
+    GraphKey key;
+    cudaGraphExec_t exec;
+    uint64_t launches;  // kernels per replay
+    uint64_t last_use;
+  };
+  // A few captured steps per eviction period: callers that rotate their
+  // input/output buffers get one graph per buffer set (the pointers are
+  // kernel arguments of the captured launches).
+  static constexpr size_t kMaxGraphs = 8;
+  std::vector<StepGraph> graphs;
+  uint64_t graph_replays = 0, graph_captures = 0;
 };
 
 namespace {
@@ -383,6 +418,9 @@ void free_all(ttkv_gpu* h) {
   pinned_free(h->h_k);
   pinned_free(h->h_v);
   pinned_free(h->h_ucount);
+  F(h->pos_dev);
+  for (auto& sg : h->graphs) cudaGraphExecDestroy(sg.exec);
+  h->graphs.clear();
   for (auto& r : h->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : h->pool) cudaEventDestroy(e);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
@@ -468,6 +506,7 @@ int ensure_blocks(ttkv_gpu* h, uint64_t need) {
   h->uids = nuids;
   h->umask = numask;
   h->g.n_cap = cap;
+  h->gen++;  // captured steps hold the old pointers
   if (h->opt.serial_schedule) {
     CU(h, realloc_dev((void**)&h->stage_arena, arena_bytes));
   }
@@ -487,6 +526,7 @@ int ensure_spart(ttkv_gpu* h, uint64_t chunks) {
   h->spart = nullptr;
   CU(h, cudaMalloc((void**)&h->spart, (size_t)h->g.S * h->g.G * c * (h->g.d_v + 2) * h->acc));
   h->spart_chunks = c;
+  h->gen++;
   return TTKV_OK;
 }
 
@@ -567,6 +607,7 @@ int prefill_chunk(ttkv_gpu* h, const void* in_k, const void* in_v, int in_dtype,
   h->appended = total;
   h->n_slow = nb_after;
   h->fast_front = nb_after * B;
+  h->pos_synced = false;
   return TTKV_OK;
 }
 
@@ -592,65 +633,59 @@ StepTimer::~StepTimer() {
   }
 }
 
-int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int dtype,
-                double* out, ttkv_step_report* rep) {
-  StepTimer step_timer(h);
-  {  // grow before selecting so a settle-time eviction never reallocates
-    int rc0 = ensure_blocks(h, h->n_slow + 1);
-    if (rc0) return rc0;
-  }
+// One decode step's launch parameters (decided on the host, before any
+// stream work, so that the stream work can be captured as a graph).
+struct StepPlan {
+  const float* q;
+  const void* kn;
+  const void* vn;
+  int dtype;
+  double* out;
+  bool host_io;  // stage q/k/v from and out to the handle's pinned buffers
+  uint64_t n, k, F;
+  uint32_t FCs, nfc, CH;
+  uint64_t grid_chunks;
+  bool slow, early_fork;
+  double scale_log2;
+};
+
+// Every stream operation of one decode step (append .. combine), on s0 with
+// the fast tier forked onto s1.  No host synchronization, no allocation.
+int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
   const Geometry& g = h->g;
-  uint64_t pos = h->appended;
-  if (pos - h->fast_front + 1 > g.C)
-    return set_err(h, TTKV_EERROR,
-                   "decode_step: fast tier would exceed its ring; settle pending evictions");
+  if (P.host_io) {
+    const size_t esz = P.dtype == kInF16 ? 2 : 4;
+    CU(h, cudaMemcpyAsync(h->q_dev, h->h_q, (size_t)g.S * g.G * g.d_k * 4, cudaMemcpyHostToDevice,
+                          h->s0));
+    CU(h, cudaMemcpyAsync(h->kn_dev, h->h_k, (size_t)g.S * g.d_k * esz, cudaMemcpyHostToDevice,
+                          h->s0));
+    CU(h, cudaMemcpyAsync(h->vn_dev, h->h_v, (size_t)g.S * g.d_v * esz, cudaMemcpyHostToDevice,
+                          h->s0));
+  }
   // append_kv: the new token attends to itself.  Only the fast
   // tier reads the ring, so the append runs on s1 ahead of the fast kernel and
-  // stays off the critical path score -> select -> slow on s0.
+  // stays off the critical path score -> select -> slow on s0.  Its slot is
+  // the device step position mod C.
   CU(h, cudaEventRecord(h->ev_start, h->s0));
   CU(h, cudaStreamWaitEvent(h->s1, h->ev_start, 0));
   {
     KTimer t(h, K_APPEND, h->s1);
-    CU(h, launch_append(g, h->ring_k, h->ring_v, kn, vn, dtype, pos % g.C, 1, 1, h->s1));
+    CU(h, launch_append(g, h->ring_k, h->ring_v, P.kn, P.vn, P.dtype, 0, 1, 1, h->s1, h->pos_dev));
   }
-  h->appended = pos + 1;
-  const uint64_t F = h->appended - h->fast_front;
-  const uint64_t n = h->n_slow;
-  uint64_t k = 0;
-  {
-    std::string m;
-    int rc = resolve_k(h->pol, n, k, m);
-    if (rc) return set_err(h, rc, m);
-  }
-  // softmax scale 1/sqrt(d_k) (engine.cpp:30), folded with log2(e) for exp2
-  const double scale_log2 = 1.0 / std::sqrt((double)g.d_k) * 1.4426950408889634;
-
-  // Fast tier on s1 (low priority), overlapped with the PCIe-bound slow
-  // stream on s0.  It is forked after select so it never competes with the
-  // critical path append -> score -> select for SM slots.
-  // With slow work in the step the fast tier runs hidden under it, so it is
-  // cut into at most ~16 chunks per stream: fewer partial rows for the
-  // combine, which is on the critical path (small S only; large S already
-  // has long chunks).  Without slow work it keeps the GPU-filling split.
-  uint32_t FCs = h->FC;
-  if (n > 0 && k > 0) {
-    const uint64_t want = ((h->l_fast + g.B + 15) / 16 + h->TT - 1) / h->TT * h->TT;
-    FCs = (uint32_t)std::max<uint64_t>(FCs, want);
-  }
-  const uint32_t nfc = (uint32_t)((F + FCs - 1) / FCs);
   auto fork_fast = [&]() -> int {
     CU(h, cudaEventRecord(h->ev_fork, h->s0));
     CU(h, cudaStreamWaitEvent(h->s1, h->ev_fork, 0));
     if (h->fast_tc) {
       FastTcArgs& a = h->tc;
       a.g = g;
-      a.q = q;
+      a.q = P.q;
       a.part = h->fpart;
       a.front = h->fast_front;
-      a.F = (uint32_t)F;
-      a.FC = FCs;
-      a.nfc = nfc;
-      a.scale_log2 = scale_log2;
+      a.pos = h->pos_dev;
+      a.F = (uint32_t)P.F;
+      a.FC = P.FCs;
+      a.nfc = P.nfc;
+      a.scale_log2 = P.scale_log2;
       {
         KTimer t(h, K_FAST, h->s1);
         CU(h, launch_fast_tc(a, h->s1));
@@ -662,15 +697,16 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
     a.g = g;
     a.ring_k = h->ring_k;
     a.ring_v = h->ring_v;
-    a.q = q;
+    a.q = P.q;
     a.part = h->fpart;
     a.front = h->fast_front;
-    a.F = (uint32_t)F;
-    a.FC = FCs;
-    a.nfc = nfc;
+    a.pos = h->pos_dev;
+    a.F = (uint32_t)P.F;
+    a.FC = P.FCs;
+    a.nfc = P.nfc;
     a.TT = h->TT;
     a.stages = kFastStages;
-    a.scale_log2 = scale_log2;
+    a.scale_log2 = P.scale_log2;
     {
       KTimer t(h, K_FAST, h->s1);
       CU(h, launch_fast(a, h->s1));
@@ -678,47 +714,12 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
     CU(h, cudaEventRecord(h->ev_join, h->s1));
     return TTKV_OK;
   };
-
-  uint32_t CH = 4;
-  bool slow = n > 0 && k > 0;
-  // The fast tier (low priority, s1) is forked after select: score and
-  // select are short, latency-bound kernels that should not wait for SM slots
-  // held by long fast-tier CTAs, and the PCIe stream (host tier) or the record
-  // stream (HBM tier) is the critical path after them (HBM cfg2: 1.289 ms/step
-  // forked late vs 1.338 forked at the step start; cfg3 equal).
-  static const int fork_env = [] {  // TTKV_FORK=early|late overrides (measurement)
-    const char* e = std::getenv("TTKV_FORK");
-    return e ? (std::strcmp(e, "early") == 0 ? 1 : 0) + (std::strcmp(e, "late") == 0 ? 2 : 0) : 0;
-  }();
-  const bool early_fork = fork_env == 1;
-  if (early_fork) {
+  if (P.early_fork) {
     if (int rcf = fork_fast()) return rcf;
   }
-  if (slow) {
-    if (h->slow_tc) {
-      // HBM records: every CTA pays a prologue and a pipeline fill, so the
-      // smallest chunk that fits the union's upper bound S * min(n, Gs * k)
-      // into ONE wave of resident CTAs (layer-sequential cfg2, S = 8: 308 ->
-      // 379 tok/s vs 4-record chunks; a second partial wave costs ~15 %)
-      const uint64_t ub = (uint64_t)g.S * std::min<uint64_t>(n, (uint64_t)g.Gs * k);
-      const uint64_t slots = (uint64_t)h->sms * slow_tc_ctas_per_sm();
-      CH = (uint32_t)std::min<uint64_t>(64, std::max<uint64_t>(4, (ub + slots - 1) / slots));
-    } else {
-      // host records: union entries per CTA ~4 waves of 2 CTAs/SM over the
-      // lower bound S * k (more zero-copy streams in flight)
-      const uint64_t est = (uint64_t)g.S * k;
-      CH = (uint32_t)std::min<uint64_t>(64, std::max<uint64_t>(4, (est + 1183) / 1184));
-    }
-    static const uint32_t ch_env = [] {  // TTKV_SLOW_CH=n overrides (measurement)
-      const char* e = std::getenv("TTKV_SLOW_CH");
-      return e ? (uint32_t)std::max(1, std::min(256, std::atoi(e))) : 0u;
-    }();
-    if (ch_env) CH = ch_env;
-    const uint64_t grid_chunks = (n + CH - 1) / CH;
-    int rc = ensure_spart(h, grid_chunks);
-    if (rc) return rc;
+  if (P.slow) {
     {
-      ScoreArgs a{g, q, h->cent, h->scores, (uint32_t)n};
+      ScoreArgs a{g, P.q, h->cent, h->scores, (uint32_t)P.n};
       KTimer t(h, K_SCORE, h->s0);
       CU(h, launch_score(a, h->s0));
     }
@@ -730,8 +731,8 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       a.union_ids = h->uids;
       a.union_mask = h->umask;
       a.union_count = h->ucount;
-      a.n = (uint32_t)n;
-      a.k = (uint32_t)k;
+      a.n = (uint32_t)P.n;
+      a.k = (uint32_t)P.k;
       KTimer t(h, K_SELECT, h->s0, 2);  // sort + union kernels
       CU(h, launch_select(a, h->s0));
     }
@@ -739,9 +740,9 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       // bulk phase: every selected record crosses PCIe before any compute
       KTimer t(h, K_GATHER, h->s0);
       CU(h, launch_gather(g, h->arena_dev, h->stage_arena, h->uids, h->ucount,
-                          (uint32_t)grid_chunks, CH, h->s0));
+                          (uint32_t)P.grid_chunks, P.CH, h->s0));
     }
-    if (!early_fork) {
+    if (!P.early_fork) {
       if (int rcf = fork_fast()) return rcf;
     }
     if (h->slow_tc) {
@@ -751,14 +752,14 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       a.union_ids = h->uids;
       a.union_mask = h->umask;
       a.union_count = h->ucount;
-      a.q = q;
+      a.q = P.q;
       a.part = h->spart;
-      a.CH = CH;
+      a.CH = P.CH;
       a.nsc = (uint32_t)h->spart_chunks;
       a.literal = h->opt.literal_additive_merge ? 1u : 0u;
-      a.scale_log2 = scale_log2;
+      a.scale_log2 = P.scale_log2;
       KTimer t(h, K_SLOW, h->s0);
-      CU(h, launch_slow_tc(a, (uint32_t)grid_chunks, h->s0));
+      CU(h, launch_slow_tc(a, (uint32_t)P.grid_chunks, h->s0));
     } else {
       SlowArgs a{};
       a.g = g;
@@ -767,17 +768,17 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       a.union_ids = h->uids;
       a.union_mask = h->umask;
       a.union_count = h->ucount;
-      a.q = q;
+      a.q = P.q;
       a.part = h->spart;
-      a.CH = CH;
+      a.CH = P.CH;
       a.nsc = (uint32_t)h->spart_chunks;
       a.stages = h->stages;
-      a.scale_log2 = scale_log2;
+      a.scale_log2 = P.scale_log2;
       a.literal = h->opt.literal_additive_merge ? 1u : 0u;
       KTimer t(h, K_SLOW, h->s0);
-      CU(h, launch_slow(a, (uint32_t)grid_chunks, (int)h->copy_mode, h->s0));
+      CU(h, launch_slow(a, (uint32_t)P.grid_chunks, (int)h->copy_mode, h->s0));
     }
-  } else if (!early_fork) {
+  } else if (!P.early_fork) {
     if (int rcf = fork_fast()) return rcf;
   }
   CU(h, cudaStreamWaitEvent(h->s0, h->ev_join, 0));
@@ -785,13 +786,14 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
     CombineArgs a{};
     a.g = g;
     a.fpart = h->fpart;
-    a.nfc = nfc;
-    a.spart = slow ? h->spart : nullptr;
+    a.nfc = P.nfc;
+    a.spart = P.slow ? h->spart : nullptr;
     a.nsc = (uint32_t)h->spart_chunks;
-    a.CH = CH;
-    a.union_count = slow ? h->ucount : nullptr;
-    a.out = out;
+    a.CH = P.CH;
+    a.union_count = P.slow ? h->ucount : nullptr;
+    a.out = P.out;
     a.literal = h->opt.literal_additive_merge ? 1u : 0u;
+    a.pos_inc = h->pos_dev;
     if (h->pg.active) {
       // double-buffered by step parity: a rank one step ahead never
       // overwrites rows another rank may still be consuming
@@ -816,16 +818,207 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
                 h->s0));
     }
   }
-  h->last_k = slow ? k : 0;
-  h->last_n = n;
+  if (P.host_io) {
+    CU(h, cudaMemcpyAsync(h->h_out, h->out_dev, (size_t)g.S * g.G * g.d_v * 8,
+                          cudaMemcpyDeviceToHost, h->s0));
+    if (P.slow)
+      CU(h, cudaMemcpyAsync(h->h_ucount, h->ucount, g.S * sizeof(uint32_t),
+                            cudaMemcpyDeviceToHost, h->s0));
+  }
+  return TTKV_OK;
+}
+
+// Graph replay is opt-in (TTKV_GRAPH=1): it cuts the host's issue time per
+// step (layer-sequential cfg2: 52 -> 22 us per call) but a replayed step
+// loses most of the programmatic-launch overlap of the directly launched
+// chain (cfg1 HBM: 50.9 vs 43.6 us per step on the device), so it pays only
+// for callers whose host issue time exceeds the device time.
+bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TTKV_GRAPH");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int dtype,
+                double* out, ttkv_step_report* rep, bool host_io = false) {
+  StepTimer step_timer(h);
+  {  // grow before selecting so a settle-time eviction never reallocates
+    int rc0 = ensure_blocks(h, h->n_slow + 1);
+    if (rc0) return rc0;
+  }
+  const Geometry& g = h->g;
+  const uint64_t pos = h->appended;
+  if (pos - h->fast_front + 1 > g.C)
+    return set_err(h, TTKV_EERROR,
+                   "decode_step: fast tier would exceed its ring; settle pending evictions");
+  StepPlan P{};
+  P.q = q;
+  P.kn = kn;
+  P.vn = vn;
+  P.dtype = dtype;
+  P.out = out;
+  P.host_io = host_io;
+  P.F = pos + 1 - h->fast_front;
+  P.n = h->n_slow;
+  {
+    std::string m;
+    int rc = resolve_k(h->pol, P.n, P.k, m);
+    if (rc) return set_err(h, rc, m);
+  }
+  // softmax scale 1/sqrt(d_k) (engine.cpp:30), folded with log2(e) for exp2
+  P.scale_log2 = 1.0 / std::sqrt((double)g.d_k) * 1.4426950408889634;
+  P.slow = P.n > 0 && P.k > 0;
+
+  // Fast tier on s1 (low priority), overlapped with the PCIe-bound slow
+  // stream on s0.  It is forked after select so it never competes with the
+  // critical path append -> score -> select for SM slots.
+  // With slow work in the step the fast tier runs hidden under it, so it is
+  // cut into at most ~16 chunks per stream: fewer partial rows for the
+  // combine, which is on the critical path (small S only; large S already
+  // has long chunks).  Its grid then covers the whole ring (the kernels read
+  // the fast-tier length from the device step position; chunks past it are
+  // empty partials), so the launch is the same for every step of an
+  // eviction period.  Without slow work it keeps the GPU-filling split.
+  P.FCs = h->FC;
+  if (P.slow) {
+    const uint64_t want = ((h->l_fast + g.B + 15) / 16 + h->TT - 1) / h->TT * h->TT;
+    P.FCs = (uint32_t)std::max<uint64_t>(P.FCs, want);
+    P.nfc = (uint32_t)((g.C + P.FCs - 1) / P.FCs);
+  } else {
+    P.nfc = (uint32_t)((P.F + P.FCs - 1) / P.FCs);
+  }
+
+  // The fast tier (low priority, s1) is forked after select: score and
+  // select are short, latency-bound kernels that should not wait for SM slots
+  // held by long fast-tier CTAs, and the PCIe stream (host tier) or the record
+  // stream (HBM tier) is the critical path after them (HBM cfg2: 1.289 ms/step
+  // forked late vs 1.338 forked at the step start; cfg3 equal).
+  static const int fork_env = [] {  // TTKV_FORK=early|late overrides (measurement)
+    const char* e = std::getenv("TTKV_FORK");
+    return e ? (std::strcmp(e, "early") == 0 ? 1 : 0) + (std::strcmp(e, "late") == 0 ? 2 : 0) : 0;
+  }();
+  P.early_fork = fork_env == 1;
+  P.CH = 4;
+  if (P.slow) {
+    if (h->slow_tc) {
+      // HBM records: every CTA pays a prologue and a pipeline fill, so the
+      // smallest chunk that fits the union's upper bound S * min(n, Gs * k)
+      // into ONE wave of resident CTAs (layer-sequential cfg2, S = 8: 308 ->
+      // 379 tok/s vs 4-record chunks; a second partial wave costs ~15 %)
+      const uint64_t ub = (uint64_t)g.S * std::min<uint64_t>(P.n, (uint64_t)g.Gs * P.k);
+      const uint64_t slots = (uint64_t)h->sms * slow_tc_ctas_per_sm();
+      P.CH = (uint32_t)std::min<uint64_t>(64, std::max<uint64_t>(4, (ub + slots - 1) / slots));
+    } else {
+      // host records: union entries per CTA ~4 waves of 2 CTAs/SM over the
+      // lower bound S * k (more zero-copy streams in flight)
+      const uint64_t est = (uint64_t)g.S * P.k;
+      P.CH = (uint32_t)std::min<uint64_t>(64, std::max<uint64_t>(4, (est + 1183) / 1184));
+    }
+    static const uint32_t ch_env = [] {  // TTKV_SLOW_CH=n overrides (measurement)
+      const char* e = std::getenv("TTKV_SLOW_CH");
+      return e ? (uint32_t)std::max(1, std::min(256, std::atoi(e))) : 0u;
+    }();
+    if (ch_env) P.CH = ch_env;
+    P.grid_chunks = (P.n + P.CH - 1) / P.CH;
+    int rc = ensure_spart(h, P.grid_chunks);
+    if (rc) return rc;
+  }
+  if (!h->pos_synced) {  // host-side appends / prefill / restore moved `appended`
+    CU(h, launch_set_u64(h->pos_dev, pos, h->s0));
+    h->pos_synced = true;
+  }
+
+  // CUDA graph: within an eviction period every launch of the step is the
+  // same (n, k, the grids and all pointers are fixed; the step position lives
+  // on the device), so the step is captured once and replayed.  Steps that
+  // evict, timed steps and the multi-GPU gather launch directly.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  bool use_graph = graphs_enabled() && P.slow && !h->timing && !h->pg.active && h->s0 &&
+                   P.F <= h->l_fast;
+  if (use_graph) {
+    CU(h, cudaStreamIsCapturing(h->s0, &cap));
+    use_graph = cap == cudaStreamCaptureStatusNone;  // a caller's capture takes the launches
+  }
+  if (use_graph) {
+    ttkv_gpu::GraphKey key;
+    std::memset(&key, 0, sizeof(key));
+    key.q = q;
+    key.kn = kn;
+    key.vn = vn;
+    key.out = out;
+    key.s0 = h->s0;
+    key.n = P.n;
+    key.k = P.k;
+    key.front = h->fast_front;
+    key.gen = h->gen;
+    key.grid_chunks = P.grid_chunks;
+    key.nfc = P.nfc;
+    key.CH = P.CH;
+    key.dtype = (uint32_t)dtype;
+    key.host_io = host_io ? 1u : 0u;
+    ttkv_gpu::StepGraph* hit = nullptr;
+    for (auto& sg : h->graphs)
+      if (std::memcmp(&key, &sg.key, sizeof(key)) == 0) hit = &sg;
+    const uint64_t now = h->graph_replays + h->graph_captures;
+    if (hit) {
+      CU(h, cudaGraphLaunch(hit->exec, h->s0));
+      h->launches += hit->launches;
+      hit->last_use = now;
+      h->graph_replays++;
+    } else {
+      // graphs of another eviction period / buffer generation never match
+      // again; beyond kMaxGraphs buffer sets the least recently used goes
+      for (size_t i = 0; i < h->graphs.size();) {
+        const auto& k2 = h->graphs[i].key;
+        if (k2.n != key.n || k2.front != key.front || k2.gen != key.gen || k2.s0 != key.s0) {
+          cudaGraphExecDestroy(h->graphs[i].exec);
+          h->graphs.erase(h->graphs.begin() + i);
+        } else {
+          ++i;
+        }
+      }
+      if (h->graphs.size() >= ttkv_gpu::kMaxGraphs) {
+        size_t victim = 0;
+        for (size_t j = 1; j < h->graphs.size(); ++j)
+          if (h->graphs[j].last_use < h->graphs[victim].last_use) victim = j;
+        cudaGraphExecDestroy(h->graphs[victim].exec);
+        h->graphs.erase(h->graphs.begin() + victim);
+      }
+      const uint64_t l0 = h->launches;
+      CU(h, cudaStreamBeginCapture(h->s0, cudaStreamCaptureModeRelaxed));
+      const int rc = enqueue_step(h, P);
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(h->s0, &graph);
+      if (rc) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+      }
+      CU(h, ce);
+      cudaGraphExec_t exec = nullptr;
+      const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      CU(h, ie);
+      h->graphs.push_back({key, exec, h->launches - l0, now});
+      h->graph_captures++;
+      CU(h, cudaGraphLaunch(exec, h->s0));
+    }
+  } else {
+    int rc = enqueue_step(h, P);
+    if (rc) return rc;
+  }
+  h->appended = pos + 1;
+  h->last_k = P.slow ? P.k : 0;
+  h->last_n = P.n;
   bool evicted = false;
   int rc = settle_evictions(h, &evicted);
   if (rc) return rc;
   if (rep) {
-    rep->blocks_scored = n;
-    rep->blocks_fetched = k;
-    rep->bytes_transferred = (double)k * (double)modeled_block_bytes_cfg(h->cfg);
-    rep->fast_tokens = F;
+    rep->blocks_scored = P.n;
+    rep->blocks_fetched = P.k;
+    rep->bytes_transferred = (double)P.k * (double)modeled_block_bytes_cfg(h->cfg);
+    rep->fast_tokens = P.F;
     rep->eviction_occurred = evicted ? 1 : 0;
     rep->union_blocks = 0;
     rep->pcie_bytes = 0;
@@ -1020,6 +1213,9 @@ int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* po
     // tensor-map encoding unavailable: keep the CUDA-core fast tier (64-token tiles)
     h->fast_tc = false;
   }
+  CREATE_CU(cudaMalloc((void**)&h->pos_dev, sizeof(uint64_t)));
+  CREATE_CU(cudaMemset(h->pos_dev, 0, sizeof(uint64_t)));
+  h->pos_synced = true;
   CREATE_CU(cudaMalloc((void**)&h->ucount, S * sizeof(uint32_t)));
   CREATE_CU(cudaMemset(h->ucount, 0, S * sizeof(uint32_t)));
   CREATE_CU(pinned_alloc((void**)&h->h_ucount, S * sizeof(uint32_t)));
@@ -1067,6 +1263,7 @@ int ttkv_gpu_set_stream(ttkv_gpu* h, void* stream) {
     CU(h, cudaStreamCreateWithFlags(&h->s0, cudaStreamNonBlocking));
     h->own_s0 = true;
   }
+  h->gen++;
   return TTKV_OK;
 }
 
@@ -1178,6 +1375,7 @@ int ttkv_gpu_append(ttkv_gpu* h, const void* keys, const void* values, uint64_t 
                         dtype == TTKV_DTYPE_F16 ? kInF16 : kInF32, h->appended, n, n, h->s0));
   }
   h->appended += n;
+  h->pos_synced = false;
   CU(h, cudaStreamSynchronize(h->s0));
   return TTKV_OK;
 }
@@ -1239,16 +1437,10 @@ int ttkv_gpu_decode_step(ttkv_gpu* h, const float* q, const void* kn, const void
   std::memcpy(h->h_q, q, qb);
   std::memcpy(h->h_k, kn, kb);
   std::memcpy(h->h_v, vn, vb);
-  CU(h, cudaMemcpyAsync(h->q_dev, h->h_q, qb, cudaMemcpyHostToDevice, h->s0));
-  CU(h, cudaMemcpyAsync(h->kn_dev, h->h_k, kb, cudaMemcpyHostToDevice, h->s0));
-  CU(h, cudaMemcpyAsync(h->vn_dev, h->h_v, vb, cudaMemcpyHostToDevice, h->s0));
+  // the H2D of q/k/v and the D2H of the output are part of the (captured) step
   int rc = decode_core(h, h->q_dev, h->kn_dev, h->vn_dev,
-                       dtype == TTKV_DTYPE_F16 ? kInF16 : kInF32, h->out_dev, rep);
+                       dtype == TTKV_DTYPE_F16 ? kInF16 : kInF32, h->out_dev, rep, true);
   if (rc) return rc;
-  CU(h, cudaMemcpyAsync(h->h_out, h->out_dev, ob, cudaMemcpyDeviceToHost, h->s0));
-  if (h->last_k)
-    CU(h, cudaMemcpyAsync(h->h_ucount, h->ucount, g.S * sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                          h->s0));
   CU(h, cudaStreamSynchronize(h->s0));
   std::memcpy(out, h->h_out, ob);
   if (rep) {
@@ -1290,6 +1482,8 @@ int ttkv_gpu_state(ttkv_gpu* h, ttkv_state* st) {
   st->heads_per_stream = h->g.G;
   st->block_capacity = h->g.n_cap;
   st->launches = h->launches;
+  st->graph_replays = h->graph_replays;
+  st->graph_captures = h->graph_captures;
   st->payload_bytes = h->g.rec.kp_off;
   return TTKV_OK;
 }
@@ -1711,6 +1905,8 @@ int ttkv_gpu_restore_slow_tier(ttkv_gpu* h, const char* const* paths, uint32_t n
   h->n_slow = n_blocks;
   h->appended = n_blocks * g.B;
   h->fast_front = n_blocks * g.B;
+  h->pos_synced = false;
+  h->gen++;
   // key scales no fp16 ring can produce (a dump from an fp32 engine): the
   // tensor-core slow kernel's fp16 operand bound no longer holds
   if (wide_scales) h->slow_tc = false;

@@ -16,6 +16,11 @@ constexpr int kInF16 = 1;
 // ttkv_kernels.cuh): the kernel's CTAs launch while the previous kernel on
 // the stream finishes.  TTKV_PDL=0 turns it off (measurement).
 bool pdl_enabled();
+// Per-launch scheduling priority: the step's critical path (score, select,
+// slow attention, combine) at the device's greatest priority, the overlapped
+// fast tier and its append at the least, whatever the caller's stream (or a
+// captured graph, where nodes otherwise take the launching stream's priority).
+int launch_priority(bool critical);
 template <typename... KArgs, typename... Args>
 cudaError_t launch_chained(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                            cudaStream_t st, Args&&... args) {
@@ -24,11 +29,29 @@ cudaError_t launch_chained(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributePriority;
+  attr[0].val.priority = launch_priority(true);
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+// A plain launch at the least priority (work that overlaps the critical path).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_background(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributePriority;
+  attr[0].val.priority = launch_priority(false);
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
@@ -53,10 +76,13 @@ struct EvictArgs {
 size_t evict_smem_bytes(const Geometry& g);
 cudaError_t launch_evict(const EvictArgs& a, uint32_t n_blocks, int in_dtype, cudaStream_t st);
 
-// ring[s][slot] <- new token (f32 or f16 input), grid-stride
+// ring[s][slot] <- new token (f32 or f16 input), grid-stride.  With `pos`
+// (device, decode steps) the first slot is *pos mod C instead of `slot`.
 cudaError_t launch_append(const Geometry& g, void* ring_k, void* ring_v, const void* k_new,
                           const void* v_new, int in_dtype, uint64_t slot, uint64_t in_stride_tok,
-                          uint64_t n_tok, cudaStream_t st);
+                          uint64_t n_tok, cudaStream_t st, const uint64_t* pos = nullptr);
+// *p = v, stream-ordered (the device step position of a handle)
+cudaError_t launch_set_u64(uint64_t* p, uint64_t v, cudaStream_t st);
 
 // device-generated N(0,1) tokens into staging [S][P][d] of the ring type
 cudaError_t launch_synth(const Geometry& g, void* k, void* v, uint64_t P, uint64_t pos0,
@@ -90,7 +116,8 @@ struct FastArgs {
   const float* q;
   void* part;         // [S][G][nfc][d_v+2] of the accumulation type
   uint64_t front;     // first fast position
-  uint32_t F;         // fast tokens
+  uint32_t F;         // fast tokens (when pos is null)
+  const uint64_t* pos;  // device step position: F = *pos + 1 - front (decode steps)
   uint32_t FC;        // tokens per chunk (multiple of TT)
   uint32_t nfc;
   uint32_t TT;        // tokens per staged tile
@@ -111,6 +138,7 @@ struct alignas(64) FastTcArgs {
   const float* q;
   void* part;  // float [S][G][nfc][d_v+2]
   uint64_t front;
+  const uint64_t* pos;  // device step position: F = *pos + 1 - front (null: F)
   uint32_t F, FC, nfc;
   double scale_log2;
 };
@@ -181,6 +209,7 @@ struct CombineArgs {
   const uint32_t* union_count;  // null when no slow work this step
   double* out;                  // [S][G][d_v] (reference output is double)
   uint32_t literal;
+  uint64_t* pos_inc;  // the device step position, advanced once the step is combined
   // Fused all-gather over peer memory (multi-GPU sharding): each CTA also
   // stores its (stream, head) row into every rank's gathered buffer
   // [S_global][G][d_v] at global stream gidx[s], then bumps that rank's

@@ -319,11 +319,12 @@ cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 template <typename T, typename Tin>
 __global__ void append_kernel(Geometry g, T* ring_k, T* ring_v, const Tin* kn, const Tin* vn,
-                              uint64_t slot0, uint64_t in_stride_tok, uint64_t n_tok) {
+                              uint64_t slot0, uint64_t in_stride_tok, uint64_t n_tok,
+                              const uint64_t* pos) {
   // one thread per 8-element group of a token row; K groups then V groups
   const uint32_t gk = g.d_k / 8, gv = g.d_v / 8, gr = gk + gv;
   const uint64_t total = (uint64_t)g.S * n_tok * gr;
-  const uint32_t slot_base = (uint32_t)(slot0 % g.C);
+  const uint32_t slot_base = (uint32_t)((pos ? *pos : slot0) % g.C);
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t c8 = (uint32_t)(i % gr);
@@ -353,7 +354,8 @@ __global__ void append_kernel(Geometry g, T* ring_k, T* ring_v, const Tin* kn, c
 template <typename T, typename Tin>
 __global__ void append_kernel_scalar(Geometry g, T* ring_k, T* ring_v, const Tin* kn,
                                      const Tin* vn, uint64_t slot0, uint64_t in_stride_tok,
-                                     uint64_t n_tok) {
+                                     uint64_t n_tok, const uint64_t* pos) {
+  if (pos) slot0 = *pos;
   const uint32_t dkv = g.d_k + g.d_v;
   const uint64_t total = (uint64_t)g.S * n_tok * dkv;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
@@ -373,37 +375,44 @@ __global__ void append_kernel_scalar(Geometry g, T* ring_k, T* ring_v, const Tin
 template <typename T, typename Tin>
 static void launch_append_t(const Geometry& g, void* ring_k, void* ring_v, const void* k_new,
                             const void* v_new, uint64_t slot, uint64_t in_stride_tok,
-                            uint64_t n_tok, cudaStream_t st) {
+                            uint64_t n_tok, cudaStream_t st, const uint64_t* pos) {
   const bool vec = g.d_k % 8 == 0 && g.d_v % 8 == 0 &&
                    ((reinterpret_cast<uintptr_t>(k_new) | reinterpret_cast<uintptr_t>(v_new)) & 15) == 0;
   const uint64_t total = (uint64_t)g.S * n_tok * (vec ? (g.d_k + g.d_v) / 8 : g.d_k + g.d_v);
   uint64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (vec)
-    append_kernel<T, Tin><<<(unsigned)blocks, 256, 0, st>>>(
-        g, (T*)ring_k, (T*)ring_v, (const Tin*)k_new, (const Tin*)v_new, slot, in_stride_tok,
-        n_tok);
+    launch_background(append_kernel<T, Tin>, dim3((unsigned)blocks), dim3(256), 0, st, g,
+                      (T*)ring_k, (T*)ring_v, (const Tin*)k_new, (const Tin*)v_new, slot,
+                      in_stride_tok, n_tok, pos);
   else
-    append_kernel_scalar<T, Tin><<<(unsigned)blocks, 256, 0, st>>>(
-        g, (T*)ring_k, (T*)ring_v, (const Tin*)k_new, (const Tin*)v_new, slot, in_stride_tok,
-        n_tok);
+    launch_background(append_kernel_scalar<T, Tin>, dim3((unsigned)blocks), dim3(256), 0, st, g,
+                      (T*)ring_k, (T*)ring_v, (const Tin*)k_new, (const Tin*)v_new, slot,
+                      in_stride_tok, n_tok, pos);
 }
 
 cudaError_t launch_append(const Geometry& g, void* ring_k, void* ring_v, const void* k_new,
                           const void* v_new, int in_dtype, uint64_t slot, uint64_t in_stride_tok,
-                          uint64_t n_tok, cudaStream_t st) {
+                          uint64_t n_tok, cudaStream_t st, const uint64_t* pos) {
   if (n_tok == 0) return cudaSuccess;
   if (g.elem == 2) {
     if (in_dtype == kInF16)
-      launch_append_t<__half, __half>(g, ring_k, ring_v, k_new, v_new, slot, in_stride_tok, n_tok, st);
+      launch_append_t<__half, __half>(g, ring_k, ring_v, k_new, v_new, slot, in_stride_tok, n_tok, st, pos);
     else
-      launch_append_t<__half, float>(g, ring_k, ring_v, k_new, v_new, slot, in_stride_tok, n_tok, st);
+      launch_append_t<__half, float>(g, ring_k, ring_v, k_new, v_new, slot, in_stride_tok, n_tok, st, pos);
   } else {
     if (in_dtype == kInF16)
-      launch_append_t<float, __half>(g, ring_k, ring_v, k_new, v_new, slot, in_stride_tok, n_tok, st);
+      launch_append_t<float, __half>(g, ring_k, ring_v, k_new, v_new, slot, in_stride_tok, n_tok, st, pos);
     else
-      launch_append_t<float, float>(g, ring_k, ring_v, k_new, v_new, slot, in_stride_tok, n_tok, st);
+      launch_append_t<float, float>(g, ring_k, ring_v, k_new, v_new, slot, in_stride_tok, n_tok, st, pos);
   }
+  return cudaGetLastError();
+}
+
+__global__ void set_u64_kernel(uint64_t* p, uint64_t v) { *p = v; }
+
+cudaError_t launch_set_u64(uint64_t* p, uint64_t v, cudaStream_t st) {
+  set_u64_kernel<<<1, 1, 0, st>>>(p, v);
   return cudaGetLastError();
 }
 
