@@ -618,7 +618,10 @@ __global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs
   const uint32_t idx = blockIdx.x;  // s * G + head
   const uint32_t s = idx / g.G;
   const uint32_t pitch = g.d_v + 2;
-  const uint32_t nsc_used = a.union_count ? (a.union_count[s] + a.CH - 1) / a.CH : 0u;
+  const uint32_t nsc_used = !a.union_count         ? 0u
+                            : a.union_count[s] == 0u ? 0u
+                            : a.nslots               ? a.nslots[s]
+                                                     : (a.union_count[s] + a.CH - 1) / a.CH;
   const Acc* fp = reinterpret_cast<const Acc*>(a.fpart) + (uint64_t)idx * a.nfc * pitch;
   const Acc* sp = a.spart ? reinterpret_cast<const Acc*>(a.spart) + (uint64_t)idx * a.nsc * pitch
                           : nullptr;

@@ -414,11 +414,50 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
   pdl_wait();  // the union lists (launched chained behind the selection)
   const Geometry& g = a.g;
   const uint32_t G = g.G;
-  const uint32_t s = blockIdx.y, chunk = blockIdx.x;
-  const uint32_t cnt = a.union_count[s];
-  const uint32_t i0 = chunk * a.CH;
-  if (i0 >= cnt) return;
-  const uint32_t nb = min(i0 + a.CH, cnt) - i0;
+  const uint32_t c = blockIdx.x;
+  // ---- balanced schedule: the step's records (every stream's union, in
+  // stream order) split evenly over the grid, which is one wave of resident
+  // CTAs; CTA c takes records [c per, (c + 1) per).  A stream's records span
+  // consecutive CTAs; each writes its share as partial slot
+  // j = c - (first CTA of the stream), and the CTA holding the stream's last
+  // record publishes the slot count for the combine. ----
+  __shared__ uint32_t sched[4];  // first stream, index in it, records, slot of the first
+  __shared__ uint32_t scan_w[8];
+  {
+    const uint32_t T = blockDim.x, t = threadIdx.x;
+    const uint32_t sb = (uint32_t)(((uint64_t)g.S * t) / T), se = (uint32_t)(((uint64_t)g.S * (t + 1)) / T);
+    uint32_t mine = 0;
+    for (uint32_t x = sb; x < se; ++x) mine += a.union_count[x];
+    uint32_t incl = mine;  // inclusive scan over the CTA (warps, then warp totals)
+    const uint32_t ln = t & 31, wp = t >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (ln >= (uint32_t)o) incl += v;
+    }
+    if (ln == 31) scan_w[wp] = incl;
+    __syncthreads();
+    uint32_t before = 0, R = 0;
+    for (uint32_t w = 0; w < (T + 31) / 32; ++w) {
+      before += w < wp ? scan_w[w] : 0u;
+      R += scan_w[w];
+    }
+    const uint32_t excl = before + incl - mine;
+    const uint32_t per = max((R + gridDim.x - 1) / gridDim.x, a.per_min);
+    const uint64_t lo = (uint64_t)c * per;
+    if (t == 0) sched[2] = lo < R ? (uint32_t)(R - lo < per ? R - lo : per) : 0u;
+    if (lo < R && excl <= lo && lo < excl + mine) {  // my streams hold record `lo`
+      uint32_t off = excl, x = sb;
+      while (off + a.union_count[x] <= lo) off += a.union_count[x++];
+      sched[0] = x;
+      sched[1] = (uint32_t)(lo - off);
+      sched[3] = c - off / per;
+    }
+    __syncthreads();
+  }
+  const uint32_t n_rec = sched[2];
+  if (n_rec == 0) return;
+  const uint32_t s_first = sched[0], i_first = sched[1], slot_first = sched[3];
 
   extern __shared__ uint8_t smem_raw[];
   // 1024-align by offsetting the shared array itself so the compiler keeps
@@ -447,19 +486,23 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
     fence_mbar_init();
   }
   __syncthreads();  // the barriers are initialized: the producer may start
-  const uint32_t* uids = a.union_ids + (uint64_t)s * g.n_cap + i0;
-  const uint32_t* umask = a.union_mask + (uint64_t)s * g.n_cap + i0;
 
   if (warp == 0) {
     // the first records are in flight while the consumers stage q below
     if (lane == 0) {
       const uint64_t evict_first = l2_evict_first_policy();
-      for (uint32_t i = 0; i < nb; ++i) {
+      uint32_t s = s_first, ii = i_first, cnt = a.union_count[s];
+      for (uint32_t i = 0; i < n_rec; ++i, ++ii) {
+        while (ii >= cnt) {  // next stream with records
+          ii = 0;
+          cnt = a.union_count[++s];
+        }
         const uint32_t st = i % ST;
         if (i >= ST) mbar_wait_sleep(&empty[st], ((i / ST) - 1) & 1);
-        const int rec = (int)((uint64_t)s * g.n_cap + uids[i]);
+        const uint64_t at = (uint64_t)s * g.n_cap + ii;
+        const int rec = (int)((uint64_t)s * g.n_cap + a.union_ids[at]);
         uint8_t* dst = base + st * kSlowStage;
-        hms[st] = umask[i];  // published by the arrive below (release.cta)
+        hms[st] = a.union_mask[at];  // published by the arrive below (release.cta)
         mbar_arrive_expect_tx(&full[st], kSlowStage);
         tma_load_3d(dst, &a.tk, 0, 0, rec, &full[st], evict_first);
         tma_load_3d(dst + kKBox, &a.tv, 0, 0, rec, &full[st], evict_first);
@@ -469,49 +512,13 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
     return;
   }
 
-  // ---- consumer prologue (named barrier 1 over the consumer warps only) ----
   const int nthreads_c = kSlowConsumerWarps * 32;
   const uint32_t ct = threadIdx.x - 32;
-  for (uint32_t i = ct; i < 512; i += nthreads_c) qsf[i] = make_uint4(0, 0, 0, 0);
-  // q in log2 units, normalized per head by a power of two so that
-  // |q_c s_c| <= |q|max * kTcKeyScaleBound lands below 2^15: the fp16 hi part
-  // of q * s cannot overflow for any query or record (ttkv_launch.h)
-  if (ct < 8) usc[ct] = 0.f;
-  named_bar(1, nthreads_c);
-  const float* qb = a.q + (uint64_t)s * G * 128;
   const float sl = (float)a.scale_log2;
-  for (uint32_t i = ct; i < G * 128; i += nthreads_c)
-    atomicMax(reinterpret_cast<uint32_t*>(usc) + i / 128, __float_as_uint(fabsf(qb[i] * sl)));
-  named_bar(1, nthreads_c);
-  {
-    float f = 1.f, uns = 1.f;
-    if (ct < 8) f = pow2_normalizer(usc[ct] * kTcKeyScaleBound, 24, &uns);
-    named_bar(1, nthreads_c);
-    if (ct < 8) {
-      usc[ct] = uns;  // 2^24: the subnormal K codes
-      mst[ct] = f;    // scratch until the stats are initialized below
-    }
-  }
-  named_bar(1, nthreads_c);
-  for (uint32_t i = ct; i < GT * 128; i += nthreads_c)
-    qsm[i] = (i / 128 < G) ? (qb[i] * sl) * mst[i / 128] : 0.f;
-  named_bar(1, nthreads_c);
-  if (ct < 8) {
-    mst[ct] = -INFINITY;
-    lst[ct] = 0.0f;
-  }
-  named_bar(1, nthreads_c);
-
   const uint32_t cw = warp - 1;
   const uint32_t gq = lane >> 2, qq = lane & 3;  // fragment row group / thread in group
   // PV ownership: channels c0 .. c0 + 3, heads 2qq, 2qq + 1
   const uint32_t c0 = 32 * cw + 4 * gq;
-  float acc[4][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.f;
-  uint32_t seen = 0;
-  // score unscale of this lane's heads (PK: head qq; otherwise 2qq, 2qq + 1)
-  const float uns0 = usc[PK ? qq : 2 * qq], uns1 = usc[2 * qq + 1];
   // Swizzle-folded shared-memory offsets (loop-invariant):
   //  K (128B swizzle): ldmatrix row address of matrix m = lane / 8 -- token
   //  32cw + 16mt + 8(m&1) + (lane&7), 16-byte chunk 2jp + (m>>1); the XOR
@@ -527,295 +534,347 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
   //  V (64B swizzle): tokens 16ks + 2qq + {0,1,8,9} all have ((t >> 1) & 3) = qq
   const uint32_t voff = 2 * qq * 64 + ((c0 >> 1) ^ (qq << 4));
 
-  for (uint32_t i = 0; i < nb; ++i) {
-    const uint32_t st = i % ST;
-    mbar_wait(&full[st], (i / ST) & 1);
-    uint8_t* stg = base + st * kSlowStage;
-    const uint32_t kb = smem_u32(stg);
-    const uint8_t* vn = stg + kKBox;
-    const float* kp = reinterpret_cast<const float*>(stg + kKBox + kVBox);  // {s,z} x 128
-    const float* vp = kp + 2 * 128;
-    const uint32_t hm = hms[st];
-    seen |= hm;
-
-    // ---- (q * s) B fragments (hi/lo) and this lane's share of beta = q . z
-    // for heads cw and cw + 4 (reduced after the QK MMAs are issued) ----
-    float bpart[2] = {0.f, 0.f};
-#pragma unroll
-    for (int rep = 0; rep < 2; ++rep) {
-      const uint32_t e = ct + rep * nthreads_c;  // warp-uniform: one head per warp
-      if (e >= G * 32) break;
-      const uint32_t h = e >> 5, j = (e >> 2) & 7u, q4 = e & 3u;
-      const uint32_t c = 16 * j + 4 * q4;
-      const float4 qv = *reinterpret_cast<const float4*>(qsm + h * 128 + c);
-      const float4 sz0 = *reinterpret_cast<const float4*>(kp + 2 * c);
-      const float4 sz1 = *reinterpret_cast<const float4*>(kp + 2 * c + 4);
-      uint32_t h01, l01, h23, l23;
-      split2(qv.x * sz0.x, qv.y * sz0.z, h01, l01);
-      split2(qv.z * sz1.x, qv.w * sz1.z, h23, l23);
-      if constexpr (PK) {  // column 2h: hi, 2h + 1: lo
-        uint2* qsf2 = reinterpret_cast<uint2*>(qsf);
-        qsf2[(j * 8 + 2 * h) * 4 + q4] = make_uint2(h01, h23);
-        qsf2[(j * 8 + 2 * h + 1) * 4 + q4] = make_uint2(l01, l23);
-      } else {
-        qsf[(j * 8 + h) * 4 + q4] = make_uint4(h01, h23, l01, l23);
+  // ---- consumer: one segment per stream this CTA touches ----
+  uint32_t s = s_first, ii = i_first, cnt = a.union_count[s_first], slot = slot_first;
+  for (uint32_t r0 = 0; r0 < n_rec;) {
+    while (ii >= cnt) {  // next stream with records
+      ii = 0;
+      cnt = a.union_count[++s];
+      slot = 0;
+    }
+    const uint32_t seg = min(n_rec - r0, cnt - ii);
+    // ---- stage q of stream s (named barrier 1 over the consumer warps only) ----
+    for (uint32_t i = ct; i < 512; i += nthreads_c) qsf[i] = make_uint4(0, 0, 0, 0);
+    // q in log2 units, normalized per head by a power of two so that
+    // |q_c s_c| <= |q|max * kTcKeyScaleBound lands below 2^15: the fp16 hi part
+    // of q * s cannot overflow for any query or record (ttkv_launch.h)
+    if (ct < 8) usc[ct] = 0.f;
+    named_bar(1, nthreads_c);
+    const float* qb = a.q + (uint64_t)s * G * 128;
+    for (uint32_t i = ct; i < G * 128; i += nthreads_c)
+      atomicMax(reinterpret_cast<uint32_t*>(usc) + i / 128, __float_as_uint(fabsf(qb[i] * sl)));
+    named_bar(1, nthreads_c);
+    {
+      float f = 1.f, uns = 1.f;
+      if (ct < 8) f = pow2_normalizer(usc[ct] * kTcKeyScaleBound, 24, &uns);
+      named_bar(1, nthreads_c);
+      if (ct < 8) {
+        usc[ct] = uns;  // 2^24: the subnormal K codes
+        mst[ct] = f;    // scratch until the stats are initialized below
       }
-      bpart[rep] = qv.x * sz0.y + qv.y * sz0.w + qv.z * sz1.y + qv.w * sz1.w;
+    }
+    named_bar(1, nthreads_c);
+    for (uint32_t i = ct; i < GT * 128; i += nthreads_c)
+      qsm[i] = (i / 128 < G) ? (qb[i] * sl) * mst[i / 128] : 0.f;
+    named_bar(1, nthreads_c);
+    if (ct < 8) {
+      mst[ct] = -INFINITY;
+      lst[ct] = 0.0f;
     }
     named_bar(1, nthreads_c);
 
-    // ---- QK^T: warp cw -> tokens [32cw, 32cw + 32) = 2 m-tiles; hi and lo
-    // accumulate in independent chains (PK: one chain per k-half, hi and lo
-    // in adjacent columns) ----
-    if constexpr (PK) {
-      const uint2* qsf2 = reinterpret_cast<const uint2*>(qsf);
-      float c[2][2][4];
+    float acc[4][2];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) c[mt][0][e] = c[mt][1][e] = 0.f;
-#pragma unroll
-      for (int jp = 0; jp < 4; ++jp) {
-        const uint2 b0 = qsf2[((2 * jp) * 8 + gq) * 4 + qq];
-        const uint2 b1 = qsf2[((2 * jp + 1) * 8 + gq) * 4 + qq];
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          const uint32_t addr = kb + koff[jp] + mt * 16 * 128;
-          uint32_t r0, r1, r2, r3, a0, a1, a2, a3;
-          ldsm_x4(addr, r0, r1, r2, r3);
-          codes_to_h2(r0, a0, a2);
-          codes_to_h2(r1, a1, a3);
-          mma_a4(c[mt][0], a0, a1, a2, a3, b0.x, b0.y);
-          codes_to_h2(r2, a0, a2);
-          codes_to_h2(r3, a1, a3);
-          mma_a4(c[mt][1], a0, a1, a2, a3, b1.x, b1.y);
-        }
-      }
+    for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.f;
+    uint32_t seen = 0;
+    // score unscale of this lane's heads (PK: head qq; otherwise 2qq, 2qq + 1)
+    const float uns0 = usc[PK ? qq : 2 * qq], uns1 = usc[2 * qq + 1];
+    for (uint32_t i = r0; i < r0 + seg; ++i) {
+      const uint32_t st = i % ST;
+      mbar_wait(&full[st], (i / ST) & 1);
+      uint8_t* stg = base + st * kSlowStage;
+      const uint32_t kb = smem_u32(stg);
+      const uint8_t* vn = stg + kKBox;
+      const float* kp = reinterpret_cast<const float*>(stg + kKBox + kVBox);  // {s,z} x 128
+      const float* vp = kp + 2 * 128;
+      const uint32_t hm = hms[st];
+      seen |= hm;
+
+      // ---- (q * s) B fragments (hi/lo) and this lane's share of beta = q . z
+      // for heads cw and cw + 4 (reduced after the QK MMAs are issued) ----
+      float bpart[2] = {0.f, 0.f};
 #pragma unroll
       for (int rep = 0; rep < 2; ++rep) {
-        const uint32_t h = cw + rep * kSlowConsumerWarps;
-        if (h < G) {  // warp-uniform
-          const float beta = warp_sum(bpart[rep]) * (usc[h] * (1.0f / 16777216.0f));
-          if (lane == 0) bst[h] = beta;
+        const uint32_t e = ct + rep * nthreads_c;  // warp-uniform: one head per warp
+        if (e >= G * 32) break;
+        const uint32_t h = e >> 5, j = (e >> 2) & 7u, q4 = e & 3u;
+        const uint32_t c = 16 * j + 4 * q4;
+        const float4 qv = *reinterpret_cast<const float4*>(qsm + h * 128 + c);
+        const float4 sz0 = *reinterpret_cast<const float4*>(kp + 2 * c);
+        const float4 sz1 = *reinterpret_cast<const float4*>(kp + 2 * c + 4);
+        uint32_t h01, l01, h23, l23;
+        split2(qv.x * sz0.x, qv.y * sz0.z, h01, l01);
+        split2(qv.z * sz1.x, qv.w * sz1.z, h23, l23);
+        if constexpr (PK) {  // column 2h: hi, 2h + 1: lo
+          uint2* qsf2 = reinterpret_cast<uint2*>(qsf);
+          qsf2[(j * 8 + 2 * h) * 4 + q4] = make_uint2(h01, h23);
+          qsf2[(j * 8 + 2 * h + 1) * 4 + q4] = make_uint2(l01, l23);
+        } else {
+          qsf[(j * 8 + h) * 4 + q4] = make_uint4(h01, h23, l01, l23);
         }
+        bpart[rep] = qv.x * sz0.y + qv.y * sz0.w + qv.z * sz1.y + qv.w * sz1.w;
       }
-      // thread (gq, qq): columns 2qq (hi) and 2qq + 1 (lo) of head qq
-      if (qq < G) {
+      named_bar(1, nthreads_c);
+
+      // ---- QK^T: warp cw -> tokens [32cw, 32cw + 32) = 2 m-tiles; hi and lo
+      // accumulate in independent chains (PK: one chain per k-half, hi and lo
+      // in adjacent columns) ----
+      if constexpr (PK) {
+        const uint2* qsf2 = reinterpret_cast<const uint2*>(qsf);
+        float c[2][2][4];
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-          for (int e = 0; e < 4; e += 2) {
-            const uint32_t t = 32 * cw + 16 * mt + gq + 4 * e;
-            sc[qq * kScPitch + t] =
-                ((c[mt][0][e] + c[mt][0][e + 1]) + (c[mt][1][e] + c[mt][1][e + 1])) * uns0;
+          for (int e = 0; e < 4; ++e) c[mt][0][e] = c[mt][1][e] = 0.f;
+#pragma unroll
+        for (int jp = 0; jp < 4; ++jp) {
+          const uint2 b0 = qsf2[((2 * jp) * 8 + gq) * 4 + qq];
+          const uint2 b1 = qsf2[((2 * jp + 1) * 8 + gq) * 4 + qq];
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            const uint32_t addr = kb + koff[jp] + mt * 16 * 128;
+            uint32_t r0, r1, r2, r3, a0, a1, a2, a3;
+            ldsm_x4(addr, r0, r1, r2, r3);
+            codes_to_h2(r0, a0, a2);
+            codes_to_h2(r1, a1, a3);
+            mma_a4(c[mt][0], a0, a1, a2, a3, b0.x, b0.y);
+            codes_to_h2(r2, a0, a2);
+            codes_to_h2(r3, a1, a3);
+            mma_a4(c[mt][1], a0, a1, a2, a3, b1.x, b1.y);
+          }
+        }
+#pragma unroll
+        for (int rep = 0; rep < 2; ++rep) {
+          const uint32_t h = cw + rep * kSlowConsumerWarps;
+          if (h < G) {  // warp-uniform
+            const float beta = warp_sum(bpart[rep]) * (usc[h] * (1.0f / 16777216.0f));
+            if (lane == 0) bst[h] = beta;
+          }
+        }
+        // thread (gq, qq): columns 2qq (hi) and 2qq + 1 (lo) of head qq
+        if (qq < G) {
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int e = 0; e < 4; e += 2) {
+              const uint32_t t = 32 * cw + 16 * mt + gq + 4 * e;
+              sc[qq * kScPitch + t] =
+                  ((c[mt][0][e] + c[mt][0][e + 1]) + (c[mt][1][e] + c[mt][1][e + 1])) * uns0;
+            }
+        }
+      } else {
+        float c[2][2][4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) c[mt][0][e] = c[mt][1][e] = 0.f;
+#pragma unroll
+        for (int jp = 0; jp < 4; ++jp) {
+          const uint4 b0 = qsf[((2 * jp) * 8 + gq) * 4 + qq];
+          const uint4 b1 = qsf[((2 * jp + 1) * 8 + gq) * 4 + qq];
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            // matrices: (tok 0-7, chunk 2jp), (tok 8-15, 2jp), (tok 0-7, 2jp+1), (tok 8-15, 2jp+1)
+            const uint32_t addr = kb + koff[jp] + mt * 16 * 128;
+            uint32_t r0, r1, r2, r3, a0, a1, a2, a3;
+            ldsm_x4(addr, r0, r1, r2, r3);
+            codes_to_h2(r0, a0, a2);
+            codes_to_h2(r1, a1, a3);
+            mma_a4(c[mt][0], a0, a1, a2, a3, b0.x, b0.y);
+            mma_a4(c[mt][1], a0, a1, a2, a3, b0.z, b0.w);
+            codes_to_h2(r2, a0, a2);
+            codes_to_h2(r3, a1, a3);
+            mma_a4(c[mt][0], a0, a1, a2, a3, b1.x, b1.y);
+            mma_a4(c[mt][1], a0, a1, a2, a3, b1.z, b1.w);
+          }
+        }
+#pragma unroll
+        for (int rep = 0; rep < 2; ++rep) {
+          const uint32_t h = cw + rep * kSlowConsumerWarps;
+          if (h < G) {  // warp-uniform
+            // qsm carries the pow2 normalizer 2^-k; usc[h] = 2^(24 + k)
+            const float beta = warp_sum(bpart[rep]) * (usc[h] * (1.0f / 16777216.0f));
+            if (lane == 0) bst[h] = beta;
+          }
+        }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t h = 2 * qq + (e & 1);
+            const uint32_t t = 32 * cw + 16 * mt + gq + 8 * (e >> 1);
+            if (h < G) sc[h * kScPitch + t] = (c[mt][0][e] + c[mt][1][e]) * ((e & 1) ? uns1 : uns0);
           }
       }
-    } else {
-      float c[2][2][4];
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) c[mt][0][e] = c[mt][1][e] = 0.f;
-#pragma unroll
-      for (int jp = 0; jp < 4; ++jp) {
-        const uint4 b0 = qsf[((2 * jp) * 8 + gq) * 4 + qq];
-        const uint4 b1 = qsf[((2 * jp + 1) * 8 + gq) * 4 + qq];
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          // matrices: (tok 0-7, chunk 2jp), (tok 8-15, 2jp), (tok 0-7, 2jp+1), (tok 8-15, 2jp+1)
-          const uint32_t addr = kb + koff[jp] + mt * 16 * 128;
-          uint32_t r0, r1, r2, r3, a0, a1, a2, a3;
-          ldsm_x4(addr, r0, r1, r2, r3);
-          codes_to_h2(r0, a0, a2);
-          codes_to_h2(r1, a1, a3);
-          mma_a4(c[mt][0], a0, a1, a2, a3, b0.x, b0.y);
-          mma_a4(c[mt][1], a0, a1, a2, a3, b0.z, b0.w);
-          codes_to_h2(r2, a0, a2);
-          codes_to_h2(r3, a1, a3);
-          mma_a4(c[mt][0], a0, a1, a2, a3, b1.x, b1.y);
-          mma_a4(c[mt][1], a0, a1, a2, a3, b1.z, b1.w);
-        }
-      }
-#pragma unroll
-      for (int rep = 0; rep < 2; ++rep) {
-        const uint32_t h = cw + rep * kSlowConsumerWarps;
-        if (h < G) {  // warp-uniform
-          // qsm carries the pow2 normalizer 2^-k; usc[h] = 2^(24 + k)
-          const float beta = warp_sum(bpart[rep]) * (usc[h] * (1.0f / 16777216.0f));
-          if (lane == 0) bst[h] = beta;
-        }
-      }
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint32_t h = 2 * qq + (e & 1);
-          const uint32_t t = 32 * cw + 16 * mt + gq + 8 * (e >> 1);
-          if (h < G) sc[h * kScPitch + t] = (c[mt][0][e] + c[mt][1][e]) * ((e & 1) ? uns1 : uns0);
-        }
-    }
-    named_bar(1, nthreads_c);
+      named_bar(1, nthreads_c);
 
-    // ---- block softmax statistics + P fragments (one warp per head); lane
-    // (ks, q) owns tokens 16ks + 2q + {0, 1, 8, 9} ----
-    for (uint32_t h = cw; h < G; h += kSlowConsumerWarps) {
-      const uint32_t ks = lane >> 2, q4 = lane & 3;
-      uint4* dst = phl + (ks * 8 + h) * 4 + q4;
-      uint2* dhi = reinterpret_cast<uint2*>(phl) + (ks * 8 + 2 * h) * 4 + q4;  // PK columns
-      uint2* dlo = dhi + 4;
-      if (!((hm >> h) & 1u)) {  // head did not select this block
+      // ---- block softmax statistics + P fragments (one warp per head); lane
+      // (ks, q) owns tokens 16ks + 2q + {0, 1, 8, 9} ----
+      for (uint32_t h = cw; h < G; h += kSlowConsumerWarps) {
+        const uint32_t ks = lane >> 2, q4 = lane & 3;
+        uint4* dst = phl + (ks * 8 + h) * 4 + q4;
+        uint2* dhi = reinterpret_cast<uint2*>(phl) + (ks * 8 + 2 * h) * 4 + q4;  // PK columns
+        uint2* dlo = dhi + 4;
+        if (!((hm >> h) & 1u)) {  // head did not select this block
+          if constexpr (PK) {
+            *dhi = make_uint2(0, 0);
+            *dlo = make_uint2(0, 0);
+          } else {
+            *dst = make_uint4(0, 0, 0, 0);
+          }
+          if (lane == 0) {
+            ast[h] = 1.0f;
+            pst[h] = 0.0f;
+          }
+          continue;
+        }
+        const float* row = sc + h * kScPitch + 16 * ks + 2 * q4;
+        const float beta = bst[h];
+        float2 v01 = *reinterpret_cast<const float2*>(row);
+        float2 v89 = *reinterpret_cast<const float2*>(row + 8);
+        v01.x += beta; v01.y += beta; v89.x += beta; v89.y += beta;
+        const float bm = warp_max_redux(fmaxf(fmaxf(v01.x, v01.y), fmaxf(v89.x, v89.y)));
+        const float m_old = mst[h];
+        const float m_new = a.literal ? bm : fmaxf(m_old, bm);
+        float p0 = exp2f(v01.x - m_new), p1 = exp2f(v01.y - m_new);
+        float p8 = exp2f(v89.x - m_new), p9 = exp2f(v89.y - m_new);
+        const float sum = warp_sum((p0 + p1) + (p8 + p9));
+        if (a.literal) {  // each block its own normalized partition (engine.cpp:67-72)
+          const float inv = 1.0f / sum;
+          p0 *= inv; p1 *= inv; p8 *= inv; p9 *= inv;
+        }
+        uint32_t h01, l01, h89, l89;
+        split2(p0, p1, h01, l01);
+        split2(p8, p9, h89, l89);
         if constexpr (PK) {
-          *dhi = make_uint2(0, 0);
-          *dlo = make_uint2(0, 0);
+          *dhi = make_uint2(h01, h89);
+          *dlo = make_uint2(l01, l89);
         } else {
-          *dst = make_uint4(0, 0, 0, 0);
+          *dst = make_uint4(h01, h89, l01, l89);
         }
+        __syncwarp();  // all lanes have read mst[h] before lane 0 rewrites it
         if (lane == 0) {
-          ast[h] = 1.0f;
-          pst[h] = 0.0f;
-        }
-        continue;
-      }
-      const float* row = sc + h * kScPitch + 16 * ks + 2 * q4;
-      const float beta = bst[h];
-      float2 v01 = *reinterpret_cast<const float2*>(row);
-      float2 v89 = *reinterpret_cast<const float2*>(row + 8);
-      v01.x += beta; v01.y += beta; v89.x += beta; v89.y += beta;
-      const float bm = warp_max_redux(fmaxf(fmaxf(v01.x, v01.y), fmaxf(v89.x, v89.y)));
-      const float m_old = mst[h];
-      const float m_new = a.literal ? bm : fmaxf(m_old, bm);
-      float p0 = exp2f(v01.x - m_new), p1 = exp2f(v01.y - m_new);
-      float p8 = exp2f(v89.x - m_new), p9 = exp2f(v89.y - m_new);
-      const float sum = warp_sum((p0 + p1) + (p8 + p9));
-      if (a.literal) {  // each block its own normalized partition (engine.cpp:67-72)
-        const float inv = 1.0f / sum;
-        p0 *= inv; p1 *= inv; p8 *= inv; p9 *= inv;
-      }
-      uint32_t h01, l01, h89, l89;
-      split2(p0, p1, h01, l01);
-      split2(p8, p9, h89, l89);
-      if constexpr (PK) {
-        *dhi = make_uint2(h01, h89);
-        *dlo = make_uint2(l01, l89);
-      } else {
-        *dst = make_uint4(h01, h89, l01, l89);
-      }
-      __syncwarp();  // all lanes have read mst[h] before lane 0 rewrites it
-      if (lane == 0) {
-        if (a.literal) {
-          ast[h] = 1.0f;
-          pst[h] = 1.0f;
-        } else {
-          const float alpha = exp2f(m_old - m_new);
-          lst[h] = lst[h] * alpha + sum;
-          mst[h] = m_new;
-          ast[h] = alpha;
-          pst[h] = sum;
+          if (a.literal) {
+            ast[h] = 1.0f;
+            pst[h] = 1.0f;
+          } else {
+            const float alpha = exp2f(m_old - m_new);
+            lst[h] = lst[h] * alpha + sum;
+            mst[h] = m_new;
+            ast[h] = alpha;
+            pst[h] = sum;
+          }
         }
       }
-    }
-    named_bar(1, nthreads_c);
+      named_bar(1, nthreads_c);
 
-    // ---- PV^T: warp cw -> channels [32cw, 32cw + 32) as 2 m-tiles; thread
-    // rows gq / gq + 8 of m-tile 0 = channels c0, c0 + 1, of m-tile 1 =
-    // c0 + 2, c0 + 3 (one u16 of V nibbles per token) ----
-    if constexpr (PK) {  // columns 2qq, 2qq + 1 = head qq hi, lo; chains by ks parity
-      const uint2* phl2 = reinterpret_cast<const uint2*>(phl);
-      float cf[2][2][4];
+      // ---- PV^T: warp cw -> channels [32cw, 32cw + 32) as 2 m-tiles; thread
+      // rows gq / gq + 8 of m-tile 0 = channels c0, c0 + 1, of m-tile 1 =
+      // c0 + 2, c0 + 3 (one u16 of V nibbles per token) ----
+      if constexpr (PK) {  // columns 2qq, 2qq + 1 = head qq hi, lo; chains by ks parity
+        const uint2* phl2 = reinterpret_cast<const uint2*>(phl);
+        float cf[2][2][4];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+        for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) cf[mt][0][e] = cf[mt][1][e] = 0.f;
-      const uint8_t* vt = vn + voff;
+          for (int e = 0; e < 4; ++e) cf[mt][0][e] = cf[mt][1][e] = 0.f;
+        const uint8_t* vt = vn + voff;
 #pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        const uint32_t u0 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024);
-        const uint32_t u1 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 64);
-        const uint32_t u8 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 512);
-        const uint32_t u9 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 576);
-        uint32_t x0, x1, x2, x3, y0, y1, y2, y3;
-        nibbles_to_h2(__byte_perm(u0, u1, 0x5410u), x0, x1, x2, x3);
-        nibbles_to_h2(__byte_perm(u8, u9, 0x5410u), y0, y1, y2, y3);
-        const uint2 pb = phl2[(ks * 8 + gq) * 4 + qq];
-        mma_a4(cf[0][ks & 1], x0, x1, y0, y1, pb.x, pb.y);
-        mma_a4(cf[1][ks & 1], x2, x3, y2, y3, pb.x, pb.y);
-      }
-      const uint32_t h = qq;
-      if (h < G && ((hm >> h) & 1u)) {
+        for (int ks = 0; ks < 8; ++ks) {
+          const uint32_t u0 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024);
+          const uint32_t u1 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 64);
+          const uint32_t u8 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 512);
+          const uint32_t u9 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 576);
+          uint32_t x0, x1, x2, x3, y0, y1, y2, y3;
+          nibbles_to_h2(__byte_perm(u0, u1, 0x5410u), x0, x1, x2, x3);
+          nibbles_to_h2(__byte_perm(u8, u9, 0x5410u), y0, y1, y2, y3);
+          const uint2 pb = phl2[(ks * 8 + gq) * 4 + qq];
+          mma_a4(cf[0][ks & 1], x0, x1, y0, y1, pb.x, pb.y);
+          mma_a4(cf[1][ks & 1], x2, x3, y2, y3, pb.x, pb.y);
+        }
+        const uint32_t h = qq;
+        if (h < G && ((hm >> h) & 1u)) {
+          const float4 sz01 = *reinterpret_cast<const float4*>(vp + 2 * c0);
+          const float4 sz23 = *reinterpret_cast<const float4*>(vp + 2 * c0 + 4);
+          const float vs[4] = {sz01.x * kSub20, sz01.z * kSub20, sz23.x * kSub20, sz23.z * kSub20};
+          const float vz[4] = {sz01.y, sz01.w, sz23.y, sz23.w};
+          const float alpha = ast[h], psum = pst[h];
+#pragma unroll
+          for (int ci = 0; ci < 4; ++ci) {
+            const int mt = ci >> 1, e = 2 * (ci & 1);
+            const float o = (cf[mt][0][e] + cf[mt][0][e + 1]) + (cf[mt][1][e] + cf[mt][1][e + 1]);
+            acc[ci][0] = acc[ci][0] * alpha + vs[ci] * o + vz[ci] * psum;
+          }
+        }
+      } else {
+        float cf[2][2][4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) cf[mt][0][e] = cf[mt][1][e] = 0.f;
+        const uint8_t* vt = vn + voff;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          const uint32_t u0 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024);
+          const uint32_t u1 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 64);
+          const uint32_t u8 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 512);
+          const uint32_t u9 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 576);
+          uint32_t x0, x1, x2, x3, y0, y1, y2, y3;
+          nibbles_to_h2(__byte_perm(u0, u1, 0x5410u), x0, x1, x2, x3);
+          nibbles_to_h2(__byte_perm(u8, u9, 0x5410u), y0, y1, y2, y3);
+          const uint4 pb = phl[(ks * 8 + gq) * 4 + qq];
+          mma_a4(cf[0][0], x0, x1, y0, y1, pb.x, pb.y);
+          mma_a4(cf[0][1], x0, x1, y0, y1, pb.z, pb.w);
+          mma_a4(cf[1][0], x2, x3, y2, y3, pb.x, pb.y);
+          mma_a4(cf[1][1], x2, x3, y2, y3, pb.z, pb.w);
+        }
+        // affine epilogue: acc = acc * alpha + s_c * (P . code) + z_c * sum(P)
         const float4 sz01 = *reinterpret_cast<const float4*>(vp + 2 * c0);
         const float4 sz23 = *reinterpret_cast<const float4*>(vp + 2 * c0 + 4);
         const float vs[4] = {sz01.x * kSub20, sz01.z * kSub20, sz23.x * kSub20, sz23.z * kSub20};
         const float vz[4] = {sz01.y, sz01.w, sz23.y, sz23.w};
-        const float alpha = ast[h], psum = pst[h];
 #pragma unroll
-        for (int ci = 0; ci < 4; ++ci) {
-          const int mt = ci >> 1, e = 2 * (ci & 1);
-          const float o = (cf[mt][0][e] + cf[mt][0][e + 1]) + (cf[mt][1][e] + cf[mt][1][e + 1]);
-          acc[ci][0] = acc[ci][0] * alpha + vs[ci] * o + vz[ci] * psum;
-        }
-      }
-    } else {
-      float cf[2][2][4];
+        for (int hh = 0; hh < 2; ++hh) {
+          const uint32_t h = 2 * qq + hh;
+          if (h < G && ((hm >> h) & 1u)) {
+            const float alpha = ast[h], psum = pst[h];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) cf[mt][0][e] = cf[mt][1][e] = 0.f;
-      const uint8_t* vt = vn + voff;
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        const uint32_t u0 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024);
-        const uint32_t u1 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 64);
-        const uint32_t u8 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 512);
-        const uint32_t u9 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 576);
-        uint32_t x0, x1, x2, x3, y0, y1, y2, y3;
-        nibbles_to_h2(__byte_perm(u0, u1, 0x5410u), x0, x1, x2, x3);
-        nibbles_to_h2(__byte_perm(u8, u9, 0x5410u), y0, y1, y2, y3);
-        const uint4 pb = phl[(ks * 8 + gq) * 4 + qq];
-        mma_a4(cf[0][0], x0, x1, y0, y1, pb.x, pb.y);
-        mma_a4(cf[0][1], x0, x1, y0, y1, pb.z, pb.w);
-        mma_a4(cf[1][0], x2, x3, y2, y3, pb.x, pb.y);
-        mma_a4(cf[1][1], x2, x3, y2, y3, pb.z, pb.w);
-      }
-      // affine epilogue: acc = acc * alpha + s_c * (P . code) + z_c * sum(P)
-      const float4 sz01 = *reinterpret_cast<const float4*>(vp + 2 * c0);
-      const float4 sz23 = *reinterpret_cast<const float4*>(vp + 2 * c0 + 4);
-      const float vs[4] = {sz01.x * kSub20, sz01.z * kSub20, sz23.x * kSub20, sz23.z * kSub20};
-      const float vz[4] = {sz01.y, sz01.w, sz23.y, sz23.w};
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const uint32_t h = 2 * qq + hh;
-        if (h < G && ((hm >> h) & 1u)) {
-          const float alpha = ast[h], psum = pst[h];
-#pragma unroll
-          for (int ci = 0; ci < 4; ++ci) {
-            const int mt = ci >> 1, e = 2 * (ci & 1) + hh;
-            acc[ci][hh] = acc[ci][hh] * alpha + vs[ci] * (cf[mt][0][e] + cf[mt][1][e]) +
-                          vz[ci] * psum;
+            for (int ci = 0; ci < 4; ++ci) {
+              const int mt = ci >> 1, e = 2 * (ci & 1) + hh;
+              acc[ci][hh] = acc[ci][hh] * alpha + vs[ci] * (cf[mt][0][e] + cf[mt][1][e]) +
+                            vz[ci] * psum;
+            }
           }
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
-  }
 
-  pdl_trigger();  // the combine's CTAs may get resident while partials drain
-  // ---- emit the (acc, m, l) partial of every head ----
-  named_bar(1, nthreads_c);
-  const uint32_t pitch = 128 + 2;
+
+    // ---- emit the (acc, m, l) partial of every head of stream s ----
+    // ---- emit the (acc, m, l) partial of every head ----
+    named_bar(1, nthreads_c);
+    const uint32_t pitch = 128 + 2;
 #pragma unroll
-  for (int hh = 0; hh < (PK ? 1 : 2); ++hh) {
-    const uint32_t h = PK ? qq : 2 * qq + hh;
-    if (h >= G) continue;
-    float* p = reinterpret_cast<float*>(a.part) + (((uint64_t)s * G + h) * a.nsc + chunk) * pitch;
-    const bool any = (seen >> h) & 1u;
+    for (int hh = 0; hh < (PK ? 1 : 2); ++hh) {
+      const uint32_t h = PK ? qq : 2 * qq + hh;
+      if (h >= G) continue;
+      float* p = reinterpret_cast<float*>(a.part) + (((uint64_t)s * G + h) * a.nsc + slot) * pitch;
+      const bool any = (seen >> h) & 1u;
 #pragma unroll
-    for (int ci = 0; ci < 4; ++ci) p[c0 + ci] = any ? acc[ci][hh] : 0.f;
-    if (cw == 0 && gq == 0) {
-      p[128] = any ? (a.literal ? 0.f : mst[h]) : -INFINITY;
-      p[129] = any ? (a.literal ? 1.f : lst[h]) : 0.f;
+      for (int ci = 0; ci < 4; ++ci) p[c0 + ci] = any ? acc[ci][hh] : 0.f;
+      if (cw == 0 && gq == 0) {
+        p[128] = any ? (a.literal ? 0.f : mst[h]) : -INFINITY;
+        p[129] = any ? (a.literal ? 1.f : lst[h]) : 0.f;
+      }
     }
+
+    if (ii + seg == cnt && threadIdx.x == 32) a.nslots[s] = slot + 1;  // the stream ends here
+    r0 += seg;
+    ii += seg;
   }
+  pdl_trigger();  // the combine's CTAs may get resident while partials drain
 }
 
 bool slow_tc_supported(const Geometry& g) {
@@ -838,29 +897,28 @@ static size_t slow_tc_smem() {
 }
 
 template <int GT, int ST>
-static cudaError_t launch_slow_tc_t(const SlowTcArgs& a, uint32_t grid_chunks, cudaStream_t st) {
+static cudaError_t launch_slow_tc_t(const SlowTcArgs& a, uint32_t grid_ctas, cudaStream_t st) {
   const size_t smem = slow_tc_smem<GT, ST>();
   auto kern = slow_attn_tc_kernel<GT, ST>;
   cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // max smem
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid(grid_chunks, a.g.S);
-  return launch_chained(kern, grid, dim3(32 + kSlowConsumerWarps * 32), smem, st, a);
+  return launch_chained(kern, dim3(grid_ctas), dim3(32 + kSlowConsumerWarps * 32), smem, st, a);
 }
 
 template <int ST>
-static cudaError_t launch_slow_tc_s(const SlowTcArgs& a, uint32_t grid_chunks, cudaStream_t st) {
-  if (a.g.G <= 1) return launch_slow_tc_t<1, ST>(a, grid_chunks, st);
-  if (a.g.G <= 2) return launch_slow_tc_t<2, ST>(a, grid_chunks, st);
-  if (a.g.G <= 4) return launch_slow_tc_t<4, ST>(a, grid_chunks, st);
-  return launch_slow_tc_t<8, ST>(a, grid_chunks, st);
+static cudaError_t launch_slow_tc_s(const SlowTcArgs& a, uint32_t grid_ctas, cudaStream_t st) {
+  if (a.g.G <= 1) return launch_slow_tc_t<1, ST>(a, grid_ctas, st);
+  if (a.g.G <= 2) return launch_slow_tc_t<2, ST>(a, grid_ctas, st);
+  if (a.g.G <= 4) return launch_slow_tc_t<4, ST>(a, grid_ctas, st);
+  return launch_slow_tc_t<8, ST>(a, grid_ctas, st);
 }
 
-cudaError_t launch_slow_tc(const SlowTcArgs& a, uint32_t grid_chunks, cudaStream_t st) {
-  if (grid_chunks == 0) return cudaSuccess;
+cudaError_t launch_slow_tc(const SlowTcArgs& a, uint32_t grid_ctas, cudaStream_t st) {
+  if (grid_ctas == 0) return cudaSuccess;
   static const int stages = slow_tc_stages();
-  return stages == 2 ? launch_slow_tc_s<2>(a, grid_chunks, st)
-                     : launch_slow_tc_s<3>(a, grid_chunks, st);
+  return stages == 2 ? launch_slow_tc_s<2>(a, grid_ctas, st)
+                     : launch_slow_tc_s<3>(a, grid_ctas, st);
 }
 
 // Tensor maps over the record arena (device or mapped host pointer):

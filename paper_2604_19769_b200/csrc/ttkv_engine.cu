@@ -246,6 +246,7 @@ struct ttkv_gpu {
   uint8_t* params = nullptr;  // HBM mirror of record params
   double* scores = nullptr;
   uint32_t *mask = nullptr, *uids = nullptr, *umask = nullptr, *ucount = nullptr;
+  uint32_t* nslots = nullptr;  // slow partial slots per stream (tensor-core slow tier)
   uint32_t* h_ucount = nullptr;  // pinned copy of union_count for the step report
   void* fpart = nullptr;
   void* spart = nullptr;
@@ -409,7 +410,7 @@ void free_all(ttkv_gpu* h) {
     if (p) cudaFree(p);
   };
   F(h->ring_k); F(h->ring_v); F(h->cent); F(h->params); F(h->scores); F(h->mask); F(h->uids);
-  F(h->umask); F(h->ucount); F(h->fpart); F(h->spart); F(h->q_dev);
+  F(h->umask); F(h->ucount); F(h->nslots); F(h->fpart); F(h->spart); F(h->q_dev);
   F(h->out_dev); F(h->kn_dev); F(h->vn_dev); F(h->stg_k); F(h->stg_v); F(h->stage_arena);
   if (h->arena_host) pinned_free(h->arena_host);
   else if (h->arena_dev) cudaFree(h->arena_dev);
@@ -644,7 +645,9 @@ struct StepPlan {
   bool host_io;  // stage q/k/v from and out to the handle's pinned buffers
   uint64_t n, k, F;
   uint32_t FCs, nfc, CH;
-  uint64_t grid_chunks;
+  uint64_t grid_chunks;  // slow kernel grid: chunks per stream, or CTAs (tensor-core tier)
+  uint64_t gather_chunks;
+  uint32_t per_min;      // tensor-core tier: records per CTA at least
   bool slow, early_fork;
   double scale_log2;
 };
@@ -717,7 +720,21 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
   if (P.early_fork) {
     if (int rcf = fork_fast()) return rcf;
   }
-  if (P.slow) {
+  if (P.slow && select_fused_supported(g, (uint32_t)P.n)) {
+    // score + select + union as one cluster kernel per stream
+    FusedSelectArgs a{};
+    a.g = g;
+    a.q = P.q;
+    a.cent = h->cent;
+    a.scores = h->scores;
+    a.union_ids = h->uids;
+    a.union_mask = h->umask;
+    a.union_count = h->ucount;
+    a.n = (uint32_t)P.n;
+    a.k = (uint32_t)P.k;
+    KTimer t(h, K_SELECT, h->s0);
+    CU(h, launch_select_fused(a, h->s0));
+  } else if (P.slow) {
     {
       ScoreArgs a{g, P.q, h->cent, h->scores, (uint32_t)P.n};
       KTimer t(h, K_SCORE, h->s0);
@@ -736,11 +753,13 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
       KTimer t(h, K_SELECT, h->s0, 2);  // sort + union kernels
       CU(h, launch_select(a, h->s0));
     }
+  }
+  if (P.slow) {
     if (h->opt.serial_schedule) {
       // bulk phase: every selected record crosses PCIe before any compute
       KTimer t(h, K_GATHER, h->s0);
       CU(h, launch_gather(g, h->arena_dev, h->stage_arena, h->uids, h->ucount,
-                          (uint32_t)P.grid_chunks, P.CH, h->s0));
+                          (uint32_t)P.gather_chunks, P.CH, h->s0));
     }
     if (!P.early_fork) {
       if (int rcf = fork_fast()) return rcf;
@@ -754,7 +773,8 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
       a.union_count = h->ucount;
       a.q = P.q;
       a.part = h->spart;
-      a.CH = P.CH;
+      a.nslots = h->nslots;
+      a.per_min = P.per_min;
       a.nsc = (uint32_t)h->spart_chunks;
       a.literal = h->opt.literal_additive_merge ? 1u : 0u;
       a.scale_log2 = P.scale_log2;
@@ -791,6 +811,7 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
     a.nsc = (uint32_t)h->spart_chunks;
     a.CH = P.CH;
     a.union_count = P.slow ? h->ucount : nullptr;
+    a.nslots = P.slow && h->slow_tc ? h->nslots : nullptr;
     a.out = P.out;
     a.literal = h->opt.literal_additive_merge ? 1u : 0u;
     a.pos_inc = h->pos_dev;
@@ -921,9 +942,22 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       return e ? (uint32_t)std::max(1, std::min(256, std::atoi(e))) : 0u;
     }();
     if (ch_env) P.CH = ch_env;
-    P.grid_chunks = (P.n + P.CH - 1) / P.CH;
-    int rc = ensure_spart(h, P.grid_chunks);
+    P.grid_chunks = P.gather_chunks = (P.n + P.CH - 1) / P.CH;
+    uint64_t nsc = P.grid_chunks;
+    if (h->slow_tc) {
+      // balanced schedule over one wave of CTAs; a stream's records span at
+      // most nsc CTAs when every CTA takes >= n / (nsc - 1) records, so nsc
+      // is as large as ~32 MB of partials allows (small S: every CTA a share)
+      const uint64_t ctas = (uint64_t)h->sms * slow_tc_ctas_per_sm();
+      const uint64_t row = (uint64_t)g.S * g.G * (g.d_v + 2) * h->acc;
+      nsc = std::min<uint64_t>(ctas + 1, std::max<uint64_t>(P.grid_chunks + 1, (32ull << 20) / row));
+      nsc = std::max<uint64_t>(nsc, 2);
+      P.grid_chunks = ctas;
+    }
+    int rc = ensure_spart(h, nsc);
     if (rc) return rc;
+    if (h->slow_tc)  // spart_chunks >= 2 here
+      P.per_min = (uint32_t)((P.n + h->spart_chunks - 2) / (h->spart_chunks - 1));
   }
   if (!h->pos_synced) {  // host-side appends / prefill / restore moved `appended`
     CU(h, launch_set_u64(h->pos_dev, pos, h->s0));
@@ -1217,6 +1251,7 @@ int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* po
   CREATE_CU(cudaMemset(h->pos_dev, 0, sizeof(uint64_t)));
   h->pos_synced = true;
   CREATE_CU(cudaMalloc((void**)&h->ucount, S * sizeof(uint32_t)));
+  CREATE_CU(cudaMalloc((void**)&h->nslots, S * sizeof(uint32_t)));
   CREATE_CU(cudaMemset(h->ucount, 0, S * sizeof(uint32_t)));
   CREATE_CU(pinned_alloc((void**)&h->h_ucount, S * sizeof(uint32_t)));
   CREATE_CU(cudaMalloc((void**)&h->fpart, S * g.G * h->nfc_cap * (g.d_v + 2) * h->acc));

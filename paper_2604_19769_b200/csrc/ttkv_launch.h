@@ -109,6 +109,24 @@ struct SelectArgs {
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t st);
 uint32_t select_max_blocks();
 
+// score_blocks + select_top_k + the per-stream union in ONE kernel: a thread-
+// block cluster per stream scores a slice of the blocks per CTA, CTA h of the
+// cluster radix-selects head h over the cluster's keys (distributed shared
+// memory) and CTA 0 compacts the union.  Same bits as score_kernel +
+// select_topk_kernel + select_union_kernel (the head mask `mask` is not used).
+struct FusedSelectArgs {
+  Geometry g;
+  const float* q;
+  const float* cent;
+  double* scores;
+  uint32_t* union_ids;
+  uint32_t* union_mask;
+  uint32_t* union_count;
+  uint32_t n, k;
+};
+bool select_fused_supported(const Geometry& g, uint32_t n);
+cudaError_t launch_select_fused(const FusedSelectArgs& a, cudaStream_t st);
+
 struct FastArgs {
   Geometry g;
   const void* ring_k;
@@ -153,8 +171,10 @@ struct alignas(64) SlowTcArgs {
   const uint32_t* union_mask;
   const uint32_t* union_count;
   const float* q;
-  void* part;
-  uint32_t CH, nsc, literal;
+  void* part;        // [S][G][nsc][d_v + 2]
+  uint32_t* nslots;  // [S] partial slots written per stream (balanced schedule)
+  uint32_t per_min;  // records per CTA at least: no stream spans more than nsc CTAs
+  uint32_t nsc, literal;
   double scale_log2;
 };
 bool slow_tc_supported(const Geometry& g);
@@ -166,7 +186,8 @@ uint32_t slow_tc_ctas_per_sm();  // resident CTAs per SM of the slow tensor-core
 // handle to the CUDA-core slow kernel.
 constexpr float kTcKeyScaleBound = 514.0f;
 cudaError_t make_arena_tmaps(const Geometry& g, uint8_t* arena, SlowTcArgs& a);
-cudaError_t launch_slow_tc(const SlowTcArgs& a, uint32_t grid_chunks, cudaStream_t st);
+// grid: one wave of resident CTAs (sms * slow_tc_ctas_per_sm())
+cudaError_t launch_slow_tc(const SlowTcArgs& a, uint32_t grid_ctas, cudaStream_t st);
 
 bool fast_tc_supported(const Geometry& g);
 uint32_t fast_tc_tile();
@@ -207,6 +228,8 @@ struct CombineArgs {
   uint32_t nsc;
   uint32_t CH;
   const uint32_t* union_count;  // null when no slow work this step
+  const uint32_t* nslots;       // slow partial slots per stream (balanced schedule), else
+                                // ceil(union_count / CH)
   double* out;                  // [S][G][d_v] (reference output is double)
   uint32_t literal;
   uint64_t* pos_inc;  // the device step position, advanced once the step is combined

@@ -16,6 +16,10 @@
 // Roofline: scoring reads the resident centroids once per step,
 // n_blk * d_k * 4 bytes per stream (508 KB at 128K ctx), plus G * n_blk * d_k
 // fp64 mul+add; both are microseconds at cfg2 and hide under the PCIe stream.
+#include <cooperative_groups.h>
+
+#include <cstdlib>
+
 #include "ttkv_kernels.cuh"
 #include "ttkv_launch.h"
 
@@ -142,34 +146,25 @@ __device__ __forceinline__ uint32_t topk_digit(uint64_t key, uint32_t id, int p)
   return p < 8 ? (uint32_t)(key >> (56 - 8 * p)) & 0xffu : (p == 8 ? (id >> 7) & 0x7fu : id & 0x7fu);
 }
 
-__global__ void __launch_bounds__(kTopkThreads) select_topk_kernel(SelectArgs a) {
-  pdl_trigger();  // few CTAs: let the union kernel's CTAs get resident
-  pdl_wait();     // the scores
-  const Geometry& g = a.g;
-  const uint32_t h = blockIdx.x, s = blockIdx.y;
-  const double* sc = a.scores + ((uint64_t)s * g.Gs + h) * g.n_cap;
-  __shared__ uint32_t hist[256];
-  __shared__ uint32_t sh_digit, sh_need, sh_done;
+// The radix selection proper, shared by select_topk_kernel and the fused
+// selection kernel: kTopkThreads threads find the k-th largest (key, id) pair
+// of n elements; key_of(i, pass) yields element i's order key.
+struct RadixThreshold {
+  int p;             // last pass taken (digits of passes <= p are fixed)
+  uint64_t key_pre;  // chosen key digits (passes < 8)
+  uint32_t id_pre;   // chosen id digits (passes 8, 9)
+};
+struct RadixShared {
+  uint32_t hist[256];
+  uint32_t digit, need, done;
+};
+template <typename KeyOf>
+__device__ RadixThreshold radix_threshold(KeyOf key_of, uint32_t n, uint32_t k, RadixShared& sh) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // the order keys are computed once (pass 0) and re-read from shared memory
-  // by the later passes and the final marking, not from L2 each time
-  extern __shared__ uint64_t keys_sm[];
-  const bool cached = a.n <= kTopkSmemKeys;
-  auto key_of = [&](uint32_t i, int pass) -> uint64_t {
-    if (!cached) return order_key(sc[i]);
-    if (pass == 0) {
-      const uint64_t k = order_key(sc[i]);
-      keys_sm[i] = k;
-      return k;
-    }
-    return keys_sm[i];
-  };
-
   uint64_t key_pre = 0;  // chosen key digits so far (passes < 8)
   uint32_t id_pre = 0;   // chosen id digits (passes 8, 9)
-  uint32_t need = a.k;
+  uint32_t need = k;
   int p = 0;
-  bool done = false;
   // does (key, id) agree with the chosen digits of passes < p?
   auto match = [&](uint64_t key, uint32_t id, int pp) -> bool {
     if (pp == 0) return true;
@@ -177,11 +172,11 @@ __global__ void __launch_bounds__(kTopkThreads) select_topk_kernel(SelectArgs a)
     return key == key_pre && (id >> 7) == id_pre;
   };
   for (;; ++p) {
-    for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
+    for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) sh.hist[b] = 0;
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < a.n; i += blockDim.x) {
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
       const uint64_t key = key_of(i, p);
-      if (match(key, i, p)) atomicAdd(&hist[topk_digit(key, i, p)], 1u);
+      if (match(key, i, p)) atomicAdd(&sh.hist[topk_digit(key, i, p)], 1u);
     }
     __syncthreads();
     if (warp == 0) {
@@ -189,7 +184,7 @@ __global__ void __launch_bounds__(kTopkThreads) select_topk_kernel(SelectArgs a)
       uint32_t c[8], tot = 0;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        c[e] = hist[255 - 8 * lane - e];
+        c[e] = sh.hist[255 - 8 * lane - e];
         tot += c[e];
       }
       uint32_t incl = tot;  // inclusive prefix over lanes (higher bins first)
@@ -204,9 +199,9 @@ __global__ void __launch_bounds__(kTopkThreads) select_topk_kernel(SelectArgs a)
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           if (above + c[e] >= need) {
-            sh_digit = 255 - 8 * lane - e;
-            sh_need = need - above;
-            sh_done = (c[e] == need - above) ? 1u : 0u;
+            sh.digit = 255 - 8 * lane - e;
+            sh.need = need - above;
+            sh.done = (c[e] == need - above) ? 1u : 0u;
             break;
           }
           above += c[e];
@@ -214,29 +209,50 @@ __global__ void __launch_bounds__(kTopkThreads) select_topk_kernel(SelectArgs a)
       }
     }
     __syncthreads();
-    const uint32_t d = sh_digit;
-    need = sh_need;
-    done = sh_done != 0;
+    const uint32_t d = sh.digit;
+    need = sh.need;
+    const bool done = sh.done != 0;
     if (p < 8) key_pre = (key_pre << 8) | d;
     else id_pre = (id_pre << 7) | d;
     if (done || p == 9) break;
-    __syncthreads();  // sh_* are rewritten by the next pass
+    __syncthreads();  // sh.* are rewritten by the next pass
   }
-  // selected: (key, id) >= threshold, compared on the digits fixed so far
+  return {p, key_pre, id_pre};
+}
+// selected: (key, id) >= threshold, compared on the digits fixed so far
+__device__ __forceinline__ bool radix_selected(uint64_t key, uint32_t i, const RadixThreshold& t) {
+  if (t.p < 8) return (key >> (56 - 8 * t.p)) >= t.key_pre;
+  if (t.p == 8) return key > t.key_pre || (key == t.key_pre && (i >> 7) >= t.id_pre);
+  return key > t.key_pre || (key == t.key_pre && i >= t.id_pre);
+}
+
+__global__ void __launch_bounds__(kTopkThreads) select_topk_kernel(SelectArgs a) {
+  pdl_trigger();  // few CTAs: let the union kernel's CTAs get resident
+  pdl_wait();     // the scores
+  const Geometry& g = a.g;
+  const uint32_t h = blockIdx.x, s = blockIdx.y;
+  const double* sc = a.scores + ((uint64_t)s * g.Gs + h) * g.n_cap;
+  __shared__ RadixShared sh;
+  // the order keys are computed once (pass 0) and re-read from shared memory
+  // by the later passes and the final marking, not from L2 each time
+  extern __shared__ uint64_t keys_sm[];
+  const bool cached = a.n <= kTopkSmemKeys;
+  auto key_of = [&](uint32_t i, int pass) -> uint64_t {
+    if (!cached) return order_key(sc[i]);
+    if (pass == 0) {
+      const uint64_t k = order_key(sc[i]);
+      keys_sm[i] = k;
+      return k;
+    }
+    return keys_sm[i];
+  };
+  const RadixThreshold t = radix_threshold(key_of, a.n, a.k, sh);
   uint32_t* mask = a.mask + (uint64_t)s * g.n_cap;
   const uint32_t all_heads = (g.G >= 32) ? 0xffffffffu : ((1u << g.G) - 1u);
   const uint32_t bit = (g.Gs == g.G) ? (1u << h) : all_heads;
   for (uint32_t i = threadIdx.x; i < a.n; i += blockDim.x) {
     const uint64_t key = key_of(i, 1);  // each thread re-reads only its own keys
-    bool sel;
-    if (p < 8) {
-      sel = (key >> (56 - 8 * p)) >= key_pre;
-    } else if (p == 8) {
-      sel = key > key_pre || (key == key_pre && (i >> 7) >= id_pre);
-    } else {
-      sel = key > key_pre || (key == key_pre && i >= id_pre);
-    }
-    if (sel) atomicOr(&mask[i], bit);
+    if (radix_selected(key, i, t)) atomicOr(&mask[i], bit);
   }
 }
 
@@ -300,6 +316,251 @@ __global__ void __launch_bounds__(kSelectThreads) select_union_kernel(SelectArgs
 }
 
 uint32_t select_max_blocks() { return kSelectMaxN; }
+
+// ---------------------------------------------------------------------------
+// Fused selection: score_blocks -> select_top_k -> union for one stream per
+// thread-block cluster (relevance.cpp:19-43, engine.cpp:51-58).
+//   * CTA r of the cluster owns blocks [r nb, (r+1) nb): its centroid rows are
+//     staged in 32-channel chunks with 16-byte cp.async (row pitch 36 floats:
+//     conflict-free LDS.128), then thread t scores row t against every
+//     selection head, channels in order with one fma each -- the same fp64
+//     chain as score_kernel, so the same bits.
+//   * after a cluster barrier, CTA h gathers head h's n order keys from the
+//     cluster's shared memory (DSMEM) and runs the radix selection of
+//     select_topk_kernel on them; its selected set lands as a bitmask in CTA 0.
+//   * after a second barrier CTA 0 compacts the union of the heads' sets in
+//     ascending block id with the head bitmask, like select_union_kernel.
+// One launch instead of three, and the scores never round-trip through L2
+// before selection (layer-sequential decode is latency-bound on this chain).
+// ---------------------------------------------------------------------------
+constexpr uint32_t kFusedMaxN = 2048;
+#ifndef TTKV_PHASE_STAMP  // tools/fused_probe.cu times the phases with %globaltimer
+#define TTKV_PHASE_STAMP(k)
+#endif
+constexpr uint32_t kFusedPitch = 36;  // floats per staged 32-channel row chunk
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+
+struct FusedLayout {
+  uint32_t CL, nb, nw, nch;
+  size_t off_keys, off_gkeys, off_sel, off_tile, bytes;
+};
+__host__ __device__ inline FusedLayout fused_layout(const Geometry& g, uint32_t n) {
+  FusedLayout L{};
+  uint32_t cl = 1;
+  while (cl < g.Gs || (n + cl - 1) / cl > 128) cl *= 2;
+  L.CL = cl;
+  L.nb = (n + cl - 1) / cl;
+  L.nw = (n + 31) / 32;
+  L.nch = g.d_k / 32;
+  size_t o = (size_t)g.Gs * g.d_k * 8;          // qs [Gs][d_k] f64
+  L.off_keys = o;  o += (size_t)g.Gs * L.nb * 8;  // keys [Gs][nb] (this CTA's slice)
+  L.off_gkeys = o; o += (size_t)n * 8;            // gkeys [n] (the head this CTA selects)
+  L.off_sel = o;   o += (size_t)g.Gs * L.nw * 4;  // selection bitmasks [Gs][nw] (CTA 0)
+  o = (o + 15) & ~size_t(15);
+  L.off_tile = o;  o += (size_t)L.nch * L.nb * kFusedPitch * 4;
+  L.bytes = o;
+  return L;
+}
+
+template <int GS>
+__global__ void __launch_bounds__(kTopkThreads) select_fused_kernel(FusedSelectArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const Geometry& g = a.g;
+  const uint32_t rank = blockIdx.x, s = blockIdx.y, n = a.n;
+  const FusedLayout L = fused_layout(g, n);
+  const uint32_t r0 = rank * L.nb;
+  const uint32_t rows = r0 < n ? min(L.nb, n - r0) : 0u;
+  extern __shared__ __align__(16) uint8_t fsm[];
+  double* qs = reinterpret_cast<double*>(fsm);
+  uint64_t* keys = reinterpret_cast<uint64_t*>(fsm + L.off_keys);
+  uint64_t* gkeys = reinterpret_cast<uint64_t*>(fsm + L.off_gkeys);
+  uint32_t* selbits = reinterpret_cast<uint32_t*>(fsm + L.off_sel);
+  float* tile = reinterpret_cast<float*>(fsm + L.off_tile);  // [nch][nb][kFusedPitch]
+  __shared__ RadixShared sh;
+  __shared__ uint32_t warp_tot[kTopkThreads / 32];
+  __shared__ uint32_t base_sh;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  TTKV_PHASE_STAMP(0);
+  pdl_wait();  // the query / centroids when the previous kernel produced them
+  {  // this CTA's centroid rows, every chunk in flight at once
+    const float* cb = a.cent + ((uint64_t)s * g.n_cap + r0) * g.d_k;
+    const uint32_t per_row = g.d_k / 4, pieces = rows * per_row;
+    for (uint32_t p = threadIdx.x; p < pieces; p += blockDim.x) {
+      const uint32_t r = p / per_row, c4 = p - r * per_row;
+      cp_async16(tile + ((size_t)(c4 >> 3) * L.nb + r) * kFusedPitch + 4 * (c4 & 7),
+                 cb + (size_t)r * g.d_k + 4 * c4);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (uint32_t i = threadIdx.x; i < g.Gs * g.d_k; i += blockDim.x) {
+    const uint32_t h = i / g.d_k, c = i % g.d_k;
+    const float* qb = a.q + (uint64_t)s * g.G * g.d_k;
+    if (g.Gs == g.G) {
+      qs[i] = (double)qb[h * g.d_k + c];
+    } else {  // group-shared query q' = sum_g q_g (fp32, sequential g)
+      float acc = qb[c];
+      for (uint32_t hh = 1; hh < g.G; ++hh) acc = __fadd_rn(acc, qb[hh * g.d_k + c]);
+      qs[i] = (double)acc;
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  TTKV_PHASE_STAMP(1);
+
+  // ---- score: row t against every head, s += double(q_i) * c_i in channel
+  // order (relevance.cpp:23-26), one exact-product fma per term ----
+  if (threadIdx.x < rows) {
+    const uint32_t r = threadIdx.x;
+    double acc[GS];
+#pragma unroll
+    for (int h = 0; h < GS; ++h) acc[h] = 0.0;
+    for (uint32_t ch = 0; ch < L.nch; ++ch) {
+      const float* tr = tile + ((size_t)ch * L.nb + r) * kFusedPitch;
+      const double* qc = qs + 32 * ch;
+#pragma unroll 2
+      for (uint32_t c = 0; c < 32; c += 4) {
+        const float4 cv = *reinterpret_cast<const float4*>(tr + c);
+        const double c0 = cv.x, c1 = cv.y, c2 = cv.z, c3 = cv.w;
+#pragma unroll
+        for (int h = 0; h < GS; ++h) {
+          const double2 q01 = *reinterpret_cast<const double2*>(qc + h * g.d_k + c);
+          const double2 q23 = *reinterpret_cast<const double2*>(qc + h * g.d_k + c + 2);
+          acc[h] = __fma_rn(q01.x, c0, acc[h]);
+          acc[h] = __fma_rn(q01.y, c1, acc[h]);
+          acc[h] = __fma_rn(q23.x, c2, acc[h]);
+          acc[h] = __fma_rn(q23.y, c3, acc[h]);
+        }
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < GS; ++h) {
+      a.scores[((uint64_t)s * g.Gs + h) * g.n_cap + r0 + r] = acc[h];
+      keys[h * L.nb + r] = order_key(acc[h]);
+    }
+  }
+  TTKV_PHASE_STAMP(2);
+  cluster.sync();  // every slice's keys are visible cluster-wide
+  TTKV_PHASE_STAMP(3);
+
+  // ---- select: CTA h radix-selects head h over the gathered keys ----
+  if (rank < g.Gs) {
+    const uint32_t h = rank;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint32_t src = i / L.nb;
+      const uint64_t* pk = cluster.map_shared_rank(keys, src);
+      gkeys[i] = pk[h * L.nb + (i - src * L.nb)];
+    }
+    __syncthreads();
+    TTKV_PHASE_STAMP(4);
+    auto key_of = [&](uint32_t i, int) -> uint64_t { return gkeys[i]; };
+    const RadixThreshold t = radix_threshold(key_of, n, a.k, sh);
+    TTKV_PHASE_STAMP(5);
+    uint32_t* sb0 = cluster.map_shared_rank(selbits, 0) + h * L.nw;
+    for (uint32_t base = warp * 32; base < n; base += blockDim.x) {  // warp-uniform
+      const uint32_t i = base + lane;
+      const bool sel = i < n && radix_selected(gkeys[i], i, t);
+      const uint32_t word = __ballot_sync(0xffffffffu, sel);
+      if (lane == 0) sb0[base / 32] = word;
+    }
+  }
+  cluster.sync();  // CTA 0 holds every head's set; no peer reads remain
+  TTKV_PHASE_STAMP(6);
+  pdl_trigger();   // the attention kernel's CTAs may get resident
+  if (rank != 0) return;
+
+  // ---- union (CTA 0): ascending block id with the head bitmask ----
+  const uint32_t all_heads = (g.G >= 32) ? 0xffffffffu : ((1u << g.G) - 1u);
+  if (threadIdx.x == 0) base_sh = 0;
+  __syncthreads();
+  const uint32_t nwarps = blockDim.x >> 5;
+  for (uint32_t base = 0; base < n; base += blockDim.x) {  // CTA-uniform
+    const uint32_t b = base + threadIdx.x;
+    uint32_t m = 0;
+    if (b < n)
+      for (uint32_t h = 0; h < g.Gs; ++h)
+        if ((selbits[h * L.nw + (b >> 5)] >> (b & 31)) & 1u)
+          m |= (g.Gs == g.G) ? (1u << h) : all_heads;
+    const uint32_t ballot = __ballot_sync(0xffffffffu, m != 0u);
+    if (lane == 0) warp_tot[warp] = __popc(ballot);
+    __syncthreads();
+    uint32_t before = 0, total = 0;
+    for (uint32_t w = 0; w < nwarps; ++w) {
+      const uint32_t t = warp_tot[w];
+      before += (w < warp) ? t : 0u;
+      total += t;
+    }
+    if (m != 0u) {
+      const uint32_t pos = base_sh + before + __popc(ballot & ((1u << lane) - 1u));
+      a.union_ids[(uint64_t)s * g.n_cap + pos] = b;
+      a.union_mask[(uint64_t)s * g.n_cap + pos] = m;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) base_sh += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a.union_count[s] = base_sh;
+  TTKV_PHASE_STAMP(7);
+}
+
+bool select_fused_supported(const Geometry& g, uint32_t n) {
+  static const bool on = [] {  // TTKV_FUSED_SELECT=0: the three-kernel chain (measurement)
+    const char* e = std::getenv("TTKV_FUSED_SELECT");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || n == 0 || n > kFusedMaxN || g.d_k % 32 != 0 || g.d_k > 128 || g.Gs > 8) return false;
+  const FusedLayout L = fused_layout(g, n);
+  return L.CL <= 16 && L.nb <= kTopkThreads && L.bytes <= 200 * 1024;
+}
+
+template <int GS>
+static cudaError_t launch_select_fused_t(const FusedSelectArgs& a, const FusedLayout& L,
+                                         cudaStream_t st) {
+  auto kern = select_fused_kernel<GS>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)L.bytes);
+  if (e != cudaSuccess) return e;
+  if (L.CL > 8) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(L.CL, a.g.S);
+  cfg.blockDim = dim3(kTopkThreads);
+  cfg.dynamicSmemBytes = L.bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[3];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = L.CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributePriority;
+  attr[1].val.priority = launch_priority(true);
+  attr[2].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[2].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 3 : 2;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+cudaError_t launch_select_fused(const FusedSelectArgs& a, cudaStream_t st) {
+  const FusedLayout L = fused_layout(a.g, a.n);
+  switch (a.g.Gs) {
+    case 1: return launch_select_fused_t<1>(a, L, st);
+    case 2: return launch_select_fused_t<2>(a, L, st);
+    case 3: return launch_select_fused_t<3>(a, L, st);
+    case 4: return launch_select_fused_t<4>(a, L, st);
+    case 5: return launch_select_fused_t<5>(a, L, st);
+    case 6: return launch_select_fused_t<6>(a, L, st);
+    case 7: return launch_select_fused_t<7>(a, L, st);
+    default: return launch_select_fused_t<8>(a, L, st);
+  }
+}
 
 // The head mask (a.mask) must be all-zero on entry; select_union_kernel
 // leaves it zeroed again.  `sel` is not written: the order is a cold read.
