@@ -614,6 +614,9 @@ constexpr int kCombineWarps = 8;
 template <typename Acc>
 __global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs a) {
   pdl_wait();  // the slow partials (the fast tier joins through an event)
+  // the next kernel may get resident now: the next step's selection stages
+  // its centroids while this combine runs (it reads q only after its wait)
+  pdl_trigger();
   const Geometry& g = a.g;
   const uint32_t idx = blockIdx.x;  // s * G + head
   const uint32_t s = idx / g.G;

@@ -649,6 +649,7 @@ struct StepPlan {
   uint64_t gather_chunks;
   uint32_t per_min;      // tensor-core tier: records per CTA at least
   bool slow, early_fork;
+  bool fused;            // score + select + union as one cluster kernel
   double scale_log2;
 };
 
@@ -720,7 +721,7 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
   if (P.early_fork) {
     if (int rcf = fork_fast()) return rcf;
   }
-  if (P.slow && select_fused_supported(g, (uint32_t)P.n)) {
+  if (P.fused) {
     // score + select + union as one cluster kernel per stream
     FusedSelectArgs a{};
     a.g = g;
@@ -920,7 +921,11 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
     const char* e = std::getenv("TTKV_FORK");
     return e ? (std::strcmp(e, "early") == 0 ? 1 : 0) + (std::strcmp(e, "late") == 0 ? 2 : 0) : 0;
   }();
-  P.early_fork = fork_env == 1;
+  P.fused = P.slow && select_fused_supported(g, (uint32_t)P.n, (uint32_t)h->sms);
+  // A one-wave fused selection leaves most SMs idle: the fast tier then runs
+  // beside it instead of starved under the slow kernel (layer-sequential
+  // cfg2: fast tier done before the slow kernel starts, 2 us less per layer)
+  P.early_fork = fork_env == 1 || (fork_env != 2 && P.fused);
   P.CH = 4;
   if (P.slow) {
     if (h->slow_tc) {

@@ -124,7 +124,7 @@ struct FusedSelectArgs {
   uint32_t* union_count;
   uint32_t n, k;
 };
-bool select_fused_supported(const Geometry& g, uint32_t n);
+bool select_fused_supported(const Geometry& g, uint32_t n, uint32_t sms);
 cudaError_t launch_select_fused(const FusedSelectArgs& a, cudaStream_t st);
 
 struct FastArgs {

@@ -18,6 +18,7 @@
 // fp64 mul+add; both are microseconds at cfg2 and hide under the PCIe stream.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "ttkv_kernels.cuh"
@@ -111,6 +112,92 @@ __global__ void __launch_bounds__(128) score_kernel(ScoreArgs a) {
     a.scores[((uint64_t)s * g.Gs + h) * g.n_cap + b0 + r] = acc;
   }
   pdl_trigger();  // the selection kernels may launch as the last tiles drain
+}
+
+// ---------------------------------------------------------------------------
+// Row-major scoring for the fused selection kernel (d_k a multiple of 32):
+// thread t scores centroid row t against EVERY selection head.  Rows are
+// staged as 32-channel chunks (row pitch 36 floats, conflict-free LDS.128),
+// one cp.async group per chunk, and chunk c is scored while chunks c + 1..
+// are still landing.  Each score is the reference's sequential fp64 chain
+// (one exact-product fma per term): the same bits as score_kernel.  As a
+// standalone grid it measured slower than score_kernel (cfg2 69 vs 56 us,
+// cfg3 239 vs 192 us: one chain per thread hides less latency than four).
+// ---------------------------------------------------------------------------
+constexpr uint32_t kFusedPitch = 36;  // floats per staged 32-channel row chunk
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_upto(uint32_t pending) {  // pending <= 3
+  switch (pending) {
+    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+  }
+}
+// rows [0, rows) of `cb` ([rows][d_k] floats) -> tile [nch][nb][kFusedPitch],
+// one commit group per 32-channel chunk
+__device__ __forceinline__ void stage_rows(const float* cb, uint32_t d_k, uint32_t rows,
+                                           uint32_t nb, float* tile) {
+  const uint32_t nch = d_k / 32;
+  for (uint32_t ch = 0; ch < nch; ++ch) {
+    for (uint32_t p = threadIdx.x; p < rows * 8; p += blockDim.x) {
+      const uint32_t r = p >> 3, part = p & 7;
+      cp_async16(tile + ((size_t)ch * nb + r) * kFusedPitch + 4 * part,
+                 cb + (size_t)r * d_k + 32 * ch + 4 * part);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+}
+// q (double, group-shared sum when Gs < G) of stream s -> qs [Gs][d_k]
+__device__ __forceinline__ void stage_query_f64(const Geometry& g, const float* q, uint32_t s,
+                                                double* qs) {
+  const float* qb = q + (uint64_t)s * g.G * g.d_k;
+  for (uint32_t i = threadIdx.x; i < g.Gs * g.d_k; i += blockDim.x) {
+    const uint32_t h = i / g.d_k, c = i % g.d_k;
+    if (g.Gs == g.G) {
+      qs[i] = (double)qb[h * g.d_k + c];
+    } else {  // group-shared query q' = sum_g q_g (fp32, sequential g)
+      float acc = qb[c];
+      for (uint32_t hh = 1; hh < g.G; ++hh) acc = __fadd_rn(acc, qb[hh * g.d_k + c]);
+      qs[i] = (double)acc;
+    }
+  }
+}
+// Thread t < rows: acc[h] = score of staged row t against head h.  Waits for
+// the chunks as it goes (every thread of the CTA must call it: barriers).
+template <int GS>
+__device__ __forceinline__ void score_staged_rows(const Geometry& g, const double* qs,
+                                                  const float* tile, uint32_t rows, uint32_t nb,
+                                                  double (&acc)[GS]) {
+#pragma unroll
+  for (int h = 0; h < GS; ++h) acc[h] = 0.0;
+  const uint32_t nch = g.d_k / 32;
+  for (uint32_t ch = 0; ch < nch; ++ch) {
+    cp_async_wait_upto(nch - 1 - ch);
+    __syncthreads();  // chunk ch (and q) visible to every thread
+    if (threadIdx.x < rows) {
+      const float* tr = tile + ((size_t)ch * nb + threadIdx.x) * kFusedPitch;
+      const double* qc = qs + 32 * ch;
+#pragma unroll 4
+      for (uint32_t c = 0; c < 32; c += 4) {
+        const float4 cv = *reinterpret_cast<const float4*>(tr + c);
+        const double c0 = cv.x, c1 = cv.y, c2 = cv.z, c3 = cv.w;
+#pragma unroll
+        for (int h = 0; h < GS; ++h) {
+          const double2 q01 = *reinterpret_cast<const double2*>(qc + h * g.d_k + c);
+          const double2 q23 = *reinterpret_cast<const double2*>(qc + h * g.d_k + c + 2);
+          acc[h] = __fma_rn(q01.x, c0, acc[h]);
+          acc[h] = __fma_rn(q01.y, c1, acc[h]);
+          acc[h] = __fma_rn(q23.x, c2, acc[h]);
+          acc[h] = __fma_rn(q23.y, c3, acc[h]);
+        }
+      }
+    }
+  }
 }
 
 cudaError_t launch_score(const ScoreArgs& a, cudaStream_t st) {
@@ -337,12 +424,7 @@ constexpr uint32_t kFusedMaxN = 2048;
 #ifndef TTKV_PHASE_STAMP  // tools/fused_probe.cu times the phases with %globaltimer
 #define TTKV_PHASE_STAMP(k)
 #endif
-constexpr uint32_t kFusedPitch = 36;  // floats per staged 32-channel row chunk
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
-               : "memory");
-}
 
 struct FusedLayout {
   uint32_t CL, nb, nw, nch;
@@ -387,62 +469,25 @@ __global__ void __launch_bounds__(kTopkThreads) select_fused_kernel(FusedSelectA
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
   TTKV_PHASE_STAMP(0);
-  pdl_wait();  // the query / centroids when the previous kernel produced them
-  {  // this CTA's centroid rows, every chunk in flight at once
-    const float* cb = a.cent + ((uint64_t)s * g.n_cap + r0) * g.d_k;
-    const uint32_t per_row = g.d_k / 4, pieces = rows * per_row;
-    for (uint32_t p = threadIdx.x; p < pieces; p += blockDim.x) {
-      const uint32_t r = p / per_row, c4 = p - r * per_row;
-      cp_async16(tile + ((size_t)(c4 >> 3) * L.nb + r) * kFusedPitch + 4 * (c4 & 7),
-                 cb + (size_t)r * g.d_k + 4 * c4);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-  for (uint32_t i = threadIdx.x; i < g.Gs * g.d_k; i += blockDim.x) {
-    const uint32_t h = i / g.d_k, c = i % g.d_k;
-    const float* qb = a.q + (uint64_t)s * g.G * g.d_k;
-    if (g.Gs == g.G) {
-      qs[i] = (double)qb[h * g.d_k + c];
-    } else {  // group-shared query q' = sum_g q_g (fp32, sequential g)
-      float acc = qb[c];
-      for (uint32_t hh = 1; hh < g.G; ++hh) acc = __fadd_rn(acc, qb[hh * g.d_k + c]);
-      qs[i] = (double)acc;
-    }
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncthreads();
+  // The centroid rows are staged BEFORE pdl_wait, overlapping the previous
+  // kernel's tail: every kernel that writes centroids (the evictions) is a
+  // plain launch that never triggers its dependents early, so the previous
+  // kernel is not one of them while it is still running.  q is read after.
+  stage_rows(a.cent + ((uint64_t)s * g.n_cap + r0) * g.d_k, g.d_k, rows, L.nb, tile);
+  pdl_wait();  // the query
+  stage_query_f64(g, a.q, s, qs);
   TTKV_PHASE_STAMP(1);
-
-  // ---- score: row t against every head, s += double(q_i) * c_i in channel
-  // order (relevance.cpp:23-26), one exact-product fma per term ----
-  if (threadIdx.x < rows) {
-    const uint32_t r = threadIdx.x;
+  // ---- score: row t against every head (score_staged_rows: the same fp64
+  // chain as score_kernel, so the same bits) ----
+  {
     double acc[GS];
+    score_staged_rows<GS>(g, qs, tile, rows, L.nb, acc);
+    if (threadIdx.x < rows)
 #pragma unroll
-    for (int h = 0; h < GS; ++h) acc[h] = 0.0;
-    for (uint32_t ch = 0; ch < L.nch; ++ch) {
-      const float* tr = tile + ((size_t)ch * L.nb + r) * kFusedPitch;
-      const double* qc = qs + 32 * ch;
-#pragma unroll 2
-      for (uint32_t c = 0; c < 32; c += 4) {
-        const float4 cv = *reinterpret_cast<const float4*>(tr + c);
-        const double c0 = cv.x, c1 = cv.y, c2 = cv.z, c3 = cv.w;
-#pragma unroll
-        for (int h = 0; h < GS; ++h) {
-          const double2 q01 = *reinterpret_cast<const double2*>(qc + h * g.d_k + c);
-          const double2 q23 = *reinterpret_cast<const double2*>(qc + h * g.d_k + c + 2);
-          acc[h] = __fma_rn(q01.x, c0, acc[h]);
-          acc[h] = __fma_rn(q01.y, c1, acc[h]);
-          acc[h] = __fma_rn(q23.x, c2, acc[h]);
-          acc[h] = __fma_rn(q23.y, c3, acc[h]);
-        }
+      for (int h = 0; h < GS; ++h) {
+        a.scores[((uint64_t)s * g.Gs + h) * g.n_cap + r0 + threadIdx.x] = acc[h];
+        keys[h * L.nb + threadIdx.x] = order_key(acc[h]);
       }
-    }
-#pragma unroll
-    for (int h = 0; h < GS; ++h) {
-      a.scores[((uint64_t)s * g.Gs + h) * g.n_cap + r0 + r] = acc[h];
-      keys[h * L.nb + r] = order_key(acc[h]);
-    }
   }
   TTKV_PHASE_STAMP(2);
   cluster.sync();  // every slice's keys are visible cluster-wide
@@ -474,48 +519,58 @@ __global__ void __launch_bounds__(kTopkThreads) select_fused_kernel(FusedSelectA
   pdl_trigger();   // the attention kernel's CTAs may get resident
   if (rank != 0) return;
 
-  // ---- union (CTA 0): ascending block id with the head bitmask ----
+  // ---- union (CTA 0): ascending block id with the head bitmask.  n <= 2048
+  // = 8 warps x 8 words: warp w ballots blocks [256w, 256w + 256) word by
+  // word, one barrier publishes the warp totals ----
   const uint32_t all_heads = (g.G >= 32) ? 0xffffffffu : ((1u << g.G) - 1u);
-  if (threadIdx.x == 0) base_sh = 0;
-  __syncthreads();
-  const uint32_t nwarps = blockDim.x >> 5;
-  for (uint32_t base = 0; base < n; base += blockDim.x) {  // CTA-uniform
-    const uint32_t b = base + threadIdx.x;
+  uint32_t mw[8], bal[8], cnt = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t b = 256 * warp + 32 * j + lane;
     uint32_t m = 0;
     if (b < n)
       for (uint32_t h = 0; h < g.Gs; ++h)
         if ((selbits[h * L.nw + (b >> 5)] >> (b & 31)) & 1u)
           m |= (g.Gs == g.G) ? (1u << h) : all_heads;
-    const uint32_t ballot = __ballot_sync(0xffffffffu, m != 0u);
-    if (lane == 0) warp_tot[warp] = __popc(ballot);
-    __syncthreads();
-    uint32_t before = 0, total = 0;
-    for (uint32_t w = 0; w < nwarps; ++w) {
-      const uint32_t t = warp_tot[w];
-      before += (w < warp) ? t : 0u;
-      total += t;
-    }
-    if (m != 0u) {
-      const uint32_t pos = base_sh + before + __popc(ballot & ((1u << lane) - 1u));
-      a.union_ids[(uint64_t)s * g.n_cap + pos] = b;
-      a.union_mask[(uint64_t)s * g.n_cap + pos] = m;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) base_sh += total;
-    __syncthreads();
+    mw[j] = m;
+    bal[j] = __ballot_sync(0xffffffffu, m != 0u);
+    cnt += __popc(bal[j]);
   }
+  if (lane == 0) warp_tot[warp] = cnt;
+  __syncthreads();
+  uint32_t pos = 0, total = 0;
+  for (uint32_t w = 0; w < kTopkThreads / 32; ++w) {
+    pos += (w < warp) ? warp_tot[w] : 0u;
+    total += warp_tot[w];
+  }
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (mw[j] != 0u) {
+      const uint32_t at = pos + __popc(bal[j] & lt);
+      a.union_ids[(uint64_t)s * g.n_cap + at] = 256 * warp + 32 * j + lane;
+      a.union_mask[(uint64_t)s * g.n_cap + at] = mw[j];
+    }
+    pos += __popc(bal[j]);
+  }
+  if (threadIdx.x == 0) base_sh = total;
   if (threadIdx.x == 0) a.union_count[s] = base_sh;
   TTKV_PHASE_STAMP(7);
 }
 
-bool select_fused_supported(const Geometry& g, uint32_t n) {
+bool select_fused_supported(const Geometry& g, uint32_t n, uint32_t sms) {
   static const bool on = [] {  // TTKV_FUSED_SELECT=0: the three-kernel chain (measurement)
     const char* e = std::getenv("TTKV_FUSED_SELECT");
     return !(e && e[0] == '0');
   }();
   if (!on || n == 0 || n > kFusedMaxN || g.d_k % 32 != 0 || g.d_k > 128 || g.Gs > 8) return false;
   const FusedLayout L = fused_layout(g, n);
-  return L.CL <= 16 && L.nb <= kTopkThreads && L.bytes <= 200 * 1024;
+  if (L.CL > 16 || L.nb > kTopkThreads || L.bytes > 200 * 1024) return false;
+  // one wave: the clusters hold their SMs through two barriers, so a second
+  // wave would wait for the first (cfg2, S = 256: 120 us vs 74 us unfused)
+  const uint64_t per_sm = std::min<uint64_t>(kTopkThreads == 256 ? 8 : 4,
+                                             (227u * 1024u) / (L.bytes + 2048));
+  return (uint64_t)g.S * L.CL <= (uint64_t)sms * per_sm;
 }
 
 template <int GS>

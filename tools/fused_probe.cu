@@ -36,13 +36,13 @@ int main(int argc, char** argv) {
   cudaMemcpy(q, hq.data(), hq.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(c, hc.data(), hc.size() * 4, cudaMemcpyHostToDevice);
   a.q = q; a.cent = c; a.scores = sc; a.union_ids = ui; a.union_mask = um; a.union_count = uc;
-  if (!select_fused_supported(g, n)) { printf("unsupported\n"); return 1; }
+  if (!select_fused_supported(g, n, 148)) { printf("unsupported\n"); return 1; }
   const FusedLayout L = fused_layout(g, n);
   printf("S=%u n=%u Gs=%u CL=%u nb=%u smem=%zu\n", S, n, Gs, L.CL, L.nb, L.bytes);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   for (int it = 0; it < 5; ++it) {
     cudaEventRecord(e0);
-    cudaError_t e = launch_select_fused(a, 0);
+    cudaError_t e = launch_select_fused(a, 0);  // probe: default stream
     cudaEventRecord(e1);
     cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("launch: %s\n", cudaGetErrorString(e)); return 1; }
