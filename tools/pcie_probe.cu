@@ -178,98 +178,9 @@ int main(int argc, char** argv) {
   }, 3);
   std::printf("{\"path\": \"memcpy_per_record\", \"records\": %zu, \"gbs\": %.2f}\n",
               std::min<size_t>(nrec, 2000), std::min<size_t>(nrec, 2000) * kRec / ms / 1e6);
-  // batched copy engine: one cudaMemcpyBatchAsync of scattered 24,576 B payloads
-  {
-    cudaStream_t cs;
-    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    for (size_t batch : {size_t(1000), size_t(10000)}) {
-      batch = std::min(batch, nrec);
-      std::vector<void*> dsts(batch), srcs(batch);
-      std::vector<size_t> sizes(batch, 24576);
-      for (size_t i = 0; i < batch; ++i) {
-        dsts[i] = d + i * kRec;
-        srcs[i] = h + (size_t)order[i] * kRec;
-      }
-      cudaMemcpyAttributes attr{};
-      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-      size_t aidx = 0, fail = 0;
-      float bestms = 1e30f, api_us = 0;
-      for (int r = 0; r < 5; ++r) {
-        cudaEventRecord(a, cs);
-        auto t0 = std::chrono::steady_clock::now();
-        cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), batch, &attr,
-                                             &aidx, 1, &fail, cs);
-        api_us = std::chrono::duration<float, std::micro>(std::chrono::steady_clock::now() - t0).count();
-        cudaEventRecord(b, cs);
-        cudaEventSynchronize(b);
-        if (e != cudaSuccess) {
-          std::printf("{\"path\": \"memcpy_batch\", \"error\": \"%s\"}\n", cudaGetErrorString(e));
-          break;
-        }
-        float ms;
-        cudaEventElapsedTime(&ms, a, b);
-        bestms = std::min(bestms, ms);
-      }
-      std::printf("{\"path\": \"memcpy_batch_scattered\", \"records\": %zu, \"gbs\": %.2f, "
-                  "\"api_us\": %.1f}\n", batch, batch * 24576.0 / bestms / 1e6, api_us);
-    }
-    cudaStreamDestroy(cs);
-  }
-  // copy engine on run-merged selections: arena of 32 streams x 992 payloads
-  // (24,576 B), random selection at the per-head-union density (0.91) and the
-  // group-shared density (0.45); consecutive selected blocks are merged.
-  {
-    const size_t S = 32, NB = 992, P = 24576;
-    const size_t abytes = S * NB * P;
-    uint8_t *ah = nullptr, *ad = nullptr;
-    CK(cudaHostAlloc((void**)&ah, abytes, cudaHostAllocMapped | cudaHostAllocPortable));
-    CK(cudaMalloc((void**)&ad, abytes));
-    cudaStream_t cs;
-    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    std::mt19937 rng(7);
-    for (double dens : {0.91, 0.45}) {
-      std::vector<void*> dsts, srcs;
-      std::vector<size_t> sizes;
-      size_t payload = 0;
-      for (size_t s = 0; s < S; ++s) {
-        size_t b = 0;
-        while (b < NB) {
-          if (std::uniform_real_distribution<double>(0, 1)(rng) >= dens) { ++b; continue; }
-          size_t e = b + 1;
-          while (e < NB && std::uniform_real_distribution<double>(0, 1)(rng) < dens) ++e;
-          const size_t off = (s * NB + b) * P;
-          dsts.push_back(ad + off);
-          srcs.push_back(ah + off);
-          sizes.push_back((e - b) * P);
-          payload += (e - b) * P;
-          b = e + 1;
-        }
-      }
-      cudaMemcpyAttributes attr{};
-      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-      size_t aidx = 0, fail = 0;
-      float bestms = 1e30f, api_us = 0;
-      for (int r = 0; r < 5; ++r) {
-        cudaEventRecord(a, cs);
-        auto t0 = std::chrono::steady_clock::now();
-        cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), dsts.size(),
-                                             &attr, &aidx, 1, &fail, cs);
-        api_us = std::chrono::duration<float, std::micro>(std::chrono::steady_clock::now() - t0).count();
-        cudaEventRecord(b, cs);
-        cudaEventSynchronize(b);
-        if (e != cudaSuccess) break;
-        float ms;
-        cudaEventElapsedTime(&ms, a, b);
-        bestms = std::min(bestms, ms);
-      }
-      std::printf("{\"path\": \"memcpy_batch_runs\", \"density\": %.2f, \"runs\": %zu, "
-                  "\"payload_mb\": %.1f, \"gbs\": %.2f, \"api_us\": %.1f}\n",
-                  dens, dsts.size(), payload / 1e6, payload / bestms / 1e6, api_us);
-    }
-    cudaStreamDestroy(cs);
-    cudaFreeHost(ah);
-    cudaFree(ad);
-  }
+  // The round-1 batched copy-engine measurements (scattered records and run-merged
+  // selections) are recorded in profiles/r1_pcie_probe.jsonl; the batched copy API
+  // is closed on this pool, so the probe no longer issues it.
   for (int grid_mult : {1, 2, 4, 8}) {
     const int grid = prop.multiProcessorCount * grid_mult;
     ms = best([&] { ldg_records<<<grid, 256>>>(hd, d_order, (unsigned)nrec, sink); }, 5);
