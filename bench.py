@@ -1023,6 +1023,7 @@ def run_layer_sequential(args):
         torch.cuda.synchronize()
         args.steps = int(min(args.max_auto, max(10, -(-1000.0 // max(e0.elapsed_time(e1), 1e-3)))))
     launches0 = sum(e.state()["launches"] for e in engs)
+    spec0 = sum(e.state()["spec_steps"] for e in engs)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(0) as clk:
         torch.cuda.synchronize()
@@ -1033,8 +1034,12 @@ def run_layer_sequential(args):
         torch.cuda.synchronize()
     ms_step = ev0.elapsed_time(ev1) / args.steps
     launches = sum(e.state()["launches"] for e in engs) - launches0
+    spec_calls = sum(e.state()["spec_steps"] for e in engs) - spec0
     union = sum(e.step_counters()[0] for e in engs)
     st = engs[0].state()
+    # speculative record stream (HBM tier): every record of the layer streamed
+    # beside the selection; the roofline keeps the union's (algorithmic) bytes
+    streamed = sum(S * e.state()["slow_blocks"] for e in engs) if spec_calls else union
     pcie = union * st["payload_bytes"]
     host_tier = args.slow_tier == "host"
     hbm = sum(S * st["fast_tokens"] * 2 * D * 2 + S * st["slow_blocks"] * D * 4 for _ in engs) + \
@@ -1054,6 +1059,10 @@ def run_layer_sequential(args):
         "roofline": {"tier_roofline_ms": t_roof, "tier_frac": t_roof / ms_step,
                      "pcie_gbs": pcie / (ms_step * 1e-3) / 1e9 if host_tier else None,
                      "pcie_peak": h2d_peak},
+        "record_stream": ("speculative: every record, beside the selection "
+                          "(slow_attn_tc_spec_kernel)") if spec_calls else "union after the selection",
+        "spec_calls_frac": spec_calls / float(args.steps * Lyr),
+        "records_per_token": {"union": union, "streamed": streamed},
         "clocks": clk.summary(),
         "gpu_launches": launches,
     }

@@ -112,6 +112,13 @@ typedef struct {
                                   baselines (harness.cpp:22-24): all selected
                                   records are first gathered into an HBM
                                   staging arena, then attended (no overlap) */
+  uint32_t record_stream;      /* HBM slow tier (TTKV_SLOW_DEVICE), G <= 4:
+                                  0 / 1 the selected union after the
+                                  selection (default), 2 speculative -- every
+                                  record, streamed beside the selection; the
+                                  combine merges only the selected ones (same
+                                  selections and outputs within tolerance, more
+                                  HBM bytes, the selection off the chain) */
 } ttkv_gpu_options;
 
 /* DecodeStepReport (engine.hpp:21-29) plus measured quantities. */
@@ -142,6 +149,9 @@ typedef struct {
   uint64_t graph_replays;   /* decode steps launched as a replay of the captured
                                step graph (TTKV_GRAPH=0: none) */
   uint64_t graph_captures;  /* step graphs captured (one per eviction period) */
+  uint64_t spec_steps;      /* decode steps that streamed every record beside the
+                               selection (HBM slow tier, small steps; see
+                               slow_attn_tc_spec_kernel) instead of the union */
 } ttkv_state;
 
 /* Kernel timing (enabled by ttkv_gpu_set_timing); milliseconds summed over

@@ -34,7 +34,8 @@ class OptionsC(C.Structure):
                 ("heads_per_stream", C.c_uint32), ("group_select", C.c_uint32),
                 ("reserve_tokens", C.c_uint64), ("slow_tier", C.c_uint32),
                 ("copy_mode", C.c_uint32), ("literal_additive_merge", C.c_uint32),
-                ("ring_bytes", C.c_uint32), ("serial_schedule", C.c_uint32)]
+                ("ring_bytes", C.c_uint32), ("serial_schedule", C.c_uint32),
+                ("record_stream", C.c_uint32)]
 
 
 class StepReportC(C.Structure):
@@ -48,7 +49,7 @@ class StateC(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "appended", "fast_tokens", "slow_blocks", "l_fast", "record_bytes",
         "modeled_block_bytes", "n_streams", "heads_per_stream", "block_capacity", "launches",
-        "payload_bytes", "graph_replays", "graph_captures")]
+        "payload_bytes", "graph_replays", "graph_captures", "spec_steps")]
 
 
 class KernelTimesC(C.Structure):

@@ -741,6 +741,157 @@ __global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs
   }
 }
 
+// Combine of the speculative record stream (slow_attn_tc_spec_kernel): the
+// slow partials are per-record rows rpart[s][h][b] and head h merges exactly
+// the records it selected -- the union entries with its bit set.  One CTA per
+// (stream, head, 32-channel slice); three short phases, each one round trip
+// to L2 deep:
+//   1. compaction: thread t tests a contiguous run of union entries, a CTA
+//      scan places the selected block ids (union order, ascending block id:
+//      deterministic, so the merge is bit-reproducible);
+//   2. weights: every fast-tier and selected-record row's (m, l) -> M, then
+//      w_i = exp2(m_i - M) and L = sum w_i l_i;
+//   3. weighted sum: 32 row groups x 8 float4 channel lanes, reduced in smem.
+// fp32 (the tensor-core slow tier is the fp16 ring's); d_v = 128.
+constexpr int kSpecCombineThreads = 256;
+__global__ void __launch_bounds__(kSpecCombineThreads) combine_spec_kernel(CombineArgs a) {
+  pdl_wait();  // the record stream (which itself waited for the selection)
+  pdl_trigger();
+  const Geometry& g = a.g;
+  const uint32_t idx = blockIdx.x, s = idx / g.G, h = idx - s * g.G;
+  const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint32_t cap = a.nfc + a.spec_n;
+  extern __shared__ __align__(16) uint8_t csm[];
+  float* wv = reinterpret_cast<float*>(csm);  // [cap] weights
+  float* lv = wv + cap;                       // [cap] l of each row
+  uint32_t* ids = reinterpret_cast<uint32_t*>(lv + cap);  // [spec_n] selected block ids
+  __shared__ uint32_t redu[kSpecCombineThreads / 32];
+  __shared__ float redf[kSpecCombineThreads / 32];
+  __shared__ float acc_sm[32][33];
+
+  // ---- 1. this head's selected records ----
+  const uint32_t cnt = a.union_count[s];
+  const uint64_t ub = (uint64_t)s * a.n_cap;
+  const uint32_t E = (cnt + kSpecCombineThreads - 1) / kSpecCombineThreads;  // <= 8 (n <= 2048)
+  const uint32_t u0 = min(cnt, t * E), ne = min(cnt, u0 + E) - u0;
+  uint32_t sel = 0;
+#pragma unroll
+  for (uint32_t j = 0; j < 8; ++j)
+    if (j < ne) sel |= ((a.union_mask[ub + u0 + j] >> h) & 1u) << j;
+  const uint32_t mine = __popc(sel);
+  uint32_t incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += v;
+  }
+  if (lane == 31) redu[warp] = incl;
+  __syncthreads();
+  uint32_t pos = incl - mine, nsel = 0;
+#pragma unroll
+  for (int k = 0; k < kSpecCombineThreads / 32; ++k) {
+    pos += (uint32_t)k < warp ? redu[k] : 0u;
+    nsel += redu[k];
+  }
+#pragma unroll
+  for (uint32_t j = 0; j < 8; ++j)
+    if ((sel >> j) & 1u) ids[pos++] = a.union_ids[ub + u0 + j];
+  __syncthreads();
+
+  // ---- 2. weights ----
+  const uint32_t fpitch = g.d_v + 2, np = a.nfc + nsel;
+  const float* fp = reinterpret_cast<const float*>(a.fpart) + (uint64_t)idx * a.nfc * fpitch;
+  const float* rp = a.rpart + (uint64_t)idx * a.n_cap * kSpecPitch;
+  auto row = [&](uint32_t i) -> const float* {
+    return i < a.nfc ? fp + (uint64_t)i * fpitch : rp + (uint64_t)ids[i - a.nfc] * kSpecPitch;
+  };
+  float M = -INFINITY;
+  for (uint32_t i = t; i < np; i += kSpecCombineThreads) {
+    const float* r = row(i) + g.d_v;
+    const float m = r[0], l = r[1];
+    wv[i] = m;
+    lv[i] = l;
+    if (l > 0.f) M = fmaxf(M, m);
+  }
+  M = warp_max(M);
+  if (lane == 0) redf[warp] = M;
+  __syncthreads();
+  M = redf[0];
+#pragma unroll
+  for (int k = 1; k < kSpecCombineThreads / 32; ++k) M = fmaxf(M, redf[k]);
+  __syncthreads();
+  float L = 0.f;
+  for (uint32_t i = t; i < np; i += kSpecCombineThreads) {
+    const float wi = lv[i] > 0.f ? exp2f(wv[i] - M) : 0.f;
+    wv[i] = wi;
+    L += wi * lv[i];
+  }
+  L = warp_sum(L);
+  if (lane == 0) redf[warp] = L;
+  __syncthreads();  // also publishes wv
+  float Lt = 0.f;
+#pragma unroll
+  for (int k = 0; k < kSpecCombineThreads / 32; ++k) Lt += redf[k];
+
+  // ---- 3. weighted sum over this CTA's 32 channels ----
+  const uint32_t rg = t >> 3, c4 = t & 7;
+  const uint32_t c = blockIdx.y * 32 + 4 * c4;
+  float4 A0 = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint32_t i = rg;
+  for (; i < a.nfc && i < np; i += 32) {  // fast-tier rows (pitch d_v + 2: 8-byte aligned)
+    const float* r = fp + (uint64_t)i * fpitch + c;
+    const float2 x = *reinterpret_cast<const float2*>(r), y = *reinterpret_cast<const float2*>(r + 2);
+    const float wi = wv[i];
+    A0.x += wi * x.x; A0.y += wi * x.y; A0.z += wi * y.x; A0.w += wi * y.y;
+  }
+  // record rows, kU in flight per thread (one L2 round trip per kU rows)
+  constexpr int kU = 8;
+  for (; i < np; i += 32 * kU) {
+    float4 x[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t j = i + 32 * u;
+      x[u] = j < np ? *reinterpret_cast<const float4*>(row(j) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t j = i + 32 * u;
+      const float wx = j < np ? wv[j] : 0.f;
+      A0.x += wx * x[u].x; A0.y += wx * x[u].y; A0.z += wx * x[u].z; A0.w += wx * x[u].w;
+    }
+  }
+  acc_sm[rg][4 * c4 + 0] = A0.x;
+  acc_sm[rg][4 * c4 + 1] = A0.y;
+  acc_sm[rg][4 * c4 + 2] = A0.z;
+  acc_sm[rg][4 * c4 + 3] = A0.w;
+  __syncthreads();
+  if (t < 32) {
+    float A = 0.f;
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) A += acc_sm[k][t];
+    const uint32_t ch = blockIdx.y * 32 + t;
+    const double o = (double)(A / Lt);
+    a.out[(uint64_t)idx * g.d_v + ch] = o;
+    if (a.n_peers) {
+      const uint64_t gi = ((uint64_t)a.gidx[s] * g.G + h) * g.d_v + ch;
+      for (uint32_t r = 0; r < a.n_peers; ++r) a.peer_out[r][gi] = o;
+    }
+  }
+  if (blockIdx.x == 0 && blockIdx.y == 0 && t == 0) {
+    if (a.pos_inc) *a.pos_inc += 1;
+    *a.spec_ctr = 0;  // the record queue is drained (this grid waited on its kernel)
+  }
+  if (a.n_peers) {  // this CTA's row slice is in every rank's buffer: publish it
+    __syncthreads();
+    if (t == 0) {
+      __threadfence_system();
+      for (uint32_t r = 0; r < a.n_peers; ++r)
+        asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(a.peer_flags[r] + a.my_rank)
+                     : "memory");
+    }
+  }
+}
+
 __global__ void peer_wait_kernel(const unsigned long long* flags, uint32_t n_ranks,
                                  unsigned long long target, int* status) {
   const uint32_t r = threadIdx.x;
@@ -775,7 +926,18 @@ uint32_t combine_slices(const Geometry& g) {
   return (g.d_v + 31) / 32;
 }
 
+uint32_t combine_slices(const CombineArgs& a) {
+  return a.rpart ? (a.g.d_v + 31) / 32 : combine_slices(a.g);
+}
+
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
+  if (a.rpart) {  // speculative record stream (fp32, d_v = 128)
+    const size_t smem = (size_t)(a.nfc + a.spec_n) * 8 + (size_t)a.spec_n * 4;
+    cudaFuncSetAttribute(combine_spec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    return launch_chained(combine_spec_kernel, dim3(a.g.S * a.g.G, combine_slices(a)),
+                          dim3(kSpecCombineThreads), smem, st, a);
+  }
   const size_t acc = a.g.elem == 4 ? 8 : 4;
   const size_t smem = (size_t)(a.nfc + a.nsc + 1) * acc;
   const dim3 grid(a.g.S * a.g.G, combine_slices(a.g));

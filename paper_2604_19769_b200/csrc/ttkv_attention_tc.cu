@@ -94,6 +94,10 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
   constexpr int D = 64 * ND;        // head dim
   constexpr int KSTEPS = D / 16;    // QK k-steps
   constexpr uint32_t STAGE = 2 * ND * kBox;
+  // chained launch (speculative record stream): the record stream may launch
+  // at once; the ring append and the step position come from earlier kernels
+  pdl_trigger();
+  pdl_wait();
   const Geometry& g = a.g;
   const uint32_t s = blockIdx.y, f = blockIdx.x;
   const uint32_t F = a.pos ? (uint32_t)(*a.pos + 1 - a.front) : a.F;
@@ -877,6 +881,268 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
   pdl_trigger();  // the combine's CTAs may get resident while partials drain
 }
 
+// ---------------------------------------------------------------------------
+// Speculative record stream (HBM slow tier, small steps -- one layer of a
+// layer-sequential decode).  With the records in HBM the step is latency-
+// bound on the chain selection -> record stream -> combine, and with per-head
+// selection of a fraction f of the blocks the union of G heads' sets covers
+// 1 - (1 - f)^G of them (0.91 at f = 0.45, G = 4).  This kernel therefore
+// does NOT wait for the selection: it streams EVERY record of the step while
+// the selection runs beside it (launched behind it with programmatic
+// serialization, the selection triggers at its start), and writes each
+// record's block-local partial per head -- (o_blk[128], m_blk, l_blk) with
+// p = exp2(s - m_blk) -- to `rpart` [S][G][n_cap][kSpecPitch].  The combine
+// then merges, per (stream, head), exactly the records that head selected
+// (the union lists), so outputs and selections are those of the selective
+// kernel; the extra (1 - density) of record bytes buys the selection's
+// latency.  Records are handed out from a global queue (`spec_ctr`, reset by
+// the combine) two at a time, so CTAs that start late (SMs held by the
+// selection or the fast tier) simply take fewer.  Same per-record tensor-core
+// math as slow_attn_tc_kernel (PK form, G <= 4); q is normalized per record
+// from L1-resident global q instead of once per stream segment.
+// ---------------------------------------------------------------------------
+template <int GT>
+__global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, 3)
+    slow_attn_tc_spec_kernel(const __grid_constant__ SlowTcArgs a) {
+  static_assert(GT <= 4, "speculative stream: PK form only");
+  constexpr int ST = 2;
+  constexpr uint32_t kGrab = 2;
+  constexpr uint32_t kEnd = 0xffffffffu;
+  // no pdl_wait here: q, the arena and the param mirror are not written by
+  // the selection this kernel is chained behind (it waits at its end)
+  const Geometry& g = a.g;
+  const uint32_t G = g.G, n = a.spec_n;
+  const uint32_t total = g.S * n;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint4* qsf = reinterpret_cast<uint4*>(base + ST * kSlowStage);
+  uint4* phl = qsf + 256;
+  float* sc = reinterpret_cast<float*>(phl + 256);  // [GT][kScPitch]
+  float* usc = sc + GT * kScPitch;                 // per-head score unscale of the record
+  float* mst = usc + 8;                            // m_blk per head
+  float* pst = mst + 8;                            // l_blk per head
+  float* bst = pst + 8;                            // beta = q . z per head
+  uint32_t* srec = reinterpret_cast<uint32_t*>(bst + 8);  // flat record index per stage
+  uint64_t* full = reinterpret_cast<uint64_t*>(srec + 4);
+  uint64_t* empty = full + ST;
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kSlowConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  for (uint32_t i = threadIdx.x; i < 512; i += blockDim.x) qsf[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t evict_first = l2_evict_first_policy();
+      uint32_t i = 0;
+      uint32_t cur = atomicAdd(a.spec_ctr, kGrab);
+      for (;;) {
+        // the next grab is in flight while this one waits for free stages
+        const uint32_t nxt = cur < total ? atomicAdd(a.spec_ctr, kGrab) : total;
+        bool end = false;
+        for (uint32_t r = cur; r < cur + kGrab; ++r, ++i) {
+          const uint32_t st = i % ST;
+          if (i >= ST) mbar_wait_sleep(&empty[st], ((i / ST) - 1) & 1);
+          if (r >= total) {
+            srec[st] = kEnd;
+            mbar_arrive(&full[st]);
+            end = true;
+            break;
+          }
+          const uint32_t s = r / n;
+          const int rec = (int)((uint64_t)s * g.n_cap + (r - s * n));
+          uint8_t* dst = base + st * kSlowStage;
+          srec[st] = r;  // published by the arrive below (release.cta)
+          mbar_arrive_expect_tx(&full[st], kSlowStage);
+          tma_load_3d(dst, &a.tk, 0, 0, rec, &full[st], evict_first);
+          tma_load_3d(dst + kKBox, &a.tv, 0, 0, rec, &full[st], evict_first);
+          bulk_g2s(dst + kKBox + kVBox, a.params + (uint64_t)rec * kPBytes, kPBytes, &full[st]);
+        }
+        if (end) break;
+        cur = nxt;
+      }
+    }
+    return;
+  }
+
+  const int nthreads_c = kSlowConsumerWarps * 32;
+  const float sl = (float)a.scale_log2;
+  const uint32_t cw = warp - 1;
+  const uint32_t gq = lane >> 2, qq = lane & 3;
+  const uint32_t c0 = 32 * cw + 4 * gq;
+  uint32_t koff[4];
+  {
+    const uint32_t m = lane >> 3, r = lane & 7;
+    const uint32_t row = 32 * cw + 8 * (m & 1) + r;
+#pragma unroll
+    for (int jp = 0; jp < 4; ++jp)
+      koff[jp] = row * 128 + ((((uint32_t)(2 * jp)) ^ (r & 6u)) | ((m >> 1) ^ (r & 1u))) * 16;
+  }
+  const uint32_t voff = 2 * qq * 64 + ((c0 >> 1) ^ (qq << 4));
+  uint2* qsf2 = reinterpret_cast<uint2*>(qsf);
+  const uint2* phl2c = reinterpret_cast<const uint2*>(phl);
+
+  for (uint32_t i = 0;; ++i) {
+    const uint32_t st = i % ST;
+    mbar_wait(&full[st], (i / ST) & 1);
+    const uint32_t r = srec[st];
+    if (r == kEnd) break;
+    const uint32_t s = r / n, b = r - s * n;
+    uint8_t* stg = base + st * kSlowStage;
+    const uint32_t kb = smem_u32(stg);
+    const uint8_t* vn = stg + kKBox;
+    const float* kp = reinterpret_cast<const float*>(stg + kKBox + kVBox);
+    const float* vp = kp + 2 * 128;
+
+    // ---- (q * s) fragments of head cw: q normalized by a power of two from
+    // its own max (as in slow_attn_tc_kernel), lane (j, q4) channels 16j + 4q4 ----
+    float bpart = 0.f;
+    if (cw < G) {
+      const uint32_t h = cw, j = lane >> 2, q4 = lane & 3;
+      const uint32_t c = 16 * j + 4 * q4;
+      float4 qv = __ldg(reinterpret_cast<const float4*>(a.q + ((uint64_t)s * G + h) * 128 + c));
+      qv.x *= sl; qv.y *= sl; qv.z *= sl; qv.w *= sl;
+      const float mx = warp_max_redux(fmaxf(fmaxf(fabsf(qv.x), fabsf(qv.y)),
+                                            fmaxf(fabsf(qv.z), fabsf(qv.w))));
+      float uns;
+      const float f = pow2_normalizer(mx * kTcKeyScaleBound, 24, &uns);
+      qv.x *= f; qv.y *= f; qv.z *= f; qv.w *= f;
+      if (lane == 0) usc[h] = uns;
+      const float4 sz0 = *reinterpret_cast<const float4*>(kp + 2 * c);
+      const float4 sz1 = *reinterpret_cast<const float4*>(kp + 2 * c + 4);
+      uint32_t h01, l01, h23, l23;
+      split2(qv.x * sz0.x, qv.y * sz0.z, h01, l01);
+      split2(qv.z * sz1.x, qv.w * sz1.z, h23, l23);
+      qsf2[(j * 8 + 2 * h) * 4 + q4] = make_uint2(h01, h23);
+      qsf2[(j * 8 + 2 * h + 1) * 4 + q4] = make_uint2(l01, l23);
+      bpart = qv.x * sz0.y + qv.y * sz0.w + qv.z * sz1.y + qv.w * sz1.w;
+    }
+    named_bar(1, nthreads_c);
+
+    // ---- QK^T (tokens [32cw, 32cw + 32), all heads) ----
+    {
+      float c[2][2][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) c[mt][0][e] = c[mt][1][e] = 0.f;
+#pragma unroll
+      for (int jp = 0; jp < 4; ++jp) {
+        const uint2 b0 = qsf2[((2 * jp) * 8 + gq) * 4 + qq];
+        const uint2 b1 = qsf2[((2 * jp + 1) * 8 + gq) * 4 + qq];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const uint32_t addr = kb + koff[jp] + mt * 16 * 128;
+          uint32_t r0, r1, r2, r3, a0, a1, a2, a3;
+          ldsm_x4(addr, r0, r1, r2, r3);
+          codes_to_h2(r0, a0, a2);
+          codes_to_h2(r1, a1, a3);
+          mma_a4(c[mt][0], a0, a1, a2, a3, b0.x, b0.y);
+          codes_to_h2(r2, a0, a2);
+          codes_to_h2(r3, a1, a3);
+          mma_a4(c[mt][1], a0, a1, a2, a3, b1.x, b1.y);
+        }
+      }
+      if (cw < G) {
+        const float beta = warp_sum(bpart) * (usc[cw] * (1.0f / 16777216.0f));
+        if (lane == 0) bst[cw] = beta;
+      }
+      if (qq < G) {
+        const float uns0 = usc[qq];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int e = 0; e < 4; e += 2) {
+            const uint32_t t = 32 * cw + 16 * mt + gq + 4 * e;
+            sc[qq * kScPitch + t] =
+                ((c[mt][0][e] + c[mt][0][e + 1]) + (c[mt][1][e] + c[mt][1][e + 1])) * uns0;
+          }
+      }
+    }
+    named_bar(1, nthreads_c);
+
+    // ---- block-local softmax of head cw: p = exp2(s - m_blk) ----
+    if (cw < G) {
+      const uint32_t h = cw, ks = lane >> 2, q4 = lane & 3;
+      uint2* dhi = reinterpret_cast<uint2*>(phl) + (ks * 8 + 2 * h) * 4 + q4;  // PK columns
+      uint2* dlo = dhi + 4;
+      const float* row = sc + h * kScPitch + 16 * ks + 2 * q4;
+      const float beta = bst[h];
+      float2 v01 = *reinterpret_cast<const float2*>(row);
+      float2 v89 = *reinterpret_cast<const float2*>(row + 8);
+      v01.x += beta; v01.y += beta; v89.x += beta; v89.y += beta;
+      const float bm = warp_max_redux(fmaxf(fmaxf(v01.x, v01.y), fmaxf(v89.x, v89.y)));
+      const float p0 = exp2f(v01.x - bm), p1 = exp2f(v01.y - bm);
+      const float p8 = exp2f(v89.x - bm), p9 = exp2f(v89.y - bm);
+      const float sum = warp_sum((p0 + p1) + (p8 + p9));
+      uint32_t h01, l01, h89, l89;
+      split2(p0, p1, h01, l01);
+      split2(p8, p9, h89, l89);
+      *dhi = make_uint2(h01, h89);
+      *dlo = make_uint2(l01, l89);
+      if (lane == 0) {
+        mst[h] = bm;
+        pst[h] = sum;
+      }
+    }
+    named_bar(1, nthreads_c);
+
+    // ---- PV^T (channels [32cw, 32cw + 32)), then this record's partial ----
+    {
+      float cf[2][2][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) cf[mt][0][e] = cf[mt][1][e] = 0.f;
+      const uint8_t* vt = vn + voff;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const uint32_t u0 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024);
+        const uint32_t u1 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 64);
+        const uint32_t u8 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 512);
+        const uint32_t u9 = *reinterpret_cast<const uint16_t*>(vt + ks * 1024 + 576);
+        uint32_t x0, x1, x2, x3, y0, y1, y2, y3;
+        nibbles_to_h2(__byte_perm(u0, u1, 0x5410u), x0, x1, x2, x3);
+        nibbles_to_h2(__byte_perm(u8, u9, 0x5410u), y0, y1, y2, y3);
+        const uint2 pb = phl2c[(ks * 8 + gq) * 4 + qq];
+        mma_a4(cf[0][ks & 1], x0, x1, y0, y1, pb.x, pb.y);
+        mma_a4(cf[1][ks & 1], x2, x3, y2, y3, pb.x, pb.y);
+      }
+      const uint32_t h = qq;
+      if (h < G) {
+        const float4 sz01 = *reinterpret_cast<const float4*>(vp + 2 * c0);
+        const float4 sz23 = *reinterpret_cast<const float4*>(vp + 2 * c0 + 4);
+        const float psum = pst[h];
+        float o[4];
+        const float vs[4] = {sz01.x * kSub20, sz01.z * kSub20, sz23.x * kSub20, sz23.z * kSub20};
+        const float vz[4] = {sz01.y, sz01.w, sz23.y, sz23.w};
+#pragma unroll
+        for (int ci = 0; ci < 4; ++ci) {
+          const int mt = ci >> 1, e = 2 * (ci & 1);
+          o[ci] = vs[ci] * ((cf[mt][0][e] + cf[mt][0][e + 1]) + (cf[mt][1][e] + cf[mt][1][e + 1])) +
+                  vz[ci] * psum;
+        }
+        float* dst = a.rpart + (((uint64_t)s * G + h) * g.n_cap + b) * kSpecPitch;
+        *reinterpret_cast<float4*>(dst + c0) = make_float4(o[0], o[1], o[2], o[3]);
+        if (cw == 0 && gq == 0) *reinterpret_cast<float2*>(dst + 128) = make_float2(mst[h], psum);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  // The selection must be complete before this grid is: the combine waits on
+  // this grid only, and reads the selection's union lists.
+  pdl_wait();
+  pdl_trigger();
+}
+
 bool slow_tc_supported(const Geometry& g) {
   return g.elem == 2 && g.d_k == 128 && g.d_v == 128 && g.B == 128 && g.kb == 8 && g.vb == 4 &&
          g.G <= 8 && g.rec.kp_off == kKBox + kVBox && g.rec.used == kSlowStage;
@@ -919,6 +1185,27 @@ cudaError_t launch_slow_tc(const SlowTcArgs& a, uint32_t grid_ctas, cudaStream_t
   static const int stages = slow_tc_stages();
   return stages == 2 ? launch_slow_tc_s<2>(a, grid_ctas, st)
                      : launch_slow_tc_s<3>(a, grid_ctas, st);
+}
+
+template <int GT>
+static cudaError_t launch_slow_tc_spec_t(const SlowTcArgs& a, uint32_t grid_ctas, cudaStream_t st) {
+  // 2 stages | qsf + phl | sc | usc, mst, pst, bst | srec | full, empty
+  const size_t smem = 1024 + 2 * (size_t)kSlowStage + 2 * 256 * 16 + (size_t)GT * kScPitch * 4 +
+                      4 * 8 * 4 + 16 + 2 * 2 * 8;
+  auto kern = slow_attn_tc_spec_kernel<GT>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_chained(kern, dim3(grid_ctas), dim3(32 + kSlowConsumerWarps * 32), smem, st, a);
+}
+
+bool slow_tc_spec_supported(const Geometry& g) { return slow_tc_supported(g) && g.G <= 4; }
+
+cudaError_t launch_slow_tc_spec(const SlowTcArgs& a, uint32_t grid_ctas, cudaStream_t st) {
+  if (grid_ctas == 0 || a.spec_n == 0) return cudaSuccess;
+  if (a.g.G <= 1) return launch_slow_tc_spec_t<1>(a, grid_ctas, st);
+  if (a.g.G <= 2) return launch_slow_tc_spec_t<2>(a, grid_ctas, st);
+  return launch_slow_tc_spec_t<4>(a, grid_ctas, st);
 }
 
 // Tensor maps over the record arena (device or mapped host pointer):
@@ -970,26 +1257,27 @@ static size_t fast_tc_smem(const Geometry& g) {
 }
 
 template <int ND, int GT>
-static cudaError_t launch_fast_tc_t(const FastTcArgs& a, cudaStream_t st) {
+static cudaError_t launch_fast_tc_t(const FastTcArgs& a, cudaStream_t st, bool chained) {
   const size_t smem = fast_tc_smem(a.g);
   auto kern = fast_attn_tc_kernel<ND, GT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // max smem
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid(a.nfc, a.g.S);
+  if (chained) return launch_chained(kern, grid, dim3(32 + kSlowConsumerWarps * 32), smem, st, a);
   return launch_background(kern, grid, dim3(32 + kSlowConsumerWarps * 32), smem, st, a);
 }
 
 template <int ND>
-static cudaError_t launch_fast_tc_g(const FastTcArgs& a, cudaStream_t st) {
-  if (a.g.G <= 1) return launch_fast_tc_t<ND, 1>(a, st);
-  if (a.g.G <= 2) return launch_fast_tc_t<ND, 2>(a, st);
-  if (a.g.G <= 4) return launch_fast_tc_t<ND, 4>(a, st);
-  return launch_fast_tc_t<ND, 8>(a, st);
+static cudaError_t launch_fast_tc_g(const FastTcArgs& a, cudaStream_t st, bool chained) {
+  if (a.g.G <= 1) return launch_fast_tc_t<ND, 1>(a, st, chained);
+  if (a.g.G <= 2) return launch_fast_tc_t<ND, 2>(a, st, chained);
+  if (a.g.G <= 4) return launch_fast_tc_t<ND, 4>(a, st, chained);
+  return launch_fast_tc_t<ND, 8>(a, st, chained);
 }
 
-cudaError_t launch_fast_tc(const FastTcArgs& a, cudaStream_t st) {
-  return a.g.d_k == 128 ? launch_fast_tc_g<2>(a, st) : launch_fast_tc_g<1>(a, st);
+cudaError_t launch_fast_tc(const FastTcArgs& a, cudaStream_t st, bool chained) {
+  return a.g.d_k == 128 ? launch_fast_tc_g<2>(a, st, chained) : launch_fast_tc_g<1>(a, st, chained);
 }
 
 // Tensor maps of the fp16 ring: [S*C rows][d] halves, 64 x 64 boxes, 128B swizzle.

@@ -251,6 +251,12 @@ struct ttkv_gpu {
   void* fpart = nullptr;
   void* spart = nullptr;
   uint64_t spart_chunks = 0;
+  // speculative record stream (HBM tier, small steps): per-record partials
+  // [S][G][n_cap][kSpecPitch] and the record queue head
+  float* rpart = nullptr;
+  uint64_t rpart_cap = 0;
+  uint32_t* spec_ctr = nullptr;
+  uint64_t spec_steps = 0;
   float* q_dev = nullptr;
   double* out_dev = nullptr;
   void *kn_dev = nullptr, *vn_dev = nullptr;
@@ -411,6 +417,7 @@ void free_all(ttkv_gpu* h) {
   };
   F(h->ring_k); F(h->ring_v); F(h->cent); F(h->params); F(h->scores); F(h->mask); F(h->uids);
   F(h->umask); F(h->ucount); F(h->nslots); F(h->fpart); F(h->spart); F(h->q_dev);
+  F(h->rpart); F(h->spec_ctr);
   F(h->out_dev); F(h->kn_dev); F(h->vn_dev); F(h->stg_k); F(h->stg_v); F(h->stage_arena);
   if (h->arena_host) pinned_free(h->arena_host);
   else if (h->arena_dev) cudaFree(h->arena_dev);
@@ -529,6 +536,47 @@ int ensure_spart(ttkv_gpu* h, uint64_t chunks) {
   h->spart_chunks = c;
   h->gen++;
   return TTKV_OK;
+}
+
+// Per-record partials of the speculative record stream, sized with the
+// slow-block capacity (the rows are indexed by block id).
+int ensure_rpart(ttkv_gpu* h) {
+  if (!h->spec_ctr) {
+    CU(h, cudaMalloc((void**)&h->spec_ctr, sizeof(uint32_t)));
+    CU(h, cudaMemsetAsync(h->spec_ctr, 0, sizeof(uint32_t), h->s0));
+    h->gen++;
+  }
+  if (h->rpart_cap >= h->g.n_cap && h->rpart) return TTKV_OK;
+  CU(h, cudaStreamSynchronize(h->s0));
+  if (h->rpart) cudaFree(h->rpart);
+  h->rpart = nullptr;
+  CU(h, cudaMalloc((void**)&h->rpart,
+                   (size_t)h->g.S * h->g.G * h->g.n_cap * kSpecPitch * sizeof(float)));
+  h->rpart_cap = h->g.n_cap;
+  h->gen++;
+  return TTKV_OK;
+}
+
+// Speculative record stream (slow_attn_tc_spec_kernel) for this step?  It
+// streams every record instead of the union of the G heads' selections, in
+// exchange for running beside the selection instead of after it (the union
+// covers 1 - (1 - k/n)^G of the blocks for per-head selection: 0.91 at cfg2).
+// Opt-in (record_stream = 2, or TTKV_SPEC=1): measured on one layer of cfg2
+// (8 streams x 4 heads, 128K, HBM) it is not faster than the union stream --
+// 62.4 vs 61.0 us per layer -- because the record kernel is bound by its
+// per-CTA record rate, and sharing the SMs with the selection and the fast
+// tier costs it as much as the selection's latency it hides.
+bool want_spec(const ttkv_gpu* h, uint64_t n, uint64_t k) {
+  static const int env = [] {  // TTKV_SPEC=0/1 overrides
+    const char* e = std::getenv("TTKV_SPEC");
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
+  const Geometry& g = h->g;
+  if (env == 0 || !h->slow_tc || !h->fast_tc || !slow_tc_spec_supported(g) ||
+      h->opt.literal_additive_merge || h->opt.serial_schedule || n == 0 || k == 0 ||
+      n > 0xffffffffull / g.S)
+    return false;
+  return env == 1 || h->opt.record_stream == 2;
 }
 
 int ensure_staging(ttkv_gpu* h, uint64_t tokens) {
@@ -650,6 +698,7 @@ struct StepPlan {
   uint32_t per_min;      // tensor-core tier: records per CTA at least
   bool slow, early_fork;
   bool fused;            // score + select + union as one cluster kernel
+  bool spec;             // speculative record stream beside the selection
   double scale_log2;
 };
 
@@ -670,13 +719,37 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
   // tier reads the ring, so the append runs on s1 ahead of the fast kernel and
   // stays off the critical path score -> select -> slow on s0.  Its slot is
   // the device step position mod C.
-  CU(h, cudaEventRecord(h->ev_start, h->s0));
-  CU(h, cudaStreamWaitEvent(h->s1, h->ev_start, 0));
-  {
+  // With the speculative record stream the record kernel holds every SM it
+  // can get until the step's records are done, so a fast tier on the side
+  // stream would start only at its end: append and fast tier then join the
+  // step's programmatic chain instead (append -> selection -> fast tier ->
+  // record stream -> combine), each launching as its predecessor starts.
+  if (P.spec) {
+    KTimer t(h, K_APPEND, h->s0);
+    CU(h, launch_append(g, h->ring_k, h->ring_v, P.kn, P.vn, P.dtype, 0, 1, 1, h->s0, h->pos_dev,
+                        true));
+  } else {
+    CU(h, cudaEventRecord(h->ev_start, h->s0));
+    CU(h, cudaStreamWaitEvent(h->s1, h->ev_start, 0));
     KTimer t(h, K_APPEND, h->s1);
     CU(h, launch_append(g, h->ring_k, h->ring_v, P.kn, P.vn, P.dtype, 0, 1, 1, h->s1, h->pos_dev));
   }
   auto fork_fast = [&]() -> int {
+    if (P.spec) {  // fast_tc is a precondition of the speculative stream
+      FastTcArgs& a = h->tc;
+      a.g = g;
+      a.q = P.q;
+      a.part = h->fpart;
+      a.front = h->fast_front;
+      a.pos = h->pos_dev;
+      a.F = (uint32_t)P.F;
+      a.FC = P.FCs;
+      a.nfc = P.nfc;
+      a.scale_log2 = P.scale_log2;
+      KTimer t(h, K_FAST, h->s0);
+      CU(h, launch_fast_tc(a, h->s0, true));
+      return TTKV_OK;
+    }
     CU(h, cudaEventRecord(h->ev_fork, h->s0));
     CU(h, cudaStreamWaitEvent(h->s1, h->ev_fork, 0));
     if (h->fast_tc) {
@@ -733,6 +806,7 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
     a.union_count = h->ucount;
     a.n = (uint32_t)P.n;
     a.k = (uint32_t)P.k;
+    a.early_trigger = P.spec ? 1u : 0u;
     KTimer t(h, K_SELECT, h->s0);
     CU(h, launch_select_fused(a, h->s0));
   } else if (P.slow) {
@@ -765,7 +839,19 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
     if (!P.early_fork) {
       if (int rcf = fork_fast()) return rcf;
     }
-    if (h->slow_tc) {
+    if (P.spec) {
+      SlowTcArgs& a = h->stc;
+      a.g = g;
+      a.params = h->params;
+      a.q = P.q;
+      a.literal = 0u;
+      a.scale_log2 = P.scale_log2;
+      a.spec_n = (uint32_t)P.n;
+      a.spec_ctr = h->spec_ctr;
+      a.rpart = h->rpart;
+      KTimer t(h, K_SLOW, h->s0);
+      CU(h, launch_slow_tc_spec(a, (uint32_t)P.grid_chunks, h->s0));
+    } else if (h->slow_tc) {
       SlowTcArgs& a = h->stc;
       a.g = g;
       a.params = h->params;
@@ -802,7 +888,7 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
   } else if (!P.early_fork) {
     if (int rcf = fork_fast()) return rcf;
   }
-  CU(h, cudaStreamWaitEvent(h->s0, h->ev_join, 0));
+  if (!P.spec) CU(h, cudaStreamWaitEvent(h->s0, h->ev_join, 0));
   {
     CombineArgs a{};
     a.g = g;
@@ -813,6 +899,16 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
     a.CH = P.CH;
     a.union_count = P.slow ? h->ucount : nullptr;
     a.nslots = P.slow && h->slow_tc ? h->nslots : nullptr;
+    if (P.spec) {
+      a.spart = nullptr;
+      a.nslots = nullptr;
+      a.rpart = h->rpart;
+      a.union_ids = h->uids;
+      a.union_mask = h->umask;
+      a.n_cap = g.n_cap;
+      a.spec_n = (uint32_t)P.n;
+      a.spec_ctr = h->spec_ctr;
+    }
     a.out = P.out;
     a.literal = h->opt.literal_additive_merge ? 1u : 0u;
     a.pos_inc = h->pos_dev;
@@ -835,7 +931,7 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
       h->pg.epoch += 1;
       CU(h, launch_peer_wait(
                 reinterpret_cast<const unsigned long long*>(h->pg.base + 2 * h->pg.out_bytes),
-                h->pg.n_ranks, h->pg.epoch * (unsigned long long)g.S * g.G * combine_slices(g),
+                h->pg.n_ranks, h->pg.epoch * (unsigned long long)g.S * g.G * combine_slices(a),
                 h->pg.status,
                 h->s0));
     }
@@ -922,10 +1018,11 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
     return e ? (std::strcmp(e, "early") == 0 ? 1 : 0) + (std::strcmp(e, "late") == 0 ? 2 : 0) : 0;
   }();
   P.fused = P.slow && select_fused_supported(g, (uint32_t)P.n, (uint32_t)h->sms);
+  P.spec = P.fused && want_spec(h, P.n, P.k);
   // A one-wave fused selection leaves most SMs idle: the fast tier then runs
   // beside it instead of starved under the slow kernel (layer-sequential
   // cfg2: fast tier done before the slow kernel starts, 2 us less per layer)
-  P.early_fork = fork_env == 1 || (fork_env != 2 && P.fused);
+  P.early_fork = !P.spec && (fork_env == 1 || (fork_env != 2 && P.fused));
   P.CH = 4;
   if (P.slow) {
     if (h->slow_tc) {
@@ -963,6 +1060,15 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
     if (rc) return rc;
     if (h->slow_tc)  // spart_chunks >= 2 here
       P.per_min = (uint32_t)((P.n + h->spart_chunks - 2) / (h->spart_chunks - 1));
+    if (P.spec) {  // one wave of resident CTAs fed from the record queue
+      rc = ensure_rpart(h);
+      if (rc) return rc;
+      static const uint32_t cps = [] {  // TTKV_SPEC_CPS=n: CTAs per SM (measurement)
+        const char* e = std::getenv("TTKV_SPEC_CPS");
+        return e ? (uint32_t)std::max(1, std::min(3, std::atoi(e))) : slow_tc_ctas_per_sm();
+      }();
+      P.grid_chunks = (uint64_t)h->sms * cps;
+    }
   }
   if (!h->pos_synced) {  // host-side appends / prefill / restore moved `appended`
     CU(h, launch_set_u64(h->pos_dev, pos, h->s0));
@@ -1048,6 +1154,7 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
     if (rc) return rc;
   }
   h->appended = pos + 1;
+  if (P.spec) h->spec_steps++;
   h->last_k = P.slow ? P.k : 0;
   h->last_n = P.n;
   bool evicted = false;
@@ -1158,6 +1265,8 @@ int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* po
     return set_err(nullptr, TTKV_ECONFIG, "GPU engine supports block_size <= 512");
   if (opt->n_streams == 0 || opt->heads_per_stream == 0 || opt->heads_per_stream > (uint32_t)kMaxG)
     return set_err(nullptr, TTKV_ECONFIG, "n_streams >= 1 and heads_per_stream in [1, 8]");
+  if (opt->record_stream > 2)
+    return set_err(nullptr, TTKV_ECONFIG, "record_stream must be 0 (auto), 1 (union) or 2 (speculative)");
 
   int ndev = 0;
   cudaError_t ce = cudaGetDeviceCount(&ndev);
@@ -1524,6 +1633,7 @@ int ttkv_gpu_state(ttkv_gpu* h, ttkv_state* st) {
   st->launches = h->launches;
   st->graph_replays = h->graph_replays;
   st->graph_captures = h->graph_captures;
+  st->spec_steps = h->spec_steps;
   st->payload_bytes = h->g.rec.kp_off;
   return TTKV_OK;
 }

@@ -80,7 +80,8 @@ cudaError_t launch_evict(const EvictArgs& a, uint32_t n_blocks, int in_dtype, cu
 // (device, decode steps) the first slot is *pos mod C instead of `slot`.
 cudaError_t launch_append(const Geometry& g, void* ring_k, void* ring_v, const void* k_new,
                           const void* v_new, int in_dtype, uint64_t slot, uint64_t in_stride_tok,
-                          uint64_t n_tok, cudaStream_t st, const uint64_t* pos = nullptr);
+                          uint64_t n_tok, cudaStream_t st, const uint64_t* pos = nullptr,
+                          bool chained = false);  // chained: programmatic launch, critical priority
 // *p = v, stream-ordered (the device step position of a handle)
 cudaError_t launch_set_u64(uint64_t* p, uint64_t v, cudaStream_t st);
 
@@ -123,6 +124,7 @@ struct FusedSelectArgs {
   uint32_t* union_mask;
   uint32_t* union_count;
   uint32_t n, k;
+  uint32_t early_trigger;  // let the chained kernel start at once (speculative record stream)
 };
 bool select_fused_supported(const Geometry& g, uint32_t n, uint32_t sms);
 cudaError_t launch_select_fused(const FusedSelectArgs& a, cudaStream_t st);
@@ -176,8 +178,19 @@ struct alignas(64) SlowTcArgs {
   uint32_t per_min;  // records per CTA at least: no stream spans more than nsc CTAs
   uint32_t nsc, literal;
   double scale_log2;
+  // speculative stream (slow_attn_tc_spec_kernel): every record of the step,
+  // one block-local partial per (record, head) into rpart
+  uint32_t spec_n;     // slow blocks per stream
+  uint32_t* spec_ctr;  // record queue head (reset to 0 by the combine)
+  float* rpart;        // [S][G][n_cap][kSpecPitch]
 };
 bool slow_tc_supported(const Geometry& g);
+// Per-record partial row of the speculative stream: acc[128], m, l, 2 pad
+// (16-byte aligned rows for the float4 stores).
+constexpr uint32_t kSpecPitch = 132;
+bool slow_tc_spec_supported(const Geometry& g);  // K8/V4, d = B = 128, G <= 4
+// grid: one wave of resident CTAs; records come from the *spec_ctr queue
+cudaError_t launch_slow_tc_spec(const SlowTcArgs& a, uint32_t grid_ctas, cudaStream_t st);
 uint32_t slow_tc_ctas_per_sm();  // resident CTAs per SM of the slow tensor-core kernel
 // Largest |key scale| the tensor-core slow kernel accepts: records quantized
 // from an fp16 ring have s = (max - min) / 255 <= 2 * 65504 / 255 < 514, and
@@ -192,7 +205,9 @@ cudaError_t launch_slow_tc(const SlowTcArgs& a, uint32_t grid_ctas, cudaStream_t
 bool fast_tc_supported(const Geometry& g);
 uint32_t fast_tc_tile();
 cudaError_t make_ring_tmaps(const Geometry& g, void* ring_k, void* ring_v, FastTcArgs& a);
-cudaError_t launch_fast_tc(const FastTcArgs& a, cudaStream_t st);
+// chained: programmatic launch at critical priority (speculative record
+// stream: the fast tier runs in the step's chain, not on the side stream)
+cudaError_t launch_fast_tc(const FastTcArgs& a, cudaStream_t st, bool chained = false);
 
 struct SlowArgs {
   Geometry g;
@@ -242,9 +257,19 @@ struct CombineArgs {
   const uint32_t* gidx;
   double* peer_out[kMaxPeers];
   unsigned long long* peer_flags[kMaxPeers];  // rank r's counters [n_ranks]
+  // Speculative record stream: the slow partials are per-record rows
+  // rpart[S][G][n_cap][kSpecPitch]; (stream, head) merges the rows of the
+  // union entries whose head bit is set.  spec_ctr is reset for the next step.
+  const float* rpart;  // null: slot partials (spart)
+  const uint32_t* union_ids;
+  const uint32_t* union_mask;
+  uint64_t n_cap;
+  uint32_t spec_n;
+  uint32_t* spec_ctr;
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);
 uint32_t combine_slices(const Geometry& g);  // CTAs per (stream, head) row
+uint32_t combine_slices(const CombineArgs& a);  // ... of this launch (speculative: d_v / 32)
 // Blocks the stream until every rank's arrival counter in `flags` reaches
 // `target` (acquire, system scope); gives up after ~4 s and sets *status = 1.
 cudaError_t launch_peer_wait(const unsigned long long* flags, uint32_t n_ranks,

@@ -475,6 +475,9 @@ __global__ void __launch_bounds__(kTopkThreads) select_fused_kernel(FusedSelectA
   // kernel is not one of them while it is still running.  q is read after.
   stage_rows(a.cent + ((uint64_t)s * g.n_cap + r0) * g.d_k, g.d_k, rows, L.nb, tile);
   pdl_wait();  // the query
+  // speculative record stream: it needs nothing from this kernel until its
+  // end, so its CTAs take the SMs this selection leaves free right away
+  if (a.early_trigger) pdl_trigger();
   stage_query_f64(g, a.q, s, qs);
   TTKV_PHASE_STAMP(1);
   // ---- score: row t against every head (score_staged_rows: the same fp64
@@ -637,6 +640,10 @@ template <typename T, typename Tin>
 __global__ void append_kernel(Geometry g, T* ring_k, T* ring_v, const Tin* kn, const Tin* vn,
                               uint64_t slot0, uint64_t in_stride_tok, uint64_t n_tok,
                               const uint64_t* pos) {
+  // chained launch (speculative record stream): the selection may launch at
+  // once; the step position is advanced by the previous step's combine
+  pdl_trigger();
+  pdl_wait();
   // one thread per 8-element group of a token row; K groups then V groups
   const uint32_t gk = g.d_k / 8, gv = g.d_v / 8, gr = gk + gv;
   const uint64_t total = (uint64_t)g.S * n_tok * gr;
@@ -671,6 +678,8 @@ template <typename T, typename Tin>
 __global__ void append_kernel_scalar(Geometry g, T* ring_k, T* ring_v, const Tin* kn,
                                      const Tin* vn, uint64_t slot0, uint64_t in_stride_tok,
                                      uint64_t n_tok, const uint64_t* pos) {
+  pdl_trigger();
+  pdl_wait();
   if (pos) slot0 = *pos;
   const uint32_t dkv = g.d_k + g.d_v;
   const uint64_t total = (uint64_t)g.S * n_tok * dkv;
@@ -691,36 +700,37 @@ __global__ void append_kernel_scalar(Geometry g, T* ring_k, T* ring_v, const Tin
 template <typename T, typename Tin>
 static void launch_append_t(const Geometry& g, void* ring_k, void* ring_v, const void* k_new,
                             const void* v_new, uint64_t slot, uint64_t in_stride_tok,
-                            uint64_t n_tok, cudaStream_t st, const uint64_t* pos) {
+                            uint64_t n_tok, cudaStream_t st, const uint64_t* pos, bool chained) {
   const bool vec = g.d_k % 8 == 0 && g.d_v % 8 == 0 &&
                    ((reinterpret_cast<uintptr_t>(k_new) | reinterpret_cast<uintptr_t>(v_new)) & 15) == 0;
   const uint64_t total = (uint64_t)g.S * n_tok * (vec ? (g.d_k + g.d_v) / 8 : g.d_k + g.d_v);
   uint64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  if (vec)
-    launch_background(append_kernel<T, Tin>, dim3((unsigned)blocks), dim3(256), 0, st, g,
-                      (T*)ring_k, (T*)ring_v, (const Tin*)k_new, (const Tin*)v_new, slot,
-                      in_stride_tok, n_tok, pos);
+  auto kv = append_kernel<T, Tin>;
+  auto ks = append_kernel_scalar<T, Tin>;
+  auto kern = vec ? kv : ks;
+  if (chained)
+    launch_chained(kern, dim3((unsigned)blocks), dim3(256), 0, st, g, (T*)ring_k, (T*)ring_v,
+                   (const Tin*)k_new, (const Tin*)v_new, slot, in_stride_tok, n_tok, pos);
   else
-    launch_background(append_kernel_scalar<T, Tin>, dim3((unsigned)blocks), dim3(256), 0, st, g,
-                      (T*)ring_k, (T*)ring_v, (const Tin*)k_new, (const Tin*)v_new, slot,
-                      in_stride_tok, n_tok, pos);
+    launch_background(kern, dim3((unsigned)blocks), dim3(256), 0, st, g, (T*)ring_k, (T*)ring_v,
+                      (const Tin*)k_new, (const Tin*)v_new, slot, in_stride_tok, n_tok, pos);
 }
 
 cudaError_t launch_append(const Geometry& g, void* ring_k, void* ring_v, const void* k_new,
                           const void* v_new, int in_dtype, uint64_t slot, uint64_t in_stride_tok,
-                          uint64_t n_tok, cudaStream_t st, const uint64_t* pos) {
+                          uint64_t n_tok, cudaStream_t st, const uint64_t* pos, bool chained) {
   if (n_tok == 0) return cudaSuccess;
   if (g.elem == 2) {
     if (in_dtype == kInF16)
-      launch_append_t<__half, __half>(g, ring_k, ring_v, k_new, v_new, slot, in_stride_tok, n_tok, st, pos);
+      launch_append_t<__half, __half>(g, ring_k, ring_v, k_new, v_new, slot, in_stride_tok, n_tok, st, pos, chained);
     else
-      launch_append_t<__half, float>(g, ring_k, ring_v, k_new, v_new, slot, in_stride_tok, n_tok, st, pos);
+      launch_append_t<__half, float>(g, ring_k, ring_v, k_new, v_new, slot, in_stride_tok, n_tok, st, pos, chained);
   } else {
     if (in_dtype == kInF16)
-      launch_append_t<float, __half>(g, ring_k, ring_v, k_new, v_new, slot, in_stride_tok, n_tok, st, pos);
+      launch_append_t<float, __half>(g, ring_k, ring_v, k_new, v_new, slot, in_stride_tok, n_tok, st, pos, chained);
     else
-      launch_append_t<float, float>(g, ring_k, ring_v, k_new, v_new, slot, in_stride_tok, n_tok, st, pos);
+      launch_append_t<float, float>(g, ring_k, ring_v, k_new, v_new, slot, in_stride_tok, n_tok, st, pos, chained);
   }
   return cudaGetLastError();
 }

@@ -181,7 +181,7 @@ class MultiStreamEngine:
                  heads_per_stream: int = 1, group_select: bool = False, device: int = 0,
                  reserve_tokens: int = 0, slow_tier: int = L.SLOW_PINNED_HOST,
                  copy_mode: int = 0, literal_additive_merge: bool = False,
-                 ring_bytes: int = 0, serial_schedule: bool = False):
+                 ring_bytes: int = 0, serial_schedule: bool = False, record_stream: int = 0):
         self.config = config
         self.policy = policy or SelectionPolicy(config.top_k_blocks, config.fetch_fraction)
         self.S, self.G = n_streams, heads_per_stream
@@ -192,7 +192,7 @@ class MultiStreamEngine:
         self._c_opt = L.OptionsC(device, n_streams, heads_per_stream, int(group_select),
                                  reserve_tokens, slow_tier, copy_mode,
                                  int(literal_additive_merge), ring_bytes,
-                                 int(serial_schedule))
+                                 int(serial_schedule), record_stream)
         h = C.c_void_p()
         _check(self._lib.ttkv_gpu_create(C.byref(self._c_cfg), C.byref(self._c_pol),
                                          C.byref(self._c_opt), C.byref(h)))

@@ -23,7 +23,8 @@ sys.path.insert(0, {root!r})
 import paper_2604_19769_b200 as T
 S, G, d, ctx = 6, 4, 128, 9000
 cfg = T.TierConfig(hbm_budget_bytes=1024 * 2 * d * 2, d_k=d, d_v=d, block_size=128)
-eng = T.MultiStreamEngine(cfg, n_streams=S, heads_per_stream=G, slow_tier={tier})
+eng = T.MultiStreamEngine(cfg, n_streams=S, heads_per_stream=G, slow_tier={tier},
+                          record_stream={rs})
 eng.prefill_synthetic(ctx, seed=3)
 rng = np.random.default_rng(11)
 outs, fetched = [], []
@@ -40,31 +41,39 @@ for t in range(300):  # crosses two evictions
         fetched.append(np.concatenate([np.concatenate(f) for f in r.fetched_blocks]))
 st = eng.state()
 np.savez({out!r}, out=np.stack(outs), fetched=np.concatenate(fetched),
-         replays=st["graph_replays"], captures=st["graph_captures"])
+         replays=st["graph_replays"], captures=st["graph_captures"], spec=st["spec_steps"])
 """
 
 
-def run_mode(tmp_path, tier, **env_over):
+# slow tier in pinned DRAM; in HBM with the union record stream; in HBM with
+# the speculative stream of every record (slow_attn_tc_spec_kernel)
+MODES = [(0, 0), (1, 1), (1, 2)]
+
+
+def run_mode(tmp_path, mode, **env_over):
+    tier, rs = mode
     tag = "_".join(f"{k}{v}" for k, v in sorted(env_over.items()))
-    out = str(tmp_path / f"{tag}_{tier}.npz")
+    out = str(tmp_path / f"{tag}_{tier}_{rs}.npz")
     env = dict(os.environ, **env_over)
-    subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT, tier=tier, out=out)],
+    subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT, tier=tier, rs=rs, out=out)],
                    env=env, check=True, timeout=600)
-    return np.load(out)
+    r = np.load(out)
+    assert int(r["spec"]) == (300 if rs == 2 else 0)  # every step streams speculatively
+    return r
 
 
-@pytest.mark.parametrize("tier", [0, 1])
-def test_pdl_on_off_bit_identical(tmp_path, tier):
-    a = run_mode(tmp_path, tier, TTKV_PDL="1")
-    b = run_mode(tmp_path, tier, TTKV_PDL="0")
+@pytest.mark.parametrize("mode", MODES)
+def test_pdl_on_off_bit_identical(tmp_path, mode):
+    a = run_mode(tmp_path, mode, TTKV_PDL="1")
+    b = run_mode(tmp_path, mode, TTKV_PDL="0")
     assert np.array_equal(a["out"], b["out"])
     assert np.array_equal(a["fetched"], b["fetched"])
 
 
-@pytest.mark.parametrize("tier", [0, 1])
-def test_graph_replay_bit_identical(tmp_path, tier):
-    a = run_mode(tmp_path, tier, TTKV_GRAPH="1")
-    b = run_mode(tmp_path, tier, TTKV_GRAPH="0")
+@pytest.mark.parametrize("mode", MODES)
+def test_graph_replay_bit_identical(tmp_path, mode):
+    a = run_mode(tmp_path, mode, TTKV_GRAPH="1")
+    b = run_mode(tmp_path, mode, TTKV_GRAPH="0")
     # the graph run really replayed: one capture per eviction period (plus
     # the one after the host append), every other non-evicting step a replay
     assert int(a["replays"]) >= 250 and 3 <= int(a["captures"]) <= 6

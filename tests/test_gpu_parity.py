@@ -194,7 +194,8 @@ def check_every_list(eng, S, G, k):
 
 def run_parity(T_, *, S=2, G=1, d=32, dv=None, B=32, l_fast=128, kb=8, vb=4, elem=2, ctx=600,
                steps=6, frac=0.45, top_k=None, mode=0, seed=100, prefill_chunks=1,
-               check_blocks=True, literal=False, slow_tier=0, q_mul=1.0, kv_mul=1.0):
+               check_blocks=True, literal=False, slow_tier=0, q_mul=1.0, kv_mul=1.0,
+               record_stream=0):
     dv = dv or d
     cfg = T_.TierConfig(hbm_budget_bytes=l_fast * (d + dv) * elem, d_k=d, d_v=dv,
                         bytes_full_precision=elem, block_size=B, key_bits=kb, value_bits=vb,
@@ -208,7 +209,8 @@ def run_parity(T_, *, S=2, G=1, d=32, dv=None, B=32, l_fast=128, kb=8, vb=4, ele
         if elem == 2:
             pk, pv, dk_, dv_ = map(O.fp16_round, (pk, pv, dk_, dv_))
     eng = T_.MultiStreamEngine(cfg, pol, n_streams=S, heads_per_stream=G, group_select=bool(mode),
-                               literal_additive_merge=literal, slow_tier=slow_tier)
+                               literal_additive_merge=literal, slow_tier=slow_tier,
+                               record_stream=record_stream)
     orc = [O.OracleEngine(d, dv, B, l_fast, kb, vb, top_k, frac) for _ in range(S)]
     bounds = np.linspace(0, ctx, prefill_chunks + 1).astype(int)
     for a, b in zip(bounds[:-1], bounds[1:]):
@@ -330,30 +332,34 @@ def test_engine_hot_shape_small(gpu):
 @pytest.mark.parametrize("G,mode,literal", [(4, 0, False), (4, 1, False), (1, 0, False), (2, 0, False),
                                             (3, 0, False), (6, 0, False), (5, 1, False),
                                             (8, 0, False), (4, 0, True)])
-def test_engine_hbm_resident_slow_tier(gpu, G, mode, literal):
+@pytest.mark.parametrize("record_stream", [1, 2])
+def test_engine_hbm_resident_slow_tier(gpu, G, mode, literal, record_stream):
     # slow tier in HBM: the tensor-core slow kernel (TMA tensor maps, mma.sync
-    # on raw codes) for K8/V4, d = B = 128; records still bit-exact
+    # on raw codes) for K8/V4, d = B = 128; records still bit-exact.  Both
+    # record streams: the selected union after the selection (1) and the
+    # speculative stream of every record beside it (2, G <= 4 and not literal;
+    # otherwise the handle keeps the union stream)
     run_parity(gpu, S=3, G=G, d=128, B=128, l_fast=512, ctx=5000, steps=4, mode=mode,
-               literal=literal, slow_tier=1)
+               literal=literal, slow_tier=1, record_stream=record_stream)
 
 
-@pytest.mark.parametrize("slow_tier", [0, 1])
+@pytest.mark.parametrize("slow_tier,record_stream", [(0, 0), (1, 1), (1, 2)])
 @pytest.mark.parametrize("q_mul,kv_mul", [(3e4, 1.0), (1.0, 2e3), (50.0, 2e3), (1e-6, 1e-3), (1e7, 1.0), (3e3, 5e3)])
-def test_engine_extreme_magnitudes(gpu, slow_tier, q_mul, kv_mul):
+def test_engine_extreme_magnitudes(gpu, slow_tier, record_stream, q_mul, kv_mul):
     # hot-path shape with queries / KV far from N(0, 1): the tensor-core
     # kernels' fp16 operand splits must neither overflow (scores of 1e4+ in
     # log2 units, keys near the fp16 range) nor lose the small end
     run_parity(gpu, S=2, G=4, d=128, B=128, l_fast=512, ctx=3000, steps=3, slow_tier=slow_tier,
-               q_mul=q_mul, kv_mul=kv_mul)
+               q_mul=q_mul, kv_mul=kv_mul, record_stream=record_stream)
 
 
-@pytest.mark.parametrize("slow_tier", [0, 1])
-def test_engine_long_fast_tier_short_slow(gpu, slow_tier):
+@pytest.mark.parametrize("slow_tier,record_stream", [(0, 0), (1, 1), (1, 2)])
+def test_engine_long_fast_tier_short_slow(gpu, slow_tier, record_stream):
     # a long fast tier (second stream) against a one-record slow tier: the
     # combine, launched chained behind the short slow kernel, must still wait
     # for the fast tier's event (programmatic launch must not bypass it)
     run_parity(gpu, S=4, G=4, d=128, B=128, l_fast=16384, ctx=16384 + 200, steps=4,
-               slow_tier=slow_tier, check_blocks=False)
+               slow_tier=slow_tier, check_blocks=False, record_stream=record_stream)
 
 
 def test_engine_hbm_resident_generic_shape(gpu):
@@ -572,6 +578,26 @@ def test_full_size_cfg2_sampled_streams(gpu, slow_tier):
     rep = full_size_step(eng, *step_inputs(np.random.default_rng(1), S, G, d), (7, S - 3), 447,
                          B, d)
     assert rep.eviction_occurred
+    eng.close()
+
+
+@pytest.mark.parametrize("record_stream", [1, 2])
+def test_full_size_cfg2_one_layer_hbm(gpu, record_stream):
+    """One layer of cfg2 as layer-sequential decode runs it: 8 KV streams x 4
+    query heads at 128K (n = 992, k = 447), slow tier in HBM, with the union
+    record stream (1) and the speculative one (2: every record streamed beside
+    the selection, the combine merging each head's selected records).  Every
+    stream re-derived on the host, over steps that reuse the record queue."""
+    T_ = gpu
+    S, G, d, B, lf, ctx = 8, 4, 128, 128, 4096, 131072
+    cfg = T_.TierConfig(hbm_budget_bytes=lf * 256 * 2, d_k=d, d_v=d, block_size=B)
+    eng = T_.MultiStreamEngine(cfg, n_streams=S, heads_per_stream=G, reserve_tokens=ctx + 256,
+                               slow_tier=1, record_stream=record_stream)
+    eng.prefill_synthetic(ctx, seed=29)
+    rng = np.random.default_rng(9)
+    for _ in range(3):
+        full_size_step(eng, *step_inputs(rng, S, G, d), tuple(range(S)), 447, B, d)
+    assert eng.state()["spec_steps"] == (3 if record_stream == 2 else 0)
     eng.close()
 
 
