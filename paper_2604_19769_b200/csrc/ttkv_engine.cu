@@ -697,6 +697,8 @@ struct StepPlan {
   uint64_t gather_chunks;
   uint32_t per_min;      // tensor-core tier: records per CTA at least
   bool slow, early_fork;
+  bool fast_first;       // the record stream waits for the fast tier (measurement)
+  bool fast_last;        // the fast tier runs on s0 after the record stream
   bool fused;            // score + select + union as one cluster kernel
   bool spec;             // speculative record stream beside the selection
   double scale_log2;
@@ -731,11 +733,16 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
   } else {
     CU(h, cudaEventRecord(h->ev_start, h->s0));
     CU(h, cudaStreamWaitEvent(h->s1, h->ev_start, 0));
-    KTimer t(h, K_APPEND, h->s1);
-    CU(h, launch_append(g, h->ring_k, h->ring_v, P.kn, P.vn, P.dtype, 0, 1, 1, h->s1, h->pos_dev));
+    {
+      KTimer t(h, K_APPEND, h->s1);
+      CU(h, launch_append(g, h->ring_k, h->ring_v, P.kn, P.vn, P.dtype, 0, 1, 1, h->s1,
+                          h->pos_dev));
+    }
+    if (P.fast_last) CU(h, cudaEventRecord(h->ev_join, h->s1));  // the ring holds the token
   }
   auto fork_fast = [&]() -> int {
-    if (P.spec) {  // fast_tc is a precondition of the speculative stream
+    if (P.spec || P.fast_last) {  // fast_tc is a precondition of both
+      if (P.fast_last) CU(h, cudaStreamWaitEvent(h->s0, h->ev_join, 0));
       FastTcArgs& a = h->tc;
       a.g = g;
       a.q = P.q;
@@ -836,9 +843,10 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
       CU(h, launch_gather(g, h->arena_dev, h->stage_arena, h->uids, h->ucount,
                           (uint32_t)P.gather_chunks, P.CH, h->s0));
     }
-    if (!P.early_fork) {
+    if (!P.early_fork && !P.fast_last) {
       if (int rcf = fork_fast()) return rcf;
     }
+    if (P.fast_first) CU(h, cudaStreamWaitEvent(h->s0, h->ev_join, 0));
     if (P.spec) {
       SlowTcArgs& a = h->stc;
       a.g = g;
@@ -888,7 +896,11 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
   } else if (!P.early_fork) {
     if (int rcf = fork_fast()) return rcf;
   }
-  if (!P.spec) CU(h, cudaStreamWaitEvent(h->s0, h->ev_join, 0));
+  if (P.fast_last) {
+    if (int rcf = fork_fast()) return rcf;
+  } else if (!P.spec && !P.fast_first) {
+    CU(h, cudaStreamWaitEvent(h->s0, h->ev_join, 0));
+  }
   {
     CombineArgs a{};
     a.g = g;
@@ -1023,6 +1035,14 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
   // beside it instead of starved under the slow kernel (layer-sequential
   // cfg2: fast tier done before the slow kernel starts, 2 us less per layer)
   P.early_fork = !P.spec && (fork_env == 1 || (fork_env != 2 && P.fused));
+  static const int order_env = [] {  // TTKV_FAST_ORDER=side|first|last (measurement)
+    const char* e = std::getenv("TTKV_FAST_ORDER");
+    return !e ? 0 : std::strcmp(e, "first") == 0 ? 1 : std::strcmp(e, "last") == 0 ? 2 : 0;
+  }();
+  P.fast_first = P.slow && !P.spec && order_env == 1;
+  P.fast_last = P.slow && !P.spec && h->fast_tc && order_env == 2;
+  if (P.fast_first) P.early_fork = true;
+  if (P.fast_last) P.early_fork = false;
   P.CH = 4;
   if (P.slow) {
     if (h->slow_tc) {

@@ -18,6 +18,9 @@ cases = [
     dict(S=2, G=8, d=32, B=32, l_fast=128, ctx=9000, steps=2),
     # power-of-two q normalization at query magnitudes that overflow fp16
     dict(S=1, G=4, d=128, B=128, l_fast=256, ctx=700, steps=2, slow_tier=1, q_mul=1e7),
+    # speculative record stream (every record beside the selection, per-record
+    # partials, the compacting combine) and the fused selection cluster kernel
+    dict(S=2, G=4, d=128, B=128, l_fast=256, ctx=5000, steps=2, slow_tier=1, record_stream=2),
 ]
 for c in cases:
     P.run_parity(T, **c)
