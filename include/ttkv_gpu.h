@@ -320,7 +320,8 @@ int ttkv_gpu_dequantize_block(int device, const uint8_t* packed_k, const uint8_t
                               uint32_t d_k, uint32_t d_v, uint32_t key_bits, uint32_t value_bits,
                               float* keys, float* values);
 /* score_block (relevance.cpp:19-27) for n centroids [n][d]: fp64, sequential,
- * unfused -- bit-exact. */
+ * one fma per term (the product of two float-valued doubles is exact, so this
+ * equals the reference's separate multiply + add) -- bit-exact. */
 int ttkv_gpu_score_blocks(int device, const float* query, const float* centroids, uint64_t n,
                           uint32_t d, double* scores);
 /* select_top_k (relevance.cpp:29-43): the k ids ordered by (score desc, id
