@@ -629,16 +629,13 @@ def run_ours(args):
     kt = eng.kernel_times(reset=True)
 
     # --- e2e through the public C ABI with host buffers -----------------------
-    rng = np.random.default_rng(rank)
-    hq = [rng.standard_normal((S, G, D)).astype(np.float32) for _ in range(NPOOL)]
-    hk = [rng.standard_normal((S, D)).astype(np.float16) for _ in range(NPOOL)]
-    hv = [rng.standard_normal((S, D)).astype(np.float16) for _ in range(NPOOL)]
+    pins, hq, hk, hv, hout = pinned_step_buffers(np.random.default_rng(rank), S, G, NPOOL)
     h2d = hq[0].nbytes + hk[0].nbytes + hv[0].nbytes
     d2h = S * G * D * 8 * (world if plan.needs_gather else 1)
     barrier()
     t_e2e0 = time.perf_counter()
     for i in range(args.steps):
-        r = eng.decode_step(hq[i % NPOOL], hk[i % NPOOL], hv[i % NPOOL])
+        r = eng.decode_step(hq[i % NPOOL], hk[i % NPOOL], hv[i % NPOOL], out=hout)
         if pg is not None:
             _ = pg.host()
         elif plan.needs_gather:
@@ -723,7 +720,8 @@ def run_ours(args):
         "kernel_ms_per_step": {k[3:]: v / n_kt for k, v in kt.items() if k.startswith("ms_")},
         "gpu_launches": launches,
         "e2e": {"value": tokens_per_step * 1000.0 / e2e_ms, "unit": UNIT,
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                "host_buffers": "page-locked caller buffers, DMA'd by the step (ttkv_gpu_decode_step)"},
         "prefill_s": round(prefill_s, 2),
     }
     if world > 1:
@@ -739,6 +737,34 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def pinned_step_buffers(rng, S, G, npool):
+    """The e2e leg's host buffers: `npool` sets of random q [S, G, D] f32 and
+    k, v [S, D] f16 plus one f64 output [S, G, D], all page-locked (numpy views
+    of pinned torch tensors), so every step's H2D and D2H is a DMA from / to
+    pinned host memory with no staging copy.  Returns (keep-alive, q, k, v, out)."""
+    import numpy as np
+    import torch
+
+    def pinned(a):
+        t = torch.empty(a.shape, dtype={np.float32: torch.float32, np.float16: torch.float16,
+                                        np.float64: torch.float64}[a.dtype.type],
+                        pin_memory=True)
+        v = t.numpy()
+        v[...] = a
+        return t, v
+    keep, qs, ks, vs = [], [], [], []
+    for _ in range(npool):
+        for dst, a in ((qs, rng.standard_normal((S, G, D)).astype(np.float32)),
+                       (ks, rng.standard_normal((S, D)).astype(np.float16)),
+                       (vs, rng.standard_normal((S, D)).astype(np.float16))):
+            t, v = pinned(a)
+            keep.append(t)
+            dst.append(v)
+    t, out = pinned(np.zeros((S, G, D), np.float64))
+    keep.append(t)
+    return keep, qs, ks, vs, out
 
 
 def cpu_baseline_line(ctx, G, total, tokens_per_step, warm=2, timed=5, note=""):
@@ -885,15 +911,12 @@ def run_growth(args):
     value = 1000.0 / ms_step
 
     # e2e through the C ABI with host buffers, at the last (256K) point
-    rng = np.random.default_rng(rank)
-    hq = [rng.standard_normal((S, G, D)).astype(np.float32) for _ in range(NPOOL)]
-    hk = [rng.standard_normal((S, D)).astype(np.float16) for _ in range(NPOOL)]
-    hv = [rng.standard_normal((S, D)).astype(np.float16) for _ in range(NPOOL)]
+    pins, hq, hk, hv, hout = pinned_step_buffers(np.random.default_rng(rank), S, G, NPOOL)
     n_e2e = min(K, 16)
     barrier()
     t_e2e0 = time.perf_counter()
     for i in range(n_e2e):
-        r = eng.decode_step(hq[i % NPOOL], hk[i % NPOOL], hv[i % NPOOL])
+        r = eng.decode_step(hq[i % NPOOL], hk[i % NPOOL], hv[i % NPOOL], out=hout)
         if pg is not None:
             _ = pg.host()
         elif plan.needs_gather:

@@ -294,6 +294,7 @@ struct ttkv_gpu {
   uint64_t gen = 0;         // bumped whenever a buffer a captured step uses moves
   struct GraphKey {
     const void *q, *kn, *vn, *out;
+    const void* host[4];  // host-buffer steps: the q, k, v sources and the output
     cudaStream_t s0;
     uint64_t n, k, front, gen, grid_chunks;
     uint32_t nfc, CH, dtype, host_io;
@@ -690,7 +691,11 @@ struct StepPlan {
   const void* vn;
   int dtype;
   double* out;
-  bool host_io;  // stage q/k/v from and out to the handle's pinned buffers
+  bool host_io;  // copy q/k/v in from host and the output back within the step
+  const void* hq;  // host sources: the caller's buffers when page-locked, else
+  const void* hk;  // the handle's pinned staging copies
+  const void* hv;
+  void* hout;      // host destination of the output (same rule)
   uint64_t n, k, F;
   uint32_t FCs, nfc, CH;
   uint64_t grid_chunks;  // slow kernel grid: chunks per stream, or CTAs (tensor-core tier)
@@ -710,11 +715,11 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
   const Geometry& g = h->g;
   if (P.host_io) {
     const size_t esz = P.dtype == kInF16 ? 2 : 4;
-    CU(h, cudaMemcpyAsync(h->q_dev, h->h_q, (size_t)g.S * g.G * g.d_k * 4, cudaMemcpyHostToDevice,
+    CU(h, cudaMemcpyAsync(h->q_dev, P.hq, (size_t)g.S * g.G * g.d_k * 4, cudaMemcpyHostToDevice,
                           h->s0));
-    CU(h, cudaMemcpyAsync(h->kn_dev, h->h_k, (size_t)g.S * g.d_k * esz, cudaMemcpyHostToDevice,
+    CU(h, cudaMemcpyAsync(h->kn_dev, P.hk, (size_t)g.S * g.d_k * esz, cudaMemcpyHostToDevice,
                           h->s0));
-    CU(h, cudaMemcpyAsync(h->vn_dev, h->h_v, (size_t)g.S * g.d_v * esz, cudaMemcpyHostToDevice,
+    CU(h, cudaMemcpyAsync(h->vn_dev, P.hv, (size_t)g.S * g.d_v * esz, cudaMemcpyHostToDevice,
                           h->s0));
   }
   // append_kv: the new token attends to itself.  Only the fast
@@ -949,7 +954,7 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
     }
   }
   if (P.host_io) {
-    CU(h, cudaMemcpyAsync(h->h_out, h->out_dev, (size_t)g.S * g.G * g.d_v * 8,
+    CU(h, cudaMemcpyAsync(P.hout, h->out_dev, (size_t)g.S * g.G * g.d_v * 8,
                           cudaMemcpyDeviceToHost, h->s0));
     if (P.slow)
       CU(h, cudaMemcpyAsync(h->h_ucount, h->ucount, g.S * sizeof(uint32_t),
@@ -972,7 +977,8 @@ bool graphs_enabled() {
 }
 
 int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int dtype,
-                double* out, ttkv_step_report* rep, bool host_io = false) {
+                double* out, ttkv_step_report* rep, bool host_io = false,
+                const void* const* host = nullptr) {
   StepTimer step_timer(h);
   {  // grow before selecting so a settle-time eviction never reallocates
     int rc0 = ensure_blocks(h, h->n_slow + 1);
@@ -990,6 +996,12 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
   P.dtype = dtype;
   P.out = out;
   P.host_io = host_io;
+  if (host_io) {
+    P.hq = host[0];
+    P.hk = host[1];
+    P.hv = host[2];
+    P.hout = const_cast<void*>(host[3]);
+  }
   P.F = pos + 1 - h->fast_front;
   P.n = h->n_slow;
   {
@@ -1123,6 +1135,8 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
     key.CH = P.CH;
     key.dtype = (uint32_t)dtype;
     key.host_io = host_io ? 1u : 0u;
+    if (host_io)
+      for (int i = 0; i < 4; ++i) key.host[i] = host[i];
     ttkv_gpu::StepGraph* hit = nullptr;
     for (auto& sg : h->graphs)
       if (std::memcmp(&key, &sg.key, sizeof(key)) == 0) hit = &sg;
@@ -1592,6 +1606,18 @@ int ttkv_gpu_decode_step_device(ttkv_gpu* h, const float* q, const void* kn, con
   return decode_core(h, q, kn, vn, dtype == TTKV_DTYPE_F16 ? kInF16 : kInF32, out, rep);
 }
 
+namespace {
+// Page-locked (cudaHostAlloc'd or registered) host memory?
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+}  // namespace
+
 int ttkv_gpu_decode_step(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int dtype,
                          double* out, ttkv_step_report* rep) {
   if (!h) return set_err(nullptr, TTKV_EINVAL, "null handle");
@@ -1603,15 +1629,20 @@ int ttkv_gpu_decode_step(ttkv_gpu* h, const float* q, const void* kn, const void
   const size_t esz = dtype == TTKV_DTYPE_F16 ? 2 : 4;
   const size_t qb = (size_t)g.S * g.G * g.d_k * 4, ob = (size_t)g.S * g.G * g.d_v * 8;
   const size_t kb = (size_t)g.S * g.d_k * esz, vb = (size_t)g.S * g.d_v * esz;
-  std::memcpy(h->h_q, q, qb);
-  std::memcpy(h->h_k, kn, kb);
-  std::memcpy(h->h_v, vn, vb);
+  // The caller's page-locked buffers are DMA'd directly; pageable ones go
+  // through the handle's pinned staging copies (one host memcpy each way).
+  const void* host[4];
+  host[0] = host_pinned(q) ? static_cast<const void*>(q) : (std::memcpy(h->h_q, q, qb), h->h_q);
+  host[1] = host_pinned(kn) ? kn : (std::memcpy(h->h_k, kn, kb), h->h_k);
+  host[2] = host_pinned(vn) ? vn : (std::memcpy(h->h_v, vn, vb), h->h_v);
+  const bool out_direct = host_pinned(out);
+  host[3] = out_direct ? static_cast<const void*>(out) : h->h_out;
   // the H2D of q/k/v and the D2H of the output are part of the (captured) step
   int rc = decode_core(h, h->q_dev, h->kn_dev, h->vn_dev,
-                       dtype == TTKV_DTYPE_F16 ? kInF16 : kInF32, h->out_dev, rep, true);
+                       dtype == TTKV_DTYPE_F16 ? kInF16 : kInF32, h->out_dev, rep, true, host);
   if (rc) return rc;
   CU(h, cudaStreamSynchronize(h->s0));
-  std::memcpy(out, h->h_out, ob);
+  if (!out_direct) std::memcpy(out, h->h_out, ob);
   if (rep) {
     uint64_t u = 0;
     if (h->last_k)

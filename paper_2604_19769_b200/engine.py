@@ -239,8 +239,12 @@ class MultiStreamEngine:
     def prefill_synthetic(self, n_tokens: int, seed: int = 0):
         _check(self._lib.ttkv_gpu_prefill_synthetic(self._h, n_tokens, seed), self._h)
 
-    def decode_step(self, query, key, value, fetched=False) -> DecodeStepReport:
-        """query [S, G, d_k], key [S, d_k], value [S, d_v] -> output [S, G, d_v]."""
+    def decode_step(self, query, key, value, fetched=False, out=None) -> DecodeStepReport:
+        """query [S, G, d_k], key [S, d_k], value [S, d_v] -> output [S, G, d_v].
+        `out` (optional): a C-contiguous float64 [S, G, d_v] array the output is
+        written to.  Page-locked inputs / `out` (e.g. numpy views of
+        torch.empty(..., pin_memory=True)) are DMA'd directly; pageable ones
+        go through the handle's pinned staging buffers."""
         q = _f32(query).reshape(-1)
         k, dt = _kv(key)
         v, _ = _kv(value)
@@ -250,7 +254,11 @@ class MultiStreamEngine:
             raise ShapeError("decode_step: query dimension mismatch")
         if k.size != self.S * self.config.d_k or v.size != self.S * self.config.d_v:
             raise ShapeError("append_token: key/value dimension mismatch")
-        out = np.empty((self.S, self.G, self.config.d_v), np.float64)  # fully written by the call
+        shape = (self.S, self.G, self.config.d_v)
+        if out is None:
+            out = np.empty(shape, np.float64)  # fully written by the call
+        elif out.dtype != np.float64 or out.shape != shape or not out.flags.c_contiguous:
+            raise ShapeError("decode_step: out must be a C-contiguous float64 [S, G, d_v] array")
         rep = L.StepReportC()
         _check(self._lib.ttkv_gpu_decode_step(self._h, _ptr(q), _ptr(k), _ptr(v), dt, _ptr(out),
                                               C.byref(rep)), self._h)
