@@ -592,6 +592,15 @@ def run_ours(args):
 
     for i in range(args.warmup):
         step(i)
+        if i == 0 and pg is not None:
+            # the fused peer-memory gather must reproduce the collective before
+            # it is timed; otherwise every rank falls back to NCCL together
+            ok, why = pg.verify(out)
+            if not ok:
+                pg.close()
+                pg = None
+                gather_kind = f"NCCL all_gather (peer gather self-check failed: {why})"
+                print(gather_kind, file=sys.stderr, flush=True)
     barrier()
     if not args.steps_given:
         # default K: at least 10 steps and >= ~1 s of timed region (clock samples)

@@ -182,6 +182,29 @@ class PeerGather:
             raise Error("peer gather: a rank did not deliver its rows")
         return self._view(p.value).cpu().numpy()
 
+    def verify(self, local_out, group=None) -> tuple:
+        """Self-check after a decode step, on every rank together: the rows
+        the combine kernels stored over peer memory equal an NCCL (or gloo)
+        all-gather of this rank's own output (`local_out`, [S_local][G][d_v]).
+        Returns (ok, reason), identical on every rank."""
+        import torch.distributed as dist
+        try:
+            peer = self.host()
+            ref = gather_outputs(local_out, self.plan, group).cpu().numpy()
+            mine = (bool(self._np.array_equal(peer, ref)), "" if self._np.array_equal(peer, ref)
+                    else "gathered rows differ from the collective's")
+        except Exception as e:  # noqa: BLE001 -- a rank that timed out or failed
+            mine = (False, repr(e))
+        res = [None] * self.plan.world
+        dist.all_gather_object(res, mine, group=group)
+        bad = [f"rank {r}: {why}" for r, (ok, why) in enumerate(res) if not ok]
+        return (not bad, "; ".join(bad))
+
+    def close(self):
+        """Stop storing rows into the peers (the combine writes locally only)."""
+        from .engine import _check
+        _check(self.engine._lib.ttkv_gpu_peer_gather_close(self.engine.handle), self.engine.handle)
+
     def tensor(self):
         """Zero-copy torch view of the last step's gathered rows on the device."""
         return self._view(self.device_ptr())
