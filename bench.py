@@ -596,7 +596,9 @@ def run_ours(args):
             # the fused peer-memory gather must reproduce the collective before
             # it is timed; otherwise every rank falls back to NCCL together
             ok, why = pg.verify(out)
-            if not ok:
+            if ok:
+                gather_kind += "; first step bit-identical to the collective's all-gather"
+            else:
                 pg.close()
                 pg = None
                 gather_kind = f"NCCL all_gather (peer gather self-check failed: {why})"
