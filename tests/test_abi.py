@@ -89,6 +89,8 @@ def test_gpu_limits_are_config_errors():
         T.MultiStreamEngine(T.TierConfig(hbm_budget_bytes=1 << 24), ring_bytes=3)
     with pytest.raises(T.ConfigError):
         T.MultiStreamEngine(T.TierConfig(hbm_budget_bytes=1 << 20), heads_per_stream=9)
+    with pytest.raises(T.ConfigError, match="record_stream"):
+        T.MultiStreamEngine(T.TierConfig(hbm_budget_bytes=1 << 20), record_stream=3)
 
 
 def test_null_handle_is_an_error():
