@@ -1143,6 +1143,522 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, 3)
   pdl_trigger();
 }
 
+// ---------------------------------------------------------------------------
+// slow tier on 5th-generation tensor cores (tcgen05.mma.kind::i8, TMEM
+// accumulators): the same record stream, schedule and partials as
+// slow_attn_tc_kernel, with both products as exact integer MMAs.
+//   QK: D[tok][n] = sum_c code_K[tok][c] * X[n][c], where X is q * s of head
+//       h scaled by 2^k_h (k_h from the head's max |q s| of this record) and
+//       written as three balanced base-256 s8 digit planes (n = 4 plane + h):
+//       the TMA-loaded u8 codes ARE the A operand (K-major, 128B swizzle), no
+//       conversion instruction touches them.  S = (D2 2^16 + D1 2^8 + D0) 2^-k
+//       + q . z is exact up to the 2^-22 (relative to the head's max) of X.
+//   PV: D[ch][4h + j] = sum_tok code_V[tok][ch] * byte_j(Y_h[tok]), Y = p 2^22
+//       (< 2^22): the bytes of Y are its base-256 digits, so a token's B row
+//       (MN-major, no swizzle) is just its heads' Y words -- one 16-byte store;
+//       the V nibbles are expanded to u8 over the record's consumed K codes
+//       (MN-major, 128B swizzle).  O = s (D0 + 2^8 D1 + 2^16 D2) 2^-22 +
+//       z sum(Y) 2^-22.
+// Opt-in (TTKV_SLOW_TC5=1): parity-green with a smaller output error than the
+// mma.sync kernel (2.0e-6 vs 4.2e-6, tools/err_probe.py), but slower at cfg2
+// (ncu 1.07 vs 0.95 ms per launch): the QK conversions it removes were never
+// the bound -- the V nibble expansion, the per-token softmax of every head
+// and three CTA barriers per record are.
+// One elected consumer thread issues the MMAs (4 per product, K = 32) and
+// commits them to an mbarrier; TMEM lanes are tokens (QK) or channels (PV),
+// so each consumer thread reads its own token's scores / channel's outputs
+// for every head with one tcgen05.ld.
+// ---------------------------------------------------------------------------
+namespace {
+__device__ __forceinline__ uint32_t sw128(uint32_t row, uint32_t byte) {  // SW128 tile offset
+  return row * 128 + ((((byte >> 4) ^ (row & 7)) << 4) | (byte & 15));
+}
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ uint64_t umma_desc_none(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100); SWIZZLE_NONE
+  return d;
+}
+// kind::i8 instruction descriptor: D s32, A u8, B s8 / u8, majors, N, M = 128
+__host__ __device__ constexpr uint32_t umma_idesc_i8(uint32_t N, uint32_t a_mn, uint32_t b_s8,
+                                                     uint32_t b_mn) {
+  return (2u << 4) | (0u << 7) | (b_s8 << 10) | (a_mn << 15) | (b_mn << 16) | ((N >> 3) << 17) |
+         ((128u >> 4) << 24);
+}
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void proxy_fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+template <int NC>
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&r)[NC]);
+template <>
+__device__ __forceinline__ void tmem_ld32<16>(uint32_t taddr, int32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+template <>
+__device__ __forceinline__ void tmem_ld32<32>(uint32_t taddr, int32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// balanced base-256 digits of |x| < 2^22: x = d2 2^16 + d1 2^8 + d0, d in [-128, 127]
+__device__ __forceinline__ void digits3(int32_t x, int32_t& d0, int32_t& d1, int32_t& d2) {
+  d0 = ((x + 128) & 255) - 128;
+  const int32_t x1 = (x - d0) >> 8;
+  d1 = ((x1 + 128) & 255) - 128;
+  d2 = (x1 - d1) >> 8;
+}
+__device__ __forceinline__ uint32_t pack4(int32_t a, int32_t b, int32_t c, int32_t d) {
+  return (uint32_t)(a & 255) | ((uint32_t)(b & 255) << 8) | ((uint32_t)(c & 255) << 16) |
+         ((uint32_t)d << 24);
+}
+__device__ __forceinline__ float combine3(int32_t d0, int32_t d1, int32_t d2) {
+  return fmaf((float)d2, 65536.0f, fmaf((float)d1, 256.0f, (float)d0));
+}
+template <int GT>
+constexpr uint32_t tc5_npad() { return GT <= 4 ? 16u : 32u; }
+template <int GT>
+constexpr size_t tc5_smem_bytes() {
+  // stages | Bq [NPAD][128] | Bp [NPAD][128] | per head and warp: block max,
+  // block sum, sum Y | per head: score unscale, beta | barriers, TMEM slot
+  return 1024 + 2 * (size_t)kSlowStage + 2 * (size_t)tc5_npad<GT>() * 128 +
+         (size_t)(3 * 32 + 16) * 4 + 6 * 8 + 16;
+}
+}  // namespace
+
+template <int GT>
+__global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, GT <= 4 ? 3 : 2)
+    slow_attn_tc5_kernel(const __grid_constant__ SlowTcArgs a) {
+  constexpr int ST = 2;
+  constexpr uint32_t NPAD = tc5_npad<GT>();
+  constexpr int PL = GT > 4 ? 8 : 4;  // digit plane pl of head h is row PL pl + h
+  pdl_wait();  // the union lists (launched chained behind the selection)
+  const Geometry& g = a.g;
+  const uint32_t G = g.G;
+  const uint32_t c = blockIdx.x;
+  // ---- balanced schedule (as slow_attn_tc_kernel) ----
+  __shared__ uint32_t sched[4];
+  __shared__ uint32_t scan_w[8];
+  {
+    const uint32_t T = blockDim.x, t = threadIdx.x;
+    const uint32_t sb = (uint32_t)(((uint64_t)g.S * t) / T), se = (uint32_t)(((uint64_t)g.S * (t + 1)) / T);
+    uint32_t mine = 0;
+    for (uint32_t x = sb; x < se; ++x) mine += a.union_count[x];
+    uint32_t incl = mine;
+    const uint32_t ln = t & 31, wp = t >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (ln >= (uint32_t)o) incl += v;
+    }
+    if (ln == 31) scan_w[wp] = incl;
+    __syncthreads();
+    uint32_t before = 0, R = 0;
+    for (uint32_t w = 0; w < (T + 31) / 32; ++w) {
+      before += w < wp ? scan_w[w] : 0u;
+      R += scan_w[w];
+    }
+    const uint32_t excl = before + incl - mine;
+    const uint32_t per = max((R + gridDim.x - 1) / gridDim.x, a.per_min);
+    const uint64_t lo = (uint64_t)c * per;
+    if (t == 0) sched[2] = lo < R ? (uint32_t)(R - lo < per ? R - lo : per) : 0u;
+    if (lo < R && excl <= lo && lo < excl + mine) {
+      uint32_t off = excl, x = sb;
+      while (off + a.union_count[x] <= lo) off += a.union_count[x++];
+      sched[0] = x;
+      sched[1] = (uint32_t)(lo - off);
+      sched[3] = c - off / per;
+    }
+    __syncthreads();
+  }
+  const uint32_t n_rec = sched[2];
+  if (n_rec == 0) return;
+  const uint32_t s_first = sched[0], i_first = sched[1], slot_first = sched[3];
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sBq = base + ST * kSlowStage;          // [NPAD][128] s8, SW128
+  uint8_t* sBp = sBq + NPAD * 128;                // [NPAD/16][128 tok][16] u8, MN-major
+  float* redm = reinterpret_cast<float*>(sBp + NPAD * 128);  // [8 heads][4 warps] block max
+  float* reds = redm + 32;                                   // [8 heads][4 warps] block sum
+  int32_t* redy = reinterpret_cast<int32_t*>(reds + 32);     // [8 heads][4 warps] sum Y
+  float* kun = reinterpret_cast<float*>(redy + 32);      // [8] per-head score unscale 2^-k
+  float* bst = kun + 8;                                   // [8] beta = q . z
+  uint64_t* full = reinterpret_cast<uint64_t*>(bst + 8);
+  uint64_t* empty = full + ST;
+  uint64_t* bar_qk = empty + ST;
+  uint64_t* bar_pv = bar_qk + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_pv + 1);
+  __shared__ uint32_t hms[ST];
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kSlowConsumerWarps);
+    }
+    mbar_init(bar_qk, 1);
+    mbar_init(bar_pv, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {  // TMEM: D_qk in columns [0, NPAD), D_pv in [NPAD, 2 NPAD)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(2 * NPAD));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // QK digit-plane rows past the heads stay zero
+  for (uint32_t i = threadIdx.x; i < NPAD * 128 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(sBq)[i] = make_uint4(0, 0, 0, 0);
+  proxy_fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {  // producer: the records into the stages (TMA), as slow_attn_tc_kernel
+    if (lane == 0) {
+      const uint64_t evict_first = l2_evict_first_policy();
+      uint32_t s = s_first, ii = i_first, cnt = a.union_count[s];
+      for (uint32_t i = 0; i < n_rec; ++i, ++ii) {
+        while (ii >= cnt) {
+          ii = 0;
+          cnt = a.union_count[++s];
+        }
+        const uint32_t st = i % ST;
+        if (i >= ST) mbar_wait_sleep(&empty[st], ((i / ST) - 1) & 1);
+        const uint64_t at = (uint64_t)s * g.n_cap + ii;
+        const int rec = (int)((uint64_t)s * g.n_cap + a.union_ids[at]);
+        uint8_t* dst = base + st * kSlowStage;
+        hms[st] = a.union_mask[at];
+        mbar_arrive_expect_tx(&full[st], kSlowStage);
+        tma_load_3d(dst, &a.tk, 0, 0, rec, &full[st], evict_first);
+        tma_load_3d(dst + kKBox, &a.tv, 0, 0, rec, &full[st], evict_first);
+        bulk_g2s(dst + kKBox + kVBox, a.params + (uint64_t)rec * kPBytes, kPBytes, &full[st]);
+      }
+    }
+    return;
+  }
+
+  // Consumers, software-pipelined over the CTA's records: iteration j runs
+  //   B(j): scores, softmax, P words, V(j) expanded over its consumed K codes,
+  //         PV(j) issued;
+  //   A(j+1): q * s digit planes of the next record, QK(j+1) issued;
+  //   C(j): PV(j) read back, the online-softmax update;
+  // so each MMA's latency hides behind the other record's ALU phase.  One
+  // Bq / Bp tile and one TMEM accumulator per product suffice: each is
+  // rewritten only after the MMA that read it was waited on.
+  const int nthreads_c = kSlowConsumerWarps * 32;
+  const uint32_t ct = threadIdx.x - 32;
+  const uint32_t cw = warp - 1;
+  const uint32_t tq = (warp & 3) * 32;    // TMEM lane quarter this warp may access
+  const uint32_t my_row = tq + lane;      // the token / channel this thread reads from TMEM
+  const float sl = (float)a.scale_log2;
+  const uint32_t iq = umma_idesc_i8(NPAD, 0, 1, 0), ip = umma_idesc_i8(NPAD, 1, 0, 1);
+
+  // record cursors: stream / index within the stream's union of record j (c*)
+  // and of record j + 1 (n*)
+  uint32_t cs = s_first, cii = i_first, ccnt = a.union_count[s_first];
+  auto stage_qk = [&](uint32_t j, uint32_t sj) {  // A(j): digit planes, then QK(j)
+    const uint32_t st = j % ST;
+    mbar_wait(&full[st], (j / ST) & 1);
+    uint8_t* stg = base + st * kSlowStage;
+    const float* kp = reinterpret_cast<const float*>(stg + kKBox + kVBox);  // {s,z} x 128
+    const float* qb = a.q + (uint64_t)sj * G * 128;
+#pragma unroll
+    for (int rep = 0; rep < (GT + 3) / 4; ++rep) {
+      const uint32_t h = cw + 4 * rep;
+      if (h < G) {  // warp-uniform head h, lane = channel quad
+        const uint32_t c4 = 4 * lane;
+        float4 qv = __ldg(reinterpret_cast<const float4*>(qb + h * 128 + c4));
+        qv.x *= sl; qv.y *= sl; qv.z *= sl; qv.w *= sl;  // log2 units
+        const float4 sz0 = *reinterpret_cast<const float4*>(kp + 2 * c4);
+        const float4 sz1 = *reinterpret_cast<const float4*>(kp + 2 * c4 + 4);
+        const float x0 = qv.x * sz0.x, x1 = qv.y * sz0.z, x2 = qv.z * sz1.x, x3 = qv.w * sz1.z;
+        const float mx = warp_max_redux(fmaxf(fmaxf(fabsf(x0), fabsf(x1)), fmaxf(fabsf(x2), fabsf(x3))));
+        // 2^k with max |x| 2^k < 2^22 (three balanced digits hold |X| < 2^22)
+        const int ex = mx > 0.f ? (int)((__float_as_uint(mx) >> 23) & 0xffu) - 127 : 0;
+        const int k = max(-120, min(120, 21 - ex));
+        const float up = __uint_as_float((uint32_t)(127 + k) << 23);
+        int32_t d[4][3];
+        const float xs[4] = {x0, x1, x2, x3};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) digits3(__float2int_rn(xs[e] * up), d[e][0], d[e][1], d[e][2]);
+#pragma unroll
+        for (int pl = 0; pl < 3; ++pl)
+          *reinterpret_cast<uint32_t*>(sBq + sw128(PL * pl + h, c4)) =
+              pack4(d[0][pl], d[1][pl], d[2][pl], d[3][pl]);
+        const float beta = warp_sum(qv.x * sz0.y + qv.y * sz0.w + qv.z * sz1.y + qv.w * sz1.w);
+        if (lane == 0) {
+          kun[h] = __uint_as_float((uint32_t)(127 - k) << 23);
+          bst[h] = beta;
+        }
+      }
+    }
+    proxy_fence_async_smem();
+    tc_fence_before();
+    named_bar(1, nthreads_c);
+    if (ct == 0) {  // D_qk[tok][n] = K[tok][.] . Bq[n][.]
+      tc_fence_after();
+      const uint32_t ka = smem_u32(stg), kb = smem_u32(sBq);
+#pragma unroll
+      for (uint32_t kk = 0; kk < 4; ++kk)
+        umma_i8(tmem, umma_desc_sw128(ka + 32 * kk, 16, 1024),
+                umma_desc_sw128(kb + 32 * kk, 16, 1024), iq, kk);
+      umma_commit(bar_qk);
+    }
+  };
+
+  float m_run[GT], l_run[GT], acc[GT];
+#pragma unroll
+  for (int h = 0; h < GT; ++h) {
+    m_run[h] = -INFINITY;
+    l_run[h] = 0.f;
+    acc[h] = 0.f;
+  }
+  uint32_t seen = 0, slot = slot_first;
+  while (cii >= ccnt) {  // (the schedule starts at a record, so this never loops)
+    cii = 0;
+    ccnt = a.union_count[++cs];
+  }
+  stage_qk(0, cs);
+  for (uint32_t j = 0; j < n_rec; ++j) {
+    const uint32_t st = j % ST;
+    uint8_t* stg = base + st * kSlowStage;
+    const uint8_t* vn = stg + kKBox;
+    const float* vp = reinterpret_cast<const float*>(stg + kKBox + kVBox) + 2 * 128;
+    const uint32_t hm = hms[st];
+    seen |= hm;
+    const float2 vsz = *reinterpret_cast<const float2*>(vp + 2 * my_row);  // V params of channel my_row
+
+    // ---- B(j): scores of token my_row, all heads ----
+    mbar_wait(bar_qk, j & 1);
+    tc_fence_after();
+    int32_t dq[NPAD];
+    tmem_ld32<NPAD>(tmem + (tq << 16), dq);
+    tmem_ld_wait();
+    float sc[GT];
+#pragma unroll
+    for (int h = 0; h < GT; ++h) {
+      sc[h] = -INFINITY;
+      if (h < (int)G && ((hm >> h) & 1u))
+        sc[h] = fmaf(combine3(dq[h], dq[PL + h], dq[2 * PL + h]), kun[h], bst[h]);
+    }
+#pragma unroll
+    for (int h = 0; h < GT; ++h) {
+      const float bm = warp_max_redux(sc[h]);
+      if (lane == 0) redm[h * 4 + cw] = bm;
+    }
+    named_bar(1, nthreads_c);
+    float p[GT], alpha[GT], mnew[GT];
+#pragma unroll
+    for (int h = 0; h < GT; ++h) {
+      const float4 b4 = *reinterpret_cast<const float4*>(redm + 4 * h);
+      const float bm = fmaxf(fmaxf(b4.x, b4.y), fmaxf(b4.z, b4.w));
+      const bool on = h < (int)G && ((hm >> h) & 1u);
+      mnew[h] = a.literal ? bm : fmaxf(m_run[h], bm);
+      p[h] = on ? exp2f(sc[h] - mnew[h]) : 0.f;
+      alpha[h] = on ? (a.literal ? 1.f : exp2f(m_run[h] - mnew[h])) : 1.f;
+    }
+    if (a.literal) {  // each block its own normalized partition (engine.cpp:67-72)
+#pragma unroll
+      for (int h = 0; h < GT; ++h) {
+        const float sm = warp_sum(p[h]);
+        if (lane == 0) reds[h * 4 + cw] = sm;
+      }
+      named_bar(1, nthreads_c);
+#pragma unroll
+      for (int h = 0; h < GT; ++h) {
+        const float4 t4 = *reinterpret_cast<const float4*>(reds + 4 * h);
+        const float tot = (t4.x + t4.y) + (t4.z + t4.w);
+        if (p[h] > 0.f) p[h] = p[h] / tot;
+      }
+    }
+    // P as Y = p 2^22 (clamped below 2^22): the bytes of Y are its base-256
+    // digits, so token my_row's B row is its heads' Y words
+    uint32_t yw[GT];
+#pragma unroll
+    for (int h = 0; h < GT; ++h) {
+      yw[h] = min((uint32_t)__float2uint_rn(p[h] * 4194304.0f), 4194303u);
+      const uint32_t ys = __reduce_add_sync(0xffffffffu, yw[h]);
+      if (lane == 0) redy[h * 4 + cw] = (int32_t)ys;
+    }
+#pragma unroll
+    for (int grp = 0; grp < GT / 4 + (GT < 4 ? 1 : 0); ++grp) {
+      uint32_t y4[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) y4[e] = 4 * grp + e < GT ? yw[(4 * grp + e) % GT] : 0u;
+      *reinterpret_cast<uint4*>(sBp + grp * 2048 + my_row * 16) = make_uint4(y4[0], y4[1], y4[2], y4[3]);
+    }
+    // V nibbles of token ct -> u8 row ct over the consumed K codes (MN-major
+    // A of PV: [token][channel], 128B swizzle)
+    {
+      const uint32_t t = ct;
+      uint32_t w[16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 u = *reinterpret_cast<const uint4*>(vn + t * 64 + ((q ^ ((t >> 1) & 3)) << 4));
+        w[4 * q] = u.x; w[4 * q + 1] = u.y; w[4 * q + 2] = u.z; w[4 * q + 3] = u.w;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {  // 16-byte chunk q = channels 16q .. 16q + 15
+        uint32_t o[4];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const uint32_t x = w[2 * q + e];
+          const uint32_t lo = x & 0x0F0F0F0Fu, hi = (x >> 4) & 0x0F0F0F0Fu;
+          o[2 * e] = __byte_perm(lo, hi, 0x5140);
+          o[2 * e + 1] = __byte_perm(lo, hi, 0x7362);
+        }
+        *reinterpret_cast<uint4*>(stg + sw128(t, 16 * q)) = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+    }
+    proxy_fence_async_smem();
+    tc_fence_before();
+    named_bar(1, nthreads_c);
+    float lblk[GT];
+#pragma unroll
+    for (int h = 0; h < GT; ++h) {
+      const int4 y4 = *reinterpret_cast<const int4*>(redy + 4 * h);
+      lblk[h] = (float)((y4.x + y4.y) + (y4.z + y4.w)) * (1.0f / 4194304.0f);
+    }
+    if (ct == 0) {  // D_pv[ch][n] = Vx[.][ch] . Bp[n][.]
+      tc_fence_after();
+      const uint32_t va = smem_u32(stg), pb = smem_u32(sBp);
+#pragma unroll
+      for (uint32_t kk = 0; kk < 4; ++kk)
+        umma_i8(tmem + NPAD, umma_desc_sw128(va + 4096 * kk, 16384, 1024),
+                umma_desc_none(pb + 512 * kk, 128, 2048), ip, kk);
+      umma_commit(bar_pv);
+    }
+
+    // ---- A(j+1): the next record's QK, hidden behind PV(j) ----
+    const bool stream_end = cii + 1 >= ccnt;  // the stream's union ends at record j
+    const bool seg_end = stream_end || j + 1 == n_rec;
+    const uint32_t s_this = cs;
+    if (j + 1 < n_rec) {
+      uint32_t ns = cs, nii = cii + 1, ncnt = ccnt;
+      while (nii >= ncnt) {
+        nii = 0;
+        ncnt = a.union_count[++ns];
+      }
+      stage_qk(j + 1, ns);
+      cs = ns;
+      cii = nii;
+      ccnt = ncnt;
+    }
+
+    // ---- C(j): PV(j) read back, online-softmax update ----
+    mbar_wait(bar_pv, j & 1);
+    tc_fence_after();
+    int32_t dp[NPAD];
+    tmem_ld32<NPAD>(tmem + (tq << 16) + NPAD, dp);
+    tmem_ld_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);  // the stage (Vx over K, params) is consumed
+    const float vs = vsz.x * (1.0f / 4194304.0f), vz = vsz.y;
+#pragma unroll
+    for (int h = 0; h < GT; ++h) {
+      if (!(h < (int)G && ((hm >> h) & 1u))) continue;
+      const float o = combine3(dp[4 * h], dp[4 * h + 1], dp[4 * h + 2]);
+      acc[h] = fmaf(acc[h], alpha[h], fmaf(vs, o, vz * lblk[h]));
+      if (a.literal) {
+        l_run[h] = 1.f;
+      } else {
+        l_run[h] = fmaf(l_run[h], alpha[h], lblk[h]);
+        m_run[h] = mnew[h];
+      }
+    }
+
+    if (seg_end) {  // emit the (acc, m, l) partial of every head of stream s_this
+      const uint32_t pitch = 128 + 2;
+#pragma unroll
+      for (int h = 0; h < GT; ++h) {
+        if (h >= (int)G) continue;
+        float* pp = reinterpret_cast<float*>(a.part) + (((uint64_t)s_this * G + h) * a.nsc + slot) * pitch;
+        const bool any = (seen >> h) & 1u;
+        pp[my_row] = any ? acc[h] : 0.f;
+        if (ct == 0) {
+          pp[128] = any ? (a.literal ? 0.f : m_run[h]) : -INFINITY;
+          pp[129] = any ? (a.literal ? 1.f : l_run[h]) : 0.f;
+        }
+        m_run[h] = -INFINITY;
+        l_run[h] = 0.f;
+        acc[h] = 0.f;
+      }
+      // the stream's last record is here (its union ends at this CTA)
+      if (ct == 0 && stream_end) a.nslots[s_this] = slot + 1;
+      seen = 0;
+      slot = 0;
+    }
+  }
+  tc_fence_before();
+  named_bar(1, nthreads_c);
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * NPAD));
+  }
+  pdl_trigger();
+}
+
+template <int GT>
+static cudaError_t launch_slow_tc5_t(const SlowTcArgs& a, uint32_t grid_ctas, cudaStream_t st) {
+  const size_t smem = tc5_smem_bytes<GT>();
+  auto kern = slow_attn_tc5_kernel<GT>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return launch_chained(kern, dim3(grid_ctas), dim3(32 + kSlowConsumerWarps * 32), smem, st, a);
+}
+
+static cudaError_t launch_slow_tc5(const SlowTcArgs& a, uint32_t grid_ctas, cudaStream_t st) {
+  if (a.g.G <= 1) return launch_slow_tc5_t<1>(a, grid_ctas, st);
+  if (a.g.G <= 2) return launch_slow_tc5_t<2>(a, grid_ctas, st);
+  if (a.g.G <= 4) return launch_slow_tc5_t<4>(a, grid_ctas, st);
+  return launch_slow_tc5_t<8>(a, grid_ctas, st);
+}
+
 bool slow_tc_supported(const Geometry& g) {
   return g.elem == 2 && g.d_k == 128 && g.d_v == 128 && g.B == 128 && g.kb == 8 && g.vb == 4 &&
          g.G <= 8 && g.rec.kp_off == kKBox + kVBox && g.rec.used == kSlowStage;
@@ -1155,7 +1671,19 @@ static int slow_tc_stages() {
   return (e && e[0] == '3') ? 3 : 2;
 }
 
-uint32_t slow_tc_ctas_per_sm() { return slow_tc_stages() == 3 ? 2u : 3u; }
+// TTKV_SLOW_TC5=0: the mma.sync kernel instead of the tcgen05 one (measurement)
+static bool slow_tc5_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TTKV_SLOW_TC5");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+uint32_t slow_tc_ctas_per_sm(const Geometry& g) {
+  if (slow_tc5_enabled()) return g.G <= 4 ? 3u : 2u;
+  return slow_tc_stages() == 3 ? 2u : 3u;
+}
 
 template <int GT, int ST>
 static size_t slow_tc_smem() {
@@ -1182,6 +1710,7 @@ static cudaError_t launch_slow_tc_s(const SlowTcArgs& a, uint32_t grid_ctas, cud
 
 cudaError_t launch_slow_tc(const SlowTcArgs& a, uint32_t grid_ctas, cudaStream_t st) {
   if (grid_ctas == 0) return cudaSuccess;
+  if (slow_tc5_enabled()) return launch_slow_tc5(a, grid_ctas, st);
   static const int stages = slow_tc_stages();
   return stages == 2 ? launch_slow_tc_s<2>(a, grid_ctas, st)
                      : launch_slow_tc_s<3>(a, grid_ctas, st);

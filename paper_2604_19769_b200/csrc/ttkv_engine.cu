@@ -1063,7 +1063,7 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       // into ONE wave of resident CTAs (layer-sequential cfg2, S = 8: 308 ->
       // 379 tok/s vs 4-record chunks; a second partial wave costs ~15 %)
       const uint64_t ub = (uint64_t)g.S * std::min<uint64_t>(P.n, (uint64_t)g.Gs * P.k);
-      const uint64_t slots = (uint64_t)h->sms * slow_tc_ctas_per_sm();
+      const uint64_t slots = (uint64_t)h->sms * slow_tc_ctas_per_sm(g);
       P.CH = (uint32_t)std::min<uint64_t>(64, std::max<uint64_t>(4, (ub + slots - 1) / slots));
     } else {
       // host records: union entries per CTA ~4 waves of 2 CTAs/SM over the
@@ -1082,7 +1082,7 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       // balanced schedule over one wave of CTAs; a stream's records span at
       // most nsc CTAs when every CTA takes >= n / (nsc - 1) records, so nsc
       // is as large as ~32 MB of partials allows (small S: every CTA a share)
-      const uint64_t ctas = (uint64_t)h->sms * slow_tc_ctas_per_sm();
+      const uint64_t ctas = (uint64_t)h->sms * slow_tc_ctas_per_sm(g);
       const uint64_t row = (uint64_t)g.S * g.G * (g.d_v + 2) * h->acc;
       nsc = std::min<uint64_t>(ctas + 1, std::max<uint64_t>(P.grid_chunks + 1, (32ull << 20) / row));
       nsc = std::max<uint64_t>(nsc, 2);
@@ -1095,10 +1095,11 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
     if (P.spec) {  // one wave of resident CTAs fed from the record queue
       rc = ensure_rpart(h);
       if (rc) return rc;
-      static const uint32_t cps = [] {  // TTKV_SPEC_CPS=n: CTAs per SM (measurement)
+      static const uint32_t cps_env = [] {  // TTKV_SPEC_CPS=n: CTAs per SM (measurement)
         const char* e = std::getenv("TTKV_SPEC_CPS");
-        return e ? (uint32_t)std::max(1, std::min(3, std::atoi(e))) : slow_tc_ctas_per_sm();
+        return e ? (uint32_t)std::max(1, std::min(3, std::atoi(e))) : 0u;
       }();
+      const uint32_t cps = cps_env ? cps_env : slow_tc_ctas_per_sm(g);
       P.grid_chunks = (uint64_t)h->sms * cps;
     }
   }

@@ -191,7 +191,7 @@ constexpr uint32_t kSpecPitch = 132;
 bool slow_tc_spec_supported(const Geometry& g);  // K8/V4, d = B = 128, G <= 4
 // grid: one wave of resident CTAs; records come from the *spec_ctr queue
 cudaError_t launch_slow_tc_spec(const SlowTcArgs& a, uint32_t grid_ctas, cudaStream_t st);
-uint32_t slow_tc_ctas_per_sm();  // resident CTAs per SM of the slow tensor-core kernel
+uint32_t slow_tc_ctas_per_sm(const Geometry& g);  // resident CTAs per SM of the slow tensor-core kernel
 // Largest |key scale| the tensor-core slow kernel accepts: records quantized
 // from an fp16 ring have s = (max - min) / 255 <= 2 * 65504 / 255 < 514, and
 // the kernel normalizes q by a power of two against this bound so that the
