@@ -19,6 +19,7 @@ done
 $B --layer-sequential --slow-tier device --no-cpu-baseline 2>> $O/bench.err | tail -1 > $O/bench_cfg2_layer_sequential_hbm.json
 TTKV_SPEC=1 $B --layer-sequential --slow-tier device --no-cpu-baseline 2>> $O/bench.err | tail -1 > $O/bench_cfg2_layer_sequential_hbm_spec.json
 $B --layer-sequential --no-cpu-baseline 2>> $O/bench.err | tail -1 > $O/bench_cfg2_layer_sequential.json
+TTKV_SLOW_TC5=1 $B --slow-tier device --no-cpu-baseline 2>> $O/bench.err | tail -1 > $O/bench_cfg2_hbm_tcgen05.json
 TTKV_SHARE_DEVICE=1 TTKV_DIST_BACKEND=gloo $B --gpus 2 --no-cpu-baseline 2>> $O/bench.err | tail -1 > $O/bench_n2_shared_device_gloo.json
 timeout 900 python bench.py --workload cfg5 --no-cpu-baseline > $O/bench_cfg5.json 2>> $O/bench.err
 echo done
