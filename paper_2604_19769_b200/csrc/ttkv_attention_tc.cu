@@ -70,6 +70,13 @@ __device__ __forceinline__ float pow2_normalizer(float m, int extra, float* unsc
   *unscale = __uint_as_float((uint32_t)(127 + extra + k) << 23);
   return __uint_as_float((uint32_t)(127 - k) << 23);
 }
+// 2^x in one MUFU.EX2 (exp2f adds a subnormal-range fix-up: 4 instructions);
+// results below 2^-126 flush to zero, which no softmax weight here can notice
+__device__ __forceinline__ float ex2f(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
   const __half2 h = __floats2half2_rn(x0, x1);
   const float2 hf = __half22float2(h);
@@ -241,13 +248,13 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
       const float bm = warp_max_redux(fmaxf(row[lane], row[lane + 32]));
       const float m_old = mst[h];
       const float m_new = fmaxf(m_old, bm);
-      const float p0 = exp2f(row[lane] - m_new), p1 = exp2f(row[lane + 32] - m_new);
+      const float p0 = ex2f(row[lane] - m_new), p1 = ex2f(row[lane + 32] - m_new);
       row[lane] = p0;
       row[lane + 32] = p1;
       const float sum = warp_sum(p0 + p1);
       __syncwarp();  // all lanes have read mst[h] before lane 0 rewrites it
       if (lane == 0) {
-        const float alpha = exp2f(m_old - m_new);
+        const float alpha = ex2f(m_old - m_new);
         lst[h] = lst[h] * alpha + sum;
         mst[h] = m_new;
         ast[h] = alpha;
@@ -740,8 +747,8 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
         const float bm = warp_max_redux(fmaxf(fmaxf(v01.x, v01.y), fmaxf(v89.x, v89.y)));
         const float m_old = mst[h];
         const float m_new = a.literal ? bm : fmaxf(m_old, bm);
-        float p0 = exp2f(v01.x - m_new), p1 = exp2f(v01.y - m_new);
-        float p8 = exp2f(v89.x - m_new), p9 = exp2f(v89.y - m_new);
+        float p0 = ex2f(v01.x - m_new), p1 = ex2f(v01.y - m_new);
+        float p8 = ex2f(v89.x - m_new), p9 = ex2f(v89.y - m_new);
         const float sum = warp_sum((p0 + p1) + (p8 + p9));
         if (a.literal) {  // each block its own normalized partition (engine.cpp:67-72)
           const float inv = 1.0f / sum;
@@ -762,7 +769,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
             ast[h] = 1.0f;
             pst[h] = 1.0f;
           } else {
-            const float alpha = exp2f(m_old - m_new);
+            const float alpha = ex2f(m_old - m_new);
             lst[h] = lst[h] * alpha + sum;
             mst[h] = m_new;
             ast[h] = alpha;
@@ -1079,8 +1086,8 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, 3)
       float2 v89 = *reinterpret_cast<const float2*>(row + 8);
       v01.x += beta; v01.y += beta; v89.x += beta; v89.y += beta;
       const float bm = warp_max_redux(fmaxf(fmaxf(v01.x, v01.y), fmaxf(v89.x, v89.y)));
-      const float p0 = exp2f(v01.x - bm), p1 = exp2f(v01.y - bm);
-      const float p8 = exp2f(v89.x - bm), p9 = exp2f(v89.y - bm);
+      const float p0 = ex2f(v01.x - bm), p1 = ex2f(v01.y - bm);
+      const float p8 = ex2f(v89.x - bm), p9 = ex2f(v89.y - bm);
       const float sum = warp_sum((p0 + p1) + (p8 + p9));
       uint32_t h01, l01, h89, l89;
       split2(p0, p1, h01, l01);
@@ -1497,8 +1504,8 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, GT <= 4 ? 3 : 2)
       const float bm = fmaxf(fmaxf(b4.x, b4.y), fmaxf(b4.z, b4.w));
       const bool on = h < (int)G && ((hm >> h) & 1u);
       mnew[h] = a.literal ? bm : fmaxf(m_run[h], bm);
-      p[h] = on ? exp2f(sc[h] - mnew[h]) : 0.f;
-      alpha[h] = on ? (a.literal ? 1.f : exp2f(m_run[h] - mnew[h])) : 1.f;
+      p[h] = on ? ex2f(sc[h] - mnew[h]) : 0.f;
+      alpha[h] = on ? (a.literal ? 1.f : ex2f(m_run[h] - mnew[h])) : 1.f;
     }
     if (a.literal) {  // each block its own normalized partition (engine.cpp:67-72)
 #pragma unroll
