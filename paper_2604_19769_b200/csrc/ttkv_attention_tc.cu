@@ -1154,12 +1154,13 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, 3)
 // slow tier on 5th-generation tensor cores (tcgen05.mma.kind::i8, TMEM
 // accumulators): the same record stream, schedule and partials as
 // slow_attn_tc_kernel, with both products as exact integer MMAs.
-//   QK: D[tok][n] = sum_c code_K[tok][c] * X[n][c], where X is q * s of head
-//       h scaled by 2^k_h (k_h from the head's max |q s| of this record) and
-//       written as three balanced base-256 s8 digit planes (n = 4 plane + h):
-//       the TMA-loaded u8 codes ARE the A operand (K-major, 128B swizzle), no
-//       conversion instruction touches them.  S = (D2 2^16 + D1 2^8 + D0) 2^-k
-//       + q . z is exact up to the 2^-22 (relative to the head's max) of X.
+//   QK: D[tok][n] = sum_c code_K[tok][c] * B[n][c] with u8 B: the three low
+//       bytes of X' = X + 2^21, X = q s of head h scaled by 2^k_h (k_h from
+//       the head's max |q s| in this record, |X| < 2^21), in rows n = PL pl +
+//       h, plus an all-ones row: S = (D0 + 2^8 D1 + 2^16 D2 - 2^21 D1s) 2^-k
+//       + q . z, exact in 64-bit integers up to the 2^-21 (relative to the
+//       head's max) of X.  The TMA-loaded u8 codes ARE the A operand (K-major,
+//       128B swizzle): no conversion instruction touches them.
 //   PV: D[ch][4h + j] = sum_tok code_V[tok][ch] * byte_j(Y_h[tok]), Y = p 2^22
 //       (< 2^22): the bytes of Y are its base-256 digits, so a token's B row
 //       (MN-major, no swizzle) is just its heads' Y words -- one 16-byte store;
@@ -1167,10 +1168,10 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, 3)
 //       (MN-major, 128B swizzle).  O = s (D0 + 2^8 D1 + 2^16 D2) 2^-22 +
 //       z sum(Y) 2^-22.
 // Opt-in (TTKV_SLOW_TC5=1): parity-green with a smaller output error than the
-// mma.sync kernel (2.0e-6 vs 4.2e-6, tools/err_probe.py), but slower at cfg2
-// (ncu 1.07 vs 0.95 ms per launch): the QK conversions it removes were never
-// the bound -- the V nibble expansion, the per-token softmax of every head
-// and three CTA barriers per record are.
+// mma.sync kernel (2.0e-6 vs 4.2e-6, tools/err_probe.py) and fewer issued
+// instructions, but ~1.5 % behind it (cfg2 0.99 vs 0.95 ms per launch): it is
+// latency-bound on three CTA barriers and two MMA round trips per record
+// (DESIGN.md §4).
 // One elected consumer thread issues the MMAs (4 per product, K = 32) and
 // commits them to an mbarrier; TMEM lanes are tokens (QK) or channels (PV),
 // so each consumer thread reads its own token's scores / channel's outputs
@@ -1354,9 +1355,12 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, GT <= 4 ? 3 : 2)
                  "n"(2 * NPAD));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // QK digit-plane rows past the heads stay zero
-  for (uint32_t i = threadIdx.x; i < NPAD * 128 / 16; i += blockDim.x)
-    reinterpret_cast<uint4*>(sBq)[i] = make_uint4(0, 0, 0, 0);
+  // QK digit-plane rows past the heads stay zero; the last row is all ones
+  // (D[tok][NPAD - 1] = sum_c code: the digit offset's correction)
+  for (uint32_t i = threadIdx.x; i < NPAD * 128 / 16; i += blockDim.x) {
+    const uint32_t v = i / 8 == NPAD - 1 ? 0x01010101u : 0u;
+    reinterpret_cast<uint4*>(sBq)[i] = make_uint4(v, v, v, v);
+  }
   proxy_fence_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -1401,11 +1405,23 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, GT <= 4 ? 3 : 2)
   const uint32_t tq = (warp & 3) * 32;    // TMEM lane quarter this warp may access
   const uint32_t my_row = tq + lane;      // the token / channel this thread reads from TMEM
   const float sl = (float)a.scale_log2;
-  const uint32_t iq = umma_idesc_i8(NPAD, 0, 1, 0), ip = umma_idesc_i8(NPAD, 1, 0, 1);
+  const uint32_t iq = umma_idesc_i8(NPAD, 0, 0, 0), ip = umma_idesc_i8(NPAD, 1, 0, 1);
 
   // record cursors: stream / index within the stream's union of record j (c*)
   // and of record j + 1 (n*)
   uint32_t cs = s_first, cii = i_first, ccnt = a.union_count[s_first];
+  // loop-invariant shared-memory offsets: this thread's QK digit words (head
+  // cw + 4 rep, channels 4 lane ..), and its token's V nibble / u8 rows
+  uint32_t bq_off[(GT + 3) / 4][3];
+#pragma unroll
+  for (int rep = 0; rep < (GT + 3) / 4; ++rep)
+#pragma unroll
+    for (int pl = 0; pl < 3; ++pl) bq_off[rep][pl] = sw128(PL * pl + cw + 4 * rep, 4 * lane);
+  uint32_t vin_off[4], vout_off[8];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) vin_off[q] = kKBox + ct * 64 + ((q ^ ((ct >> 1) & 3)) << 4);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) vout_off[q] = sw128(ct, 16 * q);
   auto stage_qk = [&](uint32_t j, uint32_t sj) {  // A(j): digit planes, then QK(j)
     const uint32_t st = j % ST;
     mbar_wait(&full[st], (j / ST) & 1);
@@ -1423,18 +1439,22 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, GT <= 4 ? 3 : 2)
         const float4 sz1 = *reinterpret_cast<const float4*>(kp + 2 * c4 + 4);
         const float x0 = qv.x * sz0.x, x1 = qv.y * sz0.z, x2 = qv.z * sz1.x, x3 = qv.w * sz1.z;
         const float mx = warp_max_redux(fmaxf(fmaxf(fabsf(x0), fabsf(x1)), fmaxf(fabsf(x2), fabsf(x3))));
-        // 2^k with max |x| 2^k < 2^22 (three balanced digits hold |X| < 2^22)
+        // X = x 2^k with max |x| 2^k < 2^21, offset to X' = X + 2^21 in [0, 2^22):
+        // the three low bytes of X' are its u8 digit planes (the offset comes
+        // back through the all-ones row: 2^21 sum_c code)
         const int ex = mx > 0.f ? (int)((__float_as_uint(mx) >> 23) & 0xffu) - 127 : 0;
-        const int k = max(-120, min(120, 21 - ex));
+        const int k = max(-120, min(120, 20 - ex));
         const float up = __uint_as_float((uint32_t)(127 + k) << 23);
-        int32_t d[4][3];
-        const float xs[4] = {x0, x1, x2, x3};
+        const uint32_t X0 = (uint32_t)(__float2int_rn(x0 * up) + (1 << 21));
+        const uint32_t X1 = (uint32_t)(__float2int_rn(x1 * up) + (1 << 21));
+        const uint32_t X2 = (uint32_t)(__float2int_rn(x2 * up) + (1 << 21));
+        const uint32_t X3 = (uint32_t)(__float2int_rn(x3 * up) + (1 << 21));
 #pragma unroll
-        for (int e = 0; e < 4; ++e) digits3(__float2int_rn(xs[e] * up), d[e][0], d[e][1], d[e][2]);
-#pragma unroll
-        for (int pl = 0; pl < 3; ++pl)
-          *reinterpret_cast<uint32_t*>(sBq + sw128(PL * pl + h, c4)) =
-              pack4(d[0][pl], d[1][pl], d[2][pl], d[3][pl]);
+        for (int pl = 0; pl < 3; ++pl) {
+          const uint32_t sel = (uint32_t)pl | ((uint32_t)(4 + pl) << 4);
+          *reinterpret_cast<uint32_t*>(sBq + bq_off[rep][pl]) =
+              __byte_perm(__byte_perm(X0, X1, sel), __byte_perm(X2, X3, sel), 0x5410);
+        }
         const float beta = warp_sum(qv.x * sz0.y + qv.y * sz0.w + qv.z * sz1.y + qv.w * sz1.w);
         if (lane == 0) {
           kun[h] = __uint_as_float((uint32_t)(127 - k) << 23);
@@ -1484,12 +1504,17 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, GT <= 4 ? 3 : 2)
     int32_t dq[NPAD];
     tmem_ld32<NPAD>(tmem + (tq << 16), dq);
     tmem_ld_wait();
+    const uint32_t hv = hm & ((1u << G) - 1u);  // heads that selected this record
+    const int64_t off21 = (int64_t)dq[NPAD - 1] << 21;  // 2^21 sum_c code[tok][c]
     float sc[GT];
 #pragma unroll
     for (int h = 0; h < GT; ++h) {
       sc[h] = -INFINITY;
-      if (h < (int)G && ((hm >> h) & 1u))
-        sc[h] = fmaf(combine3(dq[h], dq[PL + h], dq[2 * PL + h]), kun[h], bst[h]);
+      if ((hv >> h) & 1u) {
+        const int64_t S = (int64_t)dq[h] + ((int64_t)dq[PL + h] << 8) +
+                          ((int64_t)dq[2 * PL + h] << 16) - off21;
+        sc[h] = fmaf((float)S, kun[h], bst[h]);
+      }
     }
 #pragma unroll
     for (int h = 0; h < GT; ++h) {
@@ -1502,7 +1527,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, GT <= 4 ? 3 : 2)
     for (int h = 0; h < GT; ++h) {
       const float4 b4 = *reinterpret_cast<const float4*>(redm + 4 * h);
       const float bm = fmaxf(fmaxf(b4.x, b4.y), fmaxf(b4.z, b4.w));
-      const bool on = h < (int)G && ((hm >> h) & 1u);
+      const bool on = (hv >> h) & 1u;
       mnew[h] = a.literal ? bm : fmaxf(m_run[h], bm);
       p[h] = on ? ex2f(sc[h] - mnew[h]) : 0.f;
       alpha[h] = on ? (a.literal ? 1.f : ex2f(m_run[h] - mnew[h])) : 1.f;
@@ -1540,11 +1565,10 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, GT <= 4 ? 3 : 2)
     // V nibbles of token ct -> u8 row ct over the consumed K codes (MN-major
     // A of PV: [token][channel], 128B swizzle)
     {
-      const uint32_t t = ct;
       uint32_t w[16];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const uint4 u = *reinterpret_cast<const uint4*>(vn + t * 64 + ((q ^ ((t >> 1) & 3)) << 4));
+        const uint4 u = *reinterpret_cast<const uint4*>(stg + vin_off[q]);
         w[4 * q] = u.x; w[4 * q + 1] = u.y; w[4 * q + 2] = u.z; w[4 * q + 3] = u.w;
       }
 #pragma unroll
@@ -1557,7 +1581,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, GT <= 4 ? 3 : 2)
           o[2 * e] = __byte_perm(lo, hi, 0x5140);
           o[2 * e + 1] = __byte_perm(lo, hi, 0x7362);
         }
-        *reinterpret_cast<uint4*>(stg + sw128(t, 16 * q)) = make_uint4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<uint4*>(stg + vout_off[q]) = make_uint4(o[0], o[1], o[2], o[3]);
       }
     }
     proxy_fence_async_smem();
@@ -1607,7 +1631,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, GT <= 4 ? 3 : 2)
     const float vs = vsz.x * (1.0f / 4194304.0f), vz = vsz.y;
 #pragma unroll
     for (int h = 0; h < GT; ++h) {
-      if (!(h < (int)G && ((hm >> h) & 1u))) continue;
+      if (!((hv >> h) & 1u)) continue;
       const float o = combine3(dp[4 * h], dp[4 * h + 1], dp[4 * h + 2]);
       acc[h] = fmaf(acc[h], alpha[h], fmaf(vs, o, vz * lblk[h]));
       if (a.literal) {
