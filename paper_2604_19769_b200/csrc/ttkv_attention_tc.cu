@@ -1249,17 +1249,6 @@ __device__ __forceinline__ void tmem_ld32<32>(uint32_t taddr, int32_t (&r)[32]) 
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-// balanced base-256 digits of |x| < 2^22: x = d2 2^16 + d1 2^8 + d0, d in [-128, 127]
-__device__ __forceinline__ void digits3(int32_t x, int32_t& d0, int32_t& d1, int32_t& d2) {
-  d0 = ((x + 128) & 255) - 128;
-  const int32_t x1 = (x - d0) >> 8;
-  d1 = ((x1 + 128) & 255) - 128;
-  d2 = (x1 - d1) >> 8;
-}
-__device__ __forceinline__ uint32_t pack4(int32_t a, int32_t b, int32_t c, int32_t d) {
-  return (uint32_t)(a & 255) | ((uint32_t)(b & 255) << 8) | ((uint32_t)(c & 255) << 16) |
-         ((uint32_t)d << 24);
-}
 __device__ __forceinline__ float combine3(int32_t d0, int32_t d1, int32_t d2) {
   return fmaf((float)d2, 65536.0f, fmaf((float)d1, 256.0f, (float)d0));
 }
