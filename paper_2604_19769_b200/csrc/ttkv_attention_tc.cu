@@ -1161,11 +1161,13 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, 3)
 //       + q . z, exact in 64-bit integers up to the 2^-21 (relative to the
 //       head's max) of X.  The TMA-loaded u8 codes ARE the A operand (K-major,
 //       128B swizzle): no conversion instruction touches them.
-//   PV: D[ch][4h + j] = sum_tok code_V[tok][ch] * byte_j(Y_h[tok]), Y = p 2^22
+//   PV: D[b][4h + j] = sum_tok A[tok][b] * byte_j(Y_h[tok]), Y = p 2^22
 //       (< 2^22): the bytes of Y are its base-256 digits, so a token's B row
-//       (MN-major, no swizzle) is just its heads' Y words -- one 16-byte store;
-//       the V nibbles are expanded to u8 over the record's consumed K codes
-//       (MN-major, 128B swizzle).  O = s (D0 + 2^8 D1 + 2^16 D2) 2^-22 +
+//       (MN-major, no swizzle) is just its heads' Y words -- one 16-byte store.
+//       M = 64: A is the V tile as TMA delivered it (64 bytes per token, a
+//       byte = channel 2b + 16 x channel 2b+1, 64B swizzle), and a second MMA
+//       runs on the high nibbles (written over the consumed K codes); channel
+//       2b = D_bytes - 16 D_high.  O = s (D0 + 2^8 D1 + 2^16 D2) 2^-22 +
 //       z sum(Y) 2^-22.
 // Opt-in (TTKV_SLOW_TC5=1): parity-green with a smaller output error than the
 // mma.sync kernel (2.0e-6 vs 4.2e-6, tools/err_probe.py) and fewer issued
@@ -1187,6 +1189,14 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t lbo
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
   d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  d |= (uint64_t)4 << 61;  // SWIZZLE_64B
   return d;
 }
 __device__ __forceinline__ uint64_t umma_desc_none(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -1338,10 +1348,11 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, GT <= 4 ? 3 : 2)
     mbar_init(bar_pv, 1);
     fence_mbar_init();
   }
-  if (warp == 1) {  // TMEM: D_qk in columns [0, NPAD), D_pv in [NPAD, 2 NPAD)
+  if (warp == 1) {  // TMEM: D_qk [0, NPAD), D_pv of the packed bytes [NPAD, 2 NPAD),
+                    // of the high nibbles [2 NPAD, 3 NPAD)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "n"(2 * NPAD));
+                 "n"(4 * NPAD));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   // QK digit-plane rows past the heads stay zero; the last row is all ones
@@ -1394,7 +1405,12 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, GT <= 4 ? 3 : 2)
   const uint32_t tq = (warp & 3) * 32;    // TMEM lane quarter this warp may access
   const uint32_t my_row = tq + lane;      // the token / channel this thread reads from TMEM
   const float sl = (float)a.scale_log2;
-  const uint32_t iq = umma_idesc_i8(NPAD, 0, 0, 0), ip = umma_idesc_i8(NPAD, 1, 0, 1);
+  const uint32_t iq = umma_idesc_i8(NPAD, 0, 0, 0);
+  // PV, M = 64: the A rows are the 64 bytes of a token's V nibbles (channel
+  // pairs 2b, 2b + 1); D rows b land in TMEM lanes 32 (b / 16) + b % 16
+  const uint32_t ip = umma_idesc_i8(NPAD, 1, 0, 1) - ((128u >> 4) << 24) + ((64u >> 4) << 24);
+  const bool pv_row = lane < 16;               // this thread holds a D_pv row ...
+  const uint32_t pb_byte = 16 * (warp & 3) + (lane & 15);  // ... of byte b = channels 2b, 2b + 1
 
   // record cursors: stream / index within the stream's union of record j (c*)
   // and of record j + 1 (n*)
@@ -1406,11 +1422,9 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, GT <= 4 ? 3 : 2)
   for (int rep = 0; rep < (GT + 3) / 4; ++rep)
 #pragma unroll
     for (int pl = 0; pl < 3; ++pl) bq_off[rep][pl] = sw128(PL * pl + cw + 4 * rep, 4 * lane);
-  uint32_t vin_off[4], vout_off[8];
+  uint32_t vin_off[4];  // token ct's V nibble row (64B swizzle), relative to the V tile
 #pragma unroll
-  for (int q = 0; q < 4; ++q) vin_off[q] = kKBox + ct * 64 + ((q ^ ((ct >> 1) & 3)) << 4);
-#pragma unroll
-  for (int q = 0; q < 8; ++q) vout_off[q] = sw128(ct, 16 * q);
+  for (int q = 0; q < 4; ++q) vin_off[q] = ct * 64 + ((q ^ ((ct >> 1) & 3)) << 4);
   auto stage_qk = [&](uint32_t j, uint32_t sj) {  // A(j): digit planes, then QK(j)
     const uint32_t st = j % ST;
     mbar_wait(&full[st], (j / ST) & 1);
@@ -1465,12 +1479,12 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, GT <= 4 ? 3 : 2)
     }
   };
 
-  float m_run[GT], l_run[GT], acc[GT];
+  float m_run[GT], l_run[GT], acc[2][GT];  // acc: channels 2b, 2b + 1
 #pragma unroll
   for (int h = 0; h < GT; ++h) {
     m_run[h] = -INFINITY;
     l_run[h] = 0.f;
-    acc[h] = 0.f;
+    acc[0][h] = acc[1][h] = 0.f;
   }
   uint32_t seen = 0, slot = slot_first;
   while (cii >= ccnt) {  // (the schedule starts at a record, so this never loops)
@@ -1485,7 +1499,8 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, GT <= 4 ? 3 : 2)
     const float* vp = reinterpret_cast<const float*>(stg + kKBox + kVBox) + 2 * 128;
     const uint32_t hm = hms[st];
     seen |= hm;
-    const float2 vsz = *reinterpret_cast<const float2*>(vp + 2 * my_row);  // V params of channel my_row
+    // V params {s, z} of channels 2b, 2b + 1
+    const float4 vsz = *reinterpret_cast<const float4*>(vp + 4 * pb_byte);
 
     // ---- B(j): scores of token my_row, all heads ----
     mbar_wait(bar_qk, j & 1);
@@ -1551,27 +1566,15 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, GT <= 4 ? 3 : 2)
       for (int e = 0; e < 4; ++e) y4[e] = 4 * grp + e < GT ? yw[(4 * grp + e) % GT] : 0u;
       *reinterpret_cast<uint4*>(sBp + grp * 2048 + my_row * 16) = make_uint4(y4[0], y4[1], y4[2], y4[3]);
     }
-    // V nibbles of token ct -> u8 row ct over the consumed K codes (MN-major
-    // A of PV: [token][channel], 128B swizzle)
-    {
-      uint32_t w[16];
+    // PV runs on the V bytes as they arrived (a byte = channel 2b + 16 x
+    // channel 2b + 1) and on their high nibbles, written over the consumed K
+    // codes in the same 64B-swizzled [token][64 B] layout: lo = D_a - 16 D_b
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 u = *reinterpret_cast<const uint4*>(stg + vin_off[q]);
-        w[4 * q] = u.x; w[4 * q + 1] = u.y; w[4 * q + 2] = u.z; w[4 * q + 3] = u.w;
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {  // 16-byte chunk q = channels 16q .. 16q + 15
-        uint32_t o[4];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const uint32_t x = w[2 * q + e];
-          const uint32_t lo = x & 0x0F0F0F0Fu, hi = (x >> 4) & 0x0F0F0F0Fu;
-          o[2 * e] = __byte_perm(lo, hi, 0x5140);
-          o[2 * e + 1] = __byte_perm(lo, hi, 0x7362);
-        }
-        *reinterpret_cast<uint4*>(stg + vout_off[q]) = make_uint4(o[0], o[1], o[2], o[3]);
-      }
+    for (int q = 0; q < 4; ++q) {
+      const uint4 u = *reinterpret_cast<const uint4*>(stg + kKBox + vin_off[q]);
+      *reinterpret_cast<uint4*>(stg + vin_off[q]) =
+          make_uint4((u.x >> 4) & 0x0F0F0F0Fu, (u.y >> 4) & 0x0F0F0F0Fu, (u.z >> 4) & 0x0F0F0F0Fu,
+                     (u.w >> 4) & 0x0F0F0F0Fu);
     }
     proxy_fence_async_smem();
     tc_fence_before();
@@ -1584,11 +1587,13 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, GT <= 4 ? 3 : 2)
     }
     if (ct == 0) {  // D_pv[ch][n] = Vx[.][ch] . Bp[n][.]
       tc_fence_after();
-      const uint32_t va = smem_u32(stg), pb = smem_u32(sBp);
+      const uint32_t vb = smem_u32(stg + kKBox), vh = smem_u32(stg), pb = smem_u32(sBp);
 #pragma unroll
-      for (uint32_t kk = 0; kk < 4; ++kk)
-        umma_i8(tmem + NPAD, umma_desc_sw128(va + 4096 * kk, 16384, 1024),
-                umma_desc_none(pb + 512 * kk, 128, 2048), ip, kk);
+      for (uint32_t kk = 0; kk < 4; ++kk) {  // K = 32 tokens = 2 KB of each [token][64 B] tile
+        const uint64_t db = umma_desc_none(pb + 512 * kk, 128, 2048);
+        umma_i8(tmem + NPAD, umma_desc_sw64(vb + 2048 * kk, 8192, 512), db, ip, kk);
+        umma_i8(tmem + 2 * NPAD, umma_desc_sw64(vh + 2048 * kk, 8192, 512), db, ip, kk);
+      }
       umma_commit(bar_pv);
     }
 
@@ -1611,18 +1616,26 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, GT <= 4 ? 3 : 2)
     // ---- C(j): PV(j) read back, online-softmax update ----
     mbar_wait(bar_pv, j & 1);
     tc_fence_after();
-    int32_t dp[NPAD];
-    tmem_ld32<NPAD>(tmem + (tq << 16) + NPAD, dp);
+    int32_t da[NPAD], db[NPAD];  // lanes 32 q + [0, 16): byte rows 16 q + lane
+    tmem_ld32<NPAD>(tmem + (tq << 16) + NPAD, da);
+    tmem_ld32<NPAD>(tmem + (tq << 16) + 2 * NPAD, db);
     tmem_ld_wait();
     tc_fence_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);  // the stage (Vx over K, params) is consumed
-    const float vs = vsz.x * (1.0f / 4194304.0f), vz = vsz.y;
+    if (lane == 0) mbar_arrive(&empty[st]);  // the stage (high nibbles over K, V, params) is consumed
+    const float vs0 = vsz.x * (1.0f / 4194304.0f), vz0 = vsz.y;
+    const float vs1 = vsz.z * (1.0f / 4194304.0f), vz1 = vsz.w;
 #pragma unroll
     for (int h = 0; h < GT; ++h) {
       if (!((hv >> h) & 1u)) continue;
-      const float o = combine3(dp[4 * h], dp[4 * h + 1], dp[4 * h + 2]);
-      acc[h] = fmaf(acc[h], alpha[h], fmaf(vs, o, vz * lblk[h]));
+      if (pv_row) {
+        // channel 2b + 1 = the high nibbles; channel 2b = bytes - 16 x high (exact in s32)
+        const float o1 = combine3(db[4 * h], db[4 * h + 1], db[4 * h + 2]);
+        const float o0 = combine3(da[4 * h] - 16 * db[4 * h], da[4 * h + 1] - 16 * db[4 * h + 1],
+                                  da[4 * h + 2] - 16 * db[4 * h + 2]);
+        acc[0][h] = fmaf(acc[0][h], alpha[h], fmaf(vs0, o0, vz0 * lblk[h]));
+        acc[1][h] = fmaf(acc[1][h], alpha[h], fmaf(vs1, o1, vz1 * lblk[h]));
+      }
       if (a.literal) {
         l_run[h] = 1.f;
       } else {
@@ -1638,14 +1651,16 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, GT <= 4 ? 3 : 2)
         if (h >= (int)G) continue;
         float* pp = reinterpret_cast<float*>(a.part) + (((uint64_t)s_this * G + h) * a.nsc + slot) * pitch;
         const bool any = (seen >> h) & 1u;
-        pp[my_row] = any ? acc[h] : 0.f;
+        if (pv_row)
+          *reinterpret_cast<float2*>(pp + 2 * pb_byte) =
+              make_float2(any ? acc[0][h] : 0.f, any ? acc[1][h] : 0.f);
         if (ct == 0) {
           pp[128] = any ? (a.literal ? 0.f : m_run[h]) : -INFINITY;
           pp[129] = any ? (a.literal ? 1.f : l_run[h]) : 0.f;
         }
         m_run[h] = -INFINITY;
         l_run[h] = 0.f;
-        acc[h] = 0.f;
+        acc[0][h] = acc[1][h] = 0.f;
       }
       // the stream's last record is here (its union ends at this CTA)
       if (ct == 0 && stream_end) a.nslots[s_this] = slot + 1;
@@ -1657,7 +1672,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, GT <= 4 ? 3 : 2)
   named_bar(1, nthreads_c);
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * NPAD));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(4 * NPAD));
   }
   pdl_trigger();
 }
