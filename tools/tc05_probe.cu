@@ -4,7 +4,7 @@
 // planes (B K-major, written by threads in the SW128 pattern), and can
 // expanded V codes (A MN-major SW128) do the same for PV?  Results (s32 in
 // TMEM, read back with tcgen05.ld) are checked against the CPU.
-//   nvcc -gencode arch=compute_100a,code=sm_100a -o build/tc05_probe tools/tc05_probe.cu -lcuda
+//   make -C tools (build/tc05_probe)
 #include <cuda.h>
 #include <cuda_runtime.h>
 

@@ -2,7 +2,7 @@
 // MN-major [K = 128 tokens][M = 64 bytes] u8 tile in the 64B-swizzle layout
 // the V nibbles arrive in (TMA SWIZZLE_64B).  Dumps all 128 TMEM lanes of the
 // accumulator to find where the 64 rows land, and checks the values.
-//   nvcc -gencode arch=compute_100a,code=sm_100a -o build/tc05_probe_m64 tools/tc05_probe_m64.cu
+//   make -C tools (build/tc05_probe_m64)
 #include <cuda_runtime.h>
 
 #include <cstdint>
