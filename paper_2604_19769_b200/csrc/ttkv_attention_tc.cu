@@ -1169,13 +1169,12 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, 3)
 //       runs on the high nibbles (written over the consumed K codes); channel
 //       2b = D_bytes - 16 D_high.  O = s (D0 + 2^8 D1 + 2^16 D2) 2^-22 +
 //       z sum(Y) 2^-22.
-// Opt-in (TTKV_SLOW_TC5=1): parity-green with a smaller output error than the
-// mma.sync kernel (2.0e-6 vs 4.2e-6, tools/err_probe.py) and fewer issued
-// instructions, but ~1.5 % behind it (cfg2 0.99 vs 0.95 ms per launch): it is
-// latency-bound on three CTA barriers and two MMA round trips per record
-// (DESIGN.md §4).
-// One elected consumer thread issues the MMAs (4 per product, K = 32) and
-// commits them to an mbarrier; TMEM lanes are tokens (QK) or channels (PV),
+// Opt-in (TTKV_SLOW_TC5=1): parity-green (output error <= 3.7e-6,
+// tools/err_probe.py) with fewer issued instructions than the mma.sync kernel,
+// but ~1 % behind it (cfg2 0.985 vs 0.93 ms per launch): it is latency-bound on
+// three CTA barriers and two MMA round trips per record.
+// One elected consumer thread issues the MMAs (4 per QK, 8 per PV, K = 32) and
+// commits them to an mbarrier; TMEM lanes are tokens (QK) or byte rows (PV),
 // so each consumer thread reads its own token's scores / channel's outputs
 // for every head with one tcgen05.ld.
 // ---------------------------------------------------------------------------

@@ -1301,7 +1301,7 @@ int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* po
   if (opt->n_streams == 0 || opt->heads_per_stream == 0 || opt->heads_per_stream > (uint32_t)kMaxG)
     return set_err(nullptr, TTKV_ECONFIG, "n_streams >= 1 and heads_per_stream in [1, 8]");
   if (opt->record_stream > 2)
-    return set_err(nullptr, TTKV_ECONFIG, "record_stream must be 0 (auto), 1 (union) or 2 (speculative)");
+    return set_err(nullptr, TTKV_ECONFIG, "record_stream must be 0 or 1 (union, the default) or 2 (speculative)");
 
   int ndev = 0;
   cudaError_t ce = cudaGetDeviceCount(&ndev);
