@@ -703,8 +703,10 @@ def run_ours(args):
         t_roof_ms = hbm_bytes_step / (hbm_peak * 1e9) * 1e3
         slow_bytes = union_last * rec  # payload from the arena + params from the mirror
         ach = slow_bytes / (slow_ms * 1e-3) / 1e9 if slow_ms > 0 else 0.0
-        traffic, _, tmeta = traffic_for("slow_attn_tc_kernel", args.workload)
-        roof = {"bound": "hbm", "kernel": "slow_attn_tc_kernel", "achieved": ach,
+        kname = ("slow_attn_tc5_kernel" if os.environ.get("TTKV_SLOW_TC5") == "1"
+                 else "slow_attn_tc_kernel")  # the opt-in tcgen05 kernel has no stamped traffic
+        traffic, _, tmeta = traffic_for(kname, args.workload)
+        roof = {"bound": "hbm", "kernel": kname, "achieved": ach,
                 "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)", "traffic": traffic,
                 "algorithmic_bytes_per_launch": slow_bytes}
