@@ -621,6 +621,7 @@ __global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs
   const uint32_t idx = blockIdx.x;  // s * G + head
   const uint32_t s = idx / g.G;
   const uint32_t pitch = g.d_v + 2;
+  double* const out = a.out_ref ? *a.out_ref : a.out;
   const uint32_t nsc_used = !a.union_count         ? 0u
                             : a.union_count[s] == 0u ? 0u
                             : a.nslots               ? a.nslots[s]
@@ -721,7 +722,7 @@ __global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs
     if (a.literal)
       for (uint32_t i = 0; i < nsc_used; ++i)
         if (sp[i * pitch + g.d_v + 1] > 0) o += sp[i * pitch + c];
-    a.out[(uint64_t)idx * g.d_v + c] = (double)o;
+    out[(uint64_t)idx * g.d_v + c] = (double)o;
     if (a.n_peers) {
       const uint64_t gi = ((uint64_t)a.gidx[s] * g.G + (idx - s * g.G)) * g.d_v + c;
       for (uint32_t r = 0; r < a.n_peers; ++r) a.peer_out[r][gi] = (double)o;
@@ -730,6 +731,8 @@ __global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs
   // the step is combined: advance the device step position (nothing in this
   // kernel reads it; the next step's append and fast tier do)
   if (a.pos_inc && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *a.pos_inc += 1;
+  if (a.count_out && idx == s * g.G && blockIdx.y == 0 && threadIdx.x == 0)
+    a.count_out[s] = a.union_count ? a.union_count[s] : 0u;
   if (a.n_peers) {  // this CTA's row is in every rank's buffer: publish it
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -761,6 +764,7 @@ __global__ void __launch_bounds__(kSpecCombineThreads) combine_spec_kernel(Combi
   const uint32_t idx = blockIdx.x, s = idx / g.G, h = idx - s * g.G;
   const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const uint32_t cap = a.nfc + a.spec_n;
+  double* const out = a.out_ref ? *a.out_ref : a.out;
   extern __shared__ __align__(16) uint8_t csm[];
   float* wv = reinterpret_cast<float*>(csm);  // [cap] weights
   float* lv = wv + cap;                       // [cap] l of each row
@@ -871,7 +875,7 @@ __global__ void __launch_bounds__(kSpecCombineThreads) combine_spec_kernel(Combi
     for (int k = 0; k < 32; ++k) A += acc_sm[k][t];
     const uint32_t ch = blockIdx.y * 32 + t;
     const double o = (double)(A / Lt);
-    a.out[(uint64_t)idx * g.d_v + ch] = o;
+    out[(uint64_t)idx * g.d_v + ch] = o;
     if (a.n_peers) {
       const uint64_t gi = ((uint64_t)a.gidx[s] * g.G + h) * g.d_v + ch;
       for (uint32_t r = 0; r < a.n_peers; ++r) a.peer_out[r][gi] = o;
@@ -881,6 +885,8 @@ __global__ void __launch_bounds__(kSpecCombineThreads) combine_spec_kernel(Combi
     if (a.pos_inc) *a.pos_inc += 1;
     *a.spec_ctr = 0;  // the record queue is drained (this grid waited on its kernel)
   }
+  if (a.count_out && h == 0 && blockIdx.y == 0 && t == 0)
+    a.count_out[s] = a.union_count ? a.union_count[s] : 0u;
   if (a.n_peers) {  // this CTA's row slice is in every rank's buffer: publish it
     __syncthreads();
     if (t == 0) {

@@ -248,6 +248,10 @@ struct ttkv_gpu {
   uint32_t *mask = nullptr, *uids = nullptr, *umask = nullptr, *ucount = nullptr;
   uint32_t* nslots = nullptr;  // slow partial slots per stream (tensor-core slow tier)
   uint32_t* h_ucount = nullptr;  // pinned copy of union_count for the step report
+  uint32_t* h_ucount_dev = nullptr;  // ... its device mapping (the combine writes it)
+  IoSlot* io = nullptr;      // host-buffer steps: q/k/v/out addresses (mapped, pinned)
+  IoSlot* io_dev = nullptr;  // ... its device mapping (read by the ingest kernel)
+  double** out_ref = nullptr;  // device word: the step's output address (ingest -> combine)
   void* fpart = nullptr;
   void* spart = nullptr;
   uint64_t spart_chunks = 0;
@@ -258,7 +262,6 @@ struct ttkv_gpu {
   uint32_t* spec_ctr = nullptr;
   uint64_t spec_steps = 0;
   float* q_dev = nullptr;
-  double* out_dev = nullptr;
   void *kn_dev = nullptr, *vn_dev = nullptr;
   void *stg_k = nullptr, *stg_v = nullptr;
   uint64_t stg_tokens = 0;
@@ -294,7 +297,6 @@ struct ttkv_gpu {
   uint64_t gen = 0;         // bumped whenever a buffer a captured step uses moves
   struct GraphKey {
     const void *q, *kn, *vn, *out;
-    const void* host[4];  // host-buffer steps: the q, k, v sources and the output
     cudaStream_t s0;
     uint64_t n, k, front, gen, grid_chunks;
     uint32_t nfc, CH, dtype, host_io;
@@ -418,8 +420,8 @@ void free_all(ttkv_gpu* h) {
   };
   F(h->ring_k); F(h->ring_v); F(h->cent); F(h->params); F(h->scores); F(h->mask); F(h->uids);
   F(h->umask); F(h->ucount); F(h->nslots); F(h->fpart); F(h->spart); F(h->q_dev);
-  F(h->rpart); F(h->spec_ctr);
-  F(h->out_dev); F(h->kn_dev); F(h->vn_dev); F(h->stg_k); F(h->stg_v); F(h->stage_arena);
+  F(h->rpart); F(h->spec_ctr); F(h->out_ref);
+  F(h->kn_dev); F(h->vn_dev); F(h->stg_k); F(h->stg_v); F(h->stage_arena);
   if (h->arena_host) pinned_free(h->arena_host);
   else if (h->arena_dev) cudaFree(h->arena_dev);
   pinned_free(h->h_q);
@@ -427,6 +429,7 @@ void free_all(ttkv_gpu* h) {
   pinned_free(h->h_k);
   pinned_free(h->h_v);
   pinned_free(h->h_ucount);
+  pinned_free(h->io);
   F(h->pos_dev);
   for (auto& sg : h->graphs) cudaGraphExecDestroy(sg.exec);
   h->graphs.clear();
@@ -691,11 +694,7 @@ struct StepPlan {
   const void* vn;
   int dtype;
   double* out;
-  bool host_io;  // copy q/k/v in from host and the output back within the step
-  const void* hq;  // host sources: the caller's buffers when page-locked, else
-  const void* hk;  // the handle's pinned staging copies
-  const void* hv;
-  void* hout;      // host destination of the output (same rule)
+  bool host_io;  // q/k/v read from and the output written to host memory (h->io)
   uint64_t n, k, F;
   uint32_t FCs, nfc, CH;
   uint64_t grid_chunks;  // slow kernel grid: chunks per stream, or CTAs (tensor-core tier)
@@ -714,13 +713,14 @@ struct StepPlan {
 int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
   const Geometry& g = h->g;
   if (P.host_io) {
+    // q/k/v read from mapped page-locked host memory by one kernel (not
+    // three copy-engine transfers: ~4 us of queue latency each on a small step)
     const size_t esz = P.dtype == kInF16 ? 2 : 4;
-    CU(h, cudaMemcpyAsync(h->q_dev, P.hq, (size_t)g.S * g.G * g.d_k * 4, cudaMemcpyHostToDevice,
-                          h->s0));
-    CU(h, cudaMemcpyAsync(h->kn_dev, P.hk, (size_t)g.S * g.d_k * esz, cudaMemcpyHostToDevice,
-                          h->s0));
-    CU(h, cudaMemcpyAsync(h->vn_dev, P.hv, (size_t)g.S * g.d_v * esz, cudaMemcpyHostToDevice,
-                          h->s0));
+    void* const dst[3] = {h->q_dev, h->kn_dev, h->vn_dev};
+    const uint64_t bytes[3] = {(uint64_t)g.S * g.G * g.d_k * 4, (uint64_t)g.S * g.d_k * esz,
+                               (uint64_t)g.S * g.d_v * esz};
+    KTimer t(h, K_APPEND, h->s0);
+    CU(h, launch_ingest(dst, bytes, h->io_dev, reinterpret_cast<void**>(h->out_ref), h->s0));
   }
   // append_kv: the new token attends to itself.  Only the fast
   // tier reads the ring, so the append runs on s1 ahead of the fast kernel and
@@ -926,7 +926,9 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
       a.spec_n = (uint32_t)P.n;
       a.spec_ctr = h->spec_ctr;
     }
-    a.out = P.out;
+    a.out = P.out;  // host-buffer steps: the caller's (or the staging) page-locked buffer
+    a.out_ref = P.host_io ? h->out_ref : nullptr;
+    a.count_out = P.host_io && P.slow ? h->h_ucount_dev : nullptr;
     a.literal = h->opt.literal_additive_merge ? 1u : 0u;
     a.pos_inc = h->pos_dev;
     if (h->pg.active) {
@@ -953,32 +955,27 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
                 h->s0));
     }
   }
-  if (P.host_io) {
-    CU(h, cudaMemcpyAsync(P.hout, h->out_dev, (size_t)g.S * g.G * g.d_v * 8,
-                          cudaMemcpyDeviceToHost, h->s0));
-    if (P.slow)
-      CU(h, cudaMemcpyAsync(h->h_ucount, h->ucount, g.S * sizeof(uint32_t),
-                            cudaMemcpyDeviceToHost, h->s0));
-  }
   return TTKV_OK;
 }
 
-// Graph replay is opt-in (TTKV_GRAPH=1): it cuts the host's issue time per
-// step (layer-sequential cfg2: 52 -> 22 us per call) but a replayed step
-// loses most of the programmatic-launch overlap of the directly launched
-// chain (cfg1 HBM: 50.9 vs 43.6 us per step on the device), so it pays only
-// for callers whose host issue time exceeds the device time.
-bool graphs_enabled() {
-  static const bool on = [] {
+// Graph replay: the host's issue time of a directly launched step is ~13 us
+// (cfg1 HBM, 8 launches) against ~2 us for one graph launch, but a replayed
+// step loses part of the programmatic-launch overlap of the direct chain
+// (cfg1 HBM: 50.9 vs 43.6 us per step back to back on the device).  So the
+// synchronous host-buffer call (ttkv_gpu_decode_step), which waits for every
+// step anyway, replays by default (cfg1 HBM: 65.6 -> 49.7 us per call,
+// tools/host_issue_probe.cu), and device-buffer steps enqueued back to back
+// launch directly.  TTKV_GRAPH=1 replays both, TTKV_GRAPH=0 neither.
+bool graphs_enabled(bool host_io) {
+  static const int env = [] {
     const char* e = std::getenv("TTKV_GRAPH");
-    return e && e[0] == '1';
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
-  return on;
+  return env == 1 || (env == -1 && host_io);
 }
 
 int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int dtype,
-                double* out, ttkv_step_report* rep, bool host_io = false,
-                const void* const* host = nullptr) {
+                double* out, ttkv_step_report* rep, bool host_io = false) {
   StepTimer step_timer(h);
   {  // grow before selecting so a settle-time eviction never reallocates
     int rc0 = ensure_blocks(h, h->n_slow + 1);
@@ -996,12 +993,6 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
   P.dtype = dtype;
   P.out = out;
   P.host_io = host_io;
-  if (host_io) {
-    P.hq = host[0];
-    P.hk = host[1];
-    P.hv = host[2];
-    P.hout = const_cast<void*>(host[3]);
-  }
   P.F = pos + 1 - h->fast_front;
   P.n = h->n_slow;
   {
@@ -1113,7 +1104,7 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
   // on the device), so the step is captured once and replayed.  Steps that
   // evict, timed steps and the multi-GPU gather launch directly.
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  bool use_graph = graphs_enabled() && P.slow && !h->timing && !h->pg.active && h->s0 &&
+  bool use_graph = graphs_enabled(host_io) && P.slow && !h->timing && !h->pg.active && h->s0 &&
                    P.F <= h->l_fast;
   if (use_graph) {
     CU(h, cudaStreamIsCapturing(h->s0, &cap));
@@ -1135,9 +1126,7 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
     key.nfc = P.nfc;
     key.CH = P.CH;
     key.dtype = (uint32_t)dtype;
-    key.host_io = host_io ? 1u : 0u;
-    if (host_io)
-      for (int i = 0; i < 4; ++i) key.host[i] = host[i];
+    key.host_io = host_io ? 1u : 0u;  // host addresses live in h->io, not in the graph
     ttkv_gpu::StepGraph* hit = nullptr;
     for (auto& sg : h->graphs)
       if (std::memcmp(&key, &sg.key, sizeof(key)) == 0) hit = &sg;
@@ -1403,9 +1392,12 @@ int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* po
   CREATE_CU(cudaMalloc((void**)&h->nslots, S * sizeof(uint32_t)));
   CREATE_CU(cudaMemset(h->ucount, 0, S * sizeof(uint32_t)));
   CREATE_CU(pinned_alloc((void**)&h->h_ucount, S * sizeof(uint32_t)));
+  CREATE_CU(cudaHostGetDevicePointer((void**)&h->h_ucount_dev, h->h_ucount, 0));
+  CREATE_CU(pinned_alloc((void**)&h->io, sizeof(IoSlot)));
+  CREATE_CU(cudaHostGetDevicePointer((void**)&h->io_dev, h->io, 0));
+  CREATE_CU(cudaMalloc((void**)&h->out_ref, sizeof(double*)));
   CREATE_CU(cudaMalloc((void**)&h->fpart, S * g.G * h->nfc_cap * (g.d_v + 2) * h->acc));
   CREATE_CU(cudaMalloc((void**)&h->q_dev, S * g.G * g.d_k * sizeof(float)));
-  CREATE_CU(cudaMalloc((void**)&h->out_dev, S * g.G * g.d_v * sizeof(double)));
   CREATE_CU(cudaMalloc(&h->kn_dev, S * g.d_k * 4));
   CREATE_CU(cudaMalloc(&h->vn_dev, S * g.d_v * 4));
   CREATE_CU(pinned_alloc((void**)&h->h_q, S * g.G * g.d_k * sizeof(float)));
@@ -1608,14 +1600,15 @@ int ttkv_gpu_decode_step_device(ttkv_gpu* h, const float* q, const void* kn, con
 }
 
 namespace {
-// Page-locked (cudaHostAlloc'd or registered) host memory?
-bool host_pinned(const void* p) {
+// The device address of page-locked host memory mapped into the device's
+// address space (cudaHostAlloc'd, or registered and mapped), else null.
+void* host_mapped(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
-    return false;
+    return nullptr;
   }
-  return a.type == cudaMemoryTypeHost;
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
 }
 }  // namespace
 
@@ -1630,17 +1623,27 @@ int ttkv_gpu_decode_step(ttkv_gpu* h, const float* q, const void* kn, const void
   const size_t esz = dtype == TTKV_DTYPE_F16 ? 2 : 4;
   const size_t qb = (size_t)g.S * g.G * g.d_k * 4, ob = (size_t)g.S * g.G * g.d_v * 8;
   const size_t kb = (size_t)g.S * g.d_k * esz, vb = (size_t)g.S * g.d_v * esz;
-  // The caller's page-locked buffers are DMA'd directly; pageable ones go
-  // through the handle's pinned staging copies (one host memcpy each way).
-  const void* host[4];
-  host[0] = host_pinned(q) ? static_cast<const void*>(q) : (std::memcpy(h->h_q, q, qb), h->h_q);
-  host[1] = host_pinned(kn) ? kn : (std::memcpy(h->h_k, kn, kb), h->h_k);
-  host[2] = host_pinned(vn) ? vn : (std::memcpy(h->h_v, vn, vb), h->h_v);
-  const bool out_direct = host_pinned(out);
-  host[3] = out_direct ? static_cast<const void*>(out) : h->h_out;
-  // the H2D of q/k/v and the D2H of the output are part of the (captured) step
+  // The step's kernels read the caller's page-locked buffers and write its
+  // output through the device mapping of that memory; pageable buffers go
+  // through the handle's mapped staging copies (one host memcpy each way).
+  auto src = [&](const void* p, void* stage, size_t nb) -> const void* {
+    if (void* d = host_mapped(p)) return d;
+    std::memcpy(stage, p, nb);
+    return host_mapped(stage);
+  };
+  IoSlot& io = *h->io;
+  io.src[0] = src(q, h->h_q, qb);
+  io.src[1] = src(kn, h->h_k, kb);
+  io.src[2] = src(vn, h->h_v, vb);
+  void* out_map = host_mapped(out);
+  const bool out_direct = out_map != nullptr;
+  io.out = out_direct ? out_map : host_mapped(h->h_out);
+  if (!io.src[0] || !io.src[1] || !io.src[2] || !io.out)
+    return set_err(h, TTKV_ECUDA, "decode_step: staging buffers are not mapped");
+  // the reads of q/k/v and the write of the output are part of the (captured)
+  // step; the previous step is complete (synchronized), so h->io is free
   int rc = decode_core(h, h->q_dev, h->kn_dev, h->vn_dev,
-                       dtype == TTKV_DTYPE_F16 ? kInF16 : kInF32, h->out_dev, rep, true, host);
+                       dtype == TTKV_DTYPE_F16 ? kInF16 : kInF32, nullptr, rep, true);
   if (rc) return rc;
   CU(h, cudaStreamSynchronize(h->s0));
   if (!out_direct) std::memcpy(out, h->h_out, ob);

@@ -246,6 +246,7 @@ struct CombineArgs {
   const uint32_t* nslots;       // slow partial slots per stream (balanced schedule), else
                                 // ceil(union_count / CH)
   double* out;                  // [S][G][d_v] (reference output is double)
+  double* const* out_ref;       // non-null: the output address is *out_ref (host-buffer steps)
   uint32_t literal;
   uint64_t* pos_inc;  // the device step position, advanced once the step is combined
   // Fused all-gather over peer memory (multi-GPU sharding): each CTA also
@@ -266,8 +267,22 @@ struct CombineArgs {
   uint64_t n_cap;
   uint32_t spec_n;
   uint32_t* spec_ctr;
+  // Host-buffer steps: union_count copied into page-locked host memory for
+  // the step report (the combine writes `out` there directly as well).
+  uint32_t* count_out;
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);
+// Host-buffer steps: the device addresses of the caller's (or the staging)
+// page-locked q, k, v and output, in mapped host memory written before each
+// step (graph replays read them at run time).
+struct IoSlot {
+  const void* src[3];
+  void* out;
+};
+// Copies q, k, v from the addresses in *io (device-mapped page-locked host
+// memory) to dst in one chained launch, and forwards io->out to *out_ref.
+cudaError_t launch_ingest(void* const dst[3], const uint64_t bytes[3], const IoSlot* io,
+                          void** out_ref, cudaStream_t st);
 uint32_t combine_slices(const Geometry& g);  // CTAs per (stream, head) row
 uint32_t combine_slices(const CombineArgs& a);  // ... of this launch (speculative: d_v / 32)
 // Blocks the stream until every rank's arrival counter in `flags` reaches

@@ -742,6 +742,54 @@ cudaError_t launch_set_u64(uint64_t* p, uint64_t v, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Host-buffer steps: the step's q, k and v are read straight from page-locked
+// host memory (mapped into the device's address space) by one kernel instead
+// of three copy-engine transfers, each of which costs ~4 us of queue latency
+// on a small step (cfg1: 48 KB in).  The host addresses come from the
+// handle's mapped IoSlot, written by the host before the launch, so a
+// replayed graph of the step holds no caller pointer; the output address is
+// forwarded to *out_ref (device memory) for the combine.  Segment blockIdx.y;
+// 16-byte accesses when both ends are aligned, bytes otherwise.
+struct IngestArgs {
+  void* dst[3];
+  uint64_t bytes[3];
+  const IoSlot* io;
+  void** out_ref;
+};
+__global__ void __launch_bounds__(256) ingest_kernel(IngestArgs a) {
+  pdl_wait();  // the previous step is done with the device copies
+  pdl_trigger();
+  const uint32_t seg = blockIdx.y;
+  uint8_t* d = static_cast<uint8_t*>(a.dst[seg]);
+  const uint8_t* sp = static_cast<const uint8_t*>(a.io->src[seg]);
+  if (seg == 0 && blockIdx.x == 0 && threadIdx.x == 0) *a.out_ref = a.io->out;
+  const uint64_t nb = a.bytes[seg];
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((((uintptr_t)d | (uintptr_t)sp | nb) & 15u) == 0) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(sp);
+    uint4* d4 = reinterpret_cast<uint4*>(d);
+    for (uint64_t i = t0; i < nb / 16; i += stride) d4[i] = s4[i];
+  } else {
+    for (uint64_t i = t0; i < nb; i += stride) d[i] = sp[i];
+  }
+}
+
+cudaError_t launch_ingest(void* const dst[3], const uint64_t bytes[3], const IoSlot* io,
+                          void** out_ref, cudaStream_t st) {
+  IngestArgs a{};
+  uint64_t most = 0;
+  for (int i = 0; i < 3; ++i) {
+    a.dst[i] = dst[i];
+    a.bytes[i] = bytes[i];
+    most = std::max<uint64_t>(most, bytes[i]);
+  }
+  a.io = io;
+  a.out_ref = out_ref;
+  const uint64_t ctas = std::min<uint64_t>(256, std::max<uint64_t>(1, (most / 16 + 255) / 256));
+  return launch_chained(ingest_kernel, dim3((uint32_t)ctas, 3), dim3(256), 0, st, a);
+}
+
 // ---------------------------------------------------------------------------
 // synthetic N(0,1) KV for perf runs (on-device generation is
 // acceptable at cfg2-5 scale): counter-based hash + Box-Muller.

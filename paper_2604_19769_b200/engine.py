@@ -260,7 +260,10 @@ class MultiStreamEngine:
         elif out.dtype != np.float64 or out.shape != shape or not out.flags.c_contiguous:
             raise ShapeError("decode_step: out must be a C-contiguous float64 [S, G, d_v] array")
         rep = L.StepReportC()
-        _check(self._lib.ttkv_gpu_decode_step(self._h, _ptr(q), _ptr(k), _ptr(v), dt, _ptr(out),
+        # plain addresses (c_void_p arguments): a.ctypes.data costs half of
+        # a.ctypes.data_as(...) on this per-token path
+        _check(self._lib.ttkv_gpu_decode_step(self._h, q.ctypes.data, k.ctypes.data,
+                                              v.ctypes.data, dt, out.ctypes.data,
                                               C.byref(rep)), self._h)
         r = DecodeStepReport(output=out, blocks_scored=rep.blocks_scored,
                              blocks_fetched=rep.blocks_fetched,

@@ -52,9 +52,14 @@ MODES = [(0, 0), (1, 1), (1, 2)]
 
 def run_mode(tmp_path, mode, **env_over):
     tier, rs = mode
-    tag = "_".join(f"{k}{v}" for k, v in sorted(env_over.items()))
+    tag = "_".join(f"{k}{v if v is not None else 'unset'}" for k, v in sorted(env_over.items()))
     out = str(tmp_path / f"{tag}_{tier}_{rs}.npz")
-    env = dict(os.environ, **env_over)
+    env = dict(os.environ)
+    for k, v in env_over.items():  # None: unset (the library's default)
+        if v is None:
+            env.pop(k, None)
+        else:
+            env[k] = v
     subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT, tier=tier, rs=rs, out=out)],
                    env=env, check=True, timeout=600)
     r = np.load(out)
@@ -78,5 +83,16 @@ def test_graph_replay_bit_identical(tmp_path, mode):
     # the one after the host append), every other non-evicting step a replay
     assert int(a["replays"]) >= 250 and 3 <= int(a["captures"]) <= 6
     assert int(b["replays"]) == 0
+    assert np.array_equal(a["out"], b["out"])
+    assert np.array_equal(a["fetched"], b["fetched"])
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_host_buffer_steps_replay_by_default(tmp_path, mode):
+    """Without TTKV_GRAPH the synchronous host-buffer call replays its step as
+    a graph (it waits for every step, so no cross-step overlap is lost)."""
+    a = run_mode(tmp_path, mode, TTKV_GRAPH=None)
+    b = run_mode(tmp_path, mode, TTKV_GRAPH="0")
+    assert int(a["replays"]) >= 250 and int(b["replays"]) == 0
     assert np.array_equal(a["out"], b["out"])
     assert np.array_equal(a["fetched"], b["fetched"])
