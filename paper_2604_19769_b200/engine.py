@@ -174,6 +174,27 @@ def _ptr(a):
     return a.ctypes.data_as(C.c_void_p)
 
 
+class _AddrCache:
+    """Data addresses of the last few arrays passed to the per-token call
+    (a.ctypes.data costs ~1.3-2.4 us per array).  Each entry holds its array,
+    so its id cannot be reused by another object and its buffer cannot be
+    resized (ndarray.resize refuses while another reference exists)."""
+
+    def __init__(self, size=16):
+        self._d = {}
+        self._size = size
+
+    def __call__(self, a):
+        e = self._d.get(id(a))
+        if e is not None and e[0] is a:
+            return e[1]
+        if len(self._d) >= self._size:
+            self._d.pop(next(iter(self._d)))
+        addr = a.ctypes.data
+        self._d[id(a)] = (a, addr)
+        return addr
+
+
 class MultiStreamEngine:
     """S lockstep KV streams x G query heads on one B200 (include/ttkv_gpu.h)."""
 
@@ -187,6 +208,9 @@ class MultiStreamEngine:
         self.S, self.G = n_streams, heads_per_stream
         self.device = device
         self._lib = L.lib()
+        self._rep = L.StepReportC()  # reused by decode_step (its fields are copied out)
+        self._rep_ref = C.byref(self._rep)
+        self._addr = _AddrCache()
         self._c_cfg = config.to_c()
         self._c_pol = self.policy.to_c()
         self._c_opt = L.OptionsC(device, n_streams, heads_per_stream, int(group_select),
@@ -245,7 +269,7 @@ class MultiStreamEngine:
         written to.  Page-locked inputs / `out` (e.g. numpy views of
         torch.empty(..., pin_memory=True)) are DMA'd directly; pageable ones
         go through the handle's pinned staging buffers."""
-        q = _f32(query).reshape(-1)
+        q = _f32(query)  # the caller's array itself when already f32 and contiguous
         k, dt = _kv(key)
         v, _ = _kv(value)
         if v.dtype != k.dtype:
@@ -255,16 +279,21 @@ class MultiStreamEngine:
         if k.size != self.S * self.config.d_k or v.size != self.S * self.config.d_v:
             raise ShapeError("append_token: key/value dimension mismatch")
         shape = (self.S, self.G, self.config.d_v)
+        out_given = out is not None
         if out is None:
             out = np.empty(shape, np.float64)  # fully written by the call
         elif out.dtype != np.float64 or out.shape != shape or not out.flags.c_contiguous:
             raise ShapeError("decode_step: out must be a C-contiguous float64 [S, G, d_v] array")
-        rep = L.StepReportC()
-        # plain addresses (c_void_p arguments): a.ctypes.data costs half of
-        # a.ctypes.data_as(...) on this per-token path
-        _check(self._lib.ttkv_gpu_decode_step(self._h, q.ctypes.data, k.ctypes.data,
-                                              v.ctypes.data, dt, out.ctypes.data,
-                                              C.byref(rep)), self._h)
+        rep = self._rep
+        # cached addresses for the caller's own arrays (reused step after
+        # step); converted temporaries are looked up directly
+        ad = self._addr
+        aq = ad(q) if q is query else q.ctypes.data
+        ak = ad(k) if k is key else k.ctypes.data
+        av = ad(v) if v is value else v.ctypes.data
+        ao = ad(out) if out_given else out.ctypes.data
+        _check(self._lib.ttkv_gpu_decode_step(self._h, aq, ak, av, dt, ao, self._rep_ref),
+               self._h)
         r = DecodeStepReport(output=out, blocks_scored=rep.blocks_scored,
                              blocks_fetched=rep.blocks_fetched,
                              bytes_transferred=rep.bytes_transferred,
