@@ -167,33 +167,47 @@ __device__ __forceinline__ void stage_query_f64(const Geometry& g, const float* 
     }
   }
 }
-// Thread t < rows: acc[h] = score of staged row t against head h.  Waits for
-// the chunks as it goes (every thread of the CTA must call it: barriers).
+// Scores staged rows, waiting for the chunks as it goes (every thread of the
+// CTA must call it: barriers).  Row (threadIdx.x & 127) against heads [h0, h0 + cnt): threads 0..127 take
+// the first ceil(GS/2) heads, threads 128..255 the rest (nb <= 128 rows per
+// CTA), so all eight warps score -- the per-thread chains are what bound this
+// phase.  Each (row, head) is still one fma per channel, channels in order.
+template <int GS>
+constexpr int kScoreHeadsA = (GS + 1) / 2;
 template <int GS>
 __device__ __forceinline__ void score_staged_rows(const Geometry& g, const double* qs,
                                                   const float* tile, uint32_t rows, uint32_t nb,
-                                                  double (&acc)[GS]) {
+                                                  double (&acc)[kScoreHeadsA<GS>], uint32_t& h0,
+                                                  uint32_t& cnt) {
+  constexpr int HA = kScoreHeadsA<GS>;
+  const uint32_t row = threadIdx.x & 127u;
+  const bool upper = threadIdx.x >= 128u;
+  h0 = upper ? (uint32_t)HA : 0u;
+  cnt = upper ? (uint32_t)(GS - HA) : (uint32_t)HA;
+  if (row >= rows) cnt = 0;
 #pragma unroll
-  for (int h = 0; h < GS; ++h) acc[h] = 0.0;
+  for (int h = 0; h < HA; ++h) acc[h] = 0.0;
   const uint32_t nch = g.d_k / 32;
   for (uint32_t ch = 0; ch < nch; ++ch) {
     cp_async_wait_upto(nch - 1 - ch);
     __syncthreads();  // chunk ch (and q) visible to every thread
-    if (threadIdx.x < rows) {
-      const float* tr = tile + ((size_t)ch * nb + threadIdx.x) * kFusedPitch;
-      const double* qc = qs + 32 * ch;
+    if (cnt) {  // warp-uniform except in the last partial warp of rows
+      const float* tr = tile + ((size_t)ch * nb + row) * kFusedPitch;
+      const double* qc = qs + (size_t)h0 * g.d_k + 32 * ch;
 #pragma unroll 4
       for (uint32_t c = 0; c < 32; c += 4) {
         const float4 cv = *reinterpret_cast<const float4*>(tr + c);
         const double c0 = cv.x, c1 = cv.y, c2 = cv.z, c3 = cv.w;
 #pragma unroll
-        for (int h = 0; h < GS; ++h) {
-          const double2 q01 = *reinterpret_cast<const double2*>(qc + h * g.d_k + c);
-          const double2 q23 = *reinterpret_cast<const double2*>(qc + h * g.d_k + c + 2);
-          acc[h] = __fma_rn(q01.x, c0, acc[h]);
-          acc[h] = __fma_rn(q01.y, c1, acc[h]);
-          acc[h] = __fma_rn(q23.x, c2, acc[h]);
-          acc[h] = __fma_rn(q23.y, c3, acc[h]);
+        for (int h = 0; h < HA; ++h) {
+          if (h < (int)cnt) {
+            const double2 q01 = *reinterpret_cast<const double2*>(qc + h * g.d_k + c);
+            const double2 q23 = *reinterpret_cast<const double2*>(qc + h * g.d_k + c + 2);
+            acc[h] = __fma_rn(q01.x, c0, acc[h]);
+            acc[h] = __fma_rn(q01.y, c1, acc[h]);
+            acc[h] = __fma_rn(q23.x, c2, acc[h]);
+            acc[h] = __fma_rn(q23.y, c3, acc[h]);
+          }
         }
       }
     }
@@ -409,9 +423,10 @@ uint32_t select_max_blocks() { return kSelectMaxN; }
 // thread-block cluster (relevance.cpp:19-43, engine.cpp:51-58).
 //   * CTA r of the cluster owns blocks [r nb, (r+1) nb): its centroid rows are
 //     staged in 32-channel chunks with 16-byte cp.async (row pitch 36 floats:
-//     conflict-free LDS.128), then thread t scores row t against every
-//     selection head, channels in order with one fma each -- the same fp64
-//     chain as score_kernel, so the same bits.
+//     conflict-free LDS.128), then threads t and t + 128 score row t against
+//     half the selection heads each, channels in order with one fma each --
+//     the same fp64 chain as score_kernel, so the same bits (the chain of 128
+//     dependent fmas, not the loads, bounds this phase: 2.5 us of ~10).
 //   * after a cluster barrier, CTA h gathers head h's n order keys from the
 //     cluster's shared memory (DSMEM) and runs the radix selection of
 //     select_topk_kernel on them; its selected set lands as a bitmask in CTA 0.
@@ -483,13 +498,16 @@ __global__ void __launch_bounds__(kTopkThreads) select_fused_kernel(FusedSelectA
   // ---- score: row t against every head (score_staged_rows: the same fp64
   // chain as score_kernel, so the same bits) ----
   {
-    double acc[GS];
-    score_staged_rows<GS>(g, qs, tile, rows, L.nb, acc);
-    if (threadIdx.x < rows)
+    double acc[kScoreHeadsA<GS>];
+    uint32_t h0, cnt;
+    score_staged_rows<GS>(g, qs, tile, rows, L.nb, acc, h0, cnt);
+    const uint32_t row = threadIdx.x & 127u;
 #pragma unroll
-      for (int h = 0; h < GS; ++h) {
-        a.scores[((uint64_t)s * g.Gs + h) * g.n_cap + r0 + threadIdx.x] = acc[h];
-        keys[h * L.nb + threadIdx.x] = order_key(acc[h]);
+    for (int j = 0; j < kScoreHeadsA<GS>; ++j)
+      if (j < (int)cnt) {
+        const uint32_t h = h0 + j;
+        a.scores[((uint64_t)s * g.Gs + h) * g.n_cap + r0 + row] = acc[j];
+        keys[h * L.nb + row] = order_key(acc[j]);
       }
   }
   TTKV_PHASE_STAMP(2);
@@ -532,9 +550,10 @@ __global__ void __launch_bounds__(kTopkThreads) select_fused_kernel(FusedSelectA
     const uint32_t b = 256 * warp + 32 * j + lane;
     uint32_t m = 0;
     if (b < n)
-      for (uint32_t h = 0; h < g.Gs; ++h)
+#pragma unroll
+      for (int h = 0; h < GS; ++h)  // GS == g.Gs (launch_select_fused)
         if ((selbits[h * L.nw + (b >> 5)] >> (b & 31)) & 1u)
-          m |= (g.Gs == g.G) ? (1u << h) : all_heads;
+          m |= (GS == g.G) ? (1u << h) : all_heads;
     mw[j] = m;
     bal[j] = __ballot_sync(0xffffffffu, m != 0u);
     cnt += __popc(bal[j]);
@@ -568,7 +587,7 @@ bool select_fused_supported(const Geometry& g, uint32_t n, uint32_t sms) {
   }();
   if (!on || n == 0 || n > kFusedMaxN || g.d_k % 32 != 0 || g.d_k > 128 || g.Gs > 8) return false;
   const FusedLayout L = fused_layout(g, n);
-  if (L.CL > 16 || L.nb > kTopkThreads || L.bytes > 200 * 1024) return false;
+  if (L.CL > 16 || L.nb > 128 || L.bytes > 200 * 1024) return false;  // two thread halves per row
   // one wave: the clusters hold their SMs through two barriers, so a second
   // wave would wait for the first (cfg2, S = 256: 120 us vs 74 us for the three-kernel chain)
   const uint64_t per_sm = std::min<uint64_t>(kTopkThreads == 256 ? 8 : 4,
