@@ -751,3 +751,54 @@ def test_free_select_top_k_any_n(gpu, n):
         rc = L.lib().ttkv_gpu_select_top_k(0, p(scores), p(ids), n, k, p(out))
         assert rc == 0, L.lib().ttkv_last_error()
         assert np.array_equal(out[:k], ids[order[:k]]), (n, k)
+
+
+@pytest.mark.parametrize("slow_tier", [0, 1])
+def test_host_api_unaligned_buffers_match_device_path(gpu, slow_tier):
+    """The host-buffer step's ingest kernel reads q/k/v through the device
+    mapping of page-locked memory (16-byte accesses when aligned, bytes
+    otherwise) and the combine writes the output there: page-locked buffers at
+    odd offsets with a row size that is not a multiple of 16 bytes (d = 40,
+    fp16 k/v) give the same bits as the device-buffer step on the same inputs,
+    step after step (graph replays with changing addresses) across an eviction."""
+    import torch
+    T_ = gpu
+    S, G, d, B, lf, ctx, steps = 3, 2, 40, 32, 256, 1000, 40
+    cfg = T_.TierConfig(hbm_budget_bytes=lf * 2 * d * 2, d_k=d, d_v=d, block_size=B)
+    rng = np.random.default_rng(23)
+    pk = O.fp16_round(rng.standard_normal((S, ctx, d)))
+    pv = O.fp16_round(rng.standard_normal((S, ctx, d)))
+    ins = [(rng.standard_normal((S, G, d)).astype(np.float32),
+            rng.standard_normal((S, d)).astype(np.float16),
+            rng.standard_normal((S, d)).astype(np.float16)) for _ in range(steps)]
+    keep = []
+
+    def pinned_at(a, off):
+        raw = torch.empty(a.nbytes + 64, dtype=torch.uint8, pin_memory=True)
+        keep.append(raw)
+        v = raw.numpy()[off:off + a.nbytes].view(a.dtype).reshape(a.shape)
+        v[...] = a
+        return v
+
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.Stream(device=dev)
+    host = T_.MultiStreamEngine(cfg, n_streams=S, heads_per_stream=G, slow_tier=slow_tier)
+    devi = T_.MultiStreamEngine(cfg, n_streams=S, heads_per_stream=G, slow_tier=slow_tier)
+    devi.set_stream(stream.cuda_stream)
+    for e in (host, devi):
+        e.prefill(pk, pv)
+    out_h = pinned_at(np.zeros((S, G, d), np.float64), 8)
+    evicted = False
+    for i, (q, k, v) in enumerate(ins):
+        r = host.decode_step(pinned_at(q, 4 + 4 * (i % 3)), pinned_at(k, 2 + 2 * (i % 5)),
+                             pinned_at(v, 6), out=out_h)
+        evicted |= r.eviction_occurred
+        tq, tk, tv = (torch.from_numpy(x).to(dev) for x in (q, k, v))
+        to = torch.empty((S, G, d), dtype=torch.float64, device=dev)
+        torch.cuda.synchronize()
+        devi.decode_step_device(tq.data_ptr(), tk.data_ptr(), tv.data_ptr(), to.data_ptr())
+        devi.synchronize()
+        assert np.array_equal(out_h, to.cpu().numpy()), f"step {i}"
+    assert evicted
+    host.close()
+    devi.close()
