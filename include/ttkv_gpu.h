@@ -147,7 +147,8 @@ typedef struct {
   uint64_t payload_bytes;   /* bytes of each record streamed over PCIe (codes);
                                the per-channel params are staged from HBM */
   uint64_t graph_replays;   /* decode steps launched as a replay of the captured
-                               step graph (TTKV_GRAPH=0: none) */
+                               step graph (host-buffer steps by default;
+                               TTKV_GRAPH=1: every step, 0: none) */
   uint64_t graph_captures;  /* step graphs captured (one per eviction period) */
   uint64_t spec_steps;      /* decode steps that streamed every record beside the
                                selection (HBM slow tier, small steps; see
@@ -195,7 +196,11 @@ int ttkv_gpu_prefill_device(struct ttkv_gpu* h, const void* keys, const void* va
 /* Host buffers, synchronous: q[S][G][d_k] f32, k_new[S][d_k], v_new[S][d_v]
  * (dtype), out[S][G][d_v] f64 (DecodeStepReport::output is double; values are
  * accumulated in fp32 for an fp16 ring and in fp64 for an fp32 ring).
- * report may be NULL. */
+ * report may be NULL.  Page-locked (cudaHostAlloc'd, or registered and
+ * mapped) buffers are read and written by the step's kernels in place;
+ * pageable ones go through the handle's page-locked staging copies.  The step
+ * replays as a CUDA graph (one per eviction period; TTKV_GRAPH=0: launched
+ * kernel by kernel). */
 int ttkv_gpu_decode_step(struct ttkv_gpu* h, const float* q, const void* k_new,
                          const void* v_new, int dtype, double* out, ttkv_step_report* report);
 /* Device buffers, enqueued on the handle's stream, returns immediately.

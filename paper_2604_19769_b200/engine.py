@@ -267,8 +267,9 @@ class MultiStreamEngine:
         """query [S, G, d_k], key [S, d_k], value [S, d_v] -> output [S, G, d_v].
         `out` (optional): a C-contiguous float64 [S, G, d_v] array the output is
         written to.  Page-locked inputs / `out` (e.g. numpy views of
-        torch.empty(..., pin_memory=True)) are DMA'd directly; pageable ones
-        go through the handle's pinned staging buffers."""
+        torch.empty(..., pin_memory=True)) are read and written by the step's
+        kernels in place (device mapping); pageable ones go through the
+        handle's page-locked staging buffers."""
         q = _f32(query)  # the caller's array itself when already f32 and contiguous
         k, dt = _kv(key)
         v, _ = _kv(value)
