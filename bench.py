@@ -734,7 +734,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "e2e": {"value": tokens_per_step * 1000.0 / e2e_ms, "unit": UNIT,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-                "host_buffers": "page-locked caller buffers, DMA'd by the step (ttkv_gpu_decode_step)"},
+                "host_buffers": "page-locked caller buffers, read and written in place by the step's kernels (ttkv_gpu_decode_step)"},
         "prefill_s": round(prefill_s, 2),
     }
     if world > 1:
