@@ -637,10 +637,24 @@ __global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs
   __shared__ Acc red[kCombineWarps];
   auto part = [&](uint32_t i) { return i < a.nfc ? fp + i * pitch : sp + (i - a.nfc) * pitch; };
 
+  // one partial per thread (np <= blockDim: every step but the longest fast
+  // tiers) keeps its (m, l) in registers across the max and the sum: one
+  // round trip to L2 instead of two on the step's critical path
+  const bool one = np <= blockDim.x;
+  Acc m1 = -INFINITY, l1 = 0;
+  if (one && threadIdx.x < np) {
+    const Acc* p = part(threadIdx.x);
+    m1 = p[g.d_v];
+    l1 = p[g.d_v + 1];
+  }
   Acc M = -INFINITY;
-  for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
-    const Acc* p = part(i);
-    if (p[g.d_v + 1] > 0) M = fmax(M, p[g.d_v]);
+  if (one) {
+    if (l1 > 0) M = m1;
+  } else {
+    for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
+      const Acc* p = part(i);
+      if (p[g.d_v + 1] > 0) M = fmax(M, p[g.d_v]);
+    }
   }
   M = wmax(M);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = M;
@@ -650,11 +664,19 @@ __global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs
   for (int k = 1; k < kCombineWarps; ++k) M = fmax(M, red[k]);
   __syncthreads();
   Acc L = 0;
-  for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
-    const Acc* p = part(i);
-    const Acc wi = p[g.d_v + 1] > 0 ? ex2(p[g.d_v] - M) : Acc(0);
-    w[i] = wi;
-    L += wi * p[g.d_v + 1];
+  if (one) {
+    if (threadIdx.x < np) {
+      const Acc wi = l1 > 0 ? ex2(m1 - M) : Acc(0);
+      w[threadIdx.x] = wi;
+      L = wi * l1;
+    }
+  } else {
+    for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
+      const Acc* p = part(i);
+      const Acc wi = p[g.d_v + 1] > 0 ? ex2(p[g.d_v] - M) : Acc(0);
+      w[i] = wi;
+      L += wi * p[g.d_v + 1];
+    }
   }
   L = wsum(L);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = L;
