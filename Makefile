@@ -25,11 +25,20 @@ $(LIBDIR)/libttkv_gpu.so: $(CU_OBJ)
 oracle:
 	$(MAKE) -C oracle
 
+# measurement-only variant with %globaltimer stamps (tools/chain_stamps.py)
+STAMP_OBJ := $(patsubst $(CSRC)/%.cu,build/stamps/obj/%.o,$(CU_SRC))
+build/stamps/obj/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p build/stamps/obj
+	$(NVCC) $(NVFLAGS) -DTTKV_STAMPS -c $< -o $@ 2> build/stamps/obj/$*.ptxas.log || (cat build/stamps/obj/$*.ptxas.log; exit 1)
+build/stamps/libttkv_gpu.so: $(STAMP_OBJ)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(STAMP_OBJ)
+stamps: build/stamps/libttkv_gpu.so
+
 clean:
 	rm -rf build $(LIBDIR)
 	$(MAKE) -C oracle clean
 
-.PHONY: all lib oracle clean
+.PHONY: all lib oracle clean stamps
 
 # ---- C++ drop-in (reference ttkv:: API over the C ABI) ---------------------------
 CXX      ?= g++

@@ -31,6 +31,7 @@
 
 #include "ttkv_kernels.cuh"
 #include "ttkv_launch.h"
+#include "ttkv_dbg_stamps.cuh"
 
 namespace ttkv_dev {
 
@@ -611,9 +612,27 @@ cudaError_t launch_fast(const FastArgs& a, cudaStream_t st) {
 // One CTA per (stream, head): weights w_i = exp2(m_i - M) of every partial
 // are computed once into smem, then each thread reduces one output channel.
 constexpr int kCombineWarps = 8;
+#ifdef TTKV_STAMPS
+TTKV_DBG_TABLE(comb)
+TTKV_DBG_READER(comb)
+#endif
 template <typename Acc>
 __global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs a) {
-  pdl_wait();  // the slow partials (the fast tier joins through an event)
+  TTKV_DBG_STAMP(comb, 0);
+  pdl_wait();  // the slow partials (the fast tier joins through an event or below)
+  if (a.fast_epoch) {  // device-side join with the fast tier (other stream)
+    if (threadIdx.x == 0) {
+      const uint32_t target = *reinterpret_cast<volatile const uint32_t*>(a.comb_epoch) + 1u;
+      for (;;) {
+        uint32_t v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.fast_epoch) : "memory");
+        if ((int32_t)(v - target) >= 0) break;
+        __nanosleep(64);
+      }
+    }
+    __syncthreads();
+  }
+  TTKV_DBG_STAMP(comb, 1);
   // the next kernel may get resident now: the next step's selection stages
   // its centroids while this combine runs (it reads q only after its wait)
   pdl_trigger();
@@ -764,6 +783,14 @@ __global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs
                      : "memory");
     }
   }
+  if (a.fast_epoch) {  // every CTA has read *comb_epoch: the last one advances it
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(a.comb_arrive, 1u) == gridDim.x * gridDim.y - 1) {
+      *a.comb_arrive = 0u;
+      atomicAdd(a.comb_epoch, 1u);
+    }
+  }
+  TTKV_DBG_END(comb);
 }
 
 // Combine of the speculative record stream (slow_attn_tc_spec_kernel): the

@@ -25,6 +25,7 @@
 
 #include "ttkv_kernels.cuh"
 #include "ttkv_launch.h"
+#include "ttkv_dbg_stamps.cuh"
 
 namespace ttkv_dev {
 
@@ -95,9 +96,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 
 }  // namespace
 
+#ifdef TTKV_STAMPS
+TTKV_DBG_TABLE(fast)
+TTKV_DBG_READER(fast)
+#endif
 template <int ND, int GT>
 __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
     fast_attn_tc_kernel(const __grid_constant__ FastTcArgs a) {
+  TTKV_DBG_STAMP(fast, 0);
   constexpr int D = 64 * ND;        // head dim
   constexpr int KSTEPS = D / 16;    // QK k-steps
   constexpr uint32_t STAGE = 2 * ND * kBox;
@@ -319,6 +325,20 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32)
       p[D + 1] = ntiles ? lst[gq] : 0.f;
     }
   }
+  if (a.done_epoch) {  // device-side join: the combine waits on *done_epoch
+    named_bar(1, nthreads_c);  // every consumer's partial stores precede the fence
+    if (threadIdx.x == 32) {
+      __threadfence();
+      if (atomicAdd(a.done_arrive, 1u) == gridDim.x * gridDim.y - 1) {
+        *a.done_arrive = 0u;
+        __threadfence();
+        atomicAdd(a.done_epoch, 1u);
+#ifdef TTKV_STAMPS
+        fast_st[(fast_launch - 1) % ttkv_dbg::kSlots][15] = ttkv_dbg::now_ns();
+#endif
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -418,11 +438,21 @@ constexpr size_t slow_tc_tail_bytes() {
 }
 }  // namespace
 
+#ifdef TTKV_STAMPS
+TTKV_DBG_TABLE(slow)
+TTKV_DBG_READER(slow)
+TTKV_DBG_CTA_TABLE(slow)
+TTKV_DBG_CTA_READER(slow)
+#endif
 template <int GT, int ST>
 __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
     slow_attn_tc_kernel(const __grid_constant__ SlowTcArgs a) {
   constexpr bool PK = GT <= 4;  // hi/lo packed into the N dimension
+  TTKV_DBG_STAMP(slow, 0);
+  TTKV_DBG_CTA(slow, 0, 32);
   pdl_wait();  // the union lists (launched chained behind the selection)
+  TTKV_DBG_STAMP(slow, 1);
+  TTKV_DBG_CTA(slow, 1, 32);
   const Geometry& g = a.g;
   const uint32_t G = g.G;
   const uint32_t c = blockIdx.x;
@@ -467,6 +497,10 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
     __syncthreads();
   }
   const uint32_t n_rec = sched[2];
+#ifdef TTKV_STAMPS
+  if (threadIdx.x == 32 && blockIdx.x < 1024) slow_cta[blockIdx.x][5] = n_rec;
+#endif
+  TTKV_DBG_CTA(slow, 2, 32);
   if (n_rec == 0) return;
   const uint32_t s_first = sched[0], i_first = sched[1], slot_first = sched[3];
 
@@ -593,6 +627,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
     for (uint32_t i = r0; i < r0 + seg; ++i) {
       const uint32_t st = i % ST;
       mbar_wait(&full[st], (i / ST) & 1);
+      if (i == 0) TTKV_DBG_CTA(slow, 3, 32);
       uint8_t* stg = base + st * kSlowStage;
       const uint32_t kb = smem_u32(stg);
       const uint8_t* vn = stg + kKBox;
@@ -885,6 +920,7 @@ __global__ void __launch_bounds__(32 + kSlowConsumerWarps * 32, ST == 2 ? 3 : 2)
     r0 += seg;
     ii += seg;
   }
+  TTKV_DBG_CTA(slow, 4, 32);
   pdl_trigger();  // the combine's CTAs may get resident while partials drain
 }
 

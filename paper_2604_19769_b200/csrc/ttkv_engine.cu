@@ -252,6 +252,9 @@ struct ttkv_gpu {
   IoSlot* io = nullptr;      // host-buffer steps: q/k/v/out addresses (mapped, pinned)
   IoSlot* io_dev = nullptr;  // ... its device mapping (read by the ingest kernel)
   double** out_ref = nullptr;  // device word: the step's output address (ingest -> combine)
+  // device-side join of the fast tier into the combine: {fast arrive, fast
+  // epoch, combine arrive, combine epoch}
+  uint32_t* join = nullptr;
   void* fpart = nullptr;
   void* spart = nullptr;
   uint64_t spart_chunks = 0;
@@ -420,7 +423,7 @@ void free_all(ttkv_gpu* h) {
   };
   F(h->ring_k); F(h->ring_v); F(h->cent); F(h->params); F(h->scores); F(h->mask); F(h->uids);
   F(h->umask); F(h->ucount); F(h->nslots); F(h->fpart); F(h->spart); F(h->q_dev);
-  F(h->rpart); F(h->spec_ctr); F(h->out_ref);
+  F(h->rpart); F(h->spec_ctr); F(h->out_ref); F(h->join);
   F(h->kn_dev); F(h->vn_dev); F(h->stg_k); F(h->stg_v); F(h->stage_arena);
   if (h->arena_host) pinned_free(h->arena_host);
   else if (h->arena_dev) cudaFree(h->arena_dev);
@@ -705,6 +708,8 @@ struct StepPlan {
   bool fast_last;        // the fast tier runs on s0 after the record stream
   bool fused;            // score + select + union as one cluster kernel
   bool spec;             // speculative record stream beside the selection
+  bool dev_join;         // the combine joins the fast tier on the device (no event wait)
+  bool capturing;        // enqueue_step runs inside a graph capture
   double scale_log2;
 };
 
@@ -758,6 +763,7 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
       a.FC = P.FCs;
       a.nfc = P.nfc;
       a.scale_log2 = P.scale_log2;
+      a.done_arrive = a.done_epoch = nullptr;
       KTimer t(h, K_FAST, h->s0);
       CU(h, launch_fast_tc(a, h->s0, true));
       return TTKV_OK;
@@ -775,6 +781,8 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
       a.FC = P.FCs;
       a.nfc = P.nfc;
       a.scale_log2 = P.scale_log2;
+      a.done_arrive = P.dev_join ? h->join : nullptr;
+      a.done_epoch = P.dev_join ? h->join + 1 : nullptr;
       {
         KTimer t(h, K_FAST, h->s1);
         CU(h, launch_fast_tc(a, h->s1));
@@ -903,7 +911,7 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
   }
   if (P.fast_last) {
     if (int rcf = fork_fast()) return rcf;
-  } else if (!P.spec && !P.fast_first) {
+  } else if (!P.spec && !P.fast_first && !P.dev_join) {
     CU(h, cudaStreamWaitEvent(h->s0, h->ev_join, 0));
   }
   {
@@ -928,6 +936,11 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
     }
     a.out = P.out;  // host-buffer steps: the caller's (or the staging) page-locked buffer
     a.out_ref = P.host_io ? h->out_ref : nullptr;
+    if (P.dev_join) {
+      a.fast_epoch = h->join + 1;
+      a.comb_arrive = h->join + 2;
+      a.comb_epoch = h->join + 3;
+    }
     a.count_out = P.host_io && P.slow ? h->h_ucount_dev : nullptr;
     a.literal = h->opt.literal_additive_merge ? 1u : 0u;
     a.pos_inc = h->pos_dev;
@@ -955,6 +968,11 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
                 h->s0));
     }
   }
+  // a graph capture must join s1 back into s0; launched directly, the side
+  // stream needs no join (the combine waited for the fast tier on the device,
+  // and the append precedes it on s1), and an event wait here would cut the
+  // programmatic overlap with the next step's selection
+  if (P.dev_join && P.capturing) CU(h, cudaStreamWaitEvent(h->s0, h->ev_join, 0));
   return TTKV_OK;
 }
 
@@ -1046,6 +1064,30 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
   P.fast_last = P.slow && !P.spec && h->fast_tc && order_env == 2;
   if (P.fast_first) P.early_fork = true;
   if (P.fast_last) P.early_fork = false;
+  // The combine joins the fast tier on the device instead of through an event
+  // wait on s0, which would make it a plain launch after the record kernel's
+  // full completion (layer-sequential: ~3.6 us per layer, tools/chain_stamps.py).
+  // Only when the fast tier is forked at the step start and the combine grid
+  // is at most one CTA per SM, so its waiting CTAs always leave room for the
+  // fast tier's; and only when the fast tier's bytes are small against the
+  // record stream's (at most a quarter of the union's upper bound), so it is
+  // done long before the combine starts.  When it is not (cfg1: 67 MB of ring
+  // against ~86 MB of records), the fast tier shares the SMs with the record
+  // stream and ends last, and the early combine's waiting CTAs cost more than
+  // the launch they save (42.2 vs 39.4 us per step).
+  static const int join_env = [] {  // TTKV_DEV_JOIN=0: the event wait, 1: the device join
+    const char* e = std::getenv("TTKV_DEV_JOIN");      // whatever the byte ratio (measurement)
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
+  {
+    const double fast_bytes = (double)g.S * (double)P.F * (g.d_k + g.d_v) * g.elem;
+    const double slow_ub = (double)g.S * (double)std::min<uint64_t>(P.n, (uint64_t)g.Gs * P.k) *
+                           (double)g.rec.used;
+    P.dev_join = join_env != 0 && P.slow && h->fast_tc && P.early_fork && !P.spec &&
+                 !P.fast_first && !P.fast_last && !h->pg.active &&
+                 (uint64_t)g.S * g.G * combine_slices(g) <= (uint64_t)h->sms &&
+                 (join_env == 1 || 4.0 * fast_bytes <= slow_ub);
+  }
   P.CH = 4;
   if (P.slow) {
     if (h->slow_tc) {
@@ -1157,7 +1199,9 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
       }
       const uint64_t l0 = h->launches;
       CU(h, cudaStreamBeginCapture(h->s0, cudaStreamCaptureModeRelaxed));
+      P.capturing = true;
       const int rc = enqueue_step(h, P);
+      P.capturing = false;
       cudaGraph_t graph = nullptr;
       const cudaError_t ce = cudaStreamEndCapture(h->s0, &graph);
       if (rc) {
@@ -1396,6 +1440,8 @@ int ttkv_gpu_create(const ttkv_tier_config* cfg, const ttkv_selection_policy* po
   CREATE_CU(pinned_alloc((void**)&h->io, sizeof(IoSlot)));
   CREATE_CU(cudaHostGetDevicePointer((void**)&h->io_dev, h->io, 0));
   CREATE_CU(cudaMalloc((void**)&h->out_ref, sizeof(double*)));
+  CREATE_CU(cudaMalloc((void**)&h->join, 4 * sizeof(uint32_t)));
+  CREATE_CU(cudaMemset(h->join, 0, 4 * sizeof(uint32_t)));
   CREATE_CU(cudaMalloc((void**)&h->fpart, S * g.G * h->nfc_cap * (g.d_v + 2) * h->acc));
   CREATE_CU(cudaMalloc((void**)&h->q_dev, S * g.G * g.d_k * sizeof(float)));
   CREATE_CU(cudaMalloc(&h->kn_dev, S * g.d_k * 4));

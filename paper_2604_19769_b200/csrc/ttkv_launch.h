@@ -161,6 +161,10 @@ struct alignas(64) FastTcArgs {
   const uint64_t* pos;  // device step position: F = *pos + 1 - front (null: F)
   uint32_t F, FC, nfc;
   double scale_log2;
+  // device-side join (null: off): the last CTA to finish bumps *done_epoch
+  // (release) once every CTA's partials are stored
+  uint32_t* done_arrive;
+  uint32_t* done_epoch;
 };
 // Tensor-core slow tier (K8/V4, d = B = 128): TMA tensor maps over the
 // record arena + mma.sync on raw codes with the affine params folded in.
@@ -270,6 +274,13 @@ struct CombineArgs {
   // Host-buffer steps: union_count copied into page-locked host memory for
   // the step report (the combine writes `out` there directly as well).
   uint32_t* count_out;
+  // Device-side join with the fast tier (null: the stream waits on its event
+  // instead): wait until *fast_epoch passes *comb_epoch, and the last CTA to
+  // finish bumps *comb_epoch.  Only for grids that leave room on every SM for
+  // the fast tier's CTAs (see enqueue_step).
+  const uint32_t* fast_epoch;
+  uint32_t* comb_epoch;
+  uint32_t* comb_arrive;
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st);
 // Host-buffer steps: the device addresses of the caller's (or the staging)

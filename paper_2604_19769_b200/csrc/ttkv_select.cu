@@ -23,6 +23,7 @@
 
 #include "ttkv_kernels.cuh"
 #include "ttkv_launch.h"
+#include "ttkv_dbg_stamps.cuh"
 
 namespace ttkv_dev {
 
@@ -436,6 +437,11 @@ uint32_t select_max_blocks() { return kSelectMaxN; }
 // before selection (layer-sequential decode is latency-bound on this chain).
 // ---------------------------------------------------------------------------
 constexpr uint32_t kFusedMaxN = 2048;
+#if defined(TTKV_STAMPS) && !defined(TTKV_PHASE_STAMP)  // in-chain phases (tools/chain_stamps.py)
+TTKV_DBG_TABLE(sel)
+TTKV_DBG_READER(sel)
+#define TTKV_PHASE_STAMP(k) TTKV_DBG_STAMP(sel, k)
+#endif
 #ifndef TTKV_PHASE_STAMP  // tools/fused_probe.cu times the phases with %globaltimer
 #define TTKV_PHASE_STAMP(k)
 #endif

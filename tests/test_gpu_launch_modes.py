@@ -96,3 +96,16 @@ def test_host_buffer_steps_replay_by_default(tmp_path, mode):
     assert int(a["replays"]) >= 250 and int(b["replays"]) == 0
     assert np.array_equal(a["out"], b["out"])
     assert np.array_equal(a["fetched"], b["fetched"])
+
+
+@pytest.mark.parametrize("graph", ["0", "1"])
+def test_device_join_bit_identical(tmp_path, graph):
+    """The combine joining the fast tier on the device (TTKV_DEV_JOIN=1: an
+    epoch counter the fast tier's last CTA advances, no event wait on the
+    record stream) gives the same bits as the event join, launched directly
+    and replayed as a graph, across evictions and a host-side append."""
+    mode = (1, 1)  # HBM tier, union stream: the fused selection forks the fast tier early
+    a = run_mode(tmp_path, mode, TTKV_DEV_JOIN="1", TTKV_GRAPH=graph)
+    b = run_mode(tmp_path, mode, TTKV_DEV_JOIN="0", TTKV_GRAPH=graph)
+    assert np.array_equal(a["out"], b["out"])
+    assert np.array_equal(a["fetched"], b["fetched"])
