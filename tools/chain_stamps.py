@@ -104,11 +104,12 @@ def main():
     print(f"# record kernel, the last launch: {grid} CTAs, records per CTA "
           f"min {cta[:, 5].min():.0f} median {np.median(cta[:, 5]):.0f} max {cta[:, 5].max():.0f}; "
           "us after the first CTA's wait returns (median / max over CTAs)")
+    busy = cta[:, 5] > 0  # CTAs with records (the rest stamp no record phases)
     for k, nm in [(0, "entry"), (1, "after wait"), (2, "schedule done"), (3, "first record in smem"),
                   (4, "last partial written")]:
-        v = (cta[:, k] - t0) / 1e3
+        v = (cta[busy if k >= 3 else slice(None), k] - t0) / 1e3
         print(f"  {nm:22s} {np.median(v):8.2f} {v.max():8.2f}  (min {v.min():.2f})")
-    per = (cta[:, 4] - cta[:, 3]) / 1e3 / np.maximum(cta[:, 5] - 1, 1)
+    per = (cta[busy, 4] - cta[busy, 3]) / 1e3 / np.maximum(cta[busy, 5] - 1, 1)
     print(f"  us per record after the first: median {np.median(per):.2f}")
     print(f"# layer-sequential chain, {Lyr} layers x {tokens} tokens, medians over {n - 1} layers,")
     print("# us after the previous layer's combine end (%globaltimer, measurement build)")
