@@ -793,6 +793,166 @@ __global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs
   TTKV_DBG_END(comb);
 }
 
+// Small-step combine (fp32 partials, d_v = 128 in four 32-channel slices,
+// additive merge -- one layer of a layer-sequential decode, cfg1): the
+// partials' (m, l) AND this slice's values are loaded in one round trip
+// (thread t: (m, l) of partial t; values of partials t/4 + 64j, channels
+// c_lo + 8 (t % 4) .. + 8) before the max is known, instead of three
+// dependent passes over L2; the weighted sums are reduced with warp shuffles
+// and one shared-memory pass.  Partials beyond the first 256 take a second
+// pass.  Same merge as combine_kernel (another summation order).
+constexpr int kRow32Groups = 4;  // partial groups of 64 prefetched per thread
+__global__ void __launch_bounds__(256) combine_row32_kernel(CombineArgs a) {
+  TTKV_DBG_STAMP(comb, 0);
+  pdl_wait();  // the slow partials
+  if (a.fast_epoch) {  // device-side join with the fast tier (other stream)
+    if (threadIdx.x == 0) {
+      const uint32_t target = *reinterpret_cast<volatile const uint32_t*>(a.comb_epoch) + 1u;
+      for (;;) {
+        uint32_t v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.fast_epoch) : "memory");
+        if ((int32_t)(v - target) >= 0) break;
+        __nanosleep(64);
+      }
+    }
+    __syncthreads();
+  }
+  TTKV_DBG_STAMP(comb, 1);
+  pdl_trigger();
+  const Geometry& g = a.g;
+  const uint32_t idx = blockIdx.x, s = idx / g.G;
+  const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint32_t pitch = g.d_v + 2;
+  const uint32_t nsc_used = !a.union_count         ? 0u
+                            : a.union_count[s] == 0u ? 0u
+                            : a.nslots               ? a.nslots[s]
+                                                     : (a.union_count[s] + a.CH - 1) / a.CH;
+  const float* fp = reinterpret_cast<const float*>(a.fpart) + (uint64_t)idx * a.nfc * pitch;
+  const float* sp = a.spart ? reinterpret_cast<const float*>(a.spart) + (uint64_t)idx * a.nsc * pitch
+                            : nullptr;
+  const uint32_t np = a.nfc + nsc_used;
+  auto part = [&](uint32_t i) { return i < a.nfc ? fp + i * pitch : sp + (i - a.nfc) * pitch; };
+  const uint32_t c0 = blockIdx.y * 32 + 8 * (t & 3);  // this thread's 8 channels
+  extern __shared__ __align__(16) uint8_t csm[];
+  float* w = reinterpret_cast<float*>(csm);  // [np] weights
+  __shared__ float red[8];
+  __shared__ float red2[8];
+  __shared__ float sums[8][32];
+
+  // ---- one round trip: (m, l) of partial t and the values of partials t/4 + 64j ----
+  float m1 = -INFINITY, l1 = 0.f;
+  if (t < np) {
+    const float* p = part(t);
+    m1 = p[g.d_v];
+    l1 = p[g.d_v + 1];
+  }
+  float2 v[kRow32Groups][4];
+#pragma unroll
+  for (int j = 0; j < kRow32Groups; ++j) {
+    const uint32_t pi = (t >> 2) + 64u * j;
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      v[j][e] = pi < np ? *reinterpret_cast<const float2*>(part(pi) + c0 + 2 * e) : make_float2(0.f, 0.f);
+  }
+  // ---- block max over the partials with tokens, then the weights ----
+  float M = (t < np && l1 > 0.f) ? m1 : -INFINITY;
+  for (uint32_t i = t + 256; i < np; i += 256) {  // beyond 256 partials
+    const float* p = part(i);
+    if (p[g.d_v + 1] > 0.f) M = fmaxf(M, p[g.d_v]);
+  }
+  M = wmax(M);
+  if (lane == 0) red[warp] = M;
+  __syncthreads();
+  M = red[0];
+#pragma unroll
+  for (int k = 1; k < 8; ++k) M = fmaxf(M, red[k]);
+  float L = 0.f;
+  if (t < np) {
+    const float wi = l1 > 0.f ? ex2(m1 - M) : 0.f;
+    w[t] = wi;
+    L = wi * l1;
+  }
+  for (uint32_t i = t + 256; i < np; i += 256) {
+    const float* p = part(i);
+    const float wi = p[g.d_v + 1] > 0.f ? ex2(p[g.d_v] - M) : 0.f;
+    w[i] = wi;
+    L += wi * p[g.d_v + 1];
+  }
+  L = wsum(L);
+  if (lane == 0) red2[warp] = L;
+  __syncthreads();  // w[] and the L partials are visible
+  float Lt = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) Lt += red2[k];
+  // ---- weighted sum of this thread's partials, 8 channels ----
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+#pragma unroll
+  for (int j = 0; j < kRow32Groups; ++j) {
+    const uint32_t pi = (t >> 2) + 64u * j;
+    const float wj = pi < np ? w[pi] : 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      acc[2 * e] += wj * v[j][e].x;
+      acc[2 * e + 1] += wj * v[j][e].y;
+    }
+  }
+  for (uint32_t pi = (t >> 2) + 64u * kRow32Groups; pi < np; pi += 64) {
+    const float wj = w[pi];
+    const float* p = part(pi) + c0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] += wj * p[e];
+  }
+  // lanes with the same t % 4 hold the same channels: reduce over lane bits 2-4
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    float x = acc[e];
+    x += __shfl_xor_sync(0xffffffffu, x, 4);
+    x += __shfl_xor_sync(0xffffffffu, x, 8);
+    x += __shfl_xor_sync(0xffffffffu, x, 16);
+    acc[e] = x;
+  }
+  if (lane < 4) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) sums[warp][8 * lane + e] = acc[e];
+  }
+  __syncthreads();
+  double* const out = a.out_ref ? *a.out_ref : a.out;
+  if (t < 32) {
+    float A = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) A += sums[k][t];
+    const float o = A * (1.f / Lt);
+    const uint32_t c = blockIdx.y * 32 + t;
+    out[(uint64_t)idx * g.d_v + c] = (double)o;
+    if (a.n_peers) {
+      const uint64_t gi = ((uint64_t)a.gidx[s] * g.G + (idx - s * g.G)) * g.d_v + c;
+      for (uint32_t r = 0; r < a.n_peers; ++r) a.peer_out[r][gi] = (double)o;
+    }
+  }
+  if (a.pos_inc && blockIdx.x == 0 && blockIdx.y == 0 && t == 0) *a.pos_inc += 1;
+  if (a.count_out && idx == s * g.G && blockIdx.y == 0 && t == 0)
+    a.count_out[s] = a.union_count ? a.union_count[s] : 0u;
+  if (a.n_peers) {
+    __syncthreads();
+    if (t == 0) {
+      __threadfence_system();
+      for (uint32_t r = 0; r < a.n_peers; ++r)
+        asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(a.peer_flags[r] + a.my_rank)
+                     : "memory");
+    }
+  }
+  if (a.fast_epoch) {
+    __syncthreads();
+    if (t == 0 && atomicAdd(a.comb_arrive, 1u) == gridDim.x * gridDim.y - 1) {
+      *a.comb_arrive = 0u;
+      atomicAdd(a.comb_epoch, 1u);
+    }
+  }
+  TTKV_DBG_END(comb);
+}
+
 // Combine of the speculative record stream (slow_attn_tc_spec_kernel): the
 // slow partials are per-record rows rpart[s][h][b] and head h merges exactly
 // the records it selected -- the union entries with its bit set.  One CTA per
@@ -975,6 +1135,15 @@ cudaError_t launch_peer_wait(const unsigned long long* flags, uint32_t n_ranks,
 
 // channel slices per (stream, head): enough CTAs to keep the combine from
 // being latency-bound when S*G is small (one layer of a layer-sequential step)
+// TTKV_COMBINE_ROW32=0: the three-pass combine_kernel for small steps too (measurement)
+static bool row32_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TTKV_COMBINE_ROW32");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 uint32_t combine_slices(const Geometry& g) {
   const uint32_t rows = g.S * g.G;
   if (rows >= 256 || g.d_v <= 32) return 1;
@@ -1000,6 +1169,10 @@ cudaError_t launch_combine(const CombineArgs& a, cudaStream_t st) {
     cudaFuncSetAttribute(combine_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     return launch_chained(combine_kernel<double>, grid, dim3(kCombineWarps * 32), smem, st, a);
+  } else if (!a.literal && a.g.d_v == 128 && combine_slices(a.g) == 4 && row32_enabled()) {
+    cudaFuncSetAttribute(combine_row32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    return launch_chained(combine_row32_kernel, grid, dim3(256), smem, st, a);
   } else {
     cudaFuncSetAttribute(combine_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
