@@ -1856,26 +1856,28 @@ static size_t fast_tc_smem(const Geometry& g) {
 }
 
 template <int ND, int GT>
-static cudaError_t launch_fast_tc_t(const FastTcArgs& a, cudaStream_t st, bool chained) {
+static cudaError_t launch_fast_tc_t(const FastTcArgs& a, cudaStream_t st, int chained) {
   const size_t smem = fast_tc_smem(a.g);
   auto kern = fast_attn_tc_kernel<ND, GT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // max smem
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid(a.nfc, a.g.S);
-  if (chained) return launch_chained(kern, grid, dim3(32 + kSlowConsumerWarps * 32), smem, st, a);
+  if (chained == 1) return launch_chained(kern, grid, dim3(32 + kSlowConsumerWarps * 32), smem, st, a);
+  if (chained == 2)
+    return launch_chained_background(kern, grid, dim3(32 + kSlowConsumerWarps * 32), smem, st, a);
   return launch_background(kern, grid, dim3(32 + kSlowConsumerWarps * 32), smem, st, a);
 }
 
 template <int ND>
-static cudaError_t launch_fast_tc_g(const FastTcArgs& a, cudaStream_t st, bool chained) {
+static cudaError_t launch_fast_tc_g(const FastTcArgs& a, cudaStream_t st, int chained) {
   if (a.g.G <= 1) return launch_fast_tc_t<ND, 1>(a, st, chained);
   if (a.g.G <= 2) return launch_fast_tc_t<ND, 2>(a, st, chained);
   if (a.g.G <= 4) return launch_fast_tc_t<ND, 4>(a, st, chained);
   return launch_fast_tc_t<ND, 8>(a, st, chained);
 }
 
-cudaError_t launch_fast_tc(const FastTcArgs& a, cudaStream_t st, bool chained) {
+cudaError_t launch_fast_tc(const FastTcArgs& a, cudaStream_t st, int chained) {
   return a.g.d_k == 128 ? launch_fast_tc_g<2>(a, st, chained) : launch_fast_tc_g<1>(a, st, chained);
 }
 

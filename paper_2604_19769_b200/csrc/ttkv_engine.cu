@@ -765,11 +765,22 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
       a.scale_log2 = P.scale_log2;
       a.done_arrive = a.done_epoch = nullptr;
       KTimer t(h, K_FAST, h->s0);
-      CU(h, launch_fast_tc(a, h->s0, true));
+      CU(h, launch_fast_tc(a, h->s0, 1));
       return TTKV_OK;
     }
-    CU(h, cudaEventRecord(h->ev_fork, h->s0));
-    CU(h, cudaStreamWaitEvent(h->s1, h->ev_fork, 0));
+    // Forked at the step start, s1 already waits for this point of s0 (the
+    // append's ev_start): no second fork, and the fast tier chains behind the
+    // append on s1 (its CTAs get resident while the append runs; chained-fork
+    // env TTKV_FAST_CHAIN=0 is the control).
+    static const bool chain_env = [] {
+      const char* e = std::getenv("TTKV_FAST_CHAIN");
+      return !(e && e[0] == '0');
+    }();
+    const bool chain_s1 = P.early_fork && chain_env;
+    if (!chain_s1) {
+      CU(h, cudaEventRecord(h->ev_fork, h->s0));
+      CU(h, cudaStreamWaitEvent(h->s1, h->ev_fork, 0));
+    }
     if (h->fast_tc) {
       FastTcArgs& a = h->tc;
       a.g = g;
@@ -785,7 +796,7 @@ int enqueue_step(ttkv_gpu* h, const StepPlan& P) {
       a.done_epoch = P.dev_join ? h->join + 1 : nullptr;
       {
         KTimer t(h, K_FAST, h->s1);
-        CU(h, launch_fast_tc(a, h->s1));
+        CU(h, launch_fast_tc(a, h->s1, chain_s1 ? 2 : 0));
       }
       CU(h, cudaEventRecord(h->ev_join, h->s1));
       return TTKV_OK;

@@ -38,6 +38,25 @@ cudaError_t launch_chained(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
+// Chained (programmatic) at the least priority: side-stream work behind a
+// kernel of its own stream.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_chained_background(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                      cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributePriority;
+  attr[0].val.priority = launch_priority(false);
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 // A plain launch at the least priority (work that overlaps the critical path).
 template <typename... KArgs, typename... Args>
 cudaError_t launch_background(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
@@ -211,7 +230,10 @@ uint32_t fast_tc_tile();
 cudaError_t make_ring_tmaps(const Geometry& g, void* ring_k, void* ring_v, FastTcArgs& a);
 // chained: programmatic launch at critical priority (speculative record
 // stream: the fast tier runs in the step's chain, not on the side stream)
-cudaError_t launch_fast_tc(const FastTcArgs& a, cudaStream_t st, bool chained = false);
+// chained: 1 = programmatic behind the previous kernel at high priority (the
+// speculative chain on s0), 2 = programmatic at the least priority (behind
+// the append on the side stream)
+cudaError_t launch_fast_tc(const FastTcArgs& a, cudaStream_t st, int chained = 0);
 
 struct SlowArgs {
   Geometry g;
