@@ -611,6 +611,26 @@ cudaError_t launch_fast(const FastArgs& a, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // One CTA per (stream, head): weights w_i = exp2(m_i - M) of every partial
 // are computed once into smem, then each thread reduces one output channel.
+// Device-side join with the fast tier (CombineArgs::fast_epoch): wait until
+// the fast tier's epoch passes this combine's.  The fast tier of the step
+// was launched before the combine and never waits on it, so the wait ends;
+// a broken invariant (a step whose fast tier was never launched) traps after
+// ~2 s -- the context reports an error -- instead of hanging the device.
+__device__ __forceinline__ void wait_fast_epoch(const CombineArgs& a) {
+  const uint32_t target = *reinterpret_cast<volatile const uint32_t*>(a.comb_epoch) + 1u;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.fast_epoch) : "memory");
+    if ((int32_t)(v - target) >= 0) return;
+    __nanosleep(64);
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 2000000000ull) __trap();
+  }
+}
+
 constexpr int kCombineWarps = 8;
 #ifdef TTKV_STAMPS
 TTKV_DBG_TABLE(comb)
@@ -621,15 +641,7 @@ __global__ void __launch_bounds__(kCombineWarps * 32) combine_kernel(CombineArgs
   TTKV_DBG_STAMP(comb, 0);
   pdl_wait();  // the slow partials (the fast tier joins through an event or below)
   if (a.fast_epoch) {  // device-side join with the fast tier (other stream)
-    if (threadIdx.x == 0) {
-      const uint32_t target = *reinterpret_cast<volatile const uint32_t*>(a.comb_epoch) + 1u;
-      for (;;) {
-        uint32_t v;
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.fast_epoch) : "memory");
-        if ((int32_t)(v - target) >= 0) break;
-        __nanosleep(64);
-      }
-    }
+    if (threadIdx.x == 0) wait_fast_epoch(a);
     __syncthreads();
   }
   TTKV_DBG_STAMP(comb, 1);
@@ -806,15 +818,7 @@ __global__ void __launch_bounds__(256) combine_row32_kernel(CombineArgs a) {
   TTKV_DBG_STAMP(comb, 0);
   pdl_wait();  // the slow partials
   if (a.fast_epoch) {  // device-side join with the fast tier (other stream)
-    if (threadIdx.x == 0) {
-      const uint32_t target = *reinterpret_cast<volatile const uint32_t*>(a.comb_epoch) + 1u;
-      for (;;) {
-        uint32_t v;
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.fast_epoch) : "memory");
-        if ((int32_t)(v - target) >= 0) break;
-        __nanosleep(64);
-      }
-    }
+    if (threadIdx.x == 0) wait_fast_epoch(a);
     __syncthreads();
   }
   TTKV_DBG_STAMP(comb, 1);

@@ -1230,7 +1230,16 @@ int decode_core(ttkv_gpu* h, const float* q, const void* kn, const void* vn, int
     }
   } else {
     int rc = enqueue_step(h, P);
-    if (rc) return rc;
+    if (rc) {
+      // a step cut short may have launched the fast tier without its combine:
+      // drain both streams and restart the join epochs in step
+      if (P.dev_join) {
+        cudaStreamSynchronize(h->s1);
+        cudaStreamSynchronize(h->s0);
+        cudaMemset(h->join, 0, 4 * sizeof(uint32_t));
+      }
+      return rc;
+    }
   }
   h->appended = pos + 1;
   if (P.spec) h->spec_steps++;
