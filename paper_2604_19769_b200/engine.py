@@ -295,12 +295,10 @@ class MultiStreamEngine:
         ao = ad(out) if out_given else out.ctypes.data
         _check(self._lib.ttkv_gpu_decode_step(self._h, aq, ak, av, dt, ao, self._rep_ref),
                self._h)
-        r = DecodeStepReport(output=out, blocks_scored=rep.blocks_scored,
-                             blocks_fetched=rep.blocks_fetched,
-                             bytes_transferred=rep.bytes_transferred,
-                             eviction_occurred=bool(rep.eviction_occurred),
-                             fast_tokens=rep.fast_tokens, union_blocks=rep.union_blocks,
-                             pcie_bytes=rep.pcie_bytes)
+        # positional: the per-token path (keyword arguments cost ~0.6 us more)
+        r = DecodeStepReport(out, rep.blocks_scored, rep.blocks_fetched, [],
+                             rep.bytes_transferred, bool(rep.eviction_occurred), rep.fast_tokens,
+                             rep.union_blocks, rep.pcie_bytes)
         if fetched:
             r.fetched_blocks = [[self.read_fetched(s, g) for g in range(self.G)]
                                 for s in range(self.S)]
